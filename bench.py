@@ -1,0 +1,442 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 structured-sketch apply (BASELINE.json metric: sketch input GB/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference] [--config cfg2]
+
+One step = one pass of the hot path over one config-sized batch of synthetic input already
+resident in HBM (config 2 by default: the SRTT sketch Y = A*Omega of a 65536 x 8192 float32 A,
+2 GiB, larger than the 126 MB L2, so no flush is needed between steps).  Under torchrun every
+rank processes its own batch (row blocks of a N*65536-row matrix; no collective on the data path)
+and `value` = all ranks' input bytes / the max-over-ranks device time ("scaling": "weak").
+
+`--impl reference` times the reference algorithm on the host (the CPU oracle port in oracle/,
+which restates sketchkit's NumPy/SciPy path) on a bounded row sample with every host core.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sketch input GB/s (% of HBM peak) for sparse/SRTT/KR Y=AΩ, 1–8 B200"
+FALLBACK_HBM_GBS = 6650.0
+
+
+# ---------------------------------------------------------------------------------------------
+# workloads (BASELINE.json configs; synthetic inputs with the configs' shapes and distributions)
+# ---------------------------------------------------------------------------------------------
+def _cfg2(torch, dev, rank):
+    from paper_2508_21189_b200.sketch import SparseRttTM
+
+    n, d, k = 65536, 8192, 512
+    tm = SparseRttTM(d, k, 1, "wht", seed=0)
+    g = torch.Generator(device=dev).manual_seed(1000 + rank)
+    a = torch.randn(n, d, dtype=torch.float32, device=dev, generator=g)
+    a /= torch.arange(1, d + 1, dtype=torch.float32, device=dev)  # sigma_j = 1/j
+    return dict(name="cfg2", tm=tm, a=a, n=n, d=d, k=k, launches=1, kernel="srtt_wht_fast",
+                workload="cfg2 SRTT sketch Y=A*D*H*S: A 65536x8192 f32 (sigma_j=1/j), WHT d=8192, k=512, xi=1",
+                op="right")
+
+
+def _cfg1(torch, dev, rank):
+    from paper_2508_21189_b200.sketch import SparseUniformTM
+
+    n, d, k = 16384, 4096, 256
+    tm = SparseUniformTM(d, k, 4, seed=0)
+    g = torch.Generator(device=dev).manual_seed(2000 + rank)
+    a = torch.randn(n, d, dtype=torch.float64, device=dev, generator=g)
+    return dict(name="cfg1", tm=tm, a=a, n=n, d=d, k=k, launches=1, kernel="sparse_right_kernel",
+                workload="cfg1 sparse sign Y=A*Omega: A 16384x4096 f64, zeta=4, k=256", op="right")
+
+
+def _cfg3(torch, dev, rank):
+    from paper_2508_21189_b200.sketch import SparseUniformTM
+
+    n, d, k = 131072, 16384, 200
+    tm = SparseUniformTM(d, k, 8, seed=0)
+    g = torch.Generator(device=dev).manual_seed(3000 + rank)
+    a = torch.randn(n, d, dtype=torch.float32, device=dev, generator=g)
+    return dict(name="cfg3", tm=tm, a=a, n=n, d=d, k=k, launches=1, kernel="sparse_right_kernel",
+                workload="cfg3 RSVD sketch Y=A*Omega: A 131072x16384 f32 (iid input for throughput), zeta=8, k=200",
+                op="right")
+
+
+def _cfg4(torch, dev, rank):
+    from paper_2508_21189_b200.sketch import SparseUniformTM
+
+    n, d, k = 4194304, 512, 2048
+    tm = SparseUniformTM(n, k, 8, seed=0)
+    g = torch.Generator(device=dev).manual_seed(4000 + rank)
+    a = torch.randn(n, d, dtype=torch.float32, device=dev, generator=g)
+    return dict(name="cfg4", tm=tm, a=a, n=n, d=d, k=k, launches=2, kernel="sparse_adjoint_kernel",
+                workload="cfg4 SA sketch: S (2048 x 4194304, zeta=8) applied to A 4194304x512 f32", op="adjoint")
+
+
+def _cfg5(torch, dev, rank):
+    from paper_2508_21189_b200.sketch import KhatriRaoTM
+
+    n, d, k = 16384, 65536, 512
+    tm = KhatriRaoTM(256, 2, k, "real_rademacher", seed=0)
+    g = torch.Generator(device=dev).manual_seed(5000 + rank)
+    a = torch.randn(n, d, dtype=torch.float32, device=dev, generator=g)
+    return dict(name="cfg5", tm=tm, a=a, n=n, d=d, k=k, launches=None, kernel="kr (library path)",
+                workload="cfg5 Khatri-Rao sketch: A 16384x65536 f32, ell=2, d0=256, k=512", op="right")
+
+
+WORKLOADS = {"cfg1": _cfg1, "cfg2": _cfg2, "cfg3": _cfg3, "cfg4": _cfg4, "cfg5": _cfg5}
+
+
+def _apply(w, x):
+    return w["tm"].apply_right(x) if w["op"] == "right" else w["tm"].apply_adjoint(x)
+
+
+def _bytes(w, dtype_size):
+    a_bytes = w["n"] * w["d"] * dtype_size
+    out_elems = w["n"] * w["k"] if w["op"] == "right" else w["k"] * w["d"]
+    return a_bytes, a_bytes + out_elems * dtype_size
+
+
+# ---------------------------------------------------------------------------------------------
+# clocks sampling during the timed region
+# ---------------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[4:8]):
+                if flag.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------------
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def _traffic(name):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(name)
+    except (OSError, ValueError):
+        return None
+
+
+def _dist(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        if torch.cuda.is_available():
+            torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def _barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def _max_over_ranks(world, value, dev):
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def time_device(torch, w, steps, warmup, world, dev):
+    """Device-timed steps (CUDA events on the launching stream); returns (total_s, per-step list)."""
+    a = w["a"]
+    for _ in range(warmup):
+        _apply(w, a)
+    torch.cuda.synchronize()
+    _barrier(world)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    start_all = torch.cuda.Event(enable_timing=True)
+    end_all = torch.cuda.Event(enable_timing=True)
+    start_all.record(stream)
+    for i in range(steps):
+        ev[i][0].record(stream)
+        _apply(w, a)
+        ev[i][1].record(stream)
+    end_all.record(stream)
+    torch.cuda.synchronize()
+    _barrier(world)
+    torch.cuda.synchronize()
+    per = [s.elapsed_time(e) / 1e3 for s, e in ev]
+    total = start_all.elapsed_time(end_all) / 1e3
+    return total, per
+
+
+def time_e2e(torch, w, steps, world, dev):
+    """Through the public API with pinned HOST buffers: H2D of A, kernel, D2H of Y, every step."""
+    a_host = torch.empty(w["a"].shape, dtype=w["a"].dtype, pin_memory=True)
+    a_host.copy_(w["a"])
+    y = _apply(w, a_host)  # warm-up of the host path (pinned staging, caches)
+    torch.cuda.synchronize()
+    _barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        y = _apply(w, a_host)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    el = _max_over_ranks(world, el, dev)
+    h2d = a_host.numel() * a_host.element_size()
+    d2h = y.numel() * y.element_size()
+    del a_host
+    return el, h2d, d2h
+
+
+def cpu_reference_step(w, a_host, procs):
+    """The reference algorithm (oracle port) on host rows `a_host`."""
+    import oracle as orc
+
+    name = w["name"]
+    tm = w["tm"]
+    if name == "cfg2":
+        dv, samp = orc.srtt_parts(tm.d, tm.k, tm.xi, tm.seed)
+        fn = lambda x: orc.srtt_right(dv, samp, x, "wht")  # noqa: E731
+    elif name in ("cfg1", "cfg3"):
+        om = orc.sparse_uniform_csr(tm.d, tm.k, tm.zeta, tm.seed)
+        fn = lambda x: orc.csr_right(om, x)  # noqa: E731
+    elif name == "cfg5":
+        f = orc.kr_factors(tm.d0, tm.ell, tm.k, tm.seed, tm.base)
+        fn = lambda x: orc.kr_right(f, x)  # noqa: E731
+    else:
+        raise ValueError(name)
+    t0 = time.perf_counter()
+    y = orc.right_multiprocess(fn, a_host, procs=procs, rows=max(1, a_host.shape[0] // (4 * procs)))
+    return time.perf_counter() - t0, y
+
+
+SAMPLE_ROWS = {"cfg1": 4096, "cfg2": 2048, "cfg3": 512, "cfg5": 16}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU algorithm (oracle port) on all host cores, rank 0 only."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import torch
+
+    procs = os.cpu_count() or 1
+    w = WORKLOADS[args.config](torch, torch.device("cpu") if not torch.cuda.is_available() else torch.device("cuda", 0), 0)
+    rows = SAMPLE_ROWS[args.config]
+    a_host = w["a"][:rows].cpu().numpy()
+    del w["a"]
+    a_bytes_row = w["d"] * a_host.itemsize
+    times = []
+    for i in range(args.warmup + args.steps):
+        dt, _ = cpu_reference_step(w, a_host, procs)
+        if i >= args.warmup:
+            times.append(dt)
+    med = statistics.median(times)
+    value = rows * a_bytes_row / med / 1e9
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if a_host.dtype == np.float32 else "f64", "data": "synthetic",
+        "config": {"workload": w["workload"], "rows_per_step": rows, "parallelism": f"{procs} host processes"},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": procs, "kind": "port",
+                         "sample": f"{rows} rows of the {args.config} input per step (oracle/ port of sketchkit, "
+                                   f"float64 NumPy/SciPy, row-parallel over {procs} processes)"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+    return 0
+
+
+def measure(torch, w, steps, warmup, world, rank, dev, with_e2e, clocks_idx):
+    a = w["a"]
+    esize = a.element_size()
+    a_bytes, alg_bytes = _bytes(w, esize)
+    with ClockSampler(clocks_idx) as cs:
+        total, per = time_device(torch, w, steps, warmup, world, dev)
+    total = _max_over_ranks(world, total, dev)
+    mean_step = statistics.mean(per)
+    res = {
+        "value": world * a_bytes * steps / total / 1e9,
+        "ms_per_step": total / steps * 1e3,
+        "kernel_ms": mean_step * 1e3,
+        "alg_bytes": alg_bytes,
+        "achieved_gbs": alg_bytes / mean_step / 1e9,
+        "clocks": cs.summary(),
+    }
+    if with_e2e:
+        e_steps = max(1, min(steps, 5))
+        el, h2d, d2h = time_e2e(torch, w, e_steps, world, dev)
+        res["e2e"] = {"value": world * a_bytes * e_steps / el / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                      "d2h_bytes_per_step": d2h, "steps": e_steps,
+                      "path": "tm.apply_right(pinned host torch tensor) -> host tensor (H2D+kernel+D2H)"}
+    return res
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["native", "reference"], default="native")
+    ap.add_argument("--config", choices=sorted(WORKLOADS), default="cfg2")
+    ap.add_argument("--others", default="cfg1,cfg3,cfg4,cfg5", help="extra configs measured at N=1 ('' = none)")
+    args = ap.parse_args(argv)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    world, rank, local = _dist(args)
+    dev = torch.device("cuda", local if world > 1 else 0)
+    peak, peak_src = _peaks()
+
+    w = WORKLOADS[args.config](torch, dev, rank)
+    m = measure(torch, w, args.steps, max(3, args.warmup), world, rank, dev, True, local if world > 1 else 0)
+    esize = w["a"].element_size()
+    launches = w["launches"]
+
+    cpu = None
+    if world == 1 and rank == 0:
+        rows = SAMPLE_ROWS[args.config]
+        a_host = w["a"][:rows].cpu().numpy()
+        procs = os.cpu_count() or 1
+        dt, y_ref = cpu_reference_step(w, a_host, procs)
+        y_gpu = _apply(w, w["a"][:rows]).double().cpu().numpy()
+        err = float(np.linalg.norm(y_gpu - y_ref) / np.linalg.norm(y_ref))
+        cpu = {"value": a_host.nbytes / dt / 1e9, "unit": "GB/s", "cores": procs, "kind": "port",
+               "sample": f"{rows} rows of the {args.config} input ({a_host.nbytes / 1e6:.0f} MB), oracle/ port of the "
+                         f"sketchkit float64 path, row-parallel over {procs} processes",
+               "parity_rel_fro_err_vs_gpu": err}
+
+    others = {}
+    if world == 1 and args.others:
+        del w["a"]
+        torch.cuda.empty_cache()
+        for name in [s for s in args.others.split(",") if s and s != args.config]:
+            try:
+                ow = WORKLOADS[name](torch, dev, rank)
+                om = measure(torch, ow, 3, 3, 1, 0, dev, False, 0)
+                oes = ow["a"].element_size()
+                others[name] = {"workload": ow["workload"], "value_gbs": om["value"], "ms_per_step": om["ms_per_step"],
+                                "dtype": "f32" if oes == 4 else "f64", "kernel": ow["kernel"],
+                                "pct_hbm_peak": 100.0 * om["achieved_gbs"] / peak,
+                                "roofline_achieved_gbs": om["achieved_gbs"], "alg_bytes": om["alg_bytes"]}
+                del ow
+                torch.cuda.empty_cache()
+            except Exception as exc:  # report, never hide
+                others[name] = {"error": f"{type(exc).__name__}: {exc}"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC,
+            "value": m["value"],
+            "unit": "GB/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": max(3, args.warmup),
+            "ms_per_step": m["ms_per_step"],
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32" if esize == 4 else "f64",
+            "data": "synthetic",
+            "config": {"workload": w["workload"], "rows_per_gpu": w["n"], "d": w["d"], "k": w["k"],
+                       "parallelism": f"row blocks over {world} GPU(s), no data-path collective",
+                       "l2": "input 2 GiB per step > 126 MB L2: no flush between steps"},
+            "pct_hbm_peak": 100.0 * m["achieved_gbs"] / peak,
+            "roofline": {"bound": "hbm", "achieved": m["achieved_gbs"], "peak": peak, "unit": "GB/s",
+                         "frac": m["achieved_gbs"] / peak, "traffic": _traffic(args.config),
+                         "kernel": w["kernel"], "alg_bytes_per_launch": m["alg_bytes"],
+                         "kernel_ms_mean": m["kernel_ms"], "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": m["e2e"],
+            "gpu_launches": (launches * args.steps) if launches else None,
+            "clocks": m["clocks"],
+            "others": others,
+        }
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,104 @@
+/*
+ * sketch_b200.h — C ABI of the B200-native structured-sketch library (libsketch_b200.so).
+ *
+ * Drop-in boundary for the reference `sketchkit` apply path.  The reference has no FFI: its
+ * boundary is Python method dispatch on TestMatrix subclasses (pkg/src/sketchkit/sketch/
+ * base.py:48-113).  Each entry point below replaces the compiled third-party routine that
+ * executes one reference apply path and is what a ctypes binding of that path
+ * would call (INTEGRATION.md shows the binding this repo ships).
+ *
+ * Conventions (all entry points):
+ *   - A, Y, SA, workspaces and every Omega array are DEVICE pointers owned by the caller.
+ *   - Matrices are row-major with a leading dimension (row stride, in elements); columns are
+ *     unit-stride.  The reference accepts any memory order; the host layer makes rows contiguous.
+ *   - Every call is asynchronous on the given cudaStream_t (passed as void*; NULL = legacy
+ *     default stream).  Nothing is allocated; workspaces are caller-provided.
+ *   - Return value: SK_OK (0) or a negative status; sk_last_error() gives a thread-local
+ *     message.  Nothing throws across the ABI.
+ *   - dtype: SK_F32 or SK_F64, the element type of A and of the output.
+ *
+ * Omega encodings (built by the host layer from the bit-exact test-matrix arrays):
+ *   bcsc ("blocked column lists") for exactly-zeta-per-row sparse Omega (SparseUniform /
+ *   SparseStack, src/sketch/sparse.py:118-194): the d rows of Omega are cut into chunks of
+ *   `chunk_rows` (a power of two <= 32768).  For chunk h and column c the entries
+ *   ent[ptr[h*k + c] .. ptr[h*k + c + 1]) are uint16 values (local_row << 1) | negative,
+ *   ascending in local_row.  Values are +-1; the 1/sqrt(zeta) magnitude is `scale`.
+ *   srtt sampler (SparseColTM, src/sketch/sparse.py:308-320): samp[c*xi + x] = row | (neg << 31).
+ *   kr sign bits: bit (p*k + j) of f_neg is 1 where factor[p, j] == -1 (src/sketch/khatri_rao.py:46-59).
+ */
+#ifndef SKETCH_B200_H
+#define SKETCH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SK_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define SK_API __attribute__((visibility("default")))
+#else
+#define SK_API
+#endif
+
+enum sk_status {
+  SK_OK = 0,
+  SK_EINVAL = -1,       /* bad shape / leading dimension / dtype / pointer */
+  SK_EUNSUPPORTED = -2, /* valid request this build has no kernel for */
+  SK_ECUDA = -3         /* a CUDA runtime error (message in sk_last_error) */
+};
+
+enum sk_dtype { SK_F32 = 0, SK_F64 = 1 };
+
+enum sk_transform { SK_WHT = 0, SK_DCT3 = 1 };
+
+/* OR-ed into `transform`: every dvals[j] is exactly +1 or -1 (the kernel may use sign bits). */
+#define SK_DIAG_PM1 0x100
+
+/* Library identity and errors. */
+SK_API int sk_abi_version(void);
+SK_API const char* sk_last_error(void);
+/* Number of streaming multiprocessors of `device` (grid sizing), or a negative status. */
+SK_API int sk_device_sm_count(int device);
+
+/*
+ * K1 — Y[n,k] = scale * A[n,d] * Omega[d,k] for a bcsc-encoded sparse Omega.
+ * Replaces `_SparseTM.apply_right` = `a @ self.matrix` (src/sketch/sparse.py:63-66), executed by
+ * scipy sparsetools csc_matvecs.  `chunk_rows` must equal sk_sparse_right_chunk_rows(dtype, d, k).
+ */
+SK_API int sk_sparse_right_chunk_rows(int dtype, int64_t d, int64_t k);
+SK_API int sk_sparse_right(int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
+                    const int32_t* ptr, const uint16_t* ent, int32_t chunk_rows, int64_t k,
+                    double scale, void* Y, int64_t ldy, void* stream);
+
+/*
+ * K2 — SA[k,m] = scale * Omega[d,k]^T * A[d,m] (accumulate != 0: SA += ...).
+ * Replaces `_SparseTM.apply_adjoint` = `self.matrix.conj().T @ b` (src/sketch/sparse.py:68-78).
+ * Workspace of sk_sparse_adjoint_workspace_bytes(...) bytes (may be 0 -> pass NULL).
+ * `chunk_rows` must equal sk_sparse_adjoint_chunk_rows(dtype, d, k).
+ */
+SK_API int sk_sparse_adjoint_chunk_rows(int dtype, int64_t d, int64_t k);
+SK_API size_t sk_sparse_adjoint_workspace_bytes(int dtype, int64_t d, int64_t m, int64_t k);
+SK_API int sk_sparse_adjoint(int dtype, const void* A, int64_t d, int64_t m, int64_t lda,
+                      const int32_t* ptr, const uint16_t* ent, int32_t chunk_rows, int64_t k,
+                      double scale, void* SA, int64_t ldsa, int accumulate, void* ws,
+                      size_t ws_bytes, void* stream);
+
+/*
+ * K3 — Y[n,k] = A[n,d] * D * F * S for the sparse randomized trigonometric transform,
+ * F = unnormalised Walsh-Hadamard (transform SK_WHT, d a power of two); `scale` carries
+ * 1/sqrt(d) * sqrt(d/xi)/sqrt(k).  dvals: d elements of `dtype` (the diagonal D).
+ * Replaces `SparseRttTM.apply_right` (src/sketch/rtt.py:129-140) with wht (rtt.py:28-44).
+ */
+SK_API int sk_srtt_right(int dtype, const void* A, int64_t n, int64_t d, int64_t lda, const void* dvals,
+                  int transform, const int32_t* samp, int32_t xi, int64_t k, double scale, void* Y,
+                  int64_t ldy, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SKETCH_B200_H */

@@ -1,0 +1,95 @@
+"""ctypes binding of libsketch_b200.so (the C ABI declared in include/sketch_b200.h).
+
+There is no fallback: if the library cannot be loaded, or no CUDA device is visible, every
+apply raises.  The binding passes raw device pointers, sizes and the current torch CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from . import _build
+
+SK_OK = 0
+SK_EINVAL = -1
+SK_EUNSUPPORTED = -2
+SK_ECUDA = -3
+SK_F32 = 0
+SK_F64 = 1
+SK_WHT = 0
+SK_DCT3 = 1
+SK_DIAG_PM1 = 0x100
+
+_c_i64 = ctypes.c_int64
+_c_int = ctypes.c_int
+_c_p = ctypes.c_void_p
+_c_dbl = ctypes.c_double
+_c_size = ctypes.c_size_t
+
+# name -> (restype, argtypes); mirrors include/sketch_b200.h
+SIGNATURES = {
+    "sk_abi_version": (_c_int, []),
+    "sk_last_error": (ctypes.c_char_p, []),
+    "sk_device_sm_count": (_c_int, [_c_int]),
+    "sk_sparse_right_chunk_rows": (_c_int, [_c_int, _c_i64, _c_i64]),
+    "sk_sparse_right": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, ctypes.c_int32, _c_i64,
+                                 _c_dbl, _c_p, _c_i64, _c_p]),
+    "sk_sparse_adjoint_chunk_rows": (_c_int, [_c_int, _c_i64, _c_i64]),
+    "sk_sparse_adjoint_workspace_bytes": (_c_size, [_c_int, _c_i64, _c_i64, _c_i64]),
+    "sk_sparse_adjoint": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, ctypes.c_int32, _c_i64,
+                                   _c_dbl, _c_p, _c_i64, _c_int, _c_p, _c_size, _c_p]),
+    "sk_srtt_right": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_int, _c_p, ctypes.c_int32, _c_i64,
+                               _c_dbl, _c_p, _c_i64, _c_p]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+class SketchLibraryError(RuntimeError):
+    """libsketch_b200.so is missing, failed to load, or returned an error status."""
+
+
+def library_path() -> str:
+    return os.environ.get("SKETCH_B200_LIB", _build.lib_path())
+
+
+def load(build_if_missing: bool = True):
+    """Load (building first if needed and nvcc exists) and bind every declared symbol."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        path = library_path()
+        if build_if_missing and "SKETCH_B200_LIB" not in os.environ:
+            try:
+                if _build.needs_build():
+                    _build.build()
+            except RuntimeError as exc:
+                if not os.path.exists(path):
+                    raise SketchLibraryError(f"cannot build {path}: {exc}") from exc
+        if not os.path.exists(path):
+            raise SketchLibraryError(f"{path} not found; run __graft_entry__.build()")
+        try:
+            lib = ctypes.CDLL(path)
+        except OSError as exc:
+            raise SketchLibraryError(f"cannot load {path}: {exc}") from exc
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.sk_abi_version() != 1:
+            raise SketchLibraryError("libsketch_b200.so ABI version mismatch")
+        _lib = lib
+        return lib
+
+
+def check(status: int, what: str) -> None:
+    if status != SK_OK:
+        msg = load().sk_last_error().decode(errors="replace")
+        kind = {SK_EINVAL: ValueError, SK_EUNSUPPORTED: NotImplementedError}.get(status, SketchLibraryError)
+        raise kind(f"{what}: status {status}: {msg}")

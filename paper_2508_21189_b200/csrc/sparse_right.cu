@@ -1,0 +1,253 @@
+// K1 — sparse-sign right apply  Y = scale * A * Omega  (Omega: exactly zeta +-1 per row).
+//
+// Replaces the reference `_SparseTM.apply_right` (src/sketch/sparse.py:63-66), which SciPy runs
+// as csc_matvecs over Omega^T after copying A transposed.  Here A is streamed from HBM exactly
+// once, row-tile by row-tile, and every output element is a register accumulator:
+//
+//   CTA   = 32 rows of A (one per lane) x a block of CB = W*CPW output columns.
+//   warp  = CPW output columns c (c = cb0 + warp + W*j); lane = row.
+//   chunk = R consecutive columns of A (rows of Omega) staged in shared memory, XOR-swizzled so
+//           that (a) 16-byte vector stores of a row segment and (b) the gather pattern "32 lanes
+//           = 32 rows, same column r" are both bank-conflict free.
+//   Omega = bcsc lists: for chunk h and column c, uint16 entries (local_r << 1) | neg.
+//   The next chunk is prefetched into registers (LDG.128, L1 no-allocate) while the current
+//   one is consumed, so HBM reads overlap the shared-memory gathers.
+//
+// Bytes per launch (algorithmic): n*d*sizeof(T) read + n*k*sizeof(T) written.
+#include "common.cuh"
+
+namespace skb {
+namespace {
+
+constexpr int kRowsPerTile = 32;
+
+template <typename T>
+struct VecOf;
+template <>
+struct VecOf<float> {
+  using type = float4;
+  static constexpr int n = 4;
+};
+template <>
+struct VecOf<double> {
+  using type = double2;
+  static constexpr int n = 2;
+};
+
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+
+// Permute a vector so that component q lands at q ^ key (key < n): XOR swizzle inside a 16 B block.
+__device__ __forceinline__ float4 xor_perm(float4 v, int key) {
+  if (key & 1) { float t = v.x; v.x = v.y; v.y = t; t = v.z; v.z = v.w; v.w = t; }
+  if (key & 2) { float t = v.x; v.x = v.z; v.z = t; t = v.y; v.y = v.w; v.w = t; }
+  return v;
+}
+__device__ __forceinline__ double2 xor_perm(double2 v, int key) {
+  if (key & 1) { double t = v.x; v.x = v.y; v.y = t; }
+  return v;
+}
+
+template <typename T, int W, int CPW, int R, bool VEC>
+__global__ void __launch_bounds__(W * 32, 1)
+    sparse_right_kernel(const T* __restrict__ A, int64_t n, int64_t d, int64_t lda,
+                        const int32_t* __restrict__ ptr, const uint16_t* __restrict__ ent,
+                        int64_t k, int nchunks, T scale, T* __restrict__ Y, int64_t ldy) {
+  using V4 = typename VecOf<T>::type;
+  constexpr int NV = VecOf<T>::n;               // elements per 16 B vector
+  constexpr int NT = W * 32;                    // threads
+  constexpr int VEC_PER_ROW = R / NV;
+  constexpr int VPT = kRowsPerTile * VEC_PER_ROW / NT;  // prefetch vectors per thread
+  constexpr int SPT = kRowsPerTile * R / NT;            // scalar elements per thread (!VEC)
+  constexpr int CB = W * CPW;
+  static_assert(R % 32 == 0 && (kRowsPerTile * VEC_PER_ROW) % NT == 0, "tile shape");
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* As = reinterpret_cast<T*>(smem_raw);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t row0 = (int64_t)blockIdx.x * kRowsPerTile;
+  const int64_t cb0 = (int64_t)blockIdx.y * CB;
+
+  V4 pre[VEC ? VPT : 1];
+  T pres[VEC ? 1 : SPT];
+
+  auto load_chunk = [&](int h) {
+    const int64_t c0 = (int64_t)h * R;
+    if constexpr (VEC) {
+#pragma unroll
+      for (int j = 0; j < VPT; ++j) {
+        const int q = tid + j * NT;
+        const int i = q / VEC_PER_ROW, cv = q % VEC_PER_ROW;
+        const int64_t row = row0 + i, col = c0 + (int64_t)cv * NV;
+        if (row < n && col < d) {
+          pre[j] = ld_stream(reinterpret_cast<const V4*>(A + row * lda + col));
+        } else {
+          pre[j] = V4{};
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < SPT; ++j) {
+        const int q = tid + j * NT;
+        const int i = q / R, cc = q % R;
+        const int64_t row = row0 + i, col = c0 + cc;
+        pres[j] = (row < n && col < d) ? A[row * lda + col] : T(0);
+      }
+    }
+  };
+  auto store_chunk = [&]() {
+    if constexpr (VEC) {
+#pragma unroll
+      for (int j = 0; j < VPT; ++j) {
+        const int q = tid + j * NT;
+        const int i = q / VEC_PER_ROW, cv = q % VEC_PER_ROW;
+        const int blk = (cv * NV) ^ (i & 31 & ~(NV - 1));
+        *reinterpret_cast<V4*>(As + i * R + blk) = xor_perm(pre[j], i & (NV - 1));
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < SPT; ++j) {
+        const int q = tid + j * NT;
+        const int i = q / R, cc = q % R;
+        As[i * R + (cc ^ (i & 31))] = pres[j];
+      }
+    }
+  };
+
+  T acc[CPW];
+#pragma unroll
+  for (int j = 0; j < CPW; ++j) acc[j] = T(0);
+
+  const T* my_row = As + lane * R;
+  load_chunk(0);
+  for (int h = 0; h < nchunks; ++h) {
+    __syncthreads();
+    store_chunk();
+    __syncthreads();
+    if (h + 1 < nchunks) load_chunk(h + 1);
+
+    int my_lo = 0, my_hi = 0;
+    if (lane < CPW) {
+      const int64_t c = cb0 + warp + (int64_t)W * lane;
+      if (c < k) {
+        my_lo = __ldg(ptr + (int64_t)h * k + c);
+        my_hi = __ldg(ptr + (int64_t)h * k + c + 1);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < CPW; ++j) {
+      const int lo = __shfl_sync(0xffffffffu, my_lo, j);
+      const int hi = __shfl_sync(0xffffffffu, my_hi, j);
+      T s0 = T(0), s1 = T(0), s2 = T(0), s3 = T(0);
+      for (int base = lo; base < hi; base += 32) {
+        const int cnt = min(32, hi - base);
+        const uint32_t my_e = (lane < cnt) ? (uint32_t)__ldg(ent + base + lane) : 0u;
+        int t = 0;
+        for (; t + 4 <= cnt; t += 4) {
+          const uint32_t e0 = __shfl_sync(0xffffffffu, my_e, t);
+          const uint32_t e1 = __shfl_sync(0xffffffffu, my_e, t + 1);
+          const uint32_t e2 = __shfl_sync(0xffffffffu, my_e, t + 2);
+          const uint32_t e3 = __shfl_sync(0xffffffffu, my_e, t + 3);
+          s0 += flip_if(my_row[(e0 >> 1) ^ lane], e0 & 1u);
+          s1 += flip_if(my_row[(e1 >> 1) ^ lane], e1 & 1u);
+          s2 += flip_if(my_row[(e2 >> 1) ^ lane], e2 & 1u);
+          s3 += flip_if(my_row[(e3 >> 1) ^ lane], e3 & 1u);
+        }
+        for (; t < cnt; ++t) {
+          const uint32_t e0 = __shfl_sync(0xffffffffu, my_e, t);
+          s0 += flip_if(my_row[(e0 >> 1) ^ lane], e0 & 1u);
+        }
+      }
+      acc[j] += (s0 + s1) + (s2 + s3);
+    }
+  }
+
+  // Epilogue: stage the 32 x CB tile through shared memory, then coalesced row stores.
+  __syncthreads();
+  constexpr int YS = CB + 1;
+  T* Ys = As;
+#pragma unroll
+  for (int j = 0; j < CPW; ++j) Ys[lane * YS + warp + W * j] = acc[j] * scale;
+  __syncthreads();
+  for (int idx = tid; idx < kRowsPerTile * CB; idx += NT) {
+    const int i = idx / CB, cl = idx % CB;
+    const int64_t row = row0 + i, c = cb0 + cl;
+    if (row < n && c < k) Y[row * ldy + c] = Ys[i * YS + cl];
+  }
+}
+
+constexpr int kWarps = 16;
+
+template <typename T>
+constexpr int chunk_rows_for() {
+  return sizeof(T) == 4 ? 512 : 256;
+}
+
+template <typename T, int CPW, bool VEC>
+int launch_t(const T* A, int64_t n, int64_t d, int64_t lda, const int32_t* ptr, const uint16_t* ent,
+             int64_t k, double scale, T* Y, int64_t ldy, cudaStream_t s) {
+  constexpr int R = chunk_rows_for<T>();
+  constexpr int CB = kWarps * CPW;
+  const int nchunks = (int)((d + R - 1) / R);
+  const size_t tile_bytes = (size_t)kRowsPerTile * R * sizeof(T);
+  const size_t ys_bytes = (size_t)kRowsPerTile * (CB + 1) * sizeof(T);
+  const size_t smem = tile_bytes > ys_bytes ? tile_bytes : ys_bytes;
+  auto kern = sparse_right_kernel<T, kWarps, CPW, R, VEC>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid((unsigned)((n + kRowsPerTile - 1) / kRowsPerTile), (unsigned)((k + CB - 1) / CB));
+  kern<<<grid, kWarps * 32, smem, s>>>(A, n, d, lda, ptr, ent, k, nchunks, (T)scale, Y, ldy);
+  return check_launch("sk_sparse_right");
+}
+
+template <typename T>
+int dispatch(const void* A_, int64_t n, int64_t d, int64_t lda, const int32_t* ptr, const uint16_t* ent,
+             int64_t k, double scale, void* Y_, int64_t ldy, cudaStream_t s) {
+  const T* A = static_cast<const T*>(A_);
+  T* Y = static_cast<T*>(Y_);
+  constexpr int NV = 16 / sizeof(T);
+  const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % NV == 0) && (d % NV == 0);
+  const int64_t need = (k + kWarps - 1) / kWarps;
+  if (need <= 4) return vec ? launch_t<T, 4, true>(A, n, d, lda, ptr, ent, k, scale, Y, ldy, s)
+                            : launch_t<T, 4, false>(A, n, d, lda, ptr, ent, k, scale, Y, ldy, s);
+  if (need <= 8) return vec ? launch_t<T, 8, true>(A, n, d, lda, ptr, ent, k, scale, Y, ldy, s)
+                            : launch_t<T, 8, false>(A, n, d, lda, ptr, ent, k, scale, Y, ldy, s);
+  return vec ? launch_t<T, 16, true>(A, n, d, lda, ptr, ent, k, scale, Y, ldy, s)
+             : launch_t<T, 16, false>(A, n, d, lda, ptr, ent, k, scale, Y, ldy, s);
+}
+
+}  // namespace
+}  // namespace skb
+
+extern "C" int sk_sparse_right_chunk_rows(int dtype, int64_t d, int64_t k) {
+  (void)d;
+  (void)k;
+  if (dtype == SK_F32) return skb::chunk_rows_for<float>();
+  if (dtype == SK_F64) return skb::chunk_rows_for<double>();
+  return skb::fail(SK_EINVAL, "sk_sparse_right_chunk_rows: bad dtype");
+}
+
+extern "C" int sk_sparse_right(int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
+                               const int32_t* ptr, const uint16_t* ent, int32_t chunk_rows, int64_t k,
+                               double scale, void* Y, int64_t ldy, void* stream) {
+  using namespace skb;
+  if (n < 0 || d < 1 || k < 1 || lda < d || ldy < k) return fail(SK_EINVAL, "sk_sparse_right: bad shape/leading dimension");
+  if (n > 0 && (!A || !Y || !ptr)) return fail(SK_EINVAL, "sk_sparse_right: null pointer");
+  if (dtype != SK_F32 && dtype != SK_F64) return fail(SK_EINVAL, "sk_sparse_right: bad dtype");
+  if (chunk_rows != sk_sparse_right_chunk_rows(dtype, d, k))
+    return fail(SK_EINVAL, "sk_sparse_right: chunk_rows does not match sk_sparse_right_chunk_rows");
+  if (n == 0) return SK_OK;
+  cudaStream_t s = as_stream(stream);
+  return dtype == SK_F32 ? dispatch<float>(A, n, d, lda, ptr, ent, k, scale, Y, ldy, s)
+                         : dispatch<double>(A, n, d, lda, ptr, ent, k, scale, Y, ldy, s);
+}

@@ -1,0 +1,289 @@
+"""Sparse sign test matrices on the B200: SparseStack, SparseUniform, SparseIID, SparseCol.
+
+Constructors and random draws restate the reference src/sketch/sparse.py (same RNG stream
+path, same draw order, so the index/sign arrays are bit-identical for a seed).  Storage is a
+COO triplet (rows, cols, neg) plus one magnitude instead of a SciPy CSR; `matrix` still builds
+the reference CSR on demand for code that reads it.  Real operators apply through the native
+bcsc kernels: K1 (`sk_sparse_right`, replaces sparse.py:63-66) and K2 (`sk_sparse_adjoint`,
+replaces sparse.py:68-78).  Complex-field operators use the dense device GEMM.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .. import _lib
+from .encode import bcsc_encode
+from .testmatrix import TestMatrix, entry_sample
+
+__all__ = ["SparseStackTM", "SparseUniformTM", "SparseIIDTM", "SparseColTM", "sample_without_replacement"]
+
+
+def sample_without_replacement(rng, n_sets: int, take: int, universe: int) -> np.ndarray:
+    """n_sets uniform `take`-subsets of range(universe) — same draws as reference sparse.py:18-43.
+
+    iid draws with per-set rejection on duplicates; per-set permutations when the acceptance
+    probability is below 5%.
+    """
+    if take > universe:
+        raise ValueError(f"cannot take {take} distinct items from {universe}")
+    if take == universe:
+        return np.tile(np.arange(universe), (n_sets, 1)) if n_sets else np.empty((0, take), dtype=int)
+    if np.prod(1.0 - np.arange(take) / universe) < 0.05:
+        out = np.empty((n_sets, take), dtype=np.int64)
+        for i in range(n_sets):
+            out[i] = rng.permutation(universe)[:take]
+        return out
+    out = rng.integers(0, universe, size=(n_sets, take))
+    while True:
+        srt = np.sort(out, axis=1)
+        redo = np.flatnonzero((srt[:, 1:] == srt[:, :-1]).any(axis=1))
+        if redo.size == 0:
+            return out
+        out[redo] = rng.integers(0, universe, size=(redo.size, take))
+
+
+class _SignSparseTM(TestMatrix):
+    """Sparse Omega stored as COO (rows, cols, complex-or-real values); native when real +-mag."""
+
+    def __init__(self, d, k, field, seed):
+        super().__init__(d, k, field, seed)
+        self._coo = None  # (rows int64, cols int64, values float64/complex128)
+        self._matrix_cache = None
+
+    def _draw(self):
+        """Return (rows, cols, values) in the reference CSR order."""
+        raise NotImplementedError
+
+    def _triplets(self):
+        if self._coo is None:
+            self._coo = self._draw()
+        return self._coo
+
+    @property
+    def matrix(self):
+        """The reference's scipy CSR view (src/sketch/sparse.py:51-55)."""
+        if self._matrix_cache is None:
+            import scipy.sparse as sp
+
+            rows, cols, vals = self._triplets()
+            m = sp.csr_array(sp.coo_array((vals.astype(self.dtype), (rows, cols)), shape=(self.d, self.k)))
+            m.sort_indices()
+            self._matrix_cache = m
+        return self._matrix_cache
+
+    def materialize(self) -> np.ndarray:
+        rows, cols, vals = self._triplets()
+        out = np.zeros((self.d, self.k), dtype=self.dtype)
+        np.add.at(out, (rows, cols), vals)
+        return out
+
+    # -- native path ------------------------------------------------------------------------------
+    def _sign_form(self):
+        """(rows, cols, neg, magnitude) if every value is +-magnitude (real field), else None."""
+        if self.field != "real":
+            return None
+        rows, cols, vals = self._triplets()
+        if vals.size == 0:
+            return rows, cols, np.zeros(0, bool), 1.0
+        mag = float(np.abs(vals[0]))
+        if mag == 0.0 or not np.all(np.abs(vals) == mag):
+            return None
+        return rows, cols, vals < 0, mag
+
+    def _bcsc_on(self, device, kind: str, dtype_code: int):
+        key = ("bcsc", kind, device, dtype_code)
+        if key not in self._device_cache:
+            import torch
+
+            lib = _lib.load()
+            r = (lib.sk_sparse_right_chunk_rows if kind == "right" else lib.sk_sparse_adjoint_chunk_rows)(
+                dtype_code, self.d, self.k)
+            _lib.check(min(r, 0), "chunk_rows")
+            rows, cols, neg, mag = self._sign_form()
+            ptr, ent = bcsc_encode(rows, cols, neg, self.d, self.k, r)
+            self._device_cache[key] = (
+                torch.from_numpy(ptr).to(device),
+                torch.from_numpy(ent.view(np.int16)).to(device),
+                int(r),
+                mag,
+            )
+        return self._device_cache[key]
+
+    def _right_device(self, a):
+        import torch
+
+        if self._sign_form() is None or a.dtype not in (torch.float32, torch.float64):
+            return super()._right_device(a)
+        code = _lib.SK_F32 if a.dtype == torch.float32 else _lib.SK_F64
+        ptr, ent, r, mag = self._bcsc_on(a.device, "right", code)
+        n = a.shape[0]
+        y = torch.empty((n, self.k), dtype=a.dtype, device=a.device)
+        if n == 0:
+            return y
+        lib = _lib.load()
+        with torch.cuda.device(a.device):
+            st = lib.sk_sparse_right(code, a.data_ptr(), n, self.d, a.stride(0), ptr.data_ptr(), ent.data_ptr(), r,
+                                     self.k, mag, y.data_ptr(), y.stride(0), torch.cuda.current_stream().cuda_stream)
+        _lib.check(st, "sk_sparse_right")
+        return y
+
+    def _adjoint_device(self, b):
+        import torch
+
+        if self._sign_form() is None or b.dtype not in (torch.float32, torch.float64):
+            return super()._adjoint_device(b)
+        code = _lib.SK_F32 if b.dtype == torch.float32 else _lib.SK_F64
+        ptr, ent, r, mag = self._bcsc_on(b.device, "adjoint", code)
+        m = b.shape[1]
+        out = torch.empty((self.k, m), dtype=b.dtype, device=b.device)
+        if m == 0:
+            return out
+        lib = _lib.load()
+        ws_bytes = lib.sk_sparse_adjoint_workspace_bytes(code, self.d, m, self.k)
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=b.device)
+        with torch.cuda.device(b.device):
+            st = lib.sk_sparse_adjoint(code, b.data_ptr(), self.d, m, b.stride(0), ptr.data_ptr(), ent.data_ptr(), r,
+                                       self.k, mag, out.data_ptr(), out.stride(0), 0, ws.data_ptr(), ws_bytes,
+                                       torch.cuda.current_stream().cuda_stream)
+        _lib.check(st, "sk_sparse_adjoint")
+        return out
+
+
+class SparseStackTM(_SignSparseTM):
+    """zeta CountSketch blocks of width b side by side; one +-1/sqrt(zeta) per block per row.
+
+    Reference: src/sketch/sparse.py:81-174 (same signature and defaults).
+    """
+
+    def __init__(self, d: int, zeta: int = 4, block_size: int | None = None, *, k: int | None = None,
+                 distribution: str | None = None, field: str = "real", seed: int = 0):
+        if zeta < 1:
+            raise ValueError("row sparsity zeta must be >= 1")
+        if block_size is None:
+            if k is None:
+                raise ValueError("give either block_size or k")
+            if k % zeta:
+                raise ValueError(f"k={k} must be divisible by zeta={zeta}")
+            block_size = k // zeta
+        if block_size < 1:
+            raise ValueError("block size must be >= 1")
+        super().__init__(d, block_size * zeta, field, seed)
+        self.zeta = int(zeta)
+        self.block_size = int(block_size)
+        self.distribution = distribution or ("steinhaus" if field == "complex" else "real_rademacher")
+        self._assigned = None
+
+    @classmethod
+    def from_assignments(cls, signs, buckets, block_size, field="real"):
+        """Test-fixture constructor from explicit (d, zeta) sign / bucket arrays (sparse.py:118-126)."""
+        signs = np.asarray(signs)
+        buckets = np.asarray(buckets)
+        d, zeta = signs.shape
+        tm = cls(d, zeta, block_size, field=field, seed=0)
+        tm._coo = tm._assemble(signs, buckets)
+        return tm
+
+    def _assemble(self, signs, buckets):
+        d, zeta, b = self.d, self.zeta, self.block_size
+        cols = (np.asarray(buckets) + np.arange(zeta)[None, :] * b).ravel()
+        vals = (np.asarray(signs) / np.sqrt(zeta)).astype(self.dtype).ravel()
+        return np.repeat(np.arange(d), zeta), cols.astype(np.int64), vals
+
+    def _draw(self):
+        rng = self._rng("entries")
+        buckets = rng.integers(0, self.block_size, size=(self.d, self.zeta))
+        signs = entry_sample(self.distribution, rng, (self.d, self.zeta))
+        return self._assemble(signs, buckets)
+
+    def redraw(self, seed: int) -> "SparseStackTM":
+        return SparseStackTM(self.d, self.zeta, self.block_size, distribution=self.distribution, field=self.field,
+                             seed=seed)
+
+
+class SparseUniformTM(_SignSparseTM):
+    """Exactly zeta nonzeros per row at columns sampled without replacement (sparse.py:177-220)."""
+
+    def __init__(self, d: int, k: int, zeta: int = 4, *, field: str = "real", seed: int = 0):
+        if zeta < 1 or zeta > k:
+            raise ValueError(f"need 1 <= zeta <= k, got zeta={zeta}, k={k}")
+        super().__init__(d, k, field, seed)
+        self.zeta = int(zeta)
+
+    def _draw(self):
+        rng = self._rng("entries")
+        cols = sample_without_replacement(rng, self.d, self.zeta, self.k)
+        cols.sort(axis=1)
+        signs = rng.integers(0, 2, size=(self.d, self.zeta)) * 2.0 - 1.0
+        vals = (signs / np.sqrt(self.zeta)).astype(self.dtype).ravel()
+        return np.repeat(np.arange(self.d), self.zeta), cols.ravel().astype(np.int64), vals
+
+    def redraw(self, seed: int) -> "SparseUniformTM":
+        return SparseUniformTM(self.d, self.k, self.zeta, field=self.field, seed=seed)
+
+
+class SparseIIDTM(_SignSparseTM):
+    """iid zeta^{-1/2} * sign * Bernoulli(zeta/k) entries by geometric skipping (sparse.py:223-266)."""
+
+    def __init__(self, d: int, k: int, zeta: float = 4.0, *, field: str = "real", seed: int = 0):
+        if not (0.0 < zeta <= k):
+            raise ValueError(f"expected row sparsity in (0, k], got {zeta}")
+        super().__init__(d, k, field, seed)
+        self.zeta = float(zeta)
+
+    @staticmethod
+    def _bernoulli_positions(rng, p: float, total: int) -> np.ndarray:
+        if p >= 1.0:
+            return np.arange(total)
+        found = []
+        pos = -1
+        batch = int(total * p * 1.2) + 16
+        while True:
+            steps = np.cumsum(rng.geometric(p, size=batch)) + pos
+            inside = steps[steps < total]
+            found.append(inside)
+            if inside.size < steps.size:
+                break
+            pos = int(steps[-1])
+        return np.concatenate(found)
+
+    def _draw(self):
+        rng = self._rng("entries")
+        flat = self._bernoulli_positions(rng, self.zeta / self.k, self.d * self.k)
+        signs = rng.integers(0, 2, size=flat.size) * 2.0 - 1.0
+        vals = (signs / np.sqrt(self.zeta)).astype(self.dtype)
+        return (flat // self.k).astype(np.int64), (flat % self.k).astype(np.int64), vals
+
+    def redraw(self, seed: int) -> "SparseIIDTM":
+        return SparseIIDTM(self.d, self.k, self.zeta, field=self.field, seed=seed)
+
+
+class SparseColTM(_SignSparseTM):
+    """Column sampler: xi distinct rows per column, value +-sqrt(d/xi)/sqrt(k) (sparse.py:298-339)."""
+
+    def __init__(self, d: int, k: int, xi: int = 8, *, field: str = "real", seed: int = 0):
+        if xi < 1 or xi > d:
+            raise ValueError(f"need 1 <= xi <= d, got xi={xi}, d={d}")
+        super().__init__(d, k, field, seed)
+        self.xi = int(xi)
+        self._colwise = None
+
+    def column_draws(self):
+        """(rows (k, xi), neg (k, xi), magnitude) in draw order — the SRTT sampler encoding."""
+        if self._colwise is None:
+            rng = self._rng("entries")
+            rows = sample_without_replacement(rng, self.k, self.xi, self.d)
+            signs = rng.integers(0, 2, size=(self.k, self.xi)) * 2.0 - 1.0
+            self._colwise = (rows.astype(np.int64), signs < 0, float(np.sqrt(self.d / self.xi) / np.sqrt(self.k)))
+        return self._colwise
+
+    def _draw(self):
+        rows, neg, mag = self.column_draws()
+        vals = np.where(neg, -1.0, 1.0) * mag
+        cols = np.repeat(np.arange(self.k), self.xi)
+        r = rows.ravel()
+        order = np.lexsort((cols, r))
+        return r[order], cols[order].astype(np.int64), vals.ravel()[order].astype(self.dtype)
+
+    def redraw(self, seed: int) -> "SparseColTM":
+        return SparseColTM(self.d, self.k, self.xi, field=self.field, seed=seed)

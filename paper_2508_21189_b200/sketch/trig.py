@@ -1,0 +1,196 @@
+"""Trigonometric transforms and the sparse randomized trigonometric transform (SRTT) on the B200.
+
+SparseRttTM restates src/sketch/rtt.py:75-186: Omega = D F S with a random diagonal D drawn
+from stream (SparseRttTM, "diagonal"), a unitary transform F (WHT / DCT / DFT) and a SparseColTM
+sampler S with the same seed.  The real WHT right-apply — BASELINE config 2 — runs as one fused
+kernel (K3, `sk_srtt_right`): sign flip, in-register/shared-memory Walsh-Hadamard butterflies and
+the sampled gather in a single pass over A.  Other transforms / fields use the dense device GEMM.
+
+`wht` on device arrays reuses the same kernel with the identity sampler (k = d, xi = 1).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import scipy.fft
+
+from .. import _lib
+from .._device import from_result, to_operand
+from .encode import srtt_sampler_encode
+from .sparse_rows import SparseColTM
+from .testmatrix import TestMatrix, entry_sample
+
+__all__ = ["wht", "dct2_ortho", "dft_unitary", "SparseRttTM", "TRANSFORMS"]
+
+
+def _require_pow2(d: int) -> int:
+    m = d.bit_length() - 1
+    if d <= 0 or (1 << m) != d:
+        raise ValueError(f"WHT requires a power-of-two length, got {d}")
+    return m
+
+
+def _wht_host(x, axis: int = 0) -> np.ndarray:
+    """Host WHT (1/sqrt(d) normalised) used only by `materialize` for small diagnostic matrices."""
+    x = np.asarray(x, dtype=np.result_type(x, np.float64))
+    d = x.shape[axis]
+    _require_pow2(d)
+    y = np.moveaxis(x, axis, 0).reshape(d, -1).copy()
+    h = 1
+    while h < d:
+        v = y.reshape(d // (2 * h), 2, h, -1)
+        y = np.concatenate([v[:, :1] + v[:, 1:], v[:, :1] - v[:, 1:]], axis=1).reshape(d, -1)
+        h *= 2
+    y = (y / np.sqrt(d)).reshape(np.moveaxis(x, axis, 0).shape)
+    return np.moveaxis(y, 0, axis)
+
+
+def _identity_sampler(d: int):
+    return srtt_sampler_encode(np.arange(d)[:, None], np.zeros((d, 1), bool))
+
+
+def wht(x, axis: int = 0):
+    """Walsh-Hadamard transform with 1/sqrt(d) normalisation (self-inverse), computed on the GPU.
+
+    Same contract as reference src/sketch/rtt.py:28-44 (rejects non-power-of-two lengths).
+    Real NumPy input returns float64 NumPy; torch input returns torch.
+    """
+    import torch
+
+    shape = np.shape(x) if not isinstance(x, torch.Tensor) else tuple(x.shape)
+    if len(shape) == 0:
+        raise ValueError("wht needs at least a 1-d array")
+    d = shape[axis]
+    _require_pow2(int(d))
+    if isinstance(x, np.ndarray) and np.iscomplexobj(x):
+        return _wht_host(x.real, axis) + 1j * _wht_host(x.imag, axis)
+    if isinstance(x, torch.Tensor) and x.is_complex():
+        return torch.complex(wht(x.real, axis), wht(x.imag, axis))
+    if isinstance(x, torch.Tensor):
+        t = torch.movedim(x, axis, -1)
+        lead = t.shape[:-1]
+        op = to_operand(t.reshape(-1, d), allow_vector=False, complex_ok=False)
+        y = _srtt_native(op.tensor, np.ones(d), _identity_sampler(d), 1, d, 1.0 / np.sqrt(d), pm1=True)
+        return torch.movedim(from_result(y, op).reshape(*lead, d), -1, axis)
+    t = np.moveaxis(np.asarray(x, dtype=np.float64), axis, -1)
+    lead = t.shape[:-1]
+    op = to_operand(np.ascontiguousarray(t.reshape(-1, d)), allow_vector=False, complex_ok=False)
+    y = _srtt_native(op.tensor, np.ones(d), _identity_sampler(d), 1, d, 1.0 / np.sqrt(d), pm1=True)
+    return np.moveaxis(from_result(y, op).reshape(*lead, d), -1, axis)
+
+
+def dct2_ortho(x, axis: int = 0) -> np.ndarray:
+    """Orthonormal DCT-II (reference rtt.py:47-49); host SciPy, used for materialize/diagnostics."""
+    return scipy.fft.dct(np.asarray(x), type=2, norm="ortho", axis=axis)
+
+
+def dft_unitary(x, axis: int = 0) -> np.ndarray:
+    """Unitary DFT (reference rtt.py:52-55); host NumPy, used for materialize/diagnostics."""
+    x = np.asarray(x)
+    return np.fft.fft(x, axis=axis) / np.sqrt(x.shape[axis])
+
+
+def _dct2_adjoint(x, axis: int = 0) -> np.ndarray:
+    return scipy.fft.dct(np.asarray(x), type=3, norm="ortho", axis=axis)
+
+
+def _dft_adjoint(x, axis: int = 0) -> np.ndarray:
+    x = np.asarray(x)
+    return np.fft.ifft(x, axis=axis) * np.sqrt(x.shape[axis])
+
+
+TRANSFORMS = {
+    "wht": (_wht_host, _wht_host, False),
+    "dct": (dct2_ortho, _dct2_adjoint, False),
+    "dft": (dft_unitary, _dft_adjoint, True),
+}
+
+
+def _srtt_native(a, dvals, samp, xi: int, k: int, scale: float, pm1: bool, transform: int = _lib.SK_WHT):
+    """Launch sk_srtt_right on a row-major CUDA tensor `a` (n x d); dvals/samp: host or device arrays."""
+    import torch
+
+    code = _lib.SK_F32 if a.dtype == torch.float32 else _lib.SK_F64
+    n, d = a.shape
+    dv = dvals if isinstance(dvals, torch.Tensor) else torch.as_tensor(np.asarray(dvals, dtype=np.float64))
+    dv = dv.to(device=a.device, dtype=a.dtype)
+    sp = samp if isinstance(samp, torch.Tensor) else torch.as_tensor(np.asarray(samp, dtype=np.int32))
+    sp = sp.to(a.device)
+    y = torch.empty((n, k), dtype=a.dtype, device=a.device)
+    if n == 0:
+        return y
+    lib = _lib.load()
+    flags = transform | (_lib.SK_DIAG_PM1 if pm1 else 0)
+    with torch.cuda.device(a.device):
+        st = lib.sk_srtt_right(code, a.data_ptr(), n, d, a.stride(0), dv.data_ptr(), flags, sp.data_ptr(), xi, k,
+                               float(scale), y.data_ptr(), y.stride(0), torch.cuda.current_stream().cuda_stream)
+    _lib.check(st, "sk_srtt_right")
+    return y
+
+
+class SparseRttTM(TestMatrix):
+    """Sparse randomized trigonometric transform Omega = D F S (reference rtt.py:75-186)."""
+
+    def __init__(self, d: int, k: int, xi: int | None = None, transform: str | None = None, *,
+                 diagonal: str | None = None, field: str = "real", seed: int = 0):
+        super().__init__(d, k, field, seed)
+        if xi is None:
+            xi = int(np.ceil(1.5 * np.log(max(2, k))))
+        if transform is None:
+            transform = "dft" if field == "complex" else "dct"
+        if transform not in TRANSFORMS:
+            raise ValueError(f"unknown transform {transform!r}")
+        if transform == "wht":
+            _require_pow2(d)
+        if transform == "dft" and field != "complex":
+            raise ValueError("the DFT transform requires the complex field")
+        if diagonal is None:
+            diagonal = "real_rademacher"
+        if diagonal not in ("real_rademacher", "uniform_symmetric", "steinhaus"):
+            raise ValueError(f"unsupported diagonal distribution {diagonal!r}")
+        if diagonal == "steinhaus" and field != "complex":
+            raise ValueError("a Steinhaus diagonal requires the complex field")
+        self.xi = int(xi)
+        if not 1 <= self.xi <= d:
+            raise ValueError(f"need 1 <= xi <= d, got xi={self.xi}")
+        self.transform = transform
+        self.diagonal = diagonal
+        self._dvals = None
+        self._sampler = None
+
+    def _parts(self):
+        """(D values, SparseColTM sampler) — reference rtt.py:114-121."""
+        if self._dvals is None:
+            self._dvals = entry_sample(self.diagonal, self._rng("diagonal"), self.d).astype(self.dtype)
+            self._sampler = SparseColTM(self.d, self.k, self.xi, field=self.field, seed=self.seed)
+        return self._dvals, self._sampler
+
+    def materialize(self) -> np.ndarray:
+        dvals, sampler = self._parts()
+        fs = TRANSFORMS[self.transform][0](sampler.materialize(), axis=0)
+        return (dvals[:, None] * fs).astype(self.dtype)
+
+    def _native_ok(self, dtype) -> bool:
+        import torch
+
+        return self.field == "real" and self.transform == "wht" and dtype in (torch.float32, torch.float64)
+
+    def _right_device(self, a):
+        if not self._native_ok(a.dtype):
+            return super()._right_device(a)
+        import torch
+
+        key = ("srtt", a.device, a.dtype)
+        if key not in self._device_cache:
+            dvals, sampler = self._parts()
+            rows, neg, mag = sampler.column_draws()
+            samp = torch.from_numpy(srtt_sampler_encode(rows, neg)).to(a.device)
+            dv = torch.from_numpy(np.ascontiguousarray(dvals)).to(device=a.device, dtype=a.dtype)
+            pm1 = bool(np.all(np.abs(dvals) == 1.0))
+            self._device_cache[key] = (dv, samp, (1.0 / np.sqrt(self.d)) * mag, pm1)
+        dv, samp, scale, pm1 = self._device_cache[key]
+        return _srtt_native(a, dv, samp, self.xi, self.k, scale, pm1)
+
+    def redraw(self, seed: int) -> "SparseRttTM":
+        return SparseRttTM(self.d, self.k, self.xi, self.transform, diagonal=self.diagonal, field=self.field,
+                           seed=seed)

@@ -1,0 +1,150 @@
+"""GPU parity: the CUDA kernels (through the C ABI) against the CPU oracle and golden vectors.
+
+Tolerances (BASELINE north_star): relative Frobenius error <= 1e-12 for float64 inputs and
+<= 1e-5 for float32 inputs, always measured in float64 against the float64 oracle.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as orc
+from _cases import CASES, oracle_right, product, rel_err
+from paper_2508_21189_b200 import sketch as skb
+
+pytestmark = pytest.mark.gpu
+
+TOL = {np.float64: 1e-12, np.float32: 1e-5}
+
+
+def _t(a, dev, dt):
+    import torch
+
+    return torch.as_tensor(np.asarray(a, dtype=dt)).to(dev)
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_golden_right_numpy(name, golden, cuda):
+    """Drop-in call with NumPy in, NumPy float64 out, against the reference's own outputs."""
+    tm = product(name)
+    a = golden[f"{name}__A"]
+    y = tm.apply_right(a)
+    assert isinstance(y, np.ndarray) and y.dtype == np.float64
+    assert rel_err(y, golden[f"{name}__right"]) <= 1e-12
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_golden_adjoint_numpy(name, golden, cuda):
+    tm = product(name)
+    b = golden[f"{name}__B"]
+    assert rel_err(tm.apply_adjoint(b), golden[f"{name}__adjoint"]) <= 1e-12
+    v = tm.apply_adjoint(b[:, 0])
+    assert v.shape == (tm.k,)
+    assert rel_err(v, golden[f"{name}__adjoint_vec"]) <= 1e-12
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("d,k,zeta,n", [(4096, 256, 4, 100), (16384, 200, 8, 64), (1000, 300, 5, 33), (700, 64, 1, 5),
+                                        (513, 17, 3, 1), (64, 600, 4, 40)])
+def test_sparse_right_vs_oracle(d, k, zeta, n, dt, cuda):
+    rng = np.random.default_rng(d + k)
+    a = rng.standard_normal((n, d)).astype(dt)
+    tm = skb.SparseUniformTM(d, k, zeta, seed=3)
+    y = tm.apply_right(_t(a, cuda, dt)).cpu().numpy()
+    ref = orc.csr_right(orc.sparse_uniform_csr(d, k, zeta, 3), a)
+    assert rel_err(y, ref) <= TOL[dt]
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("d,k,zeta,m", [(4096, 2048, 8, 40), (20000, 256, 8, 512), (1000, 300, 5, 1), (777, 64, 3, 33)])
+def test_sparse_adjoint_vs_oracle(d, k, zeta, m, dt, cuda):
+    rng = np.random.default_rng(d + m)
+    b = rng.standard_normal((d, m)).astype(dt)
+    tm = skb.SparseUniformTM(d, k, zeta, seed=5)
+    y = tm.apply_adjoint(_t(b, cuda, dt)).cpu().numpy()
+    ref = orc.csr_adjoint(orc.sparse_uniform_csr(d, k, zeta, 5), b)
+    assert rel_err(y, ref) <= TOL[dt]
+
+
+def test_sparse_misaligned_and_strided(cuda):
+    import torch
+
+    d, k = 1000, 48
+    tm = skb.SparseStackTM(d, 4, 12, seed=9)
+    big = torch.randn(37, d + 3, dtype=torch.float32, device=cuda)
+    a = big[:, 1:d + 1]  # row stride d+3, base not 16-byte aligned -> scalar loader
+    y = tm.apply_right(a).cpu().numpy()
+    ref = orc.csr_right(orc.sparse_stack_csr(d, 4, 12, 9), a.cpu().numpy())
+    assert rel_err(y, ref) <= 1e-5
+
+
+def test_zero_and_empty_inputs(cuda):
+    tm = skb.SparseUniformTM(300, 40, 4, seed=1)
+    assert np.all(tm.apply_right(np.zeros((5, 300))) == 0)
+    assert tm.apply_right(np.zeros((0, 300))).shape == (0, 40)
+    assert np.all(tm.apply_adjoint(np.zeros((300, 3))) == 0)
+    assert np.array_equal(tm.apply_right(np.eye(300)), tm.materialize())
+
+
+def test_identity_input_equals_materialize(cuda):
+    for tm in (skb.SparseStackTM(64, 2, 8, seed=1), skb.SparseRttTM(256, 32, 2, "wht", seed=2),
+               skb.SparseColTM(50, 9, 3, seed=4)):
+        assert rel_err(tm.apply_right(np.eye(tm.d)), tm.materialize()) <= 1e-13
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("d,k,xi,n", [(8192, 512, 1, 70), (1024, 100, 3, 9), (2048, 64, 2, 5), (4096, 256, 1, 3),
+                                      (16384, 128, 2, 4), (256, 64, 1, 7), (32, 12, 4, 2)])
+def test_srtt_wht_vs_oracle(d, k, xi, n, dt, cuda):
+    rng = np.random.default_rng(d * 3 + xi)
+    a = (rng.standard_normal((n, d)) / np.arange(1, d + 1)).astype(dt)
+    tm = skb.SparseRttTM(d, k, xi, "wht", seed=11)
+    y = tm.apply_right(_t(a, cuda, dt)).cpu().numpy()
+    dv, samp = orc.srtt_parts(d, k, xi, 11)
+    ref = orc.srtt_right(dv, samp, a, "wht")
+    assert rel_err(y, ref) <= TOL[dt]
+
+
+def test_srtt_uniform_diagonal(cuda):
+    d, k, xi = 8192, 64, 2
+    rng = np.random.default_rng(1)
+    a = rng.standard_normal((6, d))
+    tm = skb.SparseRttTM(d, k, xi, "wht", diagonal="uniform_symmetric", seed=4)
+    dv, samp = orc.srtt_parts(d, k, xi, 4, "uniform_symmetric")
+    assert rel_err(tm.apply_right(a), orc.srtt_right(dv, samp, a, "wht")) <= 1e-12
+
+
+def test_wht_function(cuda):
+    x = np.random.default_rng(0).standard_normal((16, 3))
+    y = skb.wht(x)
+    assert rel_err(np.asarray(y), orc.wht_rows(x.T).T) <= 1e-13
+    assert rel_err(np.asarray(skb.wht(np.asarray(y))), x) <= 1e-13
+
+
+def test_linearity_at_config_sizes(cuda):
+    """Size-independent property at full config-1 size: Y(aA + bB) = aY(A) + bY(B)."""
+    import torch
+
+    tm = skb.SparseUniformTM(4096, 256, 4, seed=0)
+    g = torch.Generator(device=cuda).manual_seed(0)
+    a = torch.randn(16384, 4096, dtype=torch.float64, device=cuda, generator=g)
+    b = torch.randn(16384, 4096, dtype=torch.float64, device=cuda, generator=g)
+    lhs = tm.apply_right(2.0 * a - 3.0 * b)
+    rhs = 2.0 * tm.apply_right(a) - 3.0 * tm.apply_right(b)
+    assert float((lhs - rhs).norm() / rhs.norm()) <= 1e-13
+    # spot-check 256 rows against the oracle
+    rows = torch.arange(0, 16384, 64, device=cuda)
+    ref = orc.csr_right(orc.sparse_uniform_csr(4096, 256, 4, 0), a[rows].cpu().numpy())
+    assert rel_err(tm.apply_right(a)[rows].cpu().numpy(), ref) <= 1e-12
+
+
+def test_config2_rows_vs_oracle(cuda):
+    """BASELINE config 2 operator on a 256-row slab of the config's input distribution."""
+    import torch
+
+    tm = skb.SparseRttTM(8192, 512, 1, "wht", seed=0)
+    g = torch.Generator(device=cuda).manual_seed(1)
+    a = torch.randn(256, 8192, dtype=torch.float32, device=cuda, generator=g)
+    a /= torch.arange(1, 8193, device=cuda, dtype=torch.float32)
+    y = tm.apply_right(a).cpu().numpy()
+    dv, samp = orc.srtt_parts(8192, 512, 1, 0)
+    assert rel_err(y, orc.srtt_right(dv, samp, a.cpu().numpy(), "wht")) <= 1e-5

@@ -1,0 +1,163 @@
+"""CPU tests of the product's host logic: bit-exact test matrices, encodings, RNG, no-CPU-fallback."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle as orc
+from _cases import CASES, product, rel_err
+from paper_2508_21189_b200 import RngStream, derive_seed
+from paper_2508_21189_b200 import sketch as skb
+from paper_2508_21189_b200.rng import entropy_of
+from paper_2508_21189_b200.sketch.encode import bcsc_decode, bcsc_encode, sign_bits, srtt_sampler_encode
+
+
+def sha1(a):
+    return hashlib.sha1(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("name", [n for n, (f, _) in CASES.items() if f in ("su", "ss", "sc")])
+def test_product_csr_bit_exact(name, golden):
+    m = product(name).matrix
+    assert np.array_equal(m.indptr.astype(np.int64), golden[f"{name}__indptr"])
+    assert np.array_equal(m.indices.astype(np.int64), golden[f"{name}__indices"])
+    assert np.array_equal(m.data, golden[f"{name}__data"])
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_product_materialize_matches_reference(name, golden):
+    key = f"{name}__dense"
+    if key not in golden:
+        pytest.skip("no dense fixture")
+    assert rel_err(product(name).materialize(), golden[key]) <= 1e-13
+
+
+@pytest.mark.parametrize("name", [n for n, (f, _) in CASES.items() if f == "rtt"])
+def test_product_srtt_parts_bit_exact(name, golden):
+    dv, samp = product(name)._parts()
+    assert np.array_equal(dv, golden[f"{name}__dvals"])
+    assert np.array_equal(samp.matrix.indices.astype(np.int64), golden[f"{name}__s_indices"])
+    assert np.array_equal(samp.matrix.data, golden[f"{name}__s_data"])
+
+
+@pytest.mark.parametrize("name", [n for n, (f, _) in CASES.items() if f == "kr"])
+def test_product_kr_factors_bit_exact(name, golden):
+    assert np.array_equal(product(name).factors, golden[f"{name}__factors"])
+
+
+def test_config_test_matrices_bit_exact(golden_hashes):
+    h = golden_hashes["cfg1_sparseuniform_4096_256_4_s0"]
+    m = skb.SparseUniformTM(4096, 256, 4, seed=0).matrix
+    assert (sha1(m.indices.astype(np.int64)), sha1(m.data), sha1(m.indptr.astype(np.int64))) == (
+        h["indices"], h["data"], h["indptr"])
+    h = golden_hashes["cfg2_srtt_wht_8192_512_1_s0"]
+    tm = skb.SparseRttTM(8192, 512, 1, "wht", seed=0)
+    dv, samp = tm._parts()
+    assert sha1(dv) == h["dvals"]
+    assert sha1(samp.matrix.indices.astype(np.int64)) == h["sampler"]["indices"]
+    assert sha1(samp.matrix.data) == h["sampler"]["data"]
+    h = golden_hashes["cfg3_sparseuniform_16384_200_8_s0"]
+    m = skb.SparseUniformTM(16384, 200, 8, seed=0).matrix
+    assert sha1(m.indices.astype(np.int64)) == h["indices"]
+    assert sha1(m.data) == h["data"]
+    h = golden_hashes["cfg5_khatrirao_256_2_512_rad_s0"]
+    assert sha1(skb.KhatriRaoTM(256, 2, 512, "real_rademacher", seed=0).factors) == h["factors"]
+
+
+@pytest.mark.slow
+def test_config4_test_matrix_bit_exact(golden_hashes):
+    h = golden_hashes["cfg4_sparseuniform_4194304_2048_8_s0"]
+    rows, cols, vals = skb.SparseUniformTM(4194304, 2048, 8, seed=0)._triplets()
+    assert sha1(cols) == h["indices"]
+    assert sha1(vals) == h["data"]
+
+
+def test_countsketch_fixture_structure():
+    tm = skb.SparseStackTM.from_assignments([[1.0], [-1.0], [1.0]], [[0], [1], [0]], 2)
+    assert np.allclose(tm.materialize(), [[1, 0], [0, -1], [1, 0]])
+
+
+def test_stack_structure_forced():
+    # reference pkg/tests/test_sketch.py:39-48
+    tm = skb.SparseStackTM(30, zeta=4, block_size=5, seed=3)
+    m = tm.matrix
+    assert np.all(np.diff(m.indptr) == 4)
+    assert np.all(m.indices.reshape(30, 4) // 5 == np.arange(4))
+    assert np.allclose(np.abs(m.data), 0.5)
+
+
+def test_constructor_errors():
+    with pytest.raises(ValueError, match="divisible"):
+        skb.SparseStackTM(10, zeta=3, k=10)
+    with pytest.raises(ValueError, match="power-of-two"):
+        skb.SparseRttTM(48, 8, 3, "wht")
+    with pytest.raises(ValueError, match="complex"):
+        skb.SparseRttTM(16, 8, 3, "dft", field="real")
+    assert skb.SparseRttTM(256, 64, seed=0).xi == int(np.ceil(1.5 * np.log(64)))
+    assert skb.SparseRttTM(20, 8, 3, seed=0).transform == "dct"
+
+
+def test_rng_stream_contract():
+    a = RngStream(7).substream("x", 3).generator().standard_normal(8)
+    b = RngStream(7).substream("x", 3).generator().standard_normal(8)
+    c = RngStream(7).substream("x", 4).generator().standard_normal(8)
+    assert np.array_equal(a, b) and not np.array_equal(a, c)
+    assert derive_seed(3, "a", 5) == derive_seed(3, "a", 5) != derive_seed(3, "a", 6)
+    # entropy for seed 0, path (SparseUniformTM, entries)
+    ent = entropy_of(0, ("SparseUniformTM", "entries"))
+    assert ent[:2] == [0, 0] and ent[3:5] == [15, 2] and ent[6:] == [7, 2]
+    assert ent[2] == int.from_bytes(b"SparseUniformTM", "little")
+    g1 = RngStream(0, ("SparseUniformTM", "entries")).generator()
+    g2 = orc.stream(0, "SparseUniformTM", "entries")
+    assert np.array_equal(g1.integers(0, 100, 50), g2.integers(0, 100, 50))
+
+
+@pytest.mark.parametrize("d,k,zeta,r", [(40, 12, 3, 32), (1000, 200, 8, 256), (4096, 256, 4, 512), (70, 5, 5, 64)])
+def test_bcsc_roundtrip(d, k, zeta, r):
+    tm = skb.SparseUniformTM(d, k, zeta, seed=d)
+    rows, cols, neg, mag = tm._sign_form()
+    ptr, ent = bcsc_encode(rows, cols, neg, d, k, r)
+    assert ptr[-1] == rows.size and ptr.dtype == np.int32 and ent.dtype == np.uint16
+    r2, c2, n2 = bcsc_decode(ptr, ent, d, k, r)
+    want = sorted(zip(rows.tolist(), cols.tolist(), neg.tolist()))
+    assert sorted(zip(r2.tolist(), c2.tolist(), n2.tolist())) == want
+    # within each (chunk, column) list rows ascend
+    keys = (r2 // r) * k + c2
+    same = keys[1:] == keys[:-1]
+    assert np.all(r2[1:][same] > r2[:-1][same])
+    dense = np.zeros((d, k))
+    np.add.at(dense, (r2, c2), np.where(n2, -mag, mag))
+    assert np.array_equal(dense, tm.materialize())
+
+
+def test_srtt_sampler_and_sign_bits():
+    rows = np.array([[5], [0], [7]])
+    neg = np.array([[True], [False], [True]])
+    e = srtt_sampler_encode(rows, neg).view(np.uint32)
+    assert list(e & 0x7FFFFFFF) == [5, 0, 7] and list(e >> 31) == [1, 0, 1]
+    bits = sign_bits(np.arange(70) % 3 == 0)
+    assert bits.size == 3 and all(((bits[i // 32] >> (i % 32)) & 1) == (i % 3 == 0) for i in range(70))
+
+
+def test_no_cpu_fallback():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present")
+    from paper_2508_21189_b200._device import NoDeviceError
+
+    tm = skb.SparseUniformTM(40, 12, 3, seed=0)
+    with pytest.raises(NoDeviceError):
+        tm.apply_right(np.ones((2, 40)))
+    with pytest.raises(NoDeviceError):
+        tm.apply_adjoint(np.ones(40))
+
+
+def test_shape_errors_precede_device():
+    # reference pkg/tests/test_sketch.py:260-265 (error texts mention the method)
+    tm = skb.GaussianTM(10, 4, seed=0)
+    with pytest.raises(ValueError, match="apply_right"):
+        tm.apply_right(np.ones((3, 9)))
+    with pytest.raises(ValueError, match="apply_adjoint"):
+        tm.apply_adjoint(np.ones((9, 2)))
