@@ -214,6 +214,198 @@ __global__ void __launch_bounds__((1 << (L - 5)), (sizeof(T) == 4 ? (L <= 12 ? 3
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Wide fast path (float32, +-1 diagonal, d = 2^L, 12 <= L <= 14): T = d/128 threads per row and
+// 128 values per thread held as 64 packed float pairs, so 12 of the 13 (L=13) butterfly stages run
+// as Blackwell FADD2/FSUB2 (add.rn.f32x2) on register pairs.
+//   phase 1: registers hold index bits {0,1} u {L-5..L-1}   (32 coalesced float4 loads / thread)
+//   phase 2: registers hold bits {0,1} u {2..6}             (one float4 shared-memory transpose;
+//            each thread then owns 128 consecutive indices, so the write-back needs no barrier)
+//   gather : remaining bits {7..L-6} are folded into the sampled gather: each sampled output is a
+//            +-sum of 2^(L-12) transposed values.
+// Shared address of index j: j ^ (((j >> 7) & 7) << 2) — float4 writes and reads conflict free.
+// ---------------------------------------------------------------------------------------------
+typedef unsigned long long u64;
+
+__device__ __forceinline__ u64 f2add(u64 a, u64 b) {
+  u64 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 f2sub(u64 a, u64 b) {
+  u64 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 pk(float lo, float hi) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk(u64 p, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(p));
+}
+__device__ __forceinline__ int swz4(int j) { return j ^ (((j >> 7) & 7) << 2); }
+
+// One-instruction bulk prefetch of [p, p + bytes) into L2 (TMA unit; bytes % 16 == 0).
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <int L>
+struct WideCfg {
+  static constexpr int T = 1 << (L - 7);
+  static constexpr int MINB = L == 12 ? 8 : (L == 13 ? 4 : 2);
+};
+
+template <int L>
+__global__ void __launch_bounds__(WideCfg<L>::T, WideCfg<L>::MINB)
+    srtt_wht_wide(const float* __restrict__ A, int64_t n, int64_t lda, const float* __restrict__ dvals,
+                  const int32_t* __restrict__ samp, int xi, int k, float scale, float* __restrict__ Y,
+                  int64_t ldy) {
+  constexpr int T = WideCfg<L>::T;
+  constexpr int QS = 4 * T;        // index stride of the 32 float4 groups in phase 1
+  constexpr int M3 = L - 12;       // bits folded into the gather
+  constexpr int PF = 2;            // rows of L2 prefetch distance per CTA
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* buf = reinterpret_cast<float*>(smem_raw);
+  const int t = threadIdx.x;
+
+  // sign bits of D at this thread's 128 phase-1 positions: bit (4q + c) <-> j = 4t + c + QS*q
+  uint32_t dm[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    const float4 dv = *reinterpret_cast<const float4*>(dvals + 4 * t + QS * q);
+    const uint32_t b = (dv.x < 0.f ? 1u : 0u) | (dv.y < 0.f ? 2u : 0u) | (dv.z < 0.f ? 4u : 0u) | (dv.w < 0.f ? 8u : 0u);
+    dm[q >> 3] |= b << (4 * (q & 7));
+  }
+
+  if (t == 0) {
+    for (int j = 0; j < PF; ++j)
+      if (blockIdx.x + (int64_t)j * gridDim.x < n) prefetch_l2_bulk(A + (blockIdx.x + (int64_t)j * gridDim.x) * lda, 4u << L);
+  }
+  u64 p[64];
+  auto load_row = [&](int64_t row) {
+    const float* a = A + row * lda;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      float v[4];
+      ld4(a + 4 * t + QS * q, v);
+      p[2 * q] = pk(v[0], v[1]);
+      p[2 * q + 1] = pk(v[2], v[3]);
+    }
+  };
+  for (int64_t row = blockIdx.x; row < n; row += gridDim.x) {
+    // keep the DRAM stream busy: the CTA's row PF iterations ahead goes to L2 now
+    if (t == 0 && row + (int64_t)PF * gridDim.x < n) prefetch_l2_bulk(A + (row + (int64_t)PF * gridDim.x) * lda, 4u << L);
+    load_row(row);
+    // sign flip (D) and the stage on index bit 0
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      float v[4];
+      upk(p[2 * q], v[0], v[1]);
+      upk(p[2 * q + 1], v[2], v[3]);
+      const uint32_t w = dm[q >> 3] >> (4 * (q & 7));
+      v[0] = __int_as_float(__float_as_int(v[0]) ^ (w << 31));
+      v[1] = __int_as_float(__float_as_int(v[1]) ^ ((w << 30) & 0x80000000u));
+      v[2] = __int_as_float(__float_as_int(v[2]) ^ ((w << 29) & 0x80000000u));
+      v[3] = __int_as_float(__float_as_int(v[3]) ^ ((w << 28) & 0x80000000u));
+      p[2 * q] = pk(v[0] + v[1], v[0] - v[1]);
+      p[2 * q + 1] = pk(v[2] + v[3], v[2] - v[3]);
+    }
+    // stage on index bit 1 (pair index bit 0), then the 5 q bits (pair index bits 1..5)
+#pragma unroll
+    for (int h = 1; h < 64; h <<= 1) {
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        if ((i & h) == 0) {
+          const u64 s = f2add(p[i], p[i | h]);
+          const u64 d = f2sub(p[i], p[i | h]);
+          p[i] = s;
+          p[i | h] = d;
+        }
+      }
+    }
+    __syncthreads();  // the previous row's gather has finished reading buf
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      float v[4];
+      upk(p[2 * q], v[0], v[1]);
+      upk(p[2 * q + 1], v[2], v[3]);
+      *reinterpret_cast<float4*>(buf + swz4(4 * t + QS * q)) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    __syncthreads();
+    // phase 2: this thread owns indices 128t .. 128t+127 (bits 0..6)
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      const float4 v = *reinterpret_cast<const float4*>(buf + swz4(128 * t + 4 * u));
+      p[2 * u] = pk(v.x, v.y);
+      p[2 * u + 1] = pk(v.z, v.w);
+    }
+#pragma unroll
+    for (int h = 2; h < 64; h <<= 1) {
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        if ((i & h) == 0) {
+          const u64 s = f2add(p[i], p[i | h]);
+          const u64 d = f2sub(p[i], p[i | h]);
+          p[i] = s;
+          p[i | h] = d;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      float v[4];
+      upk(p[2 * u], v[0], v[1]);
+      upk(p[2 * u + 1], v[2], v[3]);
+      *reinterpret_cast<float4*>(buf + swz4(128 * t + 4 * u)) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    __syncthreads();
+    // gather with the last M3 stages folded in
+    float* y = Y + row * ldy;
+    for (int c = t; c < k; c += T) {
+      float s = 0.f;
+      for (int x = 0; x < xi; ++x) {
+        const uint32_t e = (uint32_t)__ldg(samp + (int64_t)c * xi + x);
+        const int r = (int)(e & 0x7fffffffu);
+        float acc;
+        if constexpr (M3 == 0) {
+          acc = buf[swz4(r)];
+        } else {
+          constexpr int MK = ((1 << M3) - 1) << 7;
+          const int rb = r & ~MK, rh = (r >> 7) & ((1 << M3) - 1);
+          acc = 0.f;
+#pragma unroll
+          for (int u = 0; u < (1 << M3); ++u) {
+            const float z = buf[swz4(rb | (u << 7))];
+            acc += flip_if(z, (uint32_t)(__popc(u & rh) & 1));
+          }
+        }
+        s += flip_if(acc, e >> 31);
+      }
+      y[c] = s * scale;
+    }
+  }
+}
+
+template <int L>
+int launch_wide(const float* A, int64_t n, int64_t lda, const float* dv, const int32_t* samp, int xi, int k,
+                double scale, float* Y, int64_t ldy, cudaStream_t s) {
+  constexpr int T = WideCfg<L>::T;
+  const size_t smem = sizeof(float) << L;
+  auto kern = srtt_wht_wide<L>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)sm_count() * per_sm;
+  if (grid > n) grid = n;
+  kern<<<(unsigned)grid, T, smem, s>>>(A, n, lda, dv, samp, xi, k, (float)scale, Y, ldy);
+  return check_launch("sk_srtt_right(wide)");
+}
+
 // Generic: one CTA per row, whole row in shared memory, log2(d) synchronised butterfly stages.
 template <typename T>
 __global__ void srtt_wht_simple(const T* __restrict__ A, int64_t n, int64_t d, int64_t lda,
@@ -285,6 +477,17 @@ int run(const void* A_, int64_t n, int64_t d, int64_t lda, const void* dv_, bool
   int L = 0;
   while ((int64_t(1) << L) < d) ++L;
   const bool aligned = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % (16 / sizeof(T)) == 0);
+  if constexpr (sizeof(T) == 4) {
+    const bool dv_aligned = (reinterpret_cast<uintptr_t>(dv) & 15) == 0;
+    if (pm1 && aligned && dv_aligned && L >= 12 && L <= 14) {
+      const float* Af = reinterpret_cast<const float*>(A);
+      const float* dvf = reinterpret_cast<const float*>(dv);
+      float* Yf = reinterpret_cast<float*>(Y);
+      if (L == 12) return launch_wide<12>(Af, n, lda, dvf, samp, xi, (int)k, scale, Yf, ldy, s);
+      if (L == 13) return launch_wide<13>(Af, n, lda, dvf, samp, xi, (int)k, scale, Yf, ldy, s);
+      return launch_wide<14>(Af, n, lda, dvf, samp, xi, (int)k, scale, Yf, ldy, s);
+    }
+  }
   const int max_fast = sizeof(T) == 4 ? 14 : 13;
   if (L >= 10 && L <= max_fast && aligned) {
     // Rademacher diagonals take the sign-mask path; any other diagonal multiplies.
