@@ -97,6 +97,22 @@ SK_API int sk_srtt_right(int dtype, const void* A, int64_t n, int64_t d, int64_t
                   int transform, const int32_t* samp, int32_t xi, int64_t k, double scale, void* Y,
                   int64_t ldy, void* stream);
 
+/*
+ * K-TC — Y[n,k] = scale * A[n,d] * B[d,k] on the tcgen05 tensor cores, float32 A split in-kernel
+ * into bf16 hi + lo, fp32 accumulation in TMEM.  B is given transposed and pre-converted: Bt_hi
+ * (k x d bf16, row stride ldb) and optionally Bt_lo (the bf16 residual of B; NULL when B is exact in
+ * bf16, e.g. the +-1 sparse-sign and Khatri-Rao matrices).  A 16-byte aligned with
+ * lda and d multiples of 4; ldb a multiple of 8.  Serves the dense form of SparseUniform/SparseStack
+ * (src/sketch/sparse.py:63-66, config 3), KhatriRaoTM.apply_right (src/sketch/khatri_rao.py:158-164,
+ * config 5) and GaussianTM (src/sketch/gaussian.py + base.py:75-79).  A workspace of
+ * sk_dense_tc_workspace_bytes(...) bytes is needed when the launch splits K (few row tiles).
+ */
+SK_API int sk_dense_tc_supported(int64_t k);
+SK_API size_t sk_dense_tc_workspace_bytes(int64_t n, int64_t d, int64_t k, int split_b);
+SK_API int sk_dense_right_tc(const float* A, int64_t n, int64_t d, int64_t lda, const uint16_t* Bt_hi,
+                             const uint16_t* Bt_lo, int64_t ldb, int64_t k, double scale, float* Y,
+                             int64_t ldy, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

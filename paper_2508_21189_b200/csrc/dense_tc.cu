@@ -1,0 +1,432 @@
+// K-TC — dense tensor-core apply  Y[n,k] = scale * A[n,d] * B[d,k]  with float32 A, on tcgen05.
+//
+// Shared engine for every test matrix whose dense form is cheap to feed the tensor cores:
+//   * sparse sign Omega (densified once to exact +-1 bf16; scale = 1/sqrt(zeta))  — config 3
+//   * Khatri-Rao Omega (columns f0[:,j] (x) f1[:,j], exact +-1 bf16; scale = 1/sqrt(k)) — config 5
+//   * Gaussian Omega (bf16 hi + lo split of the float64 draws)                       — reference
+//
+// Precision.  float32 A is split in-kernel into bf16 hi + lo (x = hi + lo + O(2^-18 |x|)):
+//   Y = A_hi B_hi + A_lo B_hi (+ A_hi B_lo when B is split).
+// The tcgen05 fp32 accumulator loses ~1e-9 * K relative accuracy over a K-long chain (measured,
+// tools/tc_precision.py: 8e-5 at K = 65536), so TMEM only ever holds CHUNK_KB k-blocks (1024 of K)
+// of a sum: the MMA warp alternates two TMEM accumulators and dedicated reducer warps fold each
+// finished chunk into fp32 register sums (round-to-nearest adds).  Result: ~3e-6 at any K.
+//
+// CTA = 512 threads (one per SM, persistent over (M-tile, N-block, K-split) work units):
+//   WG0  warp 0: TMA producer of B^T tiles (bf16, K-major, SWIZZLE_128B) | warp 1: MMA issuer
+//        warp 2: TMEM allocator                                           (regs trimmed to 32)
+//   WG1  warps 4..7 : A converters — LDG fp32 -> bf16 hi/lo -> STS in the UMMA K-major SW128
+//        layout, rows bulk-prefetched into L2 a few k-blocks ahead                     (128 regs)
+//   WG2+WG3 warps 8..15 : reducers — tcgen05.ld of finished chunks, fp32 sums in registers
+//        (warp w: TMEM lane group w%4, column half (w-8)/4), final scale + store         (168 regs)
+// smem ring of `stages` x {A_hi 16 KB, A_lo 16 KB, B_hi BN*128 B (, B_lo)}; mbarriers full/empty per
+// stage and acc_full/acc_empty per TMEM accumulator.
+#include <cuda.h>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace skb {
+namespace {
+
+using namespace sm100;
+
+constexpr int BM = 128;
+constexpr int BK = 64;               // bf16 elements per 128-byte swizzle row
+constexpr int CHUNK_KB = 16;         // k-blocks accumulated in TMEM before a register fold
+constexpr int kThreads = 512;
+constexpr int kPrefetchStages = 4;   // L2 bulk prefetch distance for A rows (k-blocks)
+constexpr int kMaxBNH = 128;         // columns per reducer thread (BN <= 256)
+
+struct TcParams {
+  const float* A;
+  int64_t M, K, lda;
+  int N, BN, nblocks, ksplit, kb_per_split, stages;
+  uint32_t tmem_cols;
+  float scale;
+  float* Y;        // final output (ksplit == 1) ...
+  int64_t ldy;
+  float* part;     // ... or partial sums [ksplit][M][N] (ksplit > 1)
+  int num_units;
+  int mtiles;
+};
+
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+
+struct Unit {
+  int mt, nb, ks;
+};
+__device__ __forceinline__ Unit unit_of(const TcParams& p, int u) {
+  Unit r;
+  r.nb = u % p.nblocks;
+  const int t = u / p.nblocks;
+  r.ks = t % p.ksplit;
+  r.mt = t / p.ksplit;
+  return r;
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kThreads, 1)
+    dense_tc_kernel(const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
+                    const TcParams p) {
+  extern __shared__ uint8_t smem_dyn[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  const uint32_t a_bytes = BM * 128;
+  const uint32_t b_bytes = (uint32_t)p.BN * 128;
+  const uint32_t stage_bytes = 2 * a_bytes + NB * b_bytes;
+  const int S = p.stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * stage_bytes);
+  uint64_t* empty = full + S;
+  uint64_t* acc_full = empty + S;   // [2]
+  uint64_t* acc_empty = acc_full + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1 + 4);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 8);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&tm_bhi);
+    if (NB == 2) tma_prefetch_desc(&tm_blo);
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, p.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int nk = (int)((p.K + BK - 1) / BK);
+
+  if (warp < 4) {
+    setmaxnreg_dec<32>();
+    if (warp == 0 && lane == 0) {
+      // ---------------------------------------------------------------- B producer (TMA)
+      int s = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+        const Unit w = unit_of(p, u);
+        const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + (size_t)s * stage_bytes;
+          mbar_arrive_expect_tx(&full[s], NB * b_bytes);
+          tma_load_2d(st + 2 * a_bytes, &tm_bhi, &full[s], kb * BK, w.nb * p.BN);
+          if (NB == 2) tma_load_2d(st + 2 * a_bytes + b_bytes, &tm_blo, &full[s], kb * BK, w.nb * p.BN);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+      }
+    } else if (warp == 1 && lane == 0) {
+      // ---------------------------------------------------------------- MMA issuer
+      const uint32_t idesc = idesc_bf16_f32(BM, p.BN);
+      int s = 0;
+      uint32_t ph = 0;
+      uint32_t chunk_seq = 0;  // global chunk counter -> accumulator buffer and phase
+      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+        const Unit w = unit_of(p, u);
+        const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
+        for (int c0 = kb0; c0 < kb1; c0 += CHUNK_KB, ++chunk_seq) {
+          const uint32_t buf = chunk_seq & 1, use = chunk_seq >> 1;
+          mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + buf * (uint32_t)p.BN;
+          const int c1 = min(kb1, c0 + CHUNK_KB);
+          for (int kb = c0; kb < c1; ++kb) {
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            const uint32_t st = smem_u32(smem + (size_t)s * stage_bytes);
+            const uint32_t a_hi = st, a_lo = st + a_bytes, b_hi = st + 2 * a_bytes, b_lo = b_hi + b_bytes;
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint64_t dah = sdesc_kmajor_sw128(a_hi + kk * 32);
+              const uint64_t dal = sdesc_kmajor_sw128(a_lo + kk * 32);
+              const uint64_t dbh = sdesc_kmajor_sw128(b_hi + kk * 32);
+              umma_bf16(d, dah, dbh, idesc, (kb > c0 || kk > 0) ? 1u : 0u);
+              umma_bf16(d, dal, dbh, idesc, 1u);
+              if (NB == 2) umma_bf16(d, dah, sdesc_kmajor_sw128(b_lo + kk * 32), idesc, 1u);
+            }
+            umma_commit(&empty[s]);
+            if (++s == S) { s = 0; ph ^= 1; }
+          }
+          umma_commit(&acc_full[buf]);
+        }
+      }
+    }
+  } else if (warp < 8) {
+    setmaxnreg_dec<128>();
+    // ---------------------------------------------------------------- A converters
+    const int ct = threadIdx.x - 128;      // 0..127
+    const int c4 = ct & 15;                // float4 column within the 64-wide K block
+    const int rsub = ct >> 4;              // 0..7
+    int s = 0;
+    uint32_t ph = 0;
+    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+      const Unit w = unit_of(p, u);
+      const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
+      const int64_t row0 = (int64_t)w.mt * BM;
+      const int64_t my_row = row0 + ct;
+      auto prefetch_kb = [&](int kb) {
+        if (kb < kb1 && my_row < p.M) {
+          const int64_t c0 = (int64_t)kb * BK;
+          const int64_t wdt = (p.K - c0) < BK ? (p.K - c0) : BK;
+          prefetch_l2(p.A + my_row * p.lda + c0, (uint32_t)(((wdt * 4) + 15) & ~15));
+        }
+      };
+      for (int j = 0; j < kPrefetchStages; ++j) prefetch_kb(kb0 + j);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        prefetch_kb(kb + kPrefetchStages);
+        float4 cur[16];
+        const int64_t col = (int64_t)kb * BK + c4 * 4;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int64_t row = row0 + rsub + 8 * i;
+          cur[i] = (row < p.M && col < p.K) ? __ldg(reinterpret_cast<const float4*>(p.A + row * p.lda + col))
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* st = smem + (size_t)s * stage_bytes;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int r = rsub + 8 * i;
+          const float4 v = cur[i];
+          const uint32_t h01 = cvt_bf16x2(v.y, v.x), h23 = cvt_bf16x2(v.w, v.z);
+          const float l0 = v.x - __uint_as_float(h01 << 16), l1 = v.y - __uint_as_float(h01 & 0xffff0000u);
+          const float l2 = v.z - __uint_as_float(h23 << 16), l3 = v.w - __uint_as_float(h23 & 0xffff0000u);
+          const uint32_t lo01 = cvt_bf16x2(l1, l0), lo23 = cvt_bf16x2(l3, l2);
+          const uint32_t off = r * 128 + (((c4 >> 1) ^ (r & 7)) << 4) + ((c4 & 1) << 3);
+          *reinterpret_cast<uint2*>(st + off) = make_uint2(h01, h23);
+          *reinterpret_cast<uint2*>(st + a_bytes + off) = make_uint2(lo01, lo23);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[s]);
+        if (++s == S) { s = 0; ph ^= 1; }
+      }
+    }
+  } else {
+    setmaxnreg_inc<168>();
+    // ---------------------------------------------------------------- reducers + output
+    const int lg = warp & 3;                 // TMEM lane group
+    const int half = (warp - 8) >> 2;        // column half
+    const int bnh = p.BN >> 1;               // multiple of 16
+    uint32_t chunk_seq = 0;
+    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+      const Unit w = unit_of(p, u);
+      const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
+      float sum[kMaxBNH];
+#pragma unroll
+      for (int j = 0; j < kMaxBNH; ++j) sum[j] = 0.f;
+      for (int c0 = kb0; c0 < kb1; c0 += CHUNK_KB, ++chunk_seq) {
+        const uint32_t buf = chunk_seq & 1, use = chunk_seq >> 1;
+        mbar_wait(&acc_full[buf], use & 1);
+        tc_fence_after();
+        const uint32_t base = tmem + ((uint32_t)(32 * lg) << 16) + buf * (uint32_t)p.BN + half * bnh;
+#pragma unroll
+        for (int g = 0; g < kMaxBNH / 16; ++g) {
+          if (g * 16 < bnh) {
+            uint32_t r[16];
+            tmem_ld16(base + g * 16, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) sum[g * 16 + j] += __uint_as_float(r[j]);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[buf]);
+      }
+      const int64_t row = (int64_t)w.mt * BM + 32 * lg + lane;
+      if (row < p.M) {
+        const int col0 = w.nb * p.BN + half * bnh;
+        float* out;
+        float sc;
+        if (p.ksplit == 1) {
+          out = p.Y + row * p.ldy + col0;
+          sc = p.scale;
+        } else {
+          out = p.part + ((int64_t)w.ks * p.M + row) * p.N + col0;
+          sc = 1.0f;
+        }
+#pragma unroll
+        for (int g = 0; g < kMaxBNH / 16; ++g) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int c = g * 16 + j;
+            if (c < bnh && col0 + c < p.N) out[c] = sum[c] * sc;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, p.tmem_cols);
+  }
+}
+
+// Y = scale * sum_s part[s] (fixed order)
+__global__ void tc_splitk_reduce(const float* __restrict__ part, int ksplit, int64_t M, int N, float scale,
+                                 float* __restrict__ Y, int64_t ldy) {
+  const int64_t total = M * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / N, c = i % N;
+    float s = 0.f;
+    for (int q = 0; q < ksplit; ++q) s += part[(q * M + r) * N + c];
+    Y[r * ldy + c] = s * scale;
+  }
+}
+
+// ------------------------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// B^T: [N rows][K cols] bf16, row stride ldb elements; box 64 (K) x box_rows (N), SWIZZLE_128B.
+int make_bt_map(CUtensorMap* m, const void* bt, int64_t N, int64_t K, int64_t ldb, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(SK_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)N};
+  cuuint64_t strides[1] = {(cuuint64_t)ldb * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(bt), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SK_EINVAL, "cuTensorMapEncodeTiled failed (alignment of B^T / ldb?)");
+  return SK_OK;
+}
+
+struct Plan {
+  int BN, nblocks, ksplit, kb_per_split, mtiles, units, stages;
+  size_t smem, ws_bytes;
+};
+
+Plan make_plan(int64_t n, int64_t d, int64_t k, int NB) {
+  Plan pl{};
+  // N blocks of at most 256 columns (two TMEM accumulators of BN columns each), BN % 32 == 0
+  pl.nblocks = (int)((k + 255) / 256);
+  const int64_t per = (k + pl.nblocks - 1) / pl.nblocks;
+  pl.BN = (int)((per + 31) / 32 * 32);
+  pl.mtiles = (int)((n + BM - 1) / BM);
+  const int nk = (int)((d + BK - 1) / BK);
+  const int tiles = pl.mtiles * pl.nblocks;
+  const int sms = sm_count();
+  // split K when there are too few tiles to keep every SM busy (each split >= 4 chunks)
+  int ks = 1;
+  while (tiles * ks < 4 * sms && (nk + 2 * ks - 1) / (2 * ks) >= 4 * CHUNK_KB) ks *= 2;
+  pl.kb_per_split = (nk + ks - 1) / ks;
+  pl.kb_per_split = (pl.kb_per_split + CHUNK_KB - 1) / CHUNK_KB * CHUNK_KB;
+  pl.ksplit = (nk + pl.kb_per_split - 1) / pl.kb_per_split;
+  pl.units = tiles * pl.ksplit;
+  const size_t stage_bytes = 2 * (size_t)BM * 128 + (size_t)NB * pl.BN * 128;
+  const size_t budget = 227 * 1024 - 1024 - 256;
+  int stages = (int)(budget / stage_bytes);
+  if (stages > 8) stages = 8;
+  pl.stages = stages;
+  pl.smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16;
+  pl.ws_bytes = pl.ksplit > 1 ? (size_t)pl.ksplit * n * k * sizeof(float) : 0;
+  return pl;
+}
+
+}  // namespace
+}  // namespace skb
+
+extern "C" int sk_dense_tc_supported(int64_t k) { return k >= 1 ? 1 : 0; }
+
+extern "C" size_t sk_dense_tc_workspace_bytes(int64_t n, int64_t d, int64_t k, int split_b) {
+  if (n < 1 || d < 1 || k < 1) return 0;
+  return skb::make_plan(n, d, k, split_b ? 2 : 1).ws_bytes;
+}
+
+extern "C" int sk_dense_right_tc(const float* A, int64_t n, int64_t d, int64_t lda, const uint16_t* Bt_hi,
+                                 const uint16_t* Bt_lo, int64_t ldb, int64_t k, double scale, float* Y, int64_t ldy,
+                                 void* ws, size_t ws_bytes, void* stream) {
+  using namespace skb;
+  if (n < 0 || d < 1 || k < 1 || lda < d || ldb < d || ldy < k)
+    return fail(SK_EINVAL, "sk_dense_right_tc: bad shape");
+  if (n == 0) return SK_OK;
+  if (!A || !Bt_hi || !Y) return fail(SK_EINVAL, "sk_dense_right_tc: null pointer");
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (lda & 3) || (d & 3))
+    return fail(SK_EINVAL, "sk_dense_right_tc: A must be 16-byte aligned with lda, d multiples of 4");
+  if ((reinterpret_cast<uintptr_t>(Bt_hi) & 15) || (ldb & 7) || (Bt_lo && (reinterpret_cast<uintptr_t>(Bt_lo) & 15)))
+    return fail(SK_EINVAL, "sk_dense_right_tc: B^T must be 16-byte aligned with ldb a multiple of 8");
+  const int NB = Bt_lo ? 2 : 1;
+  const Plan pl = make_plan(n, d, k, NB);
+  if (pl.stages < 2) return fail(SK_EUNSUPPORTED, "sk_dense_right_tc: tile does not fit shared memory");
+  if (pl.ksplit > 1 && (ws == nullptr || ws_bytes < pl.ws_bytes))
+    return fail(SK_EINVAL, "sk_dense_right_tc: workspace too small (sk_dense_tc_workspace_bytes)");
+  CUtensorMap mh, ml;
+  int st = make_bt_map(&mh, Bt_hi, k, d, ldb, pl.BN);
+  if (st != SK_OK) return st;
+  if (NB == 2) {
+    st = make_bt_map(&ml, Bt_lo, k, d, ldb, pl.BN);
+    if (st != SK_OK) return st;
+  } else {
+    ml = mh;
+  }
+  TcParams p{};
+  p.A = A;
+  p.M = n;
+  p.K = d;
+  p.lda = lda;
+  p.N = (int)k;
+  p.BN = pl.BN;
+  p.nblocks = pl.nblocks;
+  p.ksplit = pl.ksplit;
+  p.kb_per_split = pl.kb_per_split;
+  p.stages = pl.stages;
+  p.scale = (float)scale;
+  p.Y = Y;
+  p.ldy = ldy;
+  p.part = static_cast<float*>(ws);
+  p.num_units = pl.units;
+  p.mtiles = pl.mtiles;
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(2 * pl.BN)) cols <<= 1;
+  p.tmem_cols = cols;
+  cudaStream_t s = as_stream(stream);
+  const int grid = pl.units < sm_count() ? pl.units : sm_count();
+  if (NB == 1) {
+    cudaFuncSetAttribute(dense_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    dense_tc_kernel<1><<<grid, kThreads, pl.smem, s>>>(mh, ml, p);
+  } else {
+    cudaFuncSetAttribute(dense_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    dense_tc_kernel<2><<<grid, kThreads, pl.smem, s>>>(mh, ml, p);
+  }
+  st = check_launch("sk_dense_right_tc");
+  if (st != SK_OK || pl.ksplit == 1) return st;
+  const int64_t total = n * k;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 8 * (int64_t)sm_count()) blocks = 8 * (int64_t)sm_count();
+  tc_splitk_reduce<<<(unsigned)blocks, 256, 0, s>>>(p.part, pl.ksplit, n, (int)k, (float)scale, Y, ldy);
+  return check_launch("sk_dense_right_tc(reduce)");
+}

@@ -14,6 +14,7 @@ import numpy as np
 
 from .. import _lib
 from .encode import bcsc_encode
+from .tensorcore import bt_from_triplets, dense_right_tc
 from .testmatrix import TestMatrix, entry_sample
 
 __all__ = ["SparseStackTM", "SparseUniformTM", "SparseIIDTM", "SparseColTM", "sample_without_replacement"]
@@ -110,11 +111,40 @@ class _SignSparseTM(TestMatrix):
             )
         return self._device_cache[key]
 
+    def right_path(self, dtype) -> str:
+        """Kernel used by apply_right for this dtype: 'gather' (K1), 'tc' (K-TC dense) or 'dense'."""
+        import os
+
+        import torch
+
+        if self._sign_form() is None or dtype not in (torch.float32, torch.float64):
+            return "dense"
+        forced = os.environ.get("SKETCH_B200_SPARSE_RIGHT", "auto")
+        tc_ok = dtype == torch.float32 and self.k <= 4 * 512 and self.d % 4 == 0
+        if forced in ("gather", "tc"):
+            return forced if (forced == "gather" or tc_ok) else "gather"
+        rows, _, _, _ = self._sign_form()
+        per_row = rows.size / max(1, self.d)
+        # the dense tensor-core form wins when each row of Omega carries many nonzeros relative to k
+        return "tc" if (tc_ok and self.k <= 512 and per_row >= 6) else "gather"
+
+    def _tc_on(self, device):
+        key = ("tc", device)
+        if key not in self._device_cache:
+            rows, cols, neg, mag = self._sign_form()
+            hi, lo = bt_from_triplets(rows, cols, neg, self.d, self.k, device)
+            self._device_cache[key] = (hi, lo, mag)
+        return self._device_cache[key]
+
     def _right_device(self, a):
         import torch
 
-        if self._sign_form() is None or a.dtype not in (torch.float32, torch.float64):
+        path = self.right_path(a.dtype)
+        if path == "dense":
             return super()._right_device(a)
+        if path == "tc":
+            hi, lo, mag = self._tc_on(a.device)
+            return dense_right_tc(a, hi, lo, self.k, mag)
         code = _lib.SK_F32 if a.dtype == torch.float32 else _lib.SK_F64
         ptr, ent, r, mag = self._bcsc_on(a.device, "right", code)
         n = a.shape[0]
