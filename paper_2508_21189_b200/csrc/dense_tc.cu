@@ -15,8 +15,9 @@
 // CTA = 512 threads (one per SM, persistent over (M-tile, N-block, K-split) work units):
 //   WG0  warp 0: TMA producer of B^T tiles (bf16, K-major, SWIZZLE_128B) | warp 1: MMA issuer
 //        warp 2: TMEM allocator                                           (regs trimmed to 32)
-//   WG1  warps 4..7 : A converters — LDG fp32 -> bf16 hi/lo -> STS in the UMMA K-major SW128
-//        layout, rows bulk-prefetched into L2 a few k-blocks ahead                     (128 regs)
+//   warp 3: TMA producer of fp32 A tiles into a staging ring (128 rows x 64 cols, 32 KB)
+//   WG1  warps 4..7 : A converters — LDS fp32 staging -> bf16 hi/lo -> STS in the UMMA K-major
+//        SW128 layout                                                                 (128 regs)
 //   WG2+WG3 warps 8..15 : reducers — tcgen05.ld of finished chunks, fp32 sums in registers
 //        (warp w: TMEM lane group w%4, column half (w-8)/4), final scale + store         (168 regs)
 // smem ring of `stages` x {A_hi 16 KB, A_lo 16 KB, B_hi BN*128 B (, B_lo)}; mbarriers full/empty per
@@ -35,13 +36,13 @@ constexpr int BM = 128;
 constexpr int BK = 64;               // bf16 elements per 128-byte swizzle row
 constexpr int CHUNK_KB = 16;         // k-blocks accumulated in TMEM before a register fold
 constexpr int kThreads = 512;
-constexpr int kPrefetchStages = 4;   // L2 bulk prefetch distance for A rows (k-blocks)
+constexpr uint32_t kAStageBytes = BM * BK * 4;  // fp32 A staging tile (TMA, no swizzle): 32 KB
 constexpr int kMaxBNH = 128;         // columns per reducer thread (BN <= 256)
 
 struct TcParams {
   const float* A;
   int64_t M, K, lda;
-  int N, BN, nblocks, ksplit, kb_per_split, stages;
+  int N, BN, nblocks, ksplit, kb_per_split, stages, astages;
   uint32_t tmem_cols;
   float scale;
   float* Y;        // final output (ksplit == 1) ...
@@ -78,17 +79,20 @@ __device__ __forceinline__ Unit unit_of(const TcParams& p, int u) {
 
 template <int NB>
 __global__ void __launch_bounds__(kThreads, 1)
-    dense_tc_kernel(const __grid_constant__ CUtensorMap tm_bhi, const __grid_constant__ CUtensorMap tm_blo,
-                    const TcParams p) {
+    dense_tc_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_bhi,
+                    const __grid_constant__ CUtensorMap tm_blo, const TcParams p) {
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
   const uint32_t a_bytes = BM * 128;
   const uint32_t b_bytes = (uint32_t)p.BN * 128;
   const uint32_t stage_bytes = 2 * a_bytes + NB * b_bytes;
-  const int S = p.stages;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * stage_bytes);
+  const int S = p.stages, SA = p.astages;
+  uint8_t* astage = smem + (size_t)S * stage_bytes;  // SA x 32 KB fp32 staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(astage + (size_t)SA * kAStageBytes);
   uint64_t* empty = full + S;
-  uint64_t* acc_full = empty + S;   // [2]
+  uint64_t* a_full = empty + S;
+  uint64_t* a_empty = a_full + SA;
+  uint64_t* acc_full = a_empty + SA;   // [2]
   uint64_t* acc_empty = acc_full + 2;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -98,11 +102,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[s], 1 + 4);
       mbar_init(&empty[s], 1);
     }
+    for (int s2 = 0; s2 < SA; ++s2) {
+      mbar_init(&a_full[s2], 1);
+      mbar_init(&a_empty[s2], 4);
+    }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], 8);
     }
     fence_mbar_init();
+    tma_prefetch_desc(&tm_a);
     tma_prefetch_desc(&tm_bhi);
     if (NB == 2) tma_prefetch_desc(&tm_blo);
   }
@@ -129,6 +138,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_2d(st + 2 * a_bytes, &tm_bhi, &full[s], kb * BK, w.nb * p.BN);
           if (NB == 2) tma_load_2d(st + 2 * a_bytes + b_bytes, &tm_blo, &full[s], kb * BK, w.nb * p.BN);
           if (++s == S) { s = 0; ph ^= 1; }
+        }
+      }
+    } else if (warp == 3 && lane == 0) {
+      // ---------------------------------------------------------------- A producer (TMA, fp32)
+      int s = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+        const Unit w = unit_of(p, u);
+        const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&a_empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&a_full[s], kAStageBytes);
+          tma_load_2d(astage + (size_t)s * kAStageBytes, &tm_a, &a_full[s], kb * BK, w.mt * BM);
+          if (++s == SA) { s = 0; ph ^= 1; }
         }
       }
     } else if (warp == 1 && lane == 0) {
@@ -173,31 +196,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ct = threadIdx.x - 128;      // 0..127
     const int c4 = ct & 15;                // float4 column within the 64-wide K block
     const int rsub = ct >> 4;              // 0..7
-    int s = 0;
-    uint32_t ph = 0;
+    int s = 0, sa = 0;
+    uint32_t ph = 0, pha = 0;
     for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
       const Unit w = unit_of(p, u);
       const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
-      const int64_t row0 = (int64_t)w.mt * BM;
-      const int64_t my_row = row0 + ct;
-      auto prefetch_kb = [&](int kb) {
-        if (kb < kb1 && my_row < p.M) {
-          const int64_t c0 = (int64_t)kb * BK;
-          const int64_t wdt = (p.K - c0) < BK ? (p.K - c0) : BK;
-          prefetch_l2(p.A + my_row * p.lda + c0, (uint32_t)(((wdt * 4) + 15) & ~15));
-        }
-      };
-      for (int j = 0; j < kPrefetchStages; ++j) prefetch_kb(kb0 + j);
       for (int kb = kb0; kb < kb1; ++kb) {
-        prefetch_kb(kb + kPrefetchStages);
         float4 cur[16];
-        const int64_t col = (int64_t)kb * BK + c4 * 4;
+        mbar_wait(&a_full[sa], pha);
+        const float* at = reinterpret_cast<const float*>(astage + (size_t)sa * kAStageBytes);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int64_t row = row0 + rsub + 8 * i;
-          cur[i] = (row < p.M && col < p.K) ? __ldg(reinterpret_cast<const float4*>(p.A + row * p.lda + col))
-                                            : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        for (int i = 0; i < 16; ++i) cur[i] = *reinterpret_cast<const float4*>(at + (rsub + 8 * i) * BK + c4 * 4);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_empty[sa]);
+        if (++sa == SA) { sa = 0; pha ^= 1; }
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t* st = smem + (size_t)s * stage_bytes;
 #pragma unroll
@@ -325,15 +337,31 @@ int make_bt_map(CUtensorMap* m, const void* bt, int64_t N, int64_t K, int64_t ld
   return SK_OK;
 }
 
+// A: [M rows][K cols] fp32, box 64 (K) x 128 (M), no swizzle (staging tile read by the converters).
+int make_a_map(CUtensorMap* m, const float* a, int64_t M, int64_t K, int64_t lda) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(SK_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
+  cuuint64_t strides[1] = {(cuuint64_t)lda * 4};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)BM};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SK_EINVAL, "cuTensorMapEncodeTiled(A) failed (alignment of A / lda?)");
+  return SK_OK;
+}
+
 struct Plan {
-  int BN, nblocks, ksplit, kb_per_split, mtiles, units, stages;
+  int BN, nblocks, ksplit, kb_per_split, mtiles, units, stages, astages;
   size_t smem, ws_bytes;
 };
 
 Plan make_plan(int64_t n, int64_t d, int64_t k, int NB) {
   Plan pl{};
   // N blocks of at most 256 columns (two TMEM accumulators of BN columns each), BN % 32 == 0
-  pl.nblocks = (int)((k + 255) / 256);
+  const int64_t bn_max = NB == 2 ? 128 : 256;  // a split B doubles the B tile
+  pl.nblocks = (int)((k + bn_max - 1) / bn_max);
   const int64_t per = (k + pl.nblocks - 1) / pl.nblocks;
   pl.BN = (int)((per + 31) / 32 * 32);
   pl.mtiles = (int)((n + BM - 1) / BM);
@@ -348,11 +376,18 @@ Plan make_plan(int64_t n, int64_t d, int64_t k, int NB) {
   pl.ksplit = (nk + pl.kb_per_split - 1) / pl.kb_per_split;
   pl.units = tiles * pl.ksplit;
   const size_t stage_bytes = 2 * (size_t)BM * 128 + (size_t)NB * pl.BN * 128;
-  const size_t budget = 227 * 1024 - 1024 - 256;
-  int stages = (int)(budget / stage_bytes);
-  if (stages > 8) stages = 8;
+  const size_t budget = 227 * 1024 - 1024 - 512;
+  // at least 2 bf16 stages, the rest split between fp32 staging (>= 2) and more bf16 stages
+  int stages = 2, astages = (int)((budget - 2 * stage_bytes) / kAStageBytes);
+  if (astages > 4) {
+    const int extra = (int)((budget - 2 * stage_bytes - 4 * kAStageBytes) / stage_bytes);
+    stages += extra > 0 ? extra : 0;
+    astages = (int)((budget - stages * stage_bytes) / kAStageBytes);
+    if (astages > 6) astages = 6;
+  }
   pl.stages = stages;
-  pl.smem = 1024 + stages * stage_bytes + (2 * stages + 4) * 8 + 16;
+  pl.astages = astages;
+  pl.smem = 1024 + stages * stage_bytes + astages * kAStageBytes + (2 * stages + 2 * astages + 4) * 8 + 16;
   pl.ws_bytes = pl.ksplit > 1 ? (size_t)pl.ksplit * n * k * sizeof(float) : 0;
   return pl;
 }
@@ -381,11 +416,13 @@ extern "C" int sk_dense_right_tc(const float* A, int64_t n, int64_t d, int64_t l
     return fail(SK_EINVAL, "sk_dense_right_tc: B^T must be 16-byte aligned with ldb a multiple of 8");
   const int NB = Bt_lo ? 2 : 1;
   const Plan pl = make_plan(n, d, k, NB);
-  if (pl.stages < 2) return fail(SK_EUNSUPPORTED, "sk_dense_right_tc: tile does not fit shared memory");
+  if (pl.stages < 2 || pl.astages < 2) return fail(SK_EUNSUPPORTED, "sk_dense_right_tc: tile does not fit shared memory");
   if (pl.ksplit > 1 && (ws == nullptr || ws_bytes < pl.ws_bytes))
     return fail(SK_EINVAL, "sk_dense_right_tc: workspace too small (sk_dense_tc_workspace_bytes)");
-  CUtensorMap mh, ml;
-  int st = make_bt_map(&mh, Bt_hi, k, d, ldb, pl.BN);
+  CUtensorMap ma, mh, ml;
+  int st = make_a_map(&ma, A, n, d, lda);
+  if (st != SK_OK) return st;
+  st = make_bt_map(&mh, Bt_hi, k, d, ldb, pl.BN);
   if (st != SK_OK) return st;
   if (NB == 2) {
     st = make_bt_map(&ml, Bt_lo, k, d, ldb, pl.BN);
@@ -404,6 +441,7 @@ extern "C" int sk_dense_right_tc(const float* A, int64_t n, int64_t d, int64_t l
   p.ksplit = pl.ksplit;
   p.kb_per_split = pl.kb_per_split;
   p.stages = pl.stages;
+  p.astages = pl.astages;
   p.scale = (float)scale;
   p.Y = Y;
   p.ldy = ldy;
@@ -417,10 +455,10 @@ extern "C" int sk_dense_right_tc(const float* A, int64_t n, int64_t d, int64_t l
   const int grid = pl.units < sm_count() ? pl.units : sm_count();
   if (NB == 1) {
     cudaFuncSetAttribute(dense_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
-    dense_tc_kernel<1><<<grid, kThreads, pl.smem, s>>>(mh, ml, p);
+    dense_tc_kernel<1><<<grid, kThreads, pl.smem, s>>>(ma, mh, ml, p);
   } else {
     cudaFuncSetAttribute(dense_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
-    dense_tc_kernel<2><<<grid, kThreads, pl.smem, s>>>(mh, ml, p);
+    dense_tc_kernel<2><<<grid, kThreads, pl.smem, s>>>(ma, mh, ml, p);
   }
   st = check_launch("sk_dense_right_tc");
   if (st != SK_OK || pl.ksplit == 1) return st;
