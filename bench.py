@@ -180,8 +180,9 @@ def _traffic(name):
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(name)
-    except (OSError, ValueError):
+            ent = json.load(f).get(name)
+        return None if ent is None else float(ent["bytes_per_launch"])
+    except (OSError, ValueError, KeyError, TypeError):
         return None
 
 

@@ -204,14 +204,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = kb0; kb < kb1; ++kb) {
         float4 cur[16];
         mbar_wait(&a_full[sa], pha);
-        const float* at = reinterpret_cast<const float*>(astage + (size_t)sa * kAStageBytes);
+        const uint32_t at = smem_u32(astage + (size_t)sa * kAStageBytes) + (rsub * BK + c4 * 4) * 4;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) cur[i] = *reinterpret_cast<const float4*>(at + (rsub + 8 * i) * BK + c4 * 4);
+        for (int i = 0; i < 16; ++i) cur[i] = lds128(at + i * 8 * BK * 4);
         __syncwarp();
         if (lane == 0) mbar_arrive(&a_empty[sa]);
         if (++sa == SA) { sa = 0; pha ^= 1; }
         mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* st = smem + (size_t)s * stage_bytes;
+        const uint32_t st = smem_u32(smem + (size_t)s * stage_bytes);
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int r = rsub + 8 * i;
@@ -221,8 +221,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float l2 = v.z - __uint_as_float(h23 << 16), l3 = v.w - __uint_as_float(h23 & 0xffff0000u);
           const uint32_t lo01 = cvt_bf16x2(l1, l0), lo23 = cvt_bf16x2(l3, l2);
           const uint32_t off = r * 128 + (((c4 >> 1) ^ (r & 7)) << 4) + ((c4 & 1) << 3);
-          *reinterpret_cast<uint2*>(st + off) = make_uint2(h01, h23);
-          *reinterpret_cast<uint2*>(st + a_bytes + off) = make_uint2(lo01, lo23);
+          sts64(st + off, h01, h23);
+          sts64(st + a_bytes + off, lo01, lo23);
         }
         fence_proxy_async_smem();
         __syncwarp();
