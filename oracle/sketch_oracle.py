@@ -45,6 +45,10 @@ __all__ = [
     "right_chunked",
     "csr_adjoint_chunked",
     "right_multiprocess",
+    "orth",
+    "rsvd",
+    "truncated_pinv_apply",
+    "sketch_and_solve",
 ]
 
 
@@ -297,3 +301,52 @@ def right_multiprocess(fn, a, procs: int, rows: int = 256) -> np.ndarray:
     finally:
         _POOL_STATE.clear()
     return np.concatenate([parts[s] for s, _ in bounds], axis=0)
+
+
+# --------------------------------------------------------------------------
+# Downstream drivers (float64, as the reference)
+# --------------------------------------------------------------------------
+RANK_TOL = 5.0 * float(np.finfo(np.float64).eps)  # core/factor.py:27-28
+
+
+def orth(m, rel_tol: float = RANK_TOL) -> np.ndarray:
+    """core/factor.py:63-82 — Householder QR, SVD basis when R reveals rank deficiency."""
+    m = np.asarray(m)
+    if m.shape[1] == 0:
+        return m.copy()
+    q, r = np.linalg.qr(m, mode="reduced")
+    dg = np.abs(np.diag(r))
+    top = dg.max(initial=0.0)
+    if top == 0.0:
+        return q[:, :0]
+    if dg.min() > rel_tol * top:
+        return q
+    u, s, _ = np.linalg.svd(m, full_matrices=False)
+    return u[:, : int(np.count_nonzero(s > rel_tol * s[0]))]
+
+
+def rsvd(a, omega_apply, k: int):
+    """rand_nla.py:84-109 — Y = A Omega, Q = orth(Y), B = Q^* A, SVD(B) -> (Q U_B, sigma, V)."""
+    a = np.asarray(a, dtype=np.float64)
+    q = orth(omega_apply(a))
+    if q.shape[1] == 0:
+        return np.zeros((a.shape[0], 0)), np.zeros(0), np.zeros((a.shape[1], 0))
+    u, s, vh = np.linalg.svd(q.conj().T @ a, full_matrices=False)
+    return q @ u, s, vh.conj().T
+
+
+def truncated_pinv_apply(m, b, rel_tol: float = RANK_TOL):
+    """core/factor.py:112-136."""
+    b = np.asarray(b)
+    one = b.ndim == 1
+    b = b[:, None] if one else b
+    u, s, vh = np.linalg.svd(m, full_matrices=False)
+    rank = 0 if s.size == 0 or s[0] == 0.0 else int(np.count_nonzero(s > rel_tol * s[0]))
+    out = np.zeros((m.shape[1], b.shape[1])) if rank == 0 else vh[:rank].conj().T @ ((u[:, :rank].conj().T @ b) / s[:rank, None])
+    return out[:, 0] if one else out
+
+
+def sketch_and_solve(a, b, adjoint_apply):
+    """rand_nla.py:278-297 — (Psi^* A)^+ (Psi^* B)."""
+    return truncated_pinv_apply(adjoint_apply(np.asarray(a, dtype=np.float64)),
+                                adjoint_apply(np.asarray(b, dtype=np.float64)))

@@ -317,3 +317,38 @@ class SparseColTM(_SignSparseTM):
 
     def redraw(self, seed: int) -> "SparseColTM":
         return SparseColTM(self.d, self.k, self.xi, field=self.field, seed=seed)
+
+
+class SparseRowBlockTM(_SignSparseTM):
+    """Rows [r0, r1) of a sparse test matrix, as an operator of its own (multi-GPU row shards).
+
+    Rank g of a row-sharded job holds A[r0:r1, :] and applies this block: its adjoint partial
+    Omega[r0:r1]^* A_g is summed across ranks by one all-reduce.
+    """
+
+    def __init__(self, parent: _SignSparseTM, r0: int, r1: int):
+        if not (0 <= r0 < r1 <= parent.d):
+            raise ValueError(f"bad row block [{r0}, {r1}) of d={parent.d}")
+        super().__init__(r1 - r0, parent.k, parent.field, parent.seed)
+        rows, cols, vals = parent._triplets()
+        lo, hi = np.searchsorted(rows, [r0, r1])
+        if np.any(np.diff(rows) < 0):  # unsorted rows (SparseCol CSR order is sorted; others row-major)
+            sel = (rows >= r0) & (rows < r1)
+            self._coo = (rows[sel] - r0, cols[sel], vals[sel])
+        else:
+            self._coo = (rows[lo:hi] - r0, cols[lo:hi], vals[lo:hi])
+        self.parent = parent
+        self.row_offset = int(r0)
+
+    def _draw(self):
+        return self._coo
+
+    def redraw(self, seed: int):
+        raise NotImplementedError("redraw the parent operator instead")
+
+
+def _row_block(self, r0: int, r1: int) -> SparseRowBlockTM:
+    return SparseRowBlockTM(self, r0, r1)
+
+
+_SignSparseTM.row_block = _row_block

@@ -105,6 +105,23 @@ def small_fixtures() -> dict:
     out["kat_countsketch"] = cs.apply_right(np.array([[1.0, 2.0, 3.0]]))  # test_sketch.py:56-63
     out["kat_kr_column"] = KhatriRaoTM.from_factors(np.array([[[1.0], [1.0]], [[1.0], [-1.0]]])).materialize()[:, 0]
     out["kat_wht_eye8"] = wht(np.eye(8))  # test_transforms.py:18-21
+    # downstream drivers: rsvd (rand_nla.py:84-109) and sketch_and_solve (rand_nla.py:278-297)
+    from sketchkit.rand_nla import rsvd, sketch_and_solve
+
+    rng = np.random.default_rng(123)
+    u0, _ = np.linalg.qr(rng.standard_normal((600, 60)))
+    v0, _ = np.linalg.qr(rng.standard_normal((256, 60)))
+    a = (u0 * (np.arange(1, 61) ** -2.0)) @ v0.T
+    out["rsvd_A"] = a
+    for name, tm in (("rsvd_su", SparseUniformTM(256, 40, 8, seed=5)), ("rsvd_rtt", SparseRttTM(256, 40, 1, "wht", seed=6))):
+        f = rsvd(a, 40, tm)
+        out[f"{name}_sigma"] = f.sigma
+        out[f"{name}_recon"] = (f.u * f.sigma) @ f.v.conj().T
+    al = rng.standard_normal((3000, 20))
+    bl = al @ rng.standard_normal(20) + 1e-3 * rng.standard_normal(3000)
+    out["sas_A"] = al
+    out["sas_b"] = bl
+    out["sas_x"] = sketch_and_solve(al, bl, SparseUniformTM(3000, 200, 8, seed=9))
     return out
 
 

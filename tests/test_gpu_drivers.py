@@ -1,0 +1,78 @@
+"""GPU drivers: rsvd / sketch_and_solve against the reference's own outputs (golden) and the
+oracle; sketch-and-precondition LSQR against SciPy's LSQR (no reference test exists: unpinned)."""
+
+import numpy as np
+import pytest
+
+import oracle as orc
+from _cases import rel_err
+from paper_2508_21189_b200 import rand_nla
+from paper_2508_21189_b200 import sketch as skb
+
+pytestmark = pytest.mark.gpu
+
+
+def test_rsvd_matches_reference(golden, cuda):
+    a = golden["rsvd_A"]
+    for name, tm in (("rsvd_su", skb.SparseUniformTM(256, 40, 8, seed=5)),
+                     ("rsvd_rtt", skb.SparseRttTM(256, 40, 1, "wht", seed=6))):
+        f = rand_nla.rsvd(a, 40, tm)
+        assert isinstance(f.sigma, np.ndarray)
+        assert np.allclose(f.sigma, golden[f"{name}_sigma"], rtol=1e-9, atol=1e-14)
+        assert rel_err((f.u * f.sigma) @ f.v.T, golden[f"{name}_recon"]) <= 1e-9
+
+
+def test_rsvd_errors(cuda):
+    tm = skb.SparseUniformTM(64, 8, 2, seed=0)
+    with pytest.raises(ValueError, match="incompatible"):
+        rand_nla.rsvd(np.ones((10, 64)), 9, tm)
+    with pytest.raises(ValueError, match="exceeds"):
+        rand_nla.rsvd(np.ones((4, 64)), 8, tm)
+
+
+def test_rsvd_zero_matrix(cuda):
+    f = rand_nla.rsvd(np.zeros((50, 64)), 8, skb.SparseUniformTM(64, 8, 2, seed=1))
+    assert f.u.shape == (50, 0) and f.sigma.shape == (0,)
+
+
+def test_rsvd_f32_config3_like(cuda):
+    """Config-3 structure at reduced size: A = U diag(i^-2) V^T float32, k = 200, zeta = 8."""
+    import torch
+
+    n, d, k = 8192, 2048, 200
+    g = torch.Generator(device=cuda).manual_seed(0)
+    u, _ = torch.linalg.qr(torch.randn(n, d, device=cuda, dtype=torch.float64, generator=g))
+    v, _ = torch.linalg.qr(torch.randn(d, d, device=cuda, dtype=torch.float64, generator=g))
+    s = torch.arange(1, d + 1, device=cuda, dtype=torch.float64) ** -2.0
+    a = ((u * s) @ v.T).to(torch.float32)
+    tm = skb.SparseUniformTM(d, k, 8, seed=0)
+    f = rand_nla.rsvd(a, k, tm)
+    err = rand_nla.rsvd_residual(a, f)
+    a64 = a.double().cpu().numpy()
+    uo, so, vo = orc.rsvd(a64, lambda x: orc.csr_right(orc.sparse_uniform_csr(d, k, 8, 0), x), k)
+    err_ref = np.linalg.norm(a64 - (uo * so) @ vo.T) / np.linalg.norm(a64)
+    assert abs(err - err_ref) <= 1e-2 * err_ref + 1e-6
+
+
+def test_sketch_and_solve_matches_reference(golden, cuda):
+    x = rand_nla.sketch_and_solve(golden["sas_A"], golden["sas_b"], skb.SparseUniformTM(3000, 200, 8, seed=9))
+    assert rel_err(x, golden["sas_x"]) <= 1e-9
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_lsqr_vs_scipy(dt, cuda):
+    import scipy.sparse.linalg as sla
+
+    rng = np.random.default_rng(4)
+    n, d = 40000, 64
+    w = 1.0 + rng.pareto(1.5, size=n)
+    a = (rng.standard_normal((n, d)) * w[:, None]).astype(dt)
+    x0 = rng.standard_normal(d)
+    b = (a.astype(np.float64) @ x0 + 1e-3 * rng.standard_normal(n)).astype(dt)
+    tm = skb.SparseUniformTM(n, 256, 8, seed=3)
+    res = rand_nla.sketch_precondition_lsqr(a, b, tm, atol=1e-10, btol=1e-10)
+    ref = sla.lsqr(a.astype(np.float64), b.astype(np.float64), atol=1e-12, btol=1e-12, iter_lim=5000)[0]
+    r_gpu = np.linalg.norm(a.astype(np.float64) @ res.x - b) / np.linalg.norm(b)
+    r_ref = np.linalg.norm(a.astype(np.float64) @ ref - b) / np.linalg.norm(b)
+    assert abs(r_gpu - r_ref) <= 1e-4 * r_ref
+    assert res.itn < 60  # preconditioned: few iterations

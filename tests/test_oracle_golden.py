@@ -80,3 +80,15 @@ def test_oracle_config4_hash(golden_hashes):
     m = orc.sparse_uniform_csr(4194304, 2048, 8, 0)
     assert sha1(m.indices.astype(np.int64)) == h["indices"]
     assert sha1(m.data) == h["data"]
+
+
+def test_oracle_drivers_match_reference(golden):
+    a = golden["rsvd_A"]
+    for name, om in (("rsvd_su", lambda x: orc.csr_right(orc.sparse_uniform_csr(256, 40, 8, 5), x)),
+                     ("rsvd_rtt", lambda x: orc.srtt_right(*orc.srtt_parts(256, 40, 1, 6), x, "wht"))):
+        u, s, v = orc.rsvd(a, om, 40)
+        assert np.allclose(s, golden[f"{name}_sigma"], rtol=1e-10, atol=1e-15)
+        assert rel_err((u * s) @ v.T, golden[f"{name}_recon"]) <= 1e-10
+    om = orc.sparse_uniform_csr(3000, 200, 8, 9)
+    x = orc.sketch_and_solve(golden["sas_A"], golden["sas_b"], lambda b: orc.csr_adjoint(om, b))
+    assert rel_err(x, golden["sas_x"]) <= 1e-10
