@@ -215,26 +215,31 @@ def sketch_and_solve(a, b, tm_psi):
 
 
 def _matvec_blocks(A, v, block_rows):
-    """A @ v with A fp32/fp64 resident, result float64 (each entry is a d-long dot product)."""
+    """A @ v in float64 (float32 A is widened block by block: LSQR needs residuals below fp32 eps)."""
     import torch
 
-    with _no_tf32():
-        return (A @ v.to(A.dtype)).double() if A.dtype != torch.float64 else A @ v
+    if A.dtype == torch.float64:
+        return A @ v
+    out = torch.empty(A.shape[0], dtype=torch.float64, device=A.device)
+    for r0 in range(0, A.shape[0], block_rows):
+        out[r0:r0 + block_rows] = A[r0:r0 + block_rows].double() @ v
+    return out
 
 
 def _rmatvec_blocks(A, u, block_rows):
-    """A^T @ u with float64 accumulation across row blocks (long reductions are split)."""
+    """A^T @ u in float64, accumulated across row blocks."""
     import torch
 
+    if A.dtype == torch.float64:
+        return A.T @ u
     out = torch.zeros(A.shape[1], dtype=torch.float64, device=A.device)
-    with _no_tf32():
-        for r0 in range(0, A.shape[0], block_rows):
-            out += (A[r0:r0 + block_rows].T @ u[r0:r0 + block_rows].to(A.dtype)).double()
+    for r0 in range(0, A.shape[0], block_rows):
+        out += A[r0:r0 + block_rows].double().T @ u[r0:r0 + block_rows]
     return out
 
 
 def sketch_precondition_lsqr(a, b, tm_psi, *, atol: float = 1e-6, btol: float = 1e-6, iter_lim: int = 200,
-                             block_rows: int = 1 << 18, allreduce=None) -> LsqrResult:
+                             block_rows: int = 1 << 16, allreduce=None) -> LsqrResult:
     """min ||A x - b|| by sketch-and-precondition: S A = Q R, then LSQR on A R^-1.
 
     `allreduce(t)` (in place sum across ranks) makes the solver distributed: every rank holds a row
