@@ -79,13 +79,18 @@ SK_API int sk_sparse_right(int dtype, const void* A, int64_t n, int64_t d, int64
  * Replaces `_SparseTM.apply_adjoint` = `self.matrix.conj().T @ b` (src/sketch/sparse.py:68-78).
  * Workspace of sk_sparse_adjoint_workspace_bytes(...) bytes (may be 0 -> pass NULL).
  * `chunk_rows` must equal sk_sparse_adjoint_chunk_rows(dtype, d, k).
+ * Optional fast-path segment table `seg` (NULL to skip): for every chunk h and group g of 1024
+ * output rows, seg[2*(h*G + g)] = the group's first entry offset rounded down to a multiple of 8
+ * and seg[2*(h*G + g) + 1] = its entry count rounded up to a multiple of 8 (G = ceil(k/1024));
+ * `ent_cap` = the maximum such count.  With `seg`, `ptr` must stay readable for 1028 ints past
+ * its end and `ent` for 8 uint16 past its end (zero padding).
  */
 SK_API int sk_sparse_adjoint_chunk_rows(int dtype, int64_t d, int64_t k);
 SK_API size_t sk_sparse_adjoint_workspace_bytes(int dtype, int64_t d, int64_t m, int64_t k);
 SK_API int sk_sparse_adjoint(int dtype, const void* A, int64_t d, int64_t m, int64_t lda,
-                      const int32_t* ptr, const uint16_t* ent, int32_t chunk_rows, int64_t k,
-                      double scale, void* SA, int64_t ldsa, int accumulate, void* ws,
-                      size_t ws_bytes, void* stream);
+                             const int32_t* ptr, const uint16_t* ent, int32_t chunk_rows,
+                             const int32_t* seg, int32_t ent_cap, int64_t k, double scale, void* SA,
+                             int64_t ldsa, int accumulate, void* ws, size_t ws_bytes, void* stream);
 
 /*
  * K3 — Y[n,k] = A[n,d] * D * F * S for the sparse randomized trigonometric transform,

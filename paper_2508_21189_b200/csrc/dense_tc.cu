@@ -82,7 +82,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     dense_tc_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_bhi,
                     const __grid_constant__ CUtensorMap tm_blo, const TcParams p) {
   extern __shared__ uint8_t smem_dyn[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  // keep the pointer derived from the __shared__ array (integer offset) so accesses stay LDS/STS
+  uint8_t* smem = smem_dyn + ((1024u - (sm100::smem_u32(smem_dyn) & 1023u)) & 1023u);
   const uint32_t a_bytes = BM * 128;
   const uint32_t b_bytes = (uint32_t)p.BN * 128;
   const uint32_t stage_bytes = 2 * a_bytes + NB * b_bytes;

@@ -11,7 +11,11 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["bcsc_encode", "bcsc_decode", "srtt_sampler_encode", "sign_bits"]
+__all__ = ["bcsc_encode", "bcsc_decode", "bcsc_segments", "srtt_sampler_encode", "sign_bits"]
+
+ADJ_GROUP = 1024  # output rows per CTA group of the adjoint fast path (sparse_adjoint.cu V2_CG)
+PTR_PAD = 1028    # ints the fast path may read past the pointer array
+ENT_PAD = 8       # entries the fast path may read past the entry array
 
 
 def bcsc_encode(rows, cols, neg, d: int, k: int, chunk_rows: int):
@@ -36,6 +40,25 @@ def bcsc_encode(rows, cols, neg, d: int, k: int, chunk_rows: int):
     ptr = np.zeros(nchunks * k + 1, dtype=np.int64)
     np.cumsum(counts, out=ptr[1:])
     return ptr.astype(np.int32), ent
+
+
+def bcsc_segments(ptr, d: int, k: int, chunk_rows: int, group: int = ADJ_GROUP):
+    """Per (chunk, group of `group` columns): [first entry rounded down to 8, count rounded up to 8].
+
+    Returns (seg int32[nchunks * ngroups * 2], ent_cap) for sk_sparse_adjoint's fast path.
+    """
+    ptr = np.asarray(ptr, dtype=np.int64)
+    nchunks = (d + chunk_rows - 1) // chunk_rows
+    ngroups = (k + group - 1) // group
+    h = np.arange(nchunks)[:, None]
+    g0 = np.arange(ngroups)[None, :] * group
+    g1 = np.minimum(g0 + group, k)
+    start = ptr[h * k + g0]
+    end = ptr[h * k + g1]
+    e0 = start // 8 * 8
+    cnt = (end - e0 + 7) // 8 * 8
+    seg = np.stack([e0, cnt], axis=-1).astype(np.int32).ravel()
+    return seg, int(cnt.max()) if cnt.size else 0
 
 
 def bcsc_decode(ptr, ent, d: int, k: int, chunk_rows: int):

@@ -13,7 +13,7 @@ from __future__ import annotations
 import numpy as np
 
 from .. import _lib
-from .encode import bcsc_encode
+from .encode import ENT_PAD, PTR_PAD, bcsc_encode, bcsc_segments
 from .tensorcore import bt_from_triplets, dense_right_tc
 from .testmatrix import TestMatrix, entry_sample
 
@@ -103,11 +103,18 @@ class _SignSparseTM(TestMatrix):
             _lib.check(min(r, 0), "chunk_rows")
             rows, cols, neg, mag = self._sign_form()
             ptr, ent = bcsc_encode(rows, cols, neg, self.d, self.k, r)
+            seg, cap = None, 0
+            if kind == "adjoint":
+                seg, cap = bcsc_segments(ptr, self.d, self.k, r)
+                ptr = np.concatenate([ptr, np.full(PTR_PAD, ptr[-1], np.int32)])
+                ent = np.concatenate([ent, np.zeros(ENT_PAD, np.uint16)])
             self._device_cache[key] = (
                 torch.from_numpy(ptr).to(device),
                 torch.from_numpy(ent.view(np.int16)).to(device),
                 int(r),
                 mag,
+                None if seg is None else torch.from_numpy(seg).to(device),
+                cap,
             )
         return self._device_cache[key]
 
@@ -146,7 +153,7 @@ class _SignSparseTM(TestMatrix):
             hi, lo, mag = self._tc_on(a.device)
             return dense_right_tc(a, hi, lo, self.k, mag)
         code = _lib.SK_F32 if a.dtype == torch.float32 else _lib.SK_F64
-        ptr, ent, r, mag = self._bcsc_on(a.device, "right", code)
+        ptr, ent, r, mag, _, _ = self._bcsc_on(a.device, "right", code)
         n = a.shape[0]
         y = torch.empty((n, self.k), dtype=a.dtype, device=a.device)
         if n == 0:
@@ -164,7 +171,7 @@ class _SignSparseTM(TestMatrix):
         if self._sign_form() is None or b.dtype not in (torch.float32, torch.float64):
             return super()._adjoint_device(b)
         code = _lib.SK_F32 if b.dtype == torch.float32 else _lib.SK_F64
-        ptr, ent, r, mag = self._bcsc_on(b.device, "adjoint", code)
+        ptr, ent, r, mag, seg, cap = self._bcsc_on(b.device, "adjoint", code)
         m = b.shape[1]
         out = torch.empty((self.k, m), dtype=b.dtype, device=b.device)
         if m == 0:
@@ -174,7 +181,8 @@ class _SignSparseTM(TestMatrix):
         ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=b.device)
         with torch.cuda.device(b.device):
             st = lib.sk_sparse_adjoint(code, b.data_ptr(), self.d, m, b.stride(0), ptr.data_ptr(), ent.data_ptr(), r,
-                                       self.k, mag, out.data_ptr(), out.stride(0), 0, ws.data_ptr(), ws_bytes,
+                                       seg.data_ptr() if seg is not None else None, cap, self.k, mag,
+                                       out.data_ptr(), out.stride(0), 0, ws.data_ptr(), ws_bytes,
                                        torch.cuda.current_stream().cuda_stream)
         _lib.check(st, "sk_sparse_adjoint")
         return out

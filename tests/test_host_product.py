@@ -161,3 +161,19 @@ def test_shape_errors_precede_device():
         tm.apply_right(np.ones((3, 9)))
     with pytest.raises(ValueError, match="apply_adjoint"):
         tm.apply_adjoint(np.ones((9, 2)))
+
+
+def test_bcsc_segments():
+    from paper_2508_21189_b200.sketch.encode import bcsc_segments
+
+    d, k, r = 3000, 2100, 512
+    tm = skb.SparseUniformTM(d, k, 8, seed=2)
+    rows, cols, neg, _ = tm._sign_form()
+    ptr, ent = bcsc_encode(rows, cols, neg, d, k, r)
+    seg, cap = bcsc_segments(ptr, d, k, r, group=1024)
+    seg = seg.reshape(-1, 3, 2)
+    for h in range(seg.shape[0]):
+        for g in range(3):
+            e0, cnt = seg[h, g]
+            lo, hi = ptr[h * k + g * 1024], ptr[h * k + min(k, (g + 1) * 1024)]
+            assert e0 % 8 == 0 and cnt % 8 == 0 and e0 <= lo and e0 + cnt >= hi and cnt <= cap
