@@ -51,6 +51,7 @@ class LsqrResult:
     arnorm: float
     acond: float
     sketch_seconds: float = 0.0
+    normal_eq_test: float = 0.0
 
 
 def _t64(x):
@@ -337,8 +338,10 @@ def sketch_precondition_lsqr(a, b, tm_psi, *, atol: float = 1e-6, btol: float = 
         if test2 <= atol:
             istop = 2
             break
-        if test1 <= btol + atol * anorm * float(torch.linalg.norm(x)) / bnorm:
+        # btol = 0 disables the consistent-system test: for inconsistent problems (config 4) only the
+        # normal-equation test ||(A R^-1)^T r|| <= atol ||A R^-1|| ||r|| may stop the iteration
+        if btol > 0 and test1 <= btol + atol * anorm * float(torch.linalg.norm(x)) / bnorm:
             istop = 1
             break
     acond = float(np.sqrt(anorm2) * np.sqrt(ddnorm))
-    return LsqrResult(_back(rinv(x), kind), istop, itn, float(r1norm), float(arnorm), acond, t_sketch)
+    return LsqrResult(_back(rinv(x), kind), istop, itn, float(r1norm), float(arnorm), acond, t_sketch, float(test2))

@@ -81,16 +81,21 @@ class _SignSparseTM(TestMatrix):
 
     # -- native path ------------------------------------------------------------------------------
     def _sign_form(self):
-        """(rows, cols, neg, magnitude) if every value is +-magnitude (real field), else None."""
-        if self.field != "real":
-            return None
-        rows, cols, vals = self._triplets()
-        if vals.size == 0:
-            return rows, cols, np.zeros(0, bool), 1.0
-        mag = float(np.abs(vals[0]))
-        if mag == 0.0 or not np.all(np.abs(vals) == mag):
-            return None
-        return rows, cols, vals < 0, mag
+        """(rows, cols, neg, magnitude) if every value is +-magnitude (real field), else None (cached)."""
+        cached = self.__dict__.get("_sign_cache", False)
+        if cached is not False:
+            return cached
+        res = None
+        if self.field == "real":
+            rows, cols, vals = self._triplets()
+            if vals.size == 0:
+                res = (rows, cols, np.zeros(0, bool), 1.0)
+            else:
+                mag = float(np.abs(vals[0]))
+                if mag != 0.0 and np.all(np.abs(vals) == mag):
+                    res = (rows, cols, vals < 0, mag)
+        self._sign_cache = res
+        return res
 
     def _bcsc_on(self, device, kind: str, dtype_code: int):
         key = ("bcsc", kind, device, dtype_code)
