@@ -13,15 +13,15 @@
 // finished chunk into fp32 register sums (round-to-nearest adds).  Result: ~3e-6 at any K.
 //
 // CTA = 512 threads (one per SM, persistent over (M-tile, N-block, K-split) work units):
-//   WG0  warp 0: TMA producer of B^T tiles (bf16, K-major, SWIZZLE_128B) | warp 1: MMA issuer
+//   WG0  warp 0: TMA producer of A (fp32) and B^T tiles (bf16, K-major, SWIZZLE_128B) | warp 1: MMA
 //        warp 2: TMEM allocator                                           (regs trimmed to 32)
-//   warp 3: TMA producer of fp32 A tiles into a staging ring (128 rows x 64 cols, 32 KB)
-//   WG1  warps 4..7 : A converters — LDS fp32 staging -> bf16 hi/lo -> STS in the UMMA K-major
+//   WG1  warps 4..7 : A converters — the fp32 A tile lands by TMA in the stage; converters read it,
+//        meet at a named barrier, and overwrite it in place with bf16 hi/lo in the UMMA K-major
 //        SW128 layout                                                                 (128 regs)
 //   WG2+WG3 warps 8..15 : reducers — tcgen05.ld of finished chunks, fp32 sums in registers
 //        (warp w: TMEM lane group w%4, column half (w-8)/4), final scale + store         (168 regs)
-// smem ring of `stages` x {A_hi 16 KB, A_lo 16 KB, B_hi BN*128 B (, B_lo)}; mbarriers full/empty per
-// stage and acc_full/acc_empty per TMEM accumulator.
+// smem ring of `stages` x {A 32 KB (fp32 -> bf16 hi/lo in place), B_hi BN*128 B (, B_lo)}; mbarriers
+// tma_full/full/empty per stage and acc_full/acc_empty per TMEM accumulator.
 #include <cuda.h>
 
 #include "common.cuh"
@@ -84,28 +84,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_dyn[];
   // keep the pointer derived from the __shared__ array (integer offset) so accesses stay LDS/STS
   uint8_t* smem = smem_dyn + ((1024u - (sm100::smem_u32(smem_dyn) & 1023u)) & 1023u);
+  // stage = { A: fp32 tile by TMA, converted in place to bf16 hi [0,16K) + lo [16K,32K) ; B^T tile(s) }
   const uint32_t a_bytes = BM * 128;
   const uint32_t b_bytes = (uint32_t)p.BN * 128;
-  const uint32_t stage_bytes = 2 * a_bytes + NB * b_bytes;
-  const int S = p.stages, SA = p.astages;
-  uint8_t* astage = smem + (size_t)S * stage_bytes;  // SA x 32 KB fp32 staging
-  uint64_t* full = reinterpret_cast<uint64_t*>(astage + (size_t)SA * kAStageBytes);
-  uint64_t* empty = full + S;
-  uint64_t* a_full = empty + S;
-  uint64_t* a_empty = a_full + SA;
-  uint64_t* acc_full = a_empty + SA;   // [2]
+  const uint32_t stage_bytes = kAStageBytes + NB * b_bytes;
+  const int S = p.stages;
+  uint64_t* tma_full = reinterpret_cast<uint64_t*>(smem + (size_t)S * stage_bytes);
+  uint64_t* full = tma_full + S;       // converted (count: 4 converter warps)
+  uint64_t* empty = full + S;          // consumed by the MMA (tcgen05.commit)
+  uint64_t* acc_full = empty + S;      // [2]
   uint64_t* acc_empty = acc_full + 2;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1 + 4);
+      mbar_init(&tma_full[s], 1);
+      mbar_init(&full[s], 4);
       mbar_init(&empty[s], 1);
-    }
-    for (int s2 = 0; s2 < SA; ++s2) {
-      mbar_init(&a_full[s2], 1);
-      mbar_init(&a_empty[s2], 4);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -126,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < 4) {
     setmaxnreg_dec<32>();
     if (warp == 0 && lane == 0) {
-      // ---------------------------------------------------------------- B producer (TMA)
+      // ---------------------------------------------------------------- producer (TMA: A fp32 + B^T bf16)
       int s = 0;
       uint32_t ph = 0;
       for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
@@ -135,24 +131,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + (size_t)s * stage_bytes;
-          mbar_arrive_expect_tx(&full[s], NB * b_bytes);
-          tma_load_2d(st + 2 * a_bytes, &tm_bhi, &full[s], kb * BK, w.nb * p.BN);
-          if (NB == 2) tma_load_2d(st + 2 * a_bytes + b_bytes, &tm_blo, &full[s], kb * BK, w.nb * p.BN);
+          mbar_arrive_expect_tx(&tma_full[s], kAStageBytes + NB * b_bytes);
+          tma_load_2d(st, &tm_a, &tma_full[s], kb * BK, w.mt * BM);
+          tma_load_2d(st + kAStageBytes, &tm_bhi, &tma_full[s], kb * BK, w.nb * p.BN);
+          if (NB == 2) tma_load_2d(st + kAStageBytes + b_bytes, &tm_blo, &tma_full[s], kb * BK, w.nb * p.BN);
           if (++s == S) { s = 0; ph ^= 1; }
-        }
-      }
-    } else if (warp == 3 && lane == 0) {
-      // ---------------------------------------------------------------- A producer (TMA, fp32)
-      int s = 0;
-      uint32_t ph = 0;
-      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
-        const Unit w = unit_of(p, u);
-        const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&a_empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&a_full[s], kAStageBytes);
-          tma_load_2d(astage + (size_t)s * kAStageBytes, &tm_a, &a_full[s], kb * BK, w.mt * BM);
-          if (++s == SA) { s = 0; ph ^= 1; }
         }
       }
     } else if (warp == 1 && lane == 0) {
@@ -174,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&full[s], ph);
             tc_fence_after();
             const uint32_t st = smem_u32(smem + (size_t)s * stage_bytes);
-            const uint32_t a_hi = st, a_lo = st + a_bytes, b_hi = st + 2 * a_bytes, b_lo = b_hi + b_bytes;
+            const uint32_t a_hi = st, a_lo = st + a_bytes, b_hi = st + kAStageBytes, b_lo = b_hi + b_bytes;
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
               const uint64_t dah = sdesc_kmajor_sw128(a_hi + kk * 32);
@@ -197,22 +180,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ct = threadIdx.x - 128;      // 0..127
     const int c4 = ct & 15;                // float4 column within the 64-wide K block
     const int rsub = ct >> 4;              // 0..7
-    int s = 0, sa = 0;
-    uint32_t ph = 0, pha = 0;
+    int s = 0;
+    uint32_t ph = 0;
     for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
       const Unit w = unit_of(p, u);
       const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
       for (int kb = kb0; kb < kb1; ++kb) {
         float4 cur[16];
-        mbar_wait(&a_full[sa], pha);
-        const uint32_t at = smem_u32(astage + (size_t)sa * kAStageBytes) + (rsub * BK + c4 * 4) * 4;
+        mbar_wait(&tma_full[s], ph);
+        const uint32_t st = smem_u32(smem + (size_t)s * stage_bytes);
+        const uint32_t at = st + (rsub * BK + c4 * 4) * 4;
 #pragma unroll
         for (int i = 0; i < 16; ++i) cur[i] = lds128(at + i * 8 * BK * 4);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&a_empty[sa]);
-        if (++sa == SA) { sa = 0; pha ^= 1; }
-        mbar_wait(&empty[s], ph ^ 1);
-        const uint32_t st = smem_u32(smem + (size_t)s * stage_bytes);
+        // every converter thread has read its fp32 values before any bf16 write lands in place
+        asm volatile("bar.sync 1, 128;" ::: "memory");
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int r = rsub + 8 * i;
@@ -376,19 +357,13 @@ Plan make_plan(int64_t n, int64_t d, int64_t k, int NB) {
   pl.kb_per_split = (pl.kb_per_split + CHUNK_KB - 1) / CHUNK_KB * CHUNK_KB;
   pl.ksplit = (nk + pl.kb_per_split - 1) / pl.kb_per_split;
   pl.units = tiles * pl.ksplit;
-  const size_t stage_bytes = 2 * (size_t)BM * 128 + (size_t)NB * pl.BN * 128;
+  const size_t stage_bytes = kAStageBytes + (size_t)NB * pl.BN * 128;
   const size_t budget = 227 * 1024 - 1024 - 512;
-  // at least 2 bf16 stages, the rest split between fp32 staging (>= 2) and more bf16 stages
-  int stages = 2, astages = (int)((budget - 2 * stage_bytes) / kAStageBytes);
-  if (astages > 4) {
-    const int extra = (int)((budget - 2 * stage_bytes - 4 * kAStageBytes) / stage_bytes);
-    stages += extra > 0 ? extra : 0;
-    astages = (int)((budget - stages * stage_bytes) / kAStageBytes);
-    if (astages > 6) astages = 6;
-  }
+  int stages = (int)(budget / stage_bytes);
+  if (stages > 6) stages = 6;
   pl.stages = stages;
-  pl.astages = astages;
-  pl.smem = 1024 + stages * stage_bytes + astages * kAStageBytes + (2 * stages + 2 * astages + 4) * 8 + 16;
+  pl.astages = 0;
+  pl.smem = 1024 + stages * stage_bytes + (3 * stages + 4) * 8 + 16;
   pl.ws_bytes = pl.ksplit > 1 ? (size_t)pl.ksplit * n * k * sizeof(float) : 0;
   return pl;
 }
@@ -417,7 +392,7 @@ extern "C" int sk_dense_right_tc(const float* A, int64_t n, int64_t d, int64_t l
     return fail(SK_EINVAL, "sk_dense_right_tc: B^T must be 16-byte aligned with ldb a multiple of 8");
   const int NB = Bt_lo ? 2 : 1;
   const Plan pl = make_plan(n, d, k, NB);
-  if (pl.stages < 2 || pl.astages < 2) return fail(SK_EUNSUPPORTED, "sk_dense_right_tc: tile does not fit shared memory");
+  if (pl.stages < 2) return fail(SK_EUNSUPPORTED, "sk_dense_right_tc: tile does not fit shared memory");
   if (pl.ksplit > 1 && (ws == nullptr || ws_bytes < pl.ws_bytes))
     return fail(SK_EINVAL, "sk_dense_right_tc: workspace too small (sk_dense_tc_workspace_bytes)");
   CUtensorMap ma, mh, ml;
