@@ -21,6 +21,7 @@ from abc import ABC, abstractmethod
 
 import numpy as np
 
+from .. import _device
 from .._device import from_result, to_operand
 from ..rng import RngStream
 
@@ -111,6 +112,13 @@ class TestMatrix(ABC):
         if len(shape) != 2:
             raise ValueError(f"apply_right needs a 2-d A, got shape {shape}")
         self._check_right(_Shaped(shape))
+        host, kind = _device.host_tensor_of(a) if not hasattr(a, "toarray") else (None, None)
+        if host is not None and not host.is_complex() and \
+                host.numel() * host.element_size() >= _device.PIPELINE_MIN_BYTES:
+            y = _device.pipelined_right(self._right_device, host, self.k)
+            if kind == "numpy":
+                return y.numpy().astype(np.complex128 if y.is_complex() else np.float64, copy=False)
+            return y
         op = to_operand(a, allow_vector=False)
         return from_result(self._right_device(op.tensor), op)
 

@@ -148,3 +148,21 @@ def test_config2_rows_vs_oracle(cuda):
     y = tm.apply_right(a).cpu().numpy()
     dv, samp = orc.srtt_parts(8192, 512, 1, 0)
     assert rel_err(y, orc.srtt_right(dv, samp, a.cpu().numpy(), "wht")) <= 1e-5
+
+
+def test_pipelined_host_path_matches_device(cuda):
+    """Host operands >= 256 MB stream through the device in chunks (H2D / kernel / D2H overlap)."""
+    import torch
+
+    tm = skb.SparseRttTM(8192, 512, 1, "wht", seed=0)
+    g = torch.Generator().manual_seed(0)
+    a_host = torch.randn(9000, 8192, generator=g)  # 295 MB, not a multiple of the chunk
+    ref = tm.apply_right(a_host.to(cuda)).cpu()
+    y_pageable = tm.apply_right(a_host)
+    assert y_pageable.dtype == torch.float32 and not y_pageable.is_cuda
+    assert torch.equal(y_pageable, ref)
+    y_pinned = tm.apply_right(a_host.pin_memory())
+    assert torch.equal(y_pinned, ref)
+    y_np = tm.apply_right(a_host.numpy())
+    assert isinstance(y_np, np.ndarray) and y_np.dtype == np.float64
+    assert np.array_equal(y_np, ref.double().numpy())
