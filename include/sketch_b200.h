@@ -68,11 +68,13 @@ SK_API int sk_device_sm_count(int device);
  * K1 — Y[n,k] = scale * A[n,d] * Omega[d,k] for a bcsc-encoded sparse Omega.
  * Replaces `_SparseTM.apply_right` = `a @ self.matrix` (src/sketch/sparse.py:63-66), executed by
  * scipy sparsetools csc_matvecs.  `chunk_rows` must equal sk_sparse_right_chunk_rows(dtype, d, k).
+ * `nnz` = number of entries (ptr[last]); when the encoding is small the kernel stages it in
+ * shared memory (pass 0 if unknown).
  */
 SK_API int sk_sparse_right_chunk_rows(int dtype, int64_t d, int64_t k);
 SK_API int sk_sparse_right(int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
-                    const int32_t* ptr, const uint16_t* ent, int32_t chunk_rows, int64_t k,
-                    double scale, void* Y, int64_t ldy, void* stream);
+                           const int32_t* ptr, const uint16_t* ent, int32_t chunk_rows, int64_t nnz,
+                           int64_t k, double scale, void* Y, int64_t ldy, void* stream);
 
 /*
  * K2 — SA[k,m] = scale * Omega[d,k]^T * A[d,m] (accumulate != 0: SA += ...).

@@ -98,7 +98,7 @@ def from_result(y: "torch.Tensor", op: Operand):
 
 
 PIPELINE_MIN_BYTES = 256 << 20  # host operands at least this large stream through the device in chunks
-PIPELINE_CHUNK_BYTES = 64 << 20
+PIPELINE_CHUNK_BYTES = 128 << 20
 
 
 def host_tensor_of(x):

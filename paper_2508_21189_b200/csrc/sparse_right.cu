@@ -58,11 +58,12 @@ __device__ __forceinline__ double2 xor_perm(double2 v, int key) {
   return v;
 }
 
-template <typename T, int W, int CPW, int R, bool VEC>
+template <typename T, int W, int CPW, int R, bool VEC, bool OMS>
 __global__ void __launch_bounds__(W * 32, 1)
     sparse_right_kernel(const T* __restrict__ A, int64_t n, int64_t d, int64_t lda,
                         const int32_t* __restrict__ ptr, const uint16_t* __restrict__ ent,
-                        int64_t k, int nchunks, T scale, T* __restrict__ Y, int64_t ldy) {
+                        int64_t k, int nchunks, int nnz, uint32_t omega_off, T scale, T* __restrict__ Y,
+                        int64_t ldy) {
   using V4 = typename VecOf<T>::type;
   constexpr int NV = VecOf<T>::n;               // elements per 16 B vector
   constexpr int NT = W * 32;                    // threads
@@ -129,6 +130,18 @@ __global__ void __launch_bounds__(W * 32, 1)
 #pragma unroll
   for (int j = 0; j < CPW; ++j) acc[j] = T(0);
 
+  // OMS: the whole bcsc encoding of Omega sits in shared memory (small Omega, e.g. config 1:
+  // 48 KB); entry and pointer reads are then uniform shared loads (broadcast, no L1 traffic).
+  const int nptr = nchunks * (int)k + 1;
+  int32_t* ptr_s = reinterpret_cast<int32_t*>(smem_raw + omega_off);
+  uint16_t* ent_s = reinterpret_cast<uint16_t*>(ptr_s + ((nptr + 3) & ~3));
+  if constexpr (OMS) {
+    for (int i = tid; i < nptr; i += NT) ptr_s[i] = __ldg(ptr + i);
+    for (int i = tid; i < nnz; i += NT) ent_s[i] = __ldg(ent + i);
+  }
+  auto P = [&](int64_t i) -> int { return OMS ? ptr_s[i] : __ldg(ptr + i); };
+  auto E = [&](int i) -> uint32_t { return OMS ? (uint32_t)ent_s[i] : (uint32_t)__ldg(ent + i); };
+
   const T* my_row = As + lane * R;
   load_chunk(0);
   for (int h = 0; h < nchunks; ++h) {
@@ -137,39 +150,26 @@ __global__ void __launch_bounds__(W * 32, 1)
     __syncthreads();
     if (h + 1 < nchunks) load_chunk(h + 1);
 
-    int my_lo = 0, my_hi = 0;
-    if (lane < CPW) {
-      const int64_t c = cb0 + warp + (int64_t)W * lane;
-      if (c < k) {
-        my_lo = __ldg(ptr + (int64_t)h * k + c);
-        my_hi = __ldg(ptr + (int64_t)h * k + c + 1);
-      }
-    }
 #pragma unroll
     for (int j = 0; j < CPW; ++j) {
-      const int lo = __shfl_sync(0xffffffffu, my_lo, j);
-      const int hi = __shfl_sync(0xffffffffu, my_hi, j);
-      T s0 = T(0), s1 = T(0), s2 = T(0), s3 = T(0);
-      for (int base = lo; base < hi; base += 32) {
-        const int cnt = min(32, hi - base);
-        const uint32_t my_e = (lane < cnt) ? (uint32_t)__ldg(ent + base + lane) : 0u;
-        int t = 0;
-        for (; t + 4 <= cnt; t += 4) {
-          const uint32_t e0 = __shfl_sync(0xffffffffu, my_e, t);
-          const uint32_t e1 = __shfl_sync(0xffffffffu, my_e, t + 1);
-          const uint32_t e2 = __shfl_sync(0xffffffffu, my_e, t + 2);
-          const uint32_t e3 = __shfl_sync(0xffffffffu, my_e, t + 3);
-          s0 += flip_if(my_row[(e0 >> 1) ^ lane], e0 & 1u);
-          s1 += flip_if(my_row[(e1 >> 1) ^ lane], e1 & 1u);
-          s2 += flip_if(my_row[(e2 >> 1) ^ lane], e2 & 1u);
-          s3 += flip_if(my_row[(e3 >> 1) ^ lane], e3 & 1u);
-        }
-        for (; t < cnt; ++t) {
-          const uint32_t e0 = __shfl_sync(0xffffffffu, my_e, t);
-          s0 += flip_if(my_row[(e0 >> 1) ^ lane], e0 & 1u);
-        }
+      const int64_t c = cb0 + warp + (int64_t)W * j;
+      int lo = 0, hi = 0;
+      if (c < k) {
+        lo = P((int64_t)h * k + c);
+        hi = P((int64_t)h * k + c + 1);
       }
-      acc[j] += (s0 + s1) + (s2 + s3);
+      T s0 = T(0), s1 = T(0);
+      int e = lo;
+      for (; e + 2 <= hi; e += 2) {
+        const uint32_t e0 = E(e), e1 = E(e + 1);
+        s0 += flip_if(my_row[(e0 >> 1) ^ lane], e0 & 1u);
+        s1 += flip_if(my_row[(e1 >> 1) ^ lane], e1 & 1u);
+      }
+      if (e < hi) {
+        const uint32_t e0 = E(e);
+        s0 += flip_if(my_row[(e0 >> 1) ^ lane], e0 & 1u);
+      }
+      acc[j] += s0 + s1;
     }
   }
 
@@ -196,34 +196,49 @@ constexpr int chunk_rows_for() {
 
 template <typename T, int CPW, bool VEC>
 int launch_t(const T* A, int64_t n, int64_t d, int64_t lda, const int32_t* ptr, const uint16_t* ent,
-             int64_t k, double scale, T* Y, int64_t ldy, cudaStream_t s) {
+             int64_t nnz, int64_t k, double scale, T* Y, int64_t ldy, cudaStream_t s) {
   constexpr int R = chunk_rows_for<T>();
   constexpr int CB = kWarps * CPW;
   const int nchunks = (int)((d + R - 1) / R);
   const size_t tile_bytes = (size_t)kRowsPerTile * R * sizeof(T);
   const size_t ys_bytes = (size_t)kRowsPerTile * (CB + 1) * sizeof(T);
-  const size_t smem = tile_bytes > ys_bytes ? tile_bytes : ys_bytes;
-  auto kern = sparse_right_kernel<T, kWarps, CPW, R, VEC>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t base = ((tile_bytes > ys_bytes ? tile_bytes : ys_bytes) + 15) & ~(size_t)15;
+  // the whole encoding of a small Omega is staged in shared memory (nnz supplied by the caller)
+  const int64_t nptr = (int64_t)nchunks * k + 1;
+  const size_t ptr_bytes = (size_t)((nptr + 3) & ~3) * 4;
+  const size_t oms_bytes = nnz > 0 ? ptr_bytes + (size_t)nnz * 2 : (size_t)1 << 30;
   dim3 grid((unsigned)((n + kRowsPerTile - 1) / kRowsPerTile), (unsigned)((k + CB - 1) / CB));
-  kern<<<grid, kWarps * 32, smem, s>>>(A, n, d, lda, ptr, ent, k, nchunks, (T)scale, Y, ldy);
+  if (base + oms_bytes <= 200 * 1024) {
+    const size_t smem = base + oms_bytes;
+    auto kern = sparse_right_kernel<T, kWarps, CPW, R, VEC, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, kWarps * 32, smem, s>>>(A, n, d, lda, ptr, ent, k, nchunks, (int)nnz, (uint32_t)base, (T)scale, Y,
+                                         ldy);
+  } else {
+    auto kern = sparse_right_kernel<T, kWarps, CPW, R, VEC, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)base);
+    kern<<<grid, kWarps * 32, base, s>>>(A, n, d, lda, ptr, ent, k, nchunks, 0, (uint32_t)base, (T)scale, Y, ldy);
+  }
   return check_launch("sk_sparse_right");
 }
 
 template <typename T>
 int dispatch(const void* A_, int64_t n, int64_t d, int64_t lda, const int32_t* ptr, const uint16_t* ent,
-             int64_t k, double scale, void* Y_, int64_t ldy, cudaStream_t s) {
+             int64_t nnz, int64_t k, double scale, void* Y_, int64_t ldy, cudaStream_t s) {
   const T* A = static_cast<const T*>(A_);
   T* Y = static_cast<T*>(Y_);
   constexpr int NV = 16 / sizeof(T);
   const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % NV == 0) && (d % NV == 0);
-  const int64_t need = (k + kWarps - 1) / kWarps;
-  if (need <= 4) return vec ? launch_t<T, 4, true>(A, n, d, lda, ptr, ent, k, scale, Y, ldy, s)
-                            : launch_t<T, 4, false>(A, n, d, lda, ptr, ent, k, scale, Y, ldy, s);
-  if (need <= 8) return vec ? launch_t<T, 8, true>(A, n, d, lda, ptr, ent, k, scale, Y, ldy, s)
-                            : launch_t<T, 8, false>(A, n, d, lda, ptr, ent, k, scale, Y, ldy, s);
-  return vec ? launch_t<T, 16, true>(A, n, d, lda, ptr, ent, k, scale, Y, ldy, s)
-             : launch_t<T, 16, false>(A, n, d, lda, ptr, ent, k, scale, Y, ldy, s);
+  int64_t need = (k + kWarps - 1) / kWarps;
+  // split the output columns over more CTAs when there are few row tiles (wave balance)
+  const int64_t tiles = (n + kRowsPerTile - 1) / kRowsPerTile;
+  if (tiles < 8 * (int64_t)sm_count() && need > 8) need = 8;
+  if (need <= 4) return vec ? launch_t<T, 4, true>(A, n, d, lda, ptr, ent, nnz, k, scale, Y, ldy, s)
+                            : launch_t<T, 4, false>(A, n, d, lda, ptr, ent, nnz, k, scale, Y, ldy, s);
+  if (need <= 8) return vec ? launch_t<T, 8, true>(A, n, d, lda, ptr, ent, nnz, k, scale, Y, ldy, s)
+                            : launch_t<T, 8, false>(A, n, d, lda, ptr, ent, nnz, k, scale, Y, ldy, s);
+  return vec ? launch_t<T, 16, true>(A, n, d, lda, ptr, ent, nnz, k, scale, Y, ldy, s)
+             : launch_t<T, 16, false>(A, n, d, lda, ptr, ent, nnz, k, scale, Y, ldy, s);
 }
 
 }  // namespace
@@ -238,8 +253,8 @@ extern "C" int sk_sparse_right_chunk_rows(int dtype, int64_t d, int64_t k) {
 }
 
 extern "C" int sk_sparse_right(int dtype, const void* A, int64_t n, int64_t d, int64_t lda,
-                               const int32_t* ptr, const uint16_t* ent, int32_t chunk_rows, int64_t k,
-                               double scale, void* Y, int64_t ldy, void* stream) {
+                               const int32_t* ptr, const uint16_t* ent, int32_t chunk_rows, int64_t nnz,
+                               int64_t k, double scale, void* Y, int64_t ldy, void* stream) {
   using namespace skb;
   if (n < 0 || d < 1 || k < 1 || lda < d || ldy < k) return fail(SK_EINVAL, "sk_sparse_right: bad shape/leading dimension");
   if (n > 0 && (!A || !Y || !ptr)) return fail(SK_EINVAL, "sk_sparse_right: null pointer");
@@ -248,6 +263,6 @@ extern "C" int sk_sparse_right(int dtype, const void* A, int64_t n, int64_t d, i
     return fail(SK_EINVAL, "sk_sparse_right: chunk_rows does not match sk_sparse_right_chunk_rows");
   if (n == 0) return SK_OK;
   cudaStream_t s = as_stream(stream);
-  return dtype == SK_F32 ? dispatch<float>(A, n, d, lda, ptr, ent, k, scale, Y, ldy, s)
-                         : dispatch<double>(A, n, d, lda, ptr, ent, k, scale, Y, ldy, s);
+  return dtype == SK_F32 ? dispatch<float>(A, n, d, lda, ptr, ent, nnz, k, scale, Y, ldy, s)
+                         : dispatch<double>(A, n, d, lda, ptr, ent, nnz, k, scale, Y, ldy, s);
 }

@@ -166,7 +166,8 @@ class _SignSparseTM(TestMatrix):
         lib = _lib.load()
         with torch.cuda.device(a.device):
             st = lib.sk_sparse_right(code, a.data_ptr(), n, self.d, a.stride(0), ptr.data_ptr(), ent.data_ptr(), r,
-                                     self.k, mag, y.data_ptr(), y.stride(0), torch.cuda.current_stream().cuda_stream)
+                                     ent.numel(), self.k, mag, y.data_ptr(), y.stride(0),
+                                     torch.cuda.current_stream().cuda_stream)
         _lib.check(st, "sk_sparse_right")
         return y
 

@@ -37,7 +37,7 @@ def test_error_path_without_device():
 
     lib = _lib.load()
     # invalid shape is rejected before any CUDA call
-    st = lib.sk_sparse_right(0, None, 4, 0, 0, None, None, 512, 4, 1.0, None, 4, None)
+    st = lib.sk_sparse_right(0, None, 4, 0, 0, None, None, 512, 0, 4, 1.0, None, 4, None)
     assert st == _lib.SK_EINVAL
     assert b"sk_sparse_right" in lib.sk_last_error()
     assert lib.sk_sparse_right_chunk_rows(0, 100, 10) == 512
