@@ -18,9 +18,13 @@
 // the reference (`top = y0 + y1`, `bot = y0 - y1`).
 //
 // Other sizes (d = 2^L, row fits shared memory): one CTA per row, row in shared memory.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace skb {
+int launch_srtt_tc(const float* A, int64_t n, int64_t lda, const float* dv, const int32_t* samp, int xi, int k,
+                   double scale, float* Y, int64_t ldy, cudaStream_t s);
 namespace {
 
 __device__ __forceinline__ int swz(int j) { return j ^ ((j >> 5) & 3) ^ (((j >> 7) & 7) << 2); }
@@ -468,6 +472,12 @@ int dispatch_L(int L, const T* A, int64_t n, int64_t lda, const T* dv, const int
   }
 }
 
+// SKETCH_B200_SRTT=regs forces the CUDA-core kernel (A/B comparisons); default: tensor cores at d = 8192
+bool srtt_tc_enabled() {
+  const char* e = getenv("SKETCH_B200_SRTT");
+  return !(e && e[0] == 'r');
+}
+
 template <typename T>
 int run(const void* A_, int64_t n, int64_t d, int64_t lda, const void* dv_, bool pm1, const int32_t* samp,
         int xi, int64_t k, double scale, void* Y_, int64_t ldy, cudaStream_t s) {
@@ -483,6 +493,7 @@ int run(const void* A_, int64_t n, int64_t d, int64_t lda, const void* dv_, bool
       const float* Af = reinterpret_cast<const float*>(A);
       const float* dvf = reinterpret_cast<const float*>(dv);
       float* Yf = reinterpret_cast<float*>(Y);
+      if (L == 13 && srtt_tc_enabled()) return launch_srtt_tc(Af, n, lda, dvf, samp, xi, (int)k, scale, Yf, ldy, s);
       if (L == 12) return launch_wide<12>(Af, n, lda, dvf, samp, xi, (int)k, scale, Yf, ldy, s);
       if (L == 13) return launch_wide<13>(Af, n, lda, dvf, samp, xi, (int)k, scale, Yf, ldy, s);
       return launch_wide<14>(Af, n, lda, dvf, samp, xi, (int)k, scale, Yf, ldy, s);
