@@ -43,7 +43,7 @@ def _cfg2(torch, dev, rank):
     g = torch.Generator(device=dev).manual_seed(1000 + rank)
     a = torch.randn(n, d, dtype=torch.float32, device=dev, generator=g)
     a /= torch.arange(1, d + 1, dtype=torch.float32, device=dev)  # sigma_j = 1/j
-    return dict(name="cfg2", tm=tm, a=a, n=n, d=d, k=k, launches=1, kernel="srtt_wht_fast",
+    return dict(name="cfg2", tm=tm, a=a, n=n, d=d, k=k, launches=1, kernel="srtt_wht_tc",
                 workload="cfg2 SRTT sketch Y=A*D*H*S: A 65536x8192 f32 (sigma_j=1/j), WHT d=8192, k=512, xi=1",
                 op="right")
 
@@ -359,6 +359,7 @@ def main(argv=None):
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
     ap.add_argument("--config", choices=sorted(WORKLOADS), default="cfg2")
     ap.add_argument("--others", default="cfg1,cfg3,cfg4,cfg5", help="extra configs measured at N=1 ('' = none)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (quick kernel experiments)")
     args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference(args)
@@ -375,7 +376,7 @@ def main(argv=None):
     launches = w["launches"]
 
     cpu = None
-    if world == 1 and rank == 0:
+    if world == 1 and rank == 0 and not args.no_cpu:
         rows = SAMPLE_ROWS[args.config]
         a_host = w["a"][:rows].cpu().numpy()
         procs = os.cpu_count() or 1

@@ -3,7 +3,7 @@
 // H_8192 = H_64 (x) H_128 in natural order: for a row x (index j = 128 a + b) viewed as X[a][b]
 // (64 x 128, row-major = the row as stored),
 //     Y = H_64 * X * H_128,   i.e.  Z^T = H_128 * X^T  (tensor cores),  Y^T = Z^T * H_64 (registers).
-// Per row of A (one 32 KB slot of a 6-deep ring, one CTA per SM):
+// Per row of A (one 32 KB slot of a 5-deep ring, one 512-thread CTA per SM):
 //   producer  : one 32 KB bulk copy (cp.async.bulk) of the row into its slot
 //   converters: (4 warps) sign flip by D, split fp32 -> bf16 hi + lo (exact +-1 H keeps BF16x2 at
 //               ~3e-6), each row written in place as its own K-major SWIZZLE_128B B operand
@@ -11,10 +11,16 @@
 //   MMA       : (1 thread) per row 16 x tcgen05.mma M=128 (b') N=64 (a) K=16 against the
 //               constant H_128 tile (A operand, built once in tensor memory: the tensor cores
 //               then read only the 32 KB of converted data per row from shared memory)
-//   epilogue  : (4 warps, thread = TMEM lane = b') tcgen05.ld 64 columns (a) per row, 64-point
-//               WHT over a in registers (6 FADD2 stages), scatter Y[a'][b'] to a row buffer,
-//               then the sampled gather out[c] = scale * sign * Y[row_c] with coalesced stores.
-// TMEM: four 64-column accumulators (epilogue of row i overlaps the MMAs of rows i+1..i+3).
+//   epilogue  : (2 warpgroups taking alternate rows, thread = TMEM lane = b') tcgen05.ld 64
+//               columns (a) per row, 64-point WHT over a in registers (6 FADD2 stages), scatter
+//               Y[a'][b'] to the warpgroup's row buffer, then the sampled gather
+//               out[c] = scale * sign * Y[row_c] with coalesced stores.
+// TMEM: H_128 (64 columns) + four 64-column accumulators.
+// Bound: shared-memory bandwidth. Per row the SM moves ~1340 shared wavefronts (TMA write 256,
+// converter read 256 + write 256, tensor-core read 256, Y row 256 + gather) against a ~1450-cycle
+// HBM budget; measured variants: converters reading global memory directly
+// (the L1 data path is the same SRAM), a 4-D TMA that lands rows pre-swizzled (no converter CTA
+// barrier), a 6-slot ring with half-row Y buffers — all slower than this layout.
 // Replaces SparseRttTM.apply_right (src/sketch/rtt.py:129-140) + wht (rtt.py:28-44) for d = 8192.
 #include <cuda.h>
 
@@ -28,11 +34,11 @@ using namespace sm100;
 
 constexpr int TC_D = 8192;
 constexpr int TC_ROW_BYTES = TC_D * 4;        // 32 KB
-constexpr int TC_SLOTS = 6;                   // row ring: 6 x 32 KB in flight per SM
+constexpr int TC_SLOTS = 5;                   // row ring: 5 x 32 KB in flight per SM
 constexpr int TC_ACC = 4;                     // TMEM accumulators of 64 columns (after H's 64)
 constexpr int TC_TMEM_COLS = 512;             // H_128 (64) + 4 x 64 accumulators, power of two
 constexpr int TC_SAMP_REGS = 8;               // sampler entries per epilogue thread kept in registers
-constexpr int TC_THREADS = 384;               // WG0: producer/MMA/alloc | WG1 converters | WG2 epilogue
+constexpr int TC_THREADS = 512;               // WG0: producer/MMA/alloc | WG1 converters | WG2,3 epilogue
 
 typedef unsigned long long u64;
 
@@ -99,8 +105,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
   uint8_t* rbuf = smem;                                               // TC_SLOTS row slots x 32 KB
-  float* ybuf = reinterpret_cast<float*>(rbuf + TC_SLOTS * TC_ROW_BYTES);  // one row of Y, 32 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(ybuf) + TC_ROW_BYTES);
+  float* ybufs = reinterpret_cast<float*>(rbuf + TC_SLOTS * TC_ROW_BYTES);  // one Y row per epilogue WG
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(ybufs) + 2 * TC_ROW_BYTES);
   uint64_t* r_tma = bars;                        // [TC_SLOTS] row landed
   uint64_t* r_conv = bars + TC_SLOTS;            // [TC_SLOTS] converted (4 converter warps)
   uint64_t* r_empty = bars + 2 * TC_SLOTS;       // [TC_SLOTS] consumed by the MMA
@@ -127,7 +133,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (warp >= 8) {
+  if (warp >= 8 && warp < 12) {
     // constant H_128 (A operand) into TMEM columns [0, 64): lane b', column c = bf16 pair
     // (H[b'][2c], H[b'][2c+1]) with H[b'][b] = (-1)^popcount(b' & b)
     const int bp = 32 * (warp & 3) + lane;
@@ -190,7 +196,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   } else if (warp < 8) {
-    maxnreg_inc<184>();
+    maxnreg_inc<152>();
     // ------------------------------------------------------------ converters (128 threads)
     // Each row is converted in place into [hi K0 | hi K1 | lo K0 | lo K1], each an 8 KB K-major
     // SWIZZLE_128B tile of 64 rows a x 64 columns b. Thread ct owns 16 groups of 4 floats
@@ -234,11 +240,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (++s == TC_SLOTS) { s = 0; ph ^= 1; }
     }
   } else {
-    maxnreg_inc<184>();
-    // ------------------------------------------------------------ epilogue (thread = TMEM lane b')
+    maxnreg_inc<152>();
+    // ------------------------------------------------------------ epilogue: two warpgroups take
+    // alternate rows (accumulators buf = i % TC_ACC, i = local row index), each with its own Y row
+    const int ew = (warp >> 2) - 2;  // 0 or 1
     const int lg = warp & 3;
-    const int bp = 32 * lg + lane;  // b'
-    const int et = tid - 256;       // 0..127
+    const int bp = 32 * lg + lane;  // b' = TMEM lane
+    const int et = tid & 127;
+    float* ybuf = ybufs + ew * (TC_ROW_BYTES / 4);
     const bool fast = (xi == 1 && k <= 128 * TC_SAMP_REGS);
     uint32_t se[TC_SAMP_REGS];      // sampler entries c = et + 128 j (xi = 1)
 #pragma unroll
@@ -246,9 +255,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int c = et + 128 * j;
       se[j] = (fast && c < k) ? (uint32_t)__ldg(samp + c) : 0u;
     }
-    int buf = 0;
+    int buf = ew;
     uint32_t tph = 0;
-    for (int64_t row = blockIdx.x; row < n; row += gridDim.x) {
+    for (int64_t row = blockIdx.x + ew * (int64_t)gridDim.x; row < n; row += 2 * (int64_t)gridDim.x) {
       mbar_wait(&t_full[buf], tph);
       tc_fence_after();
       uint32_t z[64];
@@ -257,7 +266,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&t_empty[buf]);
-      if (++buf == TC_ACC) { buf = 0; tph ^= 1; }
+      buf += 2;
+      if (buf >= TC_ACC) { buf -= TC_ACC; tph ^= 1; }
       // 64-point WHT over a (register index): a-bit 0 inside pairs, a-bits 1..5 on packed pairs
       u64 p[32];
 #pragma unroll
@@ -278,7 +288,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         }
       }
-      asm volatile("bar.sync 2, 128;" ::: "memory");  // previous row's gather finished with ybuf
+      asm volatile("bar.sync %0, 128;" ::"r"(2 + ew) : "memory");  // previous gather done with ybuf
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         float lo, hi;
@@ -286,7 +296,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         ybuf[(2 * i) * 128 + bp] = lo;
         ybuf[(2 * i + 1) * 128 + bp] = hi;
       }
-      asm volatile("bar.sync 2, 128;" ::: "memory");
+      asm volatile("bar.sync %0, 128;" ::"r"(2 + ew) : "memory");
       float* y = Y + row * ldy;
       if (fast) {
 #pragma unroll
@@ -314,14 +324,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 }
 
+
 }  // namespace
 
 // Launcher used by sk_srtt_right (srtt.cu) for float32, d = 8192, +-1 diagonal.
 int launch_srtt_tc(const float* A, int64_t n, int64_t lda, const float* dv, const int32_t* samp, int xi, int k,
                    double scale, float* Y, int64_t ldy, cudaStream_t s) {
-  const size_t smem = 1024 + TC_SLOTS * TC_ROW_BYTES + TC_ROW_BYTES + 256;
-  cudaFuncSetAttribute(srtt_wht_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = (int)(n < sm_count() ? n : sm_count());
+  const size_t smem = 1024 + TC_SLOTS * TC_ROW_BYTES + 2 * TC_ROW_BYTES + 256;
+  cudaFuncSetAttribute(srtt_wht_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   srtt_wht_tc<<<grid, TC_THREADS, smem, s>>>(A, n, lda, dv, samp, xi, k, (float)scale, Y, ldy);
   return check_launch("sk_srtt_right(tc)");
 }
