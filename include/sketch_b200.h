@@ -95,6 +95,24 @@ SK_API int sk_sparse_adjoint(int dtype, const void* A, int64_t d, int64_t m, int
                              int64_t ldsa, int accumulate, void* ws, size_t ws_bytes, void* stream);
 
 /*
+ * K2w — float32 SA[k,m] = scale * Omega^T * A with register accumulators (BASELINE config 4).
+ * Same result contract as sk_sparse_adjoint (deterministic float64 reduction of row pieces).
+ * Omega is given as its nonzero pattern (rows, cols, neg flags; any number per row, magnitude in
+ * `scale`) and encoded once on the host by sk_sparse_adjoint_wide_encode into `enc` (uint16) with
+ * segment offsets `seg_off` (sk_sparse_adjoint_wide_segments(d, k) int64) and capacity `seg_cap`;
+ * call it first with enc = NULL to get the required length. A must be 16-byte aligned, lda % 4 == 0.
+ * Replaces `_SparseTM.apply_adjoint` (src/sketch/sparse.py:68-78).
+ */
+SK_API int64_t sk_sparse_adjoint_wide_encode(int64_t d, int64_t k, int64_t nnz, const int64_t* rows,
+                                             const int64_t* cols, const uint8_t* neg, uint16_t* enc,
+                                             int64_t enc_cap, int64_t* seg_off, int32_t* seg_cap);
+SK_API int64_t sk_sparse_adjoint_wide_segments(int64_t d, int64_t k);
+SK_API size_t sk_sparse_adjoint_wide_workspace_bytes(int64_t d, int64_t m, int64_t k);
+SK_API int sk_sparse_adjoint_wide(const float* A, int64_t d, int64_t m, int64_t lda, const uint16_t* enc,
+                                  const int64_t* seg_off, int32_t seg_cap, int64_t k, double scale, float* SA,
+                                  int64_t ldsa, int accumulate, void* ws, size_t ws_bytes, void* stream);
+
+/*
  * K3 — Y[n,k] = A[n,d] * D * F * S for the sparse randomized trigonometric transform,
  * F = unnormalised Walsh-Hadamard (transform SK_WHT, d a power of two); `scale` carries
  * 1/sqrt(d) * sqrt(d/xi)/sqrt(k).  dvals: d elements of `dtype` (the diagonal D).

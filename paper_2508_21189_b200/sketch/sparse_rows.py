@@ -10,6 +10,8 @@ replaces sparse.py:68-78).  Complex-field operators use the dense device GEMM.
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 
 from .. import _lib
@@ -171,11 +173,64 @@ class _SignSparseTM(TestMatrix):
         _lib.check(st, "sk_sparse_right")
         return y
 
-    def _adjoint_device(self, b):
+    def _adjoint_wide_on(self, device):
+        """K2w encoding (sk_sparse_adjoint_wide_encode), built once on the host and cached on `device`."""
+        key = ("adjw", device)
+        if key not in self._device_cache:
+            import torch
+
+            lib = _lib.load()
+            rows, cols, neg, mag = self._sign_form()
+            rows = np.ascontiguousarray(rows, dtype=np.int64)
+            cols = np.ascontiguousarray(cols, dtype=np.int64)
+            negu = np.ascontiguousarray(neg, dtype=np.uint8)
+            nseg1 = int(lib.sk_sparse_adjoint_wide_segments(self.d, self.k))
+            _lib.check(min(nseg1, 0), "sk_sparse_adjoint_wide_segments")
+            seg_off = np.zeros(nseg1, np.int64)
+            cap = ctypes.c_int32(0)
+            args = (self.d, self.k, rows.size, rows.ctypes.data, cols.ctypes.data, negu.ctypes.data)
+            total = lib.sk_sparse_adjoint_wide_encode(*args, None, 0, seg_off.ctypes.data, ctypes.byref(cap))
+            _lib.check(min(int(total), 0), "sk_sparse_adjoint_wide_encode")
+            enc = np.zeros(max(int(total), 1), np.uint16)
+            total = lib.sk_sparse_adjoint_wide_encode(*args, enc.ctypes.data, enc.size, seg_off.ctypes.data,
+                                                      ctypes.byref(cap))
+            _lib.check(min(int(total), 0), "sk_sparse_adjoint_wide_encode")
+            self._device_cache[key] = (torch.from_numpy(enc.view(np.int16)).to(device),
+                                       torch.from_numpy(seg_off).to(device), int(cap.value), mag)
+        return self._device_cache[key]
+
+    def adjoint_path(self, b) -> str:
+        """Kernel used by apply_adjoint: 'wide' (K2w, float32), 'gather' (K2) or 'dense'."""
+        import os
+
         import torch
 
         if self._sign_form() is None or b.dtype not in (torch.float32, torch.float64):
+            return "dense"
+        forced = os.environ.get("SKETCH_B200_SPARSE_ADJOINT", "auto")
+        wide_ok = (b.dtype == torch.float32 and b.data_ptr() % 16 == 0 and b.stride(0) % 4 == 0
+                   and b.stride(1) == 1 and b.shape[1] >= 1)
+        return "wide" if (wide_ok and forced != "gather") else "gather"
+
+    def _adjoint_device(self, b):
+        import torch
+
+        path = self.adjoint_path(b)
+        if path == "dense":
             return super()._adjoint_device(b)
+        if path == "wide":
+            enc, seg_off, cap, mag = self._adjoint_wide_on(b.device)
+            m = b.shape[1]
+            out = torch.empty((self.k, m), dtype=b.dtype, device=b.device)
+            lib = _lib.load()
+            ws_bytes = lib.sk_sparse_adjoint_wide_workspace_bytes(self.d, m, self.k)
+            ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=b.device)
+            with torch.cuda.device(b.device):
+                st = lib.sk_sparse_adjoint_wide(b.data_ptr(), self.d, m, b.stride(0), enc.data_ptr(), seg_off.data_ptr(),
+                                                cap, self.k, mag, out.data_ptr(), out.stride(0), 0, ws.data_ptr(),
+                                                ws_bytes, torch.cuda.current_stream().cuda_stream)
+            _lib.check(st, "sk_sparse_adjoint_wide")
+            return out
         code = _lib.SK_F32 if b.dtype == torch.float32 else _lib.SK_F64
         ptr, ent, r, mag, seg, cap = self._bcsc_on(b.device, "adjoint", code)
         m = b.shape[1]
