@@ -3,16 +3,18 @@
 // Replaces `_SparseTM.apply_adjoint` = `self.matrix.conj().T @ b` (src/sketch/sparse.py:68-78) for
 // float32 operands (BASELINE config 4: S = Omega^T, 2048 x 4194304, zeta = 8, A 4194304 x 512).
 //
-// Work split. A CTA owns a 64-column slice of A (2 columns per lane, 8-byte shared loads) and a
-// group of 512 output rows c (16 warps x 32 rows; each lane keeps 32 float2 accumulators in
-// registers), over a contiguous piece of the row chunks (128 rows each, a 6-deep ring fed by a
-// producer warp). The 4 CTAs that own the same slice and piece but different groups form a
-// thread-block cluster: each loads a quarter of every 32 KB chunk tile and multicasts it to all
-// four (the ring slot is refilled once all four released it), so A leaves L2 once per slice.
+// Work split. A CTA owns a 128-column slice of A (4 columns per lane, 16-byte shared loads) and a
+// group of 256 output rows c (16 warps x 16 rows; each lane keeps 16 x 4 accumulators in
+// registers), over a contiguous piece of the row chunks (128 rows = one 64 KB tile each, a 3-deep
+// TMA ring fed by a producer warp). The 8 groups of a slice read the same tiles at about the same
+// time and L2 serves the repeats (DRAM reads stay ~1.04x |A|). Measured alternatives (DESIGN.md
+// §K2w): clusters that multicast each tile to the 2/4/8 groups of a slice (the per-chunk
+// cross-CTA release costs more than the L2 reads it saves: 11.0 / 13.1 / 23.3 ms vs 9.8 ms),
+// 64-column slices (13 ms), 64-row chunks (17.6 ms).
 //
 // Entries. Host-encoded per (chunk, group) segment (sk_sparse_adjoint_wide_encode): a 17-entry
 // uint16 header of warp offsets (multiples of 4) followed by uint16 entries
-// (row_in_chunk << 8) | (neg << 5) | (c mod 32), each warp list padded with no-op entries (64).
+// (row_in_chunk << 9) | (neg << 4) | (c mod 16), each warp list padded with no-op entries (32).
 // A warp reads four entries per uniform 8-byte load; each entry is one 256-byte row read (conflict
 // free) added into accumulator c mod 32 through a warp-uniform jump table. Pieces write partial sums; the float64 ordered reduction of
 // sparse_adjoint.cu forms SA (deterministic).
@@ -35,12 +37,12 @@ namespace {
 using namespace sm100;
 
 constexpr int W_R = 128;                 // rows per chunk
-constexpr int W_COLS = 64;               // columns per CTA slice
+constexpr int W_COLS = 128;              // columns per CTA slice (4 per lane)
 constexpr int W_WARPS = 16;
-constexpr int W_CPW = 32;                // output rows per warp
+constexpr int W_CPW = 16;                // output rows per warp
 constexpr int W_CG = W_WARPS * W_CPW;    // output rows per CTA (group)
 constexpr int W_HDR = 24;                // header uint16s: 17 warp offsets, padded to 48 bytes
-constexpr int W_STAGES = 6;
+constexpr int W_STAGES = 3;
 constexpr uint32_t W_TILE = W_R * W_COLS * 4;  // 64 KB
 
 typedef unsigned long long u64;
@@ -55,30 +57,6 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
   return v;
 }
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1,
-                                               uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
-      "%3}], [%4], %5;" ::"r"(dst),
-      "l"(m), "r"(c0), "r"(c1), "r"(bar), "h"(mask)
-      : "memory");
-}
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(src), "r"(bytes), "r"(bar)
@@ -87,104 +65,78 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 
 struct WParams {
   int64_t d, m, k;
-  int nchunks, ngroups, nslices, npieces, chunks_per_piece, csize;
+  int nchunks, ngroups, nslices, npieces, chunks_per_piece;
   uint32_t stage_bytes;
   const uint16_t* enc;
   const int64_t* seg_off;  // [nchunks * ngroups + 1], uint16 units
   float* part;             // [npieces][k][m]
 };
 
-// Dispatch one entry: index j = (neg << 5) | (c mod 32) selects acc[c mod 32] +=/-= v through a
-// warp-uniform indirect branch (brx.idx.uni over a 65-entry jump table); j = 64 is a padding no-op.
-#define SKB_W_DISPATCH(VV, JJ) \
+// Dispatch one entry: index j = (neg << 4) | (c mod 16) selects acc[c mod 16] +=/-= v (four columns
+// as two packed pairs) through a warp-uniform indirect branch (brx.idx.uni over a 33-entry jump
+// table); j = 32 is a padding no-op.
+#define SKB_W_DISPATCH(V0, V1, JJ) \
   asm volatile( \
       "{\n\t" \
-      "T_%=: .branchtargets A0_%=, A1_%=, A2_%=, A3_%=, A4_%=, A5_%=, A6_%=, A7_%=, A8_%=, A9_%=, A10_%=, A11_%=, A12_%=, A13_%=, A14_%=, A15_%=, A16_%=, A17_%=, A18_%=, A19_%=, A20_%=, A21_%=, A22_%=, A23_%=, A24_%=, A25_%=, A26_%=, A27_%=, A28_%=, A29_%=, A30_%=, A31_%=, S0_%=, S1_%=, S2_%=, S3_%=, S4_%=, S5_%=, S6_%=, S7_%=, S8_%=, S9_%=, S10_%=, S11_%=, S12_%=, S13_%=, S14_%=, S15_%=, S16_%=, S17_%=, S18_%=, S19_%=, S20_%=, S21_%=, S22_%=, S23_%=, S24_%=, S25_%=, S26_%=, S27_%=, S28_%=, S29_%=, S30_%=, S31_%=, D_%=;\n\t" \
-      "brx.idx.uni %33, T_%=;\n\t" \
-      "A0_%=: add.rn.f32x2 %0, %0, %32;\n\tbra.uni D_%=;\n\t" \
-      "A1_%=: add.rn.f32x2 %1, %1, %32;\n\tbra.uni D_%=;\n\t" \
-      "A2_%=: add.rn.f32x2 %2, %2, %32;\n\tbra.uni D_%=;\n\t" \
-      "A3_%=: add.rn.f32x2 %3, %3, %32;\n\tbra.uni D_%=;\n\t" \
-      "A4_%=: add.rn.f32x2 %4, %4, %32;\n\tbra.uni D_%=;\n\t" \
-      "A5_%=: add.rn.f32x2 %5, %5, %32;\n\tbra.uni D_%=;\n\t" \
-      "A6_%=: add.rn.f32x2 %6, %6, %32;\n\tbra.uni D_%=;\n\t" \
-      "A7_%=: add.rn.f32x2 %7, %7, %32;\n\tbra.uni D_%=;\n\t" \
-      "A8_%=: add.rn.f32x2 %8, %8, %32;\n\tbra.uni D_%=;\n\t" \
-      "A9_%=: add.rn.f32x2 %9, %9, %32;\n\tbra.uni D_%=;\n\t" \
-      "A10_%=: add.rn.f32x2 %10, %10, %32;\n\tbra.uni D_%=;\n\t" \
-      "A11_%=: add.rn.f32x2 %11, %11, %32;\n\tbra.uni D_%=;\n\t" \
-      "A12_%=: add.rn.f32x2 %12, %12, %32;\n\tbra.uni D_%=;\n\t" \
-      "A13_%=: add.rn.f32x2 %13, %13, %32;\n\tbra.uni D_%=;\n\t" \
-      "A14_%=: add.rn.f32x2 %14, %14, %32;\n\tbra.uni D_%=;\n\t" \
-      "A15_%=: add.rn.f32x2 %15, %15, %32;\n\tbra.uni D_%=;\n\t" \
-      "A16_%=: add.rn.f32x2 %16, %16, %32;\n\tbra.uni D_%=;\n\t" \
-      "A17_%=: add.rn.f32x2 %17, %17, %32;\n\tbra.uni D_%=;\n\t" \
-      "A18_%=: add.rn.f32x2 %18, %18, %32;\n\tbra.uni D_%=;\n\t" \
-      "A19_%=: add.rn.f32x2 %19, %19, %32;\n\tbra.uni D_%=;\n\t" \
-      "A20_%=: add.rn.f32x2 %20, %20, %32;\n\tbra.uni D_%=;\n\t" \
-      "A21_%=: add.rn.f32x2 %21, %21, %32;\n\tbra.uni D_%=;\n\t" \
-      "A22_%=: add.rn.f32x2 %22, %22, %32;\n\tbra.uni D_%=;\n\t" \
-      "A23_%=: add.rn.f32x2 %23, %23, %32;\n\tbra.uni D_%=;\n\t" \
-      "A24_%=: add.rn.f32x2 %24, %24, %32;\n\tbra.uni D_%=;\n\t" \
-      "A25_%=: add.rn.f32x2 %25, %25, %32;\n\tbra.uni D_%=;\n\t" \
-      "A26_%=: add.rn.f32x2 %26, %26, %32;\n\tbra.uni D_%=;\n\t" \
-      "A27_%=: add.rn.f32x2 %27, %27, %32;\n\tbra.uni D_%=;\n\t" \
-      "A28_%=: add.rn.f32x2 %28, %28, %32;\n\tbra.uni D_%=;\n\t" \
-      "A29_%=: add.rn.f32x2 %29, %29, %32;\n\tbra.uni D_%=;\n\t" \
-      "A30_%=: add.rn.f32x2 %30, %30, %32;\n\tbra.uni D_%=;\n\t" \
-      "A31_%=: add.rn.f32x2 %31, %31, %32;\n\tbra.uni D_%=;\n\t" \
-      "S0_%=: sub.rn.f32x2 %0, %0, %32;\n\tbra.uni D_%=;\n\t" \
-      "S1_%=: sub.rn.f32x2 %1, %1, %32;\n\tbra.uni D_%=;\n\t" \
-      "S2_%=: sub.rn.f32x2 %2, %2, %32;\n\tbra.uni D_%=;\n\t" \
-      "S3_%=: sub.rn.f32x2 %3, %3, %32;\n\tbra.uni D_%=;\n\t" \
-      "S4_%=: sub.rn.f32x2 %4, %4, %32;\n\tbra.uni D_%=;\n\t" \
-      "S5_%=: sub.rn.f32x2 %5, %5, %32;\n\tbra.uni D_%=;\n\t" \
-      "S6_%=: sub.rn.f32x2 %6, %6, %32;\n\tbra.uni D_%=;\n\t" \
-      "S7_%=: sub.rn.f32x2 %7, %7, %32;\n\tbra.uni D_%=;\n\t" \
-      "S8_%=: sub.rn.f32x2 %8, %8, %32;\n\tbra.uni D_%=;\n\t" \
-      "S9_%=: sub.rn.f32x2 %9, %9, %32;\n\tbra.uni D_%=;\n\t" \
-      "S10_%=: sub.rn.f32x2 %10, %10, %32;\n\tbra.uni D_%=;\n\t" \
-      "S11_%=: sub.rn.f32x2 %11, %11, %32;\n\tbra.uni D_%=;\n\t" \
-      "S12_%=: sub.rn.f32x2 %12, %12, %32;\n\tbra.uni D_%=;\n\t" \
-      "S13_%=: sub.rn.f32x2 %13, %13, %32;\n\tbra.uni D_%=;\n\t" \
-      "S14_%=: sub.rn.f32x2 %14, %14, %32;\n\tbra.uni D_%=;\n\t" \
-      "S15_%=: sub.rn.f32x2 %15, %15, %32;\n\tbra.uni D_%=;\n\t" \
-      "S16_%=: sub.rn.f32x2 %16, %16, %32;\n\tbra.uni D_%=;\n\t" \
-      "S17_%=: sub.rn.f32x2 %17, %17, %32;\n\tbra.uni D_%=;\n\t" \
-      "S18_%=: sub.rn.f32x2 %18, %18, %32;\n\tbra.uni D_%=;\n\t" \
-      "S19_%=: sub.rn.f32x2 %19, %19, %32;\n\tbra.uni D_%=;\n\t" \
-      "S20_%=: sub.rn.f32x2 %20, %20, %32;\n\tbra.uni D_%=;\n\t" \
-      "S21_%=: sub.rn.f32x2 %21, %21, %32;\n\tbra.uni D_%=;\n\t" \
-      "S22_%=: sub.rn.f32x2 %22, %22, %32;\n\tbra.uni D_%=;\n\t" \
-      "S23_%=: sub.rn.f32x2 %23, %23, %32;\n\tbra.uni D_%=;\n\t" \
-      "S24_%=: sub.rn.f32x2 %24, %24, %32;\n\tbra.uni D_%=;\n\t" \
-      "S25_%=: sub.rn.f32x2 %25, %25, %32;\n\tbra.uni D_%=;\n\t" \
-      "S26_%=: sub.rn.f32x2 %26, %26, %32;\n\tbra.uni D_%=;\n\t" \
-      "S27_%=: sub.rn.f32x2 %27, %27, %32;\n\tbra.uni D_%=;\n\t" \
-      "S28_%=: sub.rn.f32x2 %28, %28, %32;\n\tbra.uni D_%=;\n\t" \
-      "S29_%=: sub.rn.f32x2 %29, %29, %32;\n\tbra.uni D_%=;\n\t" \
-      "S30_%=: sub.rn.f32x2 %30, %30, %32;\n\tbra.uni D_%=;\n\t" \
-      "S31_%=: sub.rn.f32x2 %31, %31, %32;\n\tbra.uni D_%=;\n\t" \
+      "T_%=: .branchtargets A0_%=, A1_%=, A2_%=, A3_%=, A4_%=, A5_%=, A6_%=, A7_%=, A8_%=, A9_%=, A10_%=, A11_%=, A12_%=, A13_%=, A14_%=, A15_%=, S0_%=, S1_%=, S2_%=, S3_%=, S4_%=, S5_%=, S6_%=, S7_%=, S8_%=, S9_%=, S10_%=, S11_%=, S12_%=, S13_%=, S14_%=, S15_%=, D_%=;\n\t" \
+      "brx.idx.uni %34, T_%=;\n\t" \
+      "A0_%=: add.rn.f32x2 %0, %0, %32;\n\tadd.rn.f32x2 %1, %1, %33;\n\tbra.uni D_%=;\n\t" \
+      "A1_%=: add.rn.f32x2 %2, %2, %32;\n\tadd.rn.f32x2 %3, %3, %33;\n\tbra.uni D_%=;\n\t" \
+      "A2_%=: add.rn.f32x2 %4, %4, %32;\n\tadd.rn.f32x2 %5, %5, %33;\n\tbra.uni D_%=;\n\t" \
+      "A3_%=: add.rn.f32x2 %6, %6, %32;\n\tadd.rn.f32x2 %7, %7, %33;\n\tbra.uni D_%=;\n\t" \
+      "A4_%=: add.rn.f32x2 %8, %8, %32;\n\tadd.rn.f32x2 %9, %9, %33;\n\tbra.uni D_%=;\n\t" \
+      "A5_%=: add.rn.f32x2 %10, %10, %32;\n\tadd.rn.f32x2 %11, %11, %33;\n\tbra.uni D_%=;\n\t" \
+      "A6_%=: add.rn.f32x2 %12, %12, %32;\n\tadd.rn.f32x2 %13, %13, %33;\n\tbra.uni D_%=;\n\t" \
+      "A7_%=: add.rn.f32x2 %14, %14, %32;\n\tadd.rn.f32x2 %15, %15, %33;\n\tbra.uni D_%=;\n\t" \
+      "A8_%=: add.rn.f32x2 %16, %16, %32;\n\tadd.rn.f32x2 %17, %17, %33;\n\tbra.uni D_%=;\n\t" \
+      "A9_%=: add.rn.f32x2 %18, %18, %32;\n\tadd.rn.f32x2 %19, %19, %33;\n\tbra.uni D_%=;\n\t" \
+      "A10_%=: add.rn.f32x2 %20, %20, %32;\n\tadd.rn.f32x2 %21, %21, %33;\n\tbra.uni D_%=;\n\t" \
+      "A11_%=: add.rn.f32x2 %22, %22, %32;\n\tadd.rn.f32x2 %23, %23, %33;\n\tbra.uni D_%=;\n\t" \
+      "A12_%=: add.rn.f32x2 %24, %24, %32;\n\tadd.rn.f32x2 %25, %25, %33;\n\tbra.uni D_%=;\n\t" \
+      "A13_%=: add.rn.f32x2 %26, %26, %32;\n\tadd.rn.f32x2 %27, %27, %33;\n\tbra.uni D_%=;\n\t" \
+      "A14_%=: add.rn.f32x2 %28, %28, %32;\n\tadd.rn.f32x2 %29, %29, %33;\n\tbra.uni D_%=;\n\t" \
+      "A15_%=: add.rn.f32x2 %30, %30, %32;\n\tadd.rn.f32x2 %31, %31, %33;\n\tbra.uni D_%=;\n\t" \
+      "S0_%=: sub.rn.f32x2 %0, %0, %32;\n\tsub.rn.f32x2 %1, %1, %33;\n\tbra.uni D_%=;\n\t" \
+      "S1_%=: sub.rn.f32x2 %2, %2, %32;\n\tsub.rn.f32x2 %3, %3, %33;\n\tbra.uni D_%=;\n\t" \
+      "S2_%=: sub.rn.f32x2 %4, %4, %32;\n\tsub.rn.f32x2 %5, %5, %33;\n\tbra.uni D_%=;\n\t" \
+      "S3_%=: sub.rn.f32x2 %6, %6, %32;\n\tsub.rn.f32x2 %7, %7, %33;\n\tbra.uni D_%=;\n\t" \
+      "S4_%=: sub.rn.f32x2 %8, %8, %32;\n\tsub.rn.f32x2 %9, %9, %33;\n\tbra.uni D_%=;\n\t" \
+      "S5_%=: sub.rn.f32x2 %10, %10, %32;\n\tsub.rn.f32x2 %11, %11, %33;\n\tbra.uni D_%=;\n\t" \
+      "S6_%=: sub.rn.f32x2 %12, %12, %32;\n\tsub.rn.f32x2 %13, %13, %33;\n\tbra.uni D_%=;\n\t" \
+      "S7_%=: sub.rn.f32x2 %14, %14, %32;\n\tsub.rn.f32x2 %15, %15, %33;\n\tbra.uni D_%=;\n\t" \
+      "S8_%=: sub.rn.f32x2 %16, %16, %32;\n\tsub.rn.f32x2 %17, %17, %33;\n\tbra.uni D_%=;\n\t" \
+      "S9_%=: sub.rn.f32x2 %18, %18, %32;\n\tsub.rn.f32x2 %19, %19, %33;\n\tbra.uni D_%=;\n\t" \
+      "S10_%=: sub.rn.f32x2 %20, %20, %32;\n\tsub.rn.f32x2 %21, %21, %33;\n\tbra.uni D_%=;\n\t" \
+      "S11_%=: sub.rn.f32x2 %22, %22, %32;\n\tsub.rn.f32x2 %23, %23, %33;\n\tbra.uni D_%=;\n\t" \
+      "S12_%=: sub.rn.f32x2 %24, %24, %32;\n\tsub.rn.f32x2 %25, %25, %33;\n\tbra.uni D_%=;\n\t" \
+      "S13_%=: sub.rn.f32x2 %26, %26, %32;\n\tsub.rn.f32x2 %27, %27, %33;\n\tbra.uni D_%=;\n\t" \
+      "S14_%=: sub.rn.f32x2 %28, %28, %32;\n\tsub.rn.f32x2 %29, %29, %33;\n\tbra.uni D_%=;\n\t" \
+      "S15_%=: sub.rn.f32x2 %30, %30, %32;\n\tsub.rn.f32x2 %31, %31, %33;\n\tbra.uni D_%=;\n\t" \
       "D_%=:\n\t}" \
       : "+l"(acc[0]), "+l"(acc[1]), "+l"(acc[2]), "+l"(acc[3]), "+l"(acc[4]), "+l"(acc[5]), "+l"(acc[6]), "+l"(acc[7]), "+l"(acc[8]), "+l"(acc[9]), "+l"(acc[10]), "+l"(acc[11]), "+l"(acc[12]), "+l"(acc[13]), "+l"(acc[14]), "+l"(acc[15]), "+l"(acc[16]), "+l"(acc[17]), "+l"(acc[18]), "+l"(acc[19]), "+l"(acc[20]), "+l"(acc[21]), "+l"(acc[22]), "+l"(acc[23]), "+l"(acc[24]), "+l"(acc[25]), "+l"(acc[26]), "+l"(acc[27]), "+l"(acc[28]), "+l"(acc[29]), "+l"(acc[30]), "+l"(acc[31]) \
-      : "l"(VV), "r"(JJ))
+      : "l"(V0), "l"(V1), "r"(JJ))
 
 // Walk entries [a, b) of this warp (a, b multiples of 4): four entries per uniform 8-byte shared
-// load; their four row values are loaded before the four dispatches so the loads overlap.
-__device__ __forceinline__ void walk(u64 (&acc)[W_CPW], uint32_t tile_lane, uint32_t ent, int a, int b) {
+// load; their four row values (16 bytes per lane) are loaded before the four dispatches.
+__device__ __forceinline__ void lds128u(uint32_t addr, u64& x, u64& y) {
+  asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(addr));
+}
+
+__device__ __forceinline__ void walk(u64 (&acc)[2 * W_CPW], uint32_t tile_lane, uint32_t ent, int a, int b) {
   for (int e = a; e < b; e += 4) {
     const u64 q = lds64(ent + 2u * (uint32_t)e);
     const uint32_t lo = (uint32_t)q, hi = (uint32_t)(q >> 32);
     const uint32_t u0 = lo & 0xffffu, u1 = lo >> 16, u2 = hi & 0xffffu, u3 = hi >> 16;
-    const u64 v0 = lds64(tile_lane + (u0 & 0xff00u));
-    const u64 v1 = lds64(tile_lane + (u1 & 0xff00u));
-    const u64 v2 = lds64(tile_lane + (u2 & 0xff00u));
-    const u64 v3 = lds64(tile_lane + (u3 & 0xff00u));
-    const uint32_t j0 = u0 & 127u, j1 = u1 & 127u, j2 = u2 & 127u, j3 = u3 & 127u;
-    SKB_W_DISPATCH(v0, j0);
-    SKB_W_DISPATCH(v1, j1);
-    SKB_W_DISPATCH(v2, j2);
-    SKB_W_DISPATCH(v3, j3);
+    u64 a0, b0, a1, b1, a2, b2, a3, b3;
+    lds128u(tile_lane + (u0 & 0xfe00u), a0, b0);
+    lds128u(tile_lane + (u1 & 0xfe00u), a1, b1);
+    lds128u(tile_lane + (u2 & 0xfe00u), a2, b2);
+    lds128u(tile_lane + (u3 & 0xfe00u), a3, b3);
+    const uint32_t j0 = u0 & 63u, j1 = u1 & 63u, j2 = u2 & 63u, j3 = u3 & 63u;
+    SKB_W_DISPATCH(a0, b0, j0);
+    SKB_W_DISPATCH(a1, b1, j1);
+    SKB_W_DISPATCH(a2, b2, j2);
+    SKB_W_DISPATCH(a3, b3, j3);
   }
 }
 
@@ -193,95 +145,77 @@ __global__ void __launch_bounds__((W_WARPS + 1) * 32, 1)
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + W_STAGES * p.stage_bytes);
-  uint64_t* empty = full + W_STAGES;       // cluster-wide: slot s free in every CTA (csize arrivals)
-  uint64_t* consumed = empty + W_STAGES;   // local: all 16 consumer warps done with slot s
+  uint64_t* consumed = full + W_STAGES;  // all 16 consumer warps done with slot s
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = blockIdx.x, slice = blockIdx.y, piece = blockIdx.z;
-  const int csize = p.csize;
-  const uint32_t rank = cluster_ctarank();
   const int h0 = piece * p.chunks_per_piece;
   const int nch = (int)min((int64_t)p.chunks_per_piece, (int64_t)p.nchunks - h0);
-  const bool live = g < p.ngroups;  // padding CTAs of the last cluster still load their quarter
 
   if (tid == 0) {
     for (int s = 0; s < W_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], csize);
       mbar_init(&consumed[s], W_WARPS);
     }
     fence_mbar_init();
     tma_prefetch_desc(&tm);
   }
-  cluster_sync_all();  // every barrier of the cluster initialised before multicasts / remote arrivals
+  __syncthreads();
 
-  const int rows_per = W_R / csize;
-  const uint16_t mask = (uint16_t)((1u << csize) - 1u);
-  auto produce = [&](int i, int s) {
-    const int h = h0 + i;
-    const int64_t sg = (int64_t)h * p.ngroups + g;
-    const uint32_t seg_bytes = live ? (uint32_t)(p.seg_off[sg + 1] - p.seg_off[sg]) * 2u : 0u;
-    const uint32_t st = smem_u32(smem + (size_t)s * p.stage_bytes);
-    mbar_arrive_expect_tx(&full[s], W_TILE + seg_bytes);
-    tma_load_2d_mc(st + rank * (uint32_t)rows_per * W_COLS * 4u, &tm, smem_u32(&full[s]), slice * W_COLS,
-                   h * W_R + (int)rank * rows_per, mask);
-    if (seg_bytes) bulk_g2s(st + W_TILE, p.enc + p.seg_off[sg], seg_bytes, smem_u32(&full[s]));
-  };
   if (warp == W_WARPS) {
     // ------------------------------------------------------------ producer warp (one thread)
     if (lane == 0) {
       for (int i = 0; i < nch; ++i) {
         const int s = i % W_STAGES;
-        if (i >= W_STAGES) {
-          const uint32_t ph = (uint32_t)(i / W_STAGES - 1) & 1u;
-          mbar_wait(&consumed[s], ph);  // this CTA's warps are done with the slot: tell every peer
-          for (int r = 0; r < csize; ++r) mbar_arrive_remote(mapa_shared(smem_u32(&empty[s]), (uint32_t)r));
-          mbar_wait(&empty[s], ph);     // ... and wait until every peer has released it too
-        }
-        produce(i, s);
+        if (i >= W_STAGES) mbar_wait(&consumed[s], (uint32_t)(i / W_STAGES - 1) & 1u);
+        const int h = h0 + i;
+        const int64_t sg = (int64_t)h * p.ngroups + g;
+        const uint32_t seg_bytes = (uint32_t)(p.seg_off[sg + 1] - p.seg_off[sg]) * 2u;
+        const uint32_t st = smem_u32(smem + (size_t)s * p.stage_bytes);
+        mbar_arrive_expect_tx(&full[s], W_TILE + seg_bytes);
+        tma_load_2d(smem + (size_t)s * p.stage_bytes, &tm, &full[s], slice * W_COLS, h * W_R);
+        bulk_g2s(st + W_TILE, p.enc + p.seg_off[sg], seg_bytes, smem_u32(&full[s]));
       }
     }
-    cluster_sync_all();
     return;
   }
 
-  u64 acc[W_CPW];
+  u64 acc[2 * W_CPW];
 #pragma unroll
-  for (int j = 0; j < W_CPW; ++j) acc[j] = 0ull;
+  for (int j = 0; j < 2 * W_CPW; ++j) acc[j] = 0ull;
 
   for (int i = 0; i < nch; ++i) {
     const int s = i % W_STAGES;
     const uint32_t ph = (uint32_t)(i / W_STAGES) & 1u;
     mbar_wait(&full[s], ph);
     const uint32_t st = smem_u32(smem + (size_t)s * p.stage_bytes);
-    if (live) {
-      const uint32_t hdr = st + W_TILE;
-      const int a = (int)lds_u16(hdr + 2u * warp), b = (int)lds_u16(hdr + 2u * warp + 2u);
-      walk(acc, st + 8u * lane, hdr + 2u * W_HDR, a, b);
-    }
+    const uint32_t hdr = st + W_TILE;
+    const int a = (int)lds_u16(hdr + 2u * warp), b = (int)lds_u16(hdr + 2u * warp + 2u);
+    walk(acc, st + 16u * lane, hdr + 2u * W_HDR, a, b);
     __syncwarp();
     if (lane == 0) mbar_arrive(&consumed[s]);
   }
 
-  if (live) {
-    const int64_t col = (int64_t)slice * W_COLS + 2 * lane;
+  {
+    const int64_t col = (int64_t)slice * W_COLS + 4 * lane;
     float* out = p.part + (int64_t)piece * p.k * p.m;
 #pragma unroll
     for (int j = 0; j < W_CPW; ++j) {
       const int64_t c = (int64_t)g * W_CG + warp * W_CPW + j;
       if (c < p.k) {
-        const float lo = __uint_as_float((uint32_t)(acc[j] & 0xffffffffull));
-        const float hi = __uint_as_float((uint32_t)(acc[j] >> 32));
-        if (col < p.m) out[c * p.m + col] = lo;
-        if (col + 1 < p.m) out[c * p.m + col + 1] = hi;
+        const float v[4] = {__uint_as_float((uint32_t)acc[2 * j]), __uint_as_float((uint32_t)(acc[2 * j] >> 32)),
+                            __uint_as_float((uint32_t)acc[2 * j + 1]),
+                            __uint_as_float((uint32_t)(acc[2 * j + 1] >> 32))};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (col + q < p.m) out[c * p.m + col + q] = v[q];
       }
     }
   }
-  cluster_sync_all();  // no CTA leaves while a peer may still arrive on its barriers
 }
 
 struct WPlan {
-  int nchunks, ngroups, ngroups_pad, nslices, npieces, chunks_per_piece, csize;
+  int nchunks, ngroups, nslices, npieces, chunks_per_piece;
   uint32_t stage_bytes;
   size_t smem, ws_bytes;
 };
@@ -290,17 +224,15 @@ WPlan wide_plan(int64_t d, int64_t m, int64_t k, int32_t seg_cap) {
   WPlan pl{};
   pl.nchunks = (int)((d + W_R - 1) / W_R);
   pl.ngroups = (int)((k + W_CG - 1) / W_CG);
-  pl.csize = pl.ngroups >= 4 ? 4 : (pl.ngroups >= 2 ? 2 : 1);
-  pl.ngroups_pad = (pl.ngroups + pl.csize - 1) / pl.csize * pl.csize;
   pl.nslices = (int)((m + W_COLS - 1) / W_COLS);
-  const int64_t roles = (int64_t)pl.ngroups_pad * pl.nslices;
+  const int64_t roles = (int64_t)pl.ngroups * pl.nslices;
   int64_t pieces = (4 * (int64_t)sm_count() + roles - 1) / roles;
   if (pieces > pl.nchunks) pieces = pl.nchunks;
   if (pieces < 1) pieces = 1;
   pl.chunks_per_piece = (int)((pl.nchunks + pieces - 1) / pieces);
   pl.npieces = (pl.nchunks + pl.chunks_per_piece - 1) / pl.chunks_per_piece;
   pl.stage_bytes = (W_TILE + (uint32_t)seg_cap * 2u + 1023u) & ~1023u;
-  pl.smem = 1024 + (size_t)W_STAGES * pl.stage_bytes + 3 * W_STAGES * 8;
+  pl.smem = 1024 + (size_t)W_STAGES * pl.stage_bytes + 2 * W_STAGES * 8;
   pl.ws_bytes = (size_t)pl.npieces * k * m * sizeof(float);
   return pl;
 }
@@ -338,7 +270,7 @@ extern "C" int64_t sk_sparse_adjoint_wide_encode(int64_t d, int64_t k, int64_t n
   *seg_cap = cap;
   if (!enc) return total;
   if (enc_cap < total) return fail(SK_EINVAL, "sk_sparse_adjoint_wide_encode: output too small");
-  std::fill(enc, enc + total, (uint16_t)64);  // 64 = no-op dispatch index (row 0)
+  std::fill(enc, enc + total, (uint16_t)32);  // 32 = no-op dispatch index (row 0)
   std::vector<int32_t> pos((size_t)nseg * W_WARPS);
   for (int64_t sg = 0; sg < nseg; ++sg) {
     uint16_t* h = enc + seg_off[sg];
@@ -355,7 +287,7 @@ extern "C" int64_t sk_sparse_adjoint_wide_encode(int64_t d, int64_t k, int64_t n
     const int64_t r = rows[e], c = cols[e];
     const int64_t sg = (r / W_R) * ngroups + c / W_CG;
     int32_t& q = pos[(size_t)sg * W_WARPS + (c % W_CG) / W_CPW];
-    enc[seg_off[sg] + W_HDR + q] = (uint16_t)(((r % W_R) << 8) | (neg[e] ? 32 : 0) | (c % W_CPW));
+    enc[seg_off[sg] + W_HDR + q] = (uint16_t)(((r % W_R) << 9) | (neg[e] ? 16 : 0) | (c % W_CPW));
     ++q;
   }
   return total;
@@ -388,7 +320,7 @@ extern "C" int sk_sparse_adjoint_wide(const float* A, int64_t d, int64_t m, int6
   CUtensorMap tm;
   cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)d};
   cuuint64_t strides[1] = {(cuuint64_t)lda * 4};
-  cuuint32_t box[2] = {(cuuint32_t)W_COLS, (cuuint32_t)(W_R / pl.csize)};
+  cuuint32_t box[2] = {(cuuint32_t)W_COLS, (cuuint32_t)W_R};
   cuuint32_t estr[2] = {1, 1};
   if (fn(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), dims, strides, box, estr,
          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -403,26 +335,14 @@ extern "C" int sk_sparse_adjoint_wide(const float* A, int64_t d, int64_t m, int6
   p.nslices = pl.nslices;
   p.npieces = pl.npieces;
   p.chunks_per_piece = pl.chunks_per_piece;
-  p.csize = pl.csize;
   p.stage_bytes = pl.stage_bytes;
   p.enc = enc;
   p.seg_off = seg_off;
   p.part = static_cast<float*>(ws);
   cudaStream_t s = as_stream(stream);
   cudaFuncSetAttribute(sparse_adjoint_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)pl.ngroups_pad, (unsigned)pl.nslices, (unsigned)pl.npieces);
-  cfg.blockDim = dim3((W_WARPS + 1) * 32, 1, 1);
-  cfg.dynamicSmemBytes = pl.smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)pl.csize;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, sparse_adjoint_wide, tm, p) != cudaSuccess) return check_launch("sk_sparse_adjoint_wide");
+  sparse_adjoint_wide<<<dim3((unsigned)pl.ngroups, (unsigned)pl.nslices, (unsigned)pl.npieces), (W_WARPS + 1) * 32,
+                        pl.smem, s>>>(tm, p);
   int st = check_launch("sk_sparse_adjoint_wide");
   if (st != SK_OK) return st;
   return adjoint_reduce_f32(p.part, pl.npieces, k, m, scale, SA, ldsa, accumulate, s);

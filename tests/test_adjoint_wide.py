@@ -10,7 +10,7 @@ from _cases import rel_err
 from paper_2508_21189_b200 import _lib
 from paper_2508_21189_b200 import sketch as skb
 
-R, CG, CPW, WARPS, HDR = 128, 512, 32, 16, 24
+R, CG, CPW, WARPS, HDR = 128, 256, 16, 16, 24
 
 
 def _encode(d, k, rows, cols, neg):
@@ -46,9 +46,9 @@ def test_encoder_roundtrip(d, k, zeta):
         for w in range(WARPS):
             for u in s[HDR + h[w]:HDR + h[w + 1]]:
                 u = int(u)
-                if u == 64:  # padding no-op
+                if u == 32:  # padding no-op
                     continue
-                got.append((chunk * R + (u >> 8), g * CG + w * CPW + (u & 31), (u >> 5) & 1))
+                got.append((chunk * R + (u >> 9), g * CG + w * CPW + (u & 15), (u >> 4) & 1))
     want = sorted(zip(rows.tolist(), cols.tolist(), neg.astype(int).tolist()))
     assert sorted(got) == want
 
