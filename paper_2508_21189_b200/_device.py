@@ -174,3 +174,10 @@ def pipelined_right(apply_dev, host, k: int):
     if y_host is None:
         y_host = torch.empty((0, k), dtype=dt)
     return y_host
+
+
+def transposed(x):
+    """A fresh row-major copy of x^T (standard strides even when a dimension is 1)."""
+    out = torch.empty((x.shape[1], x.shape[0]), dtype=x.dtype, device=x.device)
+    out.copy_(x.T)
+    return out

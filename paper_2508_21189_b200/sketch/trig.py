@@ -16,11 +16,12 @@ import scipy.fft
 
 from .. import _lib
 from .._device import from_result, to_operand
+from .._device import transposed as _transposed
 from .encode import srtt_sampler_encode
 from .sparse_rows import SparseColTM
 from .testmatrix import TestMatrix, entry_sample
 
-__all__ = ["wht", "dct2_ortho", "dft_unitary", "SparseRttTM", "TRANSFORMS"]
+__all__ = ["wht", "dct2_ortho", "dft_unitary", "dct3_rows", "SparseRttTM", "TRANSFORMS"]
 
 
 def _require_pow2(d: int) -> int:
@@ -128,6 +129,39 @@ def _srtt_native(a, dvals, samp, xi: int, k: int, scale: float, pm1: bool, trans
     return y
 
 
+def dct3_rows(x):
+    """Orthonormal DCT-III along the last axis of a real device tensor (inverse of DCT-II ortho).
+
+    Same transform as the reference's `_dct2_adjoint` = scipy.fft.dct(type=3, norm="ortho")
+    (src/sketch/rtt.py:58-60), computed in O(d log d) on the GPU: with s_k the ortho weights,
+    v = N * IFFT(s_k e^{i pi k / 2N} X_k) gives x_{2n} = Re v_n and x_{2n+1} = Re v_{N-1-n}.
+    Complex64 for float32 input (~1e-7 relative), complex128 for float64 (~1e-16).
+    """
+    import math
+
+    import torch
+
+    n_ = x.shape[-1]
+    ct = torch.complex64 if x.dtype == torch.float32 else torch.complex128
+    key = (x.device, ct, n_)
+    w = _DCT_TWIDDLE.get(key)
+    if w is None:
+        k = torch.arange(n_, dtype=torch.float64, device=x.device)
+        s = torch.full((n_,), math.sqrt(2.0 / n_), dtype=torch.float64, device=x.device)
+        s[0] = math.sqrt(1.0 / n_)
+        w = _DCT_TWIDDLE[key] = torch.polar(s, math.pi * k / (2 * n_)).to(ct) * n_
+    v = torch.fft.ifft(x.to(ct) * w, dim=-1)
+    out = torch.empty_like(x)
+    h = (n_ + 1) // 2
+    out[..., 0::2] = v[..., :h].real
+    out[..., 1::2] = v[..., h:].real.flip(-1)
+    return out
+
+
+_DCT_TWIDDLE: dict = {}
+_DCT_CHUNK_ELEMS = 1 << 26  # rows per FFT batch bounded to ~64M elements (complex intermediates)
+
+
 class SparseRttTM(TestMatrix):
     """Sparse randomized trigonometric transform Omega = D F S (reference rtt.py:75-186)."""
 
@@ -175,7 +209,43 @@ class SparseRttTM(TestMatrix):
 
         return self.field == "real" and self.transform == "wht" and dtype in (torch.float32, torch.float64)
 
+    def _dct_ok(self, dtype) -> bool:
+        import torch
+
+        return self.field == "real" and self.transform == "dct" and dtype in (torch.float32, torch.float64)
+
+    def _dct_right(self, a):
+        """Y = (A D) C^T S for the real DCT transform: D scale, DCT-III per row (cuFFT), sampled gather."""
+        import torch
+
+        key = ("srtt_dct", a.device, a.dtype)
+        if key not in self._device_cache:
+            dvals, sampler = self._parts()
+            rows, neg, mag = sampler.column_draws()
+            idx = torch.from_numpy(np.ascontiguousarray(rows.reshape(-1))).to(a.device)
+            sgn = torch.from_numpy(np.where(neg, -mag, mag).reshape(self.k, self.xi)).to(a.device, a.dtype)
+            dv = torch.from_numpy(np.ascontiguousarray(dvals)).to(device=a.device, dtype=a.dtype)
+            self._device_cache[key] = (idx, sgn, dv)
+        idx, sgn, dv = self._device_cache[key]
+        n = a.shape[0]
+        y = torch.empty((n, self.k), dtype=a.dtype, device=a.device)
+        step = max(1, _DCT_CHUNK_ELEMS // max(1, self.d))
+        for r0 in range(0, n, step):
+            z = dct3_rows(a[r0:r0 + step] * dv)
+            y[r0:r0 + step] = (z[:, idx].view(-1, self.k, self.xi) * sgn).sum(-1)
+        return y
+
+    def _adjoint_device(self, b):
+        """Omega^T B = (B^T Omega)^T for the real transforms: the row kernels on B^T."""
+        import torch
+
+        if (self._native_ok(b.dtype) or self._dct_ok(b.dtype)) and b.dim() == 2:
+            return self._right_device(_transposed(b)).T.contiguous()
+        return super()._adjoint_device(b)
+
     def _right_device(self, a):
+        if self._dct_ok(a.dtype):
+            return self._dct_right(a)
         if not self._native_ok(a.dtype):
             return super()._right_device(a)
         import torch

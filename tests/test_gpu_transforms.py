@@ -1,0 +1,67 @@
+"""SRTT with the DCT transform (the reference's real-field default), SRTT and Khatri-Rao adjoints.
+
+DCT rows run as DCT-III through the device FFT (O(d log d)); adjoints of the real SRTT / KR
+operators run the row kernels on B^T (Omega^T B = (B^T Omega)^T). Oracles: oracle/ restatement
+(src/sketch/rtt.py:129-154, khatri_rao.py:147-164) and the reference's materialised matrix.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as orc
+from _cases import rel_err
+from paper_2508_21189_b200 import sketch as skb
+
+pytestmark = pytest.mark.gpu
+
+TOL = {np.float64: 1e-12, np.float32: 1e-5}
+
+
+def _t(a, dev, dt):
+    import torch
+
+    return torch.as_tensor(np.asarray(a, dtype=dt)).to(dev)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("d,k,xi,n", [(8192, 512, 1, 40), (1000, 64, 3, 9), (4097, 100, 10, 5), (2, 1, 1, 3)])
+def test_srtt_dct_right_vs_oracle(d, k, xi, n, dt, cuda):
+    rng = np.random.default_rng(d + xi)
+    a = (rng.standard_normal((n, d)) / np.arange(1, d + 1)).astype(dt)
+    tm = skb.SparseRttTM(d, k, xi, seed=5)  # real field -> DCT (reference default)
+    assert tm.transform == "dct"
+    dv, samp = orc.srtt_parts(d, k, xi, 5)
+    ref = orc.srtt_right(dv, samp, a, "dct")
+    assert rel_err(tm.apply_right(_t(a, cuda, dt)).cpu().numpy(), ref) <= TOL[dt]
+    if dt == np.float64:  # NumPy in / NumPy out, as the reference
+        assert rel_err(tm.apply_right(a), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("transform", ["wht", "dct"])
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_srtt_adjoint(transform, dt, cuda):
+    d, k, xi, m = 2048, 96, 2, 7
+    tm = skb.SparseRttTM(d, k, xi, transform, seed=3)
+    b = np.random.default_rng(1).standard_normal((d, m)).astype(dt)
+    ref = tm.materialize().T @ b.astype(np.float64)
+    assert rel_err(tm.apply_adjoint(_t(b, cuda, dt)).cpu().numpy(), ref) <= TOL[dt]
+    v = tm.apply_adjoint(b[:, 0].astype(np.float64))
+    assert v.shape == (k,) and rel_err(v, ref[:, 0]) <= 1e-12
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_kr_adjoint(dt, cuda):
+    tm = skb.KhatriRaoTM(32, 2, 200, "real_rademacher", seed=4)
+    b = np.random.default_rng(2).standard_normal((tm.d, 11)).astype(dt)
+    ref = tm.materialize().T @ b.astype(np.float64)
+    assert rel_err(tm.apply_adjoint(_t(b, cuda, dt)).cpu().numpy(), ref) <= TOL[dt]
+
+
+def test_dct3_rows_matches_scipy(cuda):
+    import scipy.fft
+    import torch
+
+    for n in (1, 5, 64, 3000):
+        x = np.random.default_rng(n).standard_normal((4, n))
+        got = skb.dct3_rows(torch.as_tensor(x, device=cuda)).cpu().numpy()
+        assert rel_err(got, scipy.fft.dct(x, type=3, norm="ortho", axis=1)) <= 1e-14
