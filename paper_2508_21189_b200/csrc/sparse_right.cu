@@ -14,6 +14,8 @@
 //   one is consumed, so HBM reads overlap the shared-memory gathers.
 //
 // Bytes per launch (algorithmic): n*d*sizeof(T) read + n*k*sizeof(T) written.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace skb {
@@ -58,6 +60,21 @@ __device__ __forceinline__ double2 xor_perm(double2 v, int key) {
   return v;
 }
 
+template <typename T>
+__device__ __forceinline__ T lds_t(uint32_t addr);
+template <>
+__device__ __forceinline__ float lds_t<float>(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+template <>
+__device__ __forceinline__ double lds_t<double>(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
 template <typename T, int W, int CPW, int R, bool VEC, bool OMS>
 __global__ void __launch_bounds__(W * 32, 1)
     sparse_right_kernel(const T* __restrict__ A, int64_t n, int64_t d, int64_t lda,
@@ -77,8 +94,11 @@ __global__ void __launch_bounds__(W * 32, 1)
   T* As = reinterpret_cast<T*>(smem_raw);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t row0 = (int64_t)blockIdx.x * kRowsPerTile;
-  const int64_t cb0 = (int64_t)blockIdx.y * CB;
+  // 1-D grid, column blocks fastest: the CTAs that share a row tile run back to back, so the
+  // tile is read from DRAM once and from L2 by the others
+  const int ncb = (int)((k + CB - 1) / CB);
+  const int64_t row0 = (int64_t)(blockIdx.x / ncb) * kRowsPerTile;
+  const int64_t cb0 = (int64_t)(blockIdx.x % ncb) * CB;
 
   V4 pre[VEC ? VPT : 1];
   T pres[VEC ? 1 : SPT];
@@ -107,14 +127,27 @@ __global__ void __launch_bounds__(W * 32, 1)
       }
     }
   };
+  // every prefetch vector of a thread lies in rows of the same residue mod NV (NT is a multiple of
+  // NV * VEC_PER_ROW), so the in-vector permutation is one warp-uniform choice per chunk
+  static_assert(!VEC || (NT / VEC_PER_ROW) % NV == 0, "row residue per thread");
+  auto store_vecs = [&](auto key_c) {
+    constexpr int KEY = decltype(key_c)::value;
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      const int q = tid + j * NT;
+      const int i = q / VEC_PER_ROW, cv = q % VEC_PER_ROW;
+      const int blk = (cv * NV) ^ (i & 31 & ~(NV - 1));
+      *reinterpret_cast<V4*>(As + i * R + blk) = xor_perm(pre[j], KEY);
+    }
+  };
   auto store_chunk = [&]() {
     if constexpr (VEC) {
-#pragma unroll
-      for (int j = 0; j < VPT; ++j) {
-        const int q = tid + j * NT;
-        const int i = q / VEC_PER_ROW, cv = q % VEC_PER_ROW;
-        const int blk = (cv * NV) ^ (i & 31 & ~(NV - 1));
-        *reinterpret_cast<V4*>(As + i * R + blk) = xor_perm(pre[j], i & (NV - 1));
+      const int key = (tid / VEC_PER_ROW) & (NV - 1);
+      if (key == 0) store_vecs(std::integral_constant<int, 0>{});
+      else if (key == 1) store_vecs(std::integral_constant<int, 1>{});
+      else if constexpr (NV == 4) {
+        if (key == 2) store_vecs(std::integral_constant<int, 2>{});
+        else store_vecs(std::integral_constant<int, 3>{});
       }
     } else {
 #pragma unroll
@@ -135,10 +168,21 @@ __global__ void __launch_bounds__(W * 32, 1)
   const int nptr = nchunks * (int)k + 1;
   int32_t* ptr_s = reinterpret_cast<int32_t*>(smem_raw + omega_off);
   uint16_t* ent_s = reinterpret_cast<uint16_t*>(ptr_s + ((nptr + 3) & ~3));
+  // OMS entries are re-coded while staged: (local_r * sizeof(T)) | (neg << 15), so the swizzled
+  // byte address inside the tile is one LOP3, (u & RMASK) ^ LXOR (rows are R * sizeof(T) = 2 KB apart
+  // and the swizzle XORs the lane into the low 5 bits of local_r).
+  constexpr uint32_t SH = sizeof(T) == 8 ? 3u : 2u;
+  constexpr uint32_t RMASK = (uint32_t)(R - 1) << SH;
+  static_assert(R * sizeof(T) == 2048, "row stride of the staged tile");
   if constexpr (OMS) {
     for (int i = tid; i < nptr; i += NT) ptr_s[i] = __ldg(ptr + i);
-    for (int i = tid; i < nnz; i += NT) ent_s[i] = __ldg(ent + i);
+    for (int i = tid; i < nnz; i += NT) {
+      const uint32_t e = __ldg(ent + i);
+      ent_s[i] = (uint16_t)(((e >> 1) << SH) | ((e & 1u) << 15));
+    }
   }
+  const uint32_t tile_s = (uint32_t)__cvta_generic_to_shared(smem_raw);
+  const uint32_t lxor = ((uint32_t)lane << 11) | ((uint32_t)lane << SH);
   auto P = [&](int64_t i) -> int { return OMS ? ptr_s[i] : __ldg(ptr + i); };
   auto E = [&](int i) -> uint32_t { return OMS ? (uint32_t)ent_s[i] : (uint32_t)__ldg(ent + i); };
 
@@ -160,14 +204,26 @@ __global__ void __launch_bounds__(W * 32, 1)
       }
       T s0 = T(0), s1 = T(0);
       int e = lo;
-      for (; e + 2 <= hi; e += 2) {
-        const uint32_t e0 = E(e), e1 = E(e + 1);
-        s0 += flip_if(my_row[(e0 >> 1) ^ lane], e0 & 1u);
-        s1 += flip_if(my_row[(e1 >> 1) ^ lane], e1 & 1u);
-      }
-      if (e < hi) {
-        const uint32_t e0 = E(e);
-        s0 += flip_if(my_row[(e0 >> 1) ^ lane], e0 & 1u);
+      if constexpr (OMS) {
+        for (; e + 2 <= hi; e += 2) {
+          const uint32_t u0 = ent_s[e], u1 = ent_s[e + 1];
+          s0 += flip_if(lds_t<T>(tile_s + ((u0 & RMASK) ^ lxor)), u0 >> 15);
+          s1 += flip_if(lds_t<T>(tile_s + ((u1 & RMASK) ^ lxor)), u1 >> 15);
+        }
+        if (e < hi) {
+          const uint32_t u0 = ent_s[e];
+          s0 += flip_if(lds_t<T>(tile_s + ((u0 & RMASK) ^ lxor)), u0 >> 15);
+        }
+      } else {
+        for (; e + 2 <= hi; e += 2) {
+          const uint32_t e0 = E(e), e1 = E(e + 1);
+          s0 += flip_if(my_row[(e0 >> 1) ^ lane], e0 & 1u);
+          s1 += flip_if(my_row[(e1 >> 1) ^ lane], e1 & 1u);
+        }
+        if (e < hi) {
+          const uint32_t e0 = E(e);
+          s0 += flip_if(my_row[(e0 >> 1) ^ lane], e0 & 1u);
+        }
       }
       acc[j] += s0 + s1;
     }
@@ -207,7 +263,7 @@ int launch_t(const T* A, int64_t n, int64_t d, int64_t lda, const int32_t* ptr, 
   const int64_t nptr = (int64_t)nchunks * k + 1;
   const size_t ptr_bytes = (size_t)((nptr + 3) & ~3) * 4;
   const size_t oms_bytes = nnz > 0 ? ptr_bytes + (size_t)nnz * 2 : (size_t)1 << 30;
-  dim3 grid((unsigned)((n + kRowsPerTile - 1) / kRowsPerTile), (unsigned)((k + CB - 1) / CB));
+  const unsigned grid = (unsigned)(((n + kRowsPerTile - 1) / kRowsPerTile) * ((k + CB - 1) / CB));
   if (base + oms_bytes <= 200 * 1024) {
     const size_t smem = base + oms_bytes;
     auto kern = sparse_right_kernel<T, kWarps, CPW, R, VEC, true>;
