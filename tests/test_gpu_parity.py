@@ -166,3 +166,33 @@ def test_pipelined_host_path_matches_device(cuda):
     y_np = tm.apply_right(a_host.numpy())
     assert isinstance(y_np, np.ndarray) and y_np.dtype == np.float64
     assert np.array_equal(y_np, ref.double().numpy())
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 149, 297])
+def test_srtt_tc_row_counts_and_strides(n, cuda):
+    """The tcgen05 SRTT kernel (d = 8192, float32): odd row counts, fewer rows than SMs, padded lda."""
+    import torch
+
+    d, k = 8192, 512
+    tm = skb.SparseRttTM(d, k, 1, "wht", seed=2)
+    g = torch.Generator(device=cuda).manual_seed(n)
+    big = torch.randn(max(n, 1), d + 12, device=cuda, generator=g)[:n]
+    a = big[:, 4:d + 4]  # lda = d + 12, rows start 16 bytes in: bulk copies stay 16-byte aligned
+    y = tm.apply_right(a)
+    assert y.shape == (n, k)
+    if n:
+        dv, samp = orc.srtt_parts(d, k, 1, 2)
+        assert rel_err(y.cpu().numpy(), orc.srtt_right(dv, samp, a.cpu().numpy(), "wht")) <= 1e-5
+        # strided and contiguous launches agree
+        assert rel_err(y.cpu().numpy(), tm.apply_right(a.contiguous()).cpu().numpy()) <= 1e-5
+
+
+def test_srtt_tc_matches_cuda_core_kernel(cuda, monkeypatch):
+    import torch
+
+    tm = skb.SparseRttTM(8192, 512, 3, "wht", seed=9)
+    a = torch.randn(1000, 8192, device=cuda)
+    y_tc = tm.apply_right(a).double()
+    monkeypatch.setenv("SKETCH_B200_SRTT", "regs")
+    y_cc = tm.apply_right(a).double()
+    assert float((y_tc - y_cc).norm() / y_cc.norm()) <= 1e-5
