@@ -111,6 +111,14 @@ SK_API size_t sk_sparse_adjoint_wide_workspace_bytes(int64_t d, int64_t m, int64
 SK_API int sk_sparse_adjoint_wide(const float* A, int64_t d, int64_t m, int64_t lda, const uint16_t* enc,
                                   const int64_t* seg_off, int32_t seg_cap, int64_t k, double scale, float* SA,
                                   int64_t ldsa, int accumulate, void* ws, size_t ws_bytes, void* stream);
+/* The same for the row block [r0, r1) of Omega (r0 % 128 == 0): A points at row r0 of the operand
+ * and holds r1 - r0 rows; SA (+)= scale * Omega[r0:r1]^T * A. Lets a caller stream A through L2 in
+ * row blocks and chain other kernels on each block (two-sided sketches). Workspace:
+ * sk_sparse_adjoint_wide_workspace_bytes(r1 - r0, m, k). */
+SK_API int sk_sparse_adjoint_wide_rows(const float* A, int64_t d, int64_t r0, int64_t r1, int64_t m, int64_t lda,
+                                       const uint16_t* enc, const int64_t* seg_off, int32_t seg_cap, int64_t k,
+                                       double scale, float* SA, int64_t ldsa, int accumulate, void* ws,
+                                       size_t ws_bytes, void* stream);
 
 /*
  * K3 — Y[n,k] = A[n,d] * D * F * S for the sparse randomized trigonometric transform,

@@ -45,6 +45,8 @@ SIGNATURES = {
     "sk_sparse_adjoint_wide_workspace_bytes": (_c_size, [_c_i64, _c_i64, _c_i64]),
     "sk_sparse_adjoint_wide": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, ctypes.c_int32, _c_i64, _c_dbl, _c_p,
                                         _c_i64, _c_int, _c_p, _c_size, _c_p]),
+    "sk_sparse_adjoint_wide_rows": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_p, ctypes.c_int32,
+                                             _c_i64, _c_dbl, _c_p, _c_i64, _c_int, _c_p, _c_size, _c_p]),
     "sk_srtt_right": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_int, _c_p, ctypes.c_int32, _c_i64,
                                _c_dbl, _c_p, _c_i64, _c_p]),
     "sk_dense_tc_supported": (_c_int, [_c_i64]),

@@ -66,6 +66,7 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 struct WParams {
   int64_t d, m, k;
   int nchunks, ngroups, nslices, npieces, chunks_per_piece;
+  int64_t chunk_base;  // first encoded chunk of this launch (row block [128 * chunk_base, ...))
   uint32_t stage_bytes;
   const uint16_t* enc;
   const int64_t* seg_off;  // [nchunks * ngroups + 1], uint16 units
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__((W_WARPS + 1) * 32, 1)
         const int s = i % W_STAGES;
         if (i >= W_STAGES) mbar_wait(&consumed[s], (uint32_t)(i / W_STAGES - 1) & 1u);
         const int h = h0 + i;
-        const int64_t sg = (int64_t)h * p.ngroups + g;
+        const int64_t sg = (p.chunk_base + h) * p.ngroups + g;
         const uint32_t seg_bytes = (uint32_t)(p.seg_off[sg + 1] - p.seg_off[sg]) * 2u;
         const uint32_t st = smem_u32(smem + (size_t)s * p.stage_bytes);
         mbar_arrive_expect_tx(&full[s], W_TILE + seg_bytes);
@@ -303,22 +304,26 @@ extern "C" size_t sk_sparse_adjoint_wide_workspace_bytes(int64_t d, int64_t m, i
   return wide_plan(d, m, k, 0).ws_bytes;
 }
 
-extern "C" int sk_sparse_adjoint_wide(const float* A, int64_t d, int64_t m, int64_t lda, const uint16_t* enc,
-                                      const int64_t* seg_off, int32_t seg_cap, int64_t k, double scale, float* SA,
-                                      int64_t ldsa, int accumulate, void* ws, size_t ws_bytes, void* stream) {
+extern "C" int sk_sparse_adjoint_wide_rows(const float* A, int64_t d, int64_t r0, int64_t r1, int64_t m,
+                                           int64_t lda, const uint16_t* enc, const int64_t* seg_off, int32_t seg_cap,
+                                           int64_t k, double scale, float* SA, int64_t ldsa, int accumulate, void* ws,
+                                           size_t ws_bytes, void* stream) {
   if (d < 1 || m < 0 || k < 1 || lda < m || ldsa < m || seg_cap < W_HDR)
     return fail(SK_EINVAL, "sk_sparse_adjoint_wide: bad shape/leading dimension");
+  if (r0 < 0 || r1 > d || r0 >= r1 || (r0 % W_R) != 0)
+    return fail(SK_EINVAL, "sk_sparse_adjoint_wide: row block must be [r0, r1) within [0, d) with r0 % 128 == 0");
   if (m == 0) return SK_OK;
   if (!A || !SA || !enc || !seg_off) return fail(SK_EINVAL, "sk_sparse_adjoint_wide: null pointer");
   if ((reinterpret_cast<uintptr_t>(A) & 15) || (lda & 3))
     return fail(SK_EUNSUPPORTED, "sk_sparse_adjoint_wide: A must be 16-byte aligned with lda % 4 == 0");
-  const WPlan pl = wide_plan(d, m, k, seg_cap);
+  const int64_t rows = r1 - r0;
+  const WPlan pl = wide_plan(rows, m, k, seg_cap);
   if (pl.smem > 227 * 1024) return fail(SK_EUNSUPPORTED, "sk_sparse_adjoint_wide: segment capacity too large");
   if (ws_bytes < pl.ws_bytes || !ws) return fail(SK_EINVAL, "sk_sparse_adjoint_wide: workspace too small");
   sm100::EncodeTiledFnT fn = sm100::encode_tiled_fn();
   if (!fn) return fail(SK_ECUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap tm;
-  cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)d};
+  cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)lda * 4};
   cuuint32_t box[2] = {(cuuint32_t)W_COLS, (cuuint32_t)W_R};
   cuuint32_t estr[2] = {1, 1};
@@ -327,7 +332,7 @@ extern "C" int sk_sparse_adjoint_wide(const float* A, int64_t d, int64_t m, int6
          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return fail(SK_EINVAL, "sk_sparse_adjoint_wide: cannot describe A for TMA");
   WParams p{};
-  p.d = d;
+  p.d = rows;
   p.m = m;
   p.k = k;
   p.nchunks = pl.nchunks;
@@ -335,6 +340,7 @@ extern "C" int sk_sparse_adjoint_wide(const float* A, int64_t d, int64_t m, int6
   p.nslices = pl.nslices;
   p.npieces = pl.npieces;
   p.chunks_per_piece = pl.chunks_per_piece;
+  p.chunk_base = r0 / W_R;
   p.stage_bytes = pl.stage_bytes;
   p.enc = enc;
   p.seg_off = seg_off;
@@ -346,4 +352,11 @@ extern "C" int sk_sparse_adjoint_wide(const float* A, int64_t d, int64_t m, int6
   int st = check_launch("sk_sparse_adjoint_wide");
   if (st != SK_OK) return st;
   return adjoint_reduce_f32(p.part, pl.npieces, k, m, scale, SA, ldsa, accumulate, s);
+}
+
+extern "C" int sk_sparse_adjoint_wide(const float* A, int64_t d, int64_t m, int64_t lda, const uint16_t* enc,
+                                      const int64_t* seg_off, int32_t seg_cap, int64_t k, double scale, float* SA,
+                                      int64_t ldsa, int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  return sk_sparse_adjoint_wide_rows(A, d, 0, d, m, lda, enc, seg_off, seg_cap, k, scale, SA, ldsa, accumulate, ws,
+                                     ws_bytes, stream);
 }

@@ -22,8 +22,10 @@ import numpy as np
 
 from ._device import require_cuda, to_operand
 
-__all__ = ["SvdFactorization", "LsqrResult", "orth", "rsvd", "rsvd_residual", "sketch_and_solve",
-           "truncated_pinv_apply", "sketch_precondition_lsqr", "EPS", "DEFAULT_RANK_TOL"]
+__all__ = ["SvdFactorization", "OuterProduct", "EigFactorization", "LsqrResult", "PositiveDefinitenessError", "orth",
+           "rsvd", "rsvd_residual", "nystrom_psd", "gen_nystrom_outer", "gen_nystrom_svd", "two_sided_sketch",
+           "default_left_dim", "sketch_and_solve", "truncated_pinv_apply", "sketch_precondition_lsqr", "EPS",
+           "DEFAULT_RANK_TOL"]
 
 EPS = float(np.finfo(np.float64).eps)
 DEFAULT_RANK_TOL = 5.0 * EPS  # reference core/factor.py:27-28
@@ -40,6 +42,40 @@ class SvdFactorization:
     def to_numpy(self) -> "SvdFactorization":
         return SvdFactorization(*(x.cpu().numpy() if hasattr(x, "cpu") else np.asarray(x)
                                   for x in (self.u, self.sigma, self.v)))
+
+
+@dataclass
+class OuterProduct:
+    """A ~= f g^* (reference core/containers.py:124-146)."""
+
+    f: object
+    g: object
+
+    @property
+    def rank(self) -> int:
+        return self.f.shape[1]
+
+    def matrix(self):
+        return self.f @ self.g.conj().T
+
+
+@dataclass
+class EigFactorization:
+    """Psd A ~= u diag(lam) u^* (reference core/containers.py:180-206)."""
+
+    u: object
+    lam: object
+
+    @property
+    def rank(self) -> int:
+        return self.lam.shape[0]
+
+    def matrix(self):
+        return (self.u * self.lam) @ self.u.conj().T
+
+
+class PositiveDefinitenessError(np.linalg.LinAlgError):
+    """Cholesky met a non-positive pivot (reference core/factor.py:31-32)."""
 
 
 @dataclass
@@ -213,6 +249,235 @@ def sketch_and_solve(a, b, tm_psi):
     if squeeze:
         out = out[:, 0]
     return _back(out, kind)
+
+
+def default_left_dim(k: int) -> int:
+    """Recommended left-sketch dimension p = ceil(1.5 k) (reference rand_nla.py:48-50)."""
+    return int(np.ceil(1.5 * k))
+
+
+def _svd_econ(m):
+    import torch
+
+    u, s, vh = torch.linalg.svd(_t64(m), full_matrices=False)
+    return u, s, vh.conj().T
+
+
+def _rank_of(s) -> int:
+    return 0 if s.numel() == 0 or float(s[0]) == 0.0 else int((s > DEFAULT_RANK_TOL * s[0]).sum())
+
+
+def two_sided_sketch(a, tm_omega, tm_psi, *, block_bytes: int = 64 << 20):
+    """Y = A Omega (n x k) and X = A^* Psi (d x p) with ONE pass of A through HBM.
+
+    For a float32 device A and a sparse-sign Psi (the register-accumulator adjoint kernel), A is
+    streamed in row blocks of about `block_bytes` (multiples of 128 rows) that stay resident in the
+    126 MB L2: the right kernel reads a block from DRAM and the adjoint kernel re-reads it from L2,
+    accumulating Psi[rows]^T A[rows] into X^*. Other operand / family combinations fall back to two
+    passes (the same results). Returns device tensors in A's precision.
+    """
+    import torch
+
+    A, _ = _as_device_2d(a)
+    n, d = A.shape
+    fused = (A.is_cuda and A.dtype == torch.float32 and hasattr(tm_psi, "adjoint_rows")
+             and tm_psi.adjoint_path(A) == "wide")
+    if not fused:
+        return tm_omega.apply_right(A), tm_psi.apply_adjoint(A).conj().T
+    rows = max(128, (block_bytes // (d * 4)) // 128 * 128)
+    y = torch.empty((n, tm_omega.k), dtype=A.dtype, device=A.device)
+    xt = torch.empty((tm_psi.k, d), dtype=A.dtype, device=A.device)
+    for r0 in range(0, n, rows):
+        r1 = min(n, r0 + rows)
+        blk = A[r0:r1]
+        y[r0:r1] = tm_omega.apply_right(blk)
+        tm_psi.adjoint_rows(blk, r0, r1, xt, accumulate=r0 > 0)
+    return y, xt.T
+
+
+def _gn_core(A, tm_omega, tm_psi) -> OuterProduct:
+    """Reference rand_nla.py:191-202 on the device (float64 small factorizations)."""
+    y, x = two_sided_sketch(A, tm_omega, tm_psi)
+    w = tm_omega.apply_right(x.conj().T.contiguous())  # (Psi^* A) Omega, p x k
+    u, s, v = _svd_econ(w)
+    r = _rank_of(s)
+    f = _t64(y) @ (v[:, :r] / s[:r])
+    g = _t64(x) @ u[:, :r]
+    return OuterProduct(f=f, g=g)
+
+
+def _validate_gn(shape, k: int, p: int, tm_omega, tm_psi):
+    n, d = shape
+    if not (k <= p <= min(n, d)):
+        raise ValueError(f"need k <= p <= min(n, d); got k={k}, p={p}, shape={shape}")
+    if tm_omega.d != d or tm_omega.k != k:
+        raise ValueError("right test matrix has wrong dimensions")
+    if tm_psi.d != n or tm_psi.k != p:
+        raise ValueError("left test matrix has wrong dimensions")
+    return n, d
+
+
+def _adjoint_dev(A):
+    import torch
+
+    out = torch.empty((A.shape[1], A.shape[0]), dtype=A.dtype, device=A.device)
+    out.copy_(A.conj().T)
+    return out
+
+
+def _back_factors(obj, kind):
+    if kind not in ("numpy", "torch-cpu"):
+        return obj
+    return type(obj)(*(_back(getattr(obj, f), kind) for f in obj.__dataclass_fields__))
+
+
+def gen_nystrom_outer(a, k: int, p: int, tm_omega, tm_psi) -> OuterProduct:
+    """Generalized Nystrom A ~= F G^* (reference rand_nla.py:216-227); wide inputs via the adjoint."""
+    require_cuda()
+    n, d = _validate_gn(tuple(a.shape), k, p, tm_omega, tm_psi)
+    A, kind = _as_device_2d(a)
+    if n < d:
+        flipped = _gn_core(_adjoint_dev(A), tm_psi, tm_omega)
+        out = OuterProduct(f=flipped.g, g=flipped.f)
+    else:
+        out = _gn_core(A, tm_omega, tm_psi)
+    return _back_factors(out, kind)
+
+
+def _gn_svd_core(A, tm_omega, tm_psi) -> SvdFactorization:
+    """Reference rand_nla.py:230-245 on the device."""
+    import torch
+
+    y, x = two_sided_sketch(A, tm_omega, tm_psi)
+    q, _ = torch.linalg.qr(_t64(y), mode="reduced")
+    pmat, t = torch.linalg.qr(_t64(x), mode="reduced")
+    w = _t64(tm_psi.apply_adjoint(q))  # p x k
+    u1, s1, v1 = _svd_econ(w)
+    r = _rank_of(s1)
+    core = v1[:, :r] @ ((u1[:, :r].conj().T @ t.conj().T) / s1[:r, None])
+    u2, s2, v2 = _svd_econ(core)
+    return SvdFactorization(u=q @ u2, sigma=s2, v=pmat @ v2)
+
+
+def _outer_to_svd(op: OuterProduct) -> SvdFactorization:
+    """Reference rand_nla.py:248-259."""
+    import torch
+
+    if op.rank == 0:
+        z = op.f.new_zeros
+        return SvdFactorization(u=z((op.f.shape[0], 0)), sigma=z(0, dtype=torch.float64), v=z((op.g.shape[0], 0)))
+    qf, rf = torch.linalg.qr(op.f, mode="reduced")
+    qg, rg = torch.linalg.qr(op.g, mode="reduced")
+    u, s, v = _svd_econ(rf @ rg.conj().T)
+    return SvdFactorization(u=qf @ u, sigma=s, v=qg @ v)
+
+
+def gen_nystrom_svd(a, k: int, p: int, tm_omega, tm_psi) -> SvdFactorization:
+    """Generalized Nystrom in compact SVD form (reference rand_nla.py:262-275)."""
+    require_cuda()
+    n, d = _validate_gn(tuple(a.shape), k, p, tm_omega, tm_psi)
+    A, kind = _as_device_2d(a)
+    if n < d:
+        flipped = _gn_core(_adjoint_dev(A), tm_psi, tm_omega)
+        out = _outer_to_svd(OuterProduct(f=flipped.g, g=flipped.f))
+    else:
+        out = _gn_svd_core(A, tm_omega, tm_psi)
+    return _back_factors(out, kind)
+
+
+def _spectral_norm(y, iters: int = 20, seed: int = 0) -> float:
+    """Power-iteration ||Y||_2 estimate, same start vector stream (reference rand_nla.py:112-131)."""
+    import torch
+
+    from .rng import RngStream
+
+    if y.numel() == 0:
+        return 0.0
+    v0 = RngStream(seed, ("spectral-norm",)).generator().standard_normal(y.shape[1])
+    y = _t64(y)
+    v = torch.as_tensor(v0, device=y.device, dtype=y.dtype)
+    v = v / torch.linalg.vector_norm(v)
+    sigma = 0.0
+    for _ in range(iters):
+        w = y @ v
+        nw = float(torch.linalg.vector_norm(w))
+        if nw == 0.0:
+            return 0.0
+        v = y.conj().T @ (w / nw)
+        sigma = float(torch.linalg.vector_norm(v))
+        if sigma == 0.0:
+            return 0.0
+        v = v / sigma
+        sigma = float(np.sqrt(sigma * nw))
+    return sigma
+
+
+def _check_psd(A, tol: float = 1e-8, probes: int = 8, seed: int = 0) -> None:
+    """Sampled self-adjointness / psd check (reference rand_nla.py:134-149)."""
+    import torch
+
+    from .rng import RngStream
+
+    n = A.shape[0]
+    v = torch.as_tensor(RngStream(seed, ("psd-check",)).generator().standard_normal((n, probes)), device=A.device)
+    with _no_tf32():
+        av = _t64(A) @ v.to(torch.complex128 if A.is_complex() else torch.float64)
+    quad = (v.conj() * av).sum(0)
+    scale = max(float(torch.linalg.vector_norm(av, dim=0).max()), 1e-300) / np.sqrt(n)
+    norms2 = (v.conj() * v).sum(0).real
+    if bool((quad.imag.abs() > tol * scale * norms2).any()) if quad.is_complex() else False:
+        raise ValueError("input is not self-adjoint to psd-check tolerance")
+    if bool((quad.real < -tol * scale * norms2).any()):
+        raise ValueError("input fails the sampled psd check")
+
+
+def _cholesky_upper(m):
+    """Upper C with M = C^* C (reference core/factor.py:85-104)."""
+    import torch
+
+    scale = float(torch.linalg.matrix_norm(m))
+    if scale > 0 and float(torch.linalg.matrix_norm(m - m.conj().T)) > 1e-10 * scale:
+        raise ValueError("input is not self-adjoint to tolerance 1e-10")
+    lower, info = torch.linalg.cholesky_ex(m)
+    if int(info) != 0:
+        raise PositiveDefinitenessError(f"leading minor of order {int(info)} is not positive")
+    return lower.conj().T
+
+
+def nystrom_psd(a, k: int, tm, *, max_shift_retries: int = 3) -> EigFactorization:
+    """Single-pass psd Nystrom with the stabilizing shift (reference rand_nla.py:152-188)."""
+    import torch
+
+    require_cuda()
+    shape = tuple(a.shape)
+    n, n2 = shape
+    if n != n2:
+        raise ValueError("nystrom_psd needs a square matrix")
+    if tm.d != n or tm.k != k:
+        raise ValueError(f"test matrix {tm!r} incompatible with A {shape} and k={k}")
+    A, kind = _as_device_2d(a)
+    _check_psd(A, seed=tm.seed)
+    y = _t64(tm.apply_right(A))
+    omega = torch.as_tensor(np.ascontiguousarray(tm.materialize()), device=y.device).to(y.dtype)
+    nu = np.sqrt(n) * EPS * _spectral_norm(y, seed=tm.seed)
+    last_exc = None
+    for _ in range(max_shift_retries + 1):
+        y_nu = y + nu * omega if nu > 0 else y.clone()
+        core = _t64(tm.apply_adjoint(y_nu))
+        core = (core + core.conj().T) / 2.0
+        try:
+            c = _cholesky_upper(core)
+        except PositiveDefinitenessError as exc:
+            last_exc = exc
+            if nu == 0.0:
+                nu = np.sqrt(n) * EPS * max(_spectral_norm(y, seed=tm.seed), 1.0)
+            nu *= 10.0
+            continue
+        b = torch.linalg.solve_triangular(c, y_nu, upper=True, left=False)  # X C = Y_nu
+        u, s, _ = _svd_econ(b)
+        lam = torch.clamp(s ** 2 - nu, min=0.0)
+        return _back_factors(EigFactorization(u=u[:, :k], lam=lam[:k]), kind)
+    raise PositiveDefinitenessError(f"Cholesky failed after {max_shift_retries} shift increases: {last_exc}")
 
 
 def _matvec_blocks(A, v, block_rows):

@@ -212,6 +212,28 @@ class _SignSparseTM(TestMatrix):
                    and b.stride(1) == 1 and b.shape[1] >= 1)
         return "wide" if (wide_ok and forced != "gather") else "gather"
 
+    def adjoint_rows(self, b_rows, r0: int, r1: int, out, accumulate: bool) -> None:
+        """out (+)= Omega[r0:r1]^T b_rows for a float32 device block b_rows = B[r0:r1] (K2w).
+
+        r0 must be a multiple of 128 (the encoding's row chunk); used to stream a tall operand
+        through L2 one row block at a time while other kernels reuse the same block.
+        """
+        import torch
+
+        if self.adjoint_path(b_rows) != "wide":
+            raise NotImplementedError("adjoint_rows needs an aligned float32 device block (wide path)")
+        enc, seg_off, cap, mag = self._adjoint_wide_on(b_rows.device)
+        m = b_rows.shape[1]
+        lib = _lib.load()
+        ws_bytes = lib.sk_sparse_adjoint_wide_workspace_bytes(r1 - r0, m, self.k)
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=b_rows.device)
+        with torch.cuda.device(b_rows.device):
+            st = lib.sk_sparse_adjoint_wide_rows(b_rows.data_ptr(), self.d, r0, r1, m, b_rows.stride(0),
+                                                 enc.data_ptr(), seg_off.data_ptr(), cap, self.k, mag,
+                                                 out.data_ptr(), out.stride(0), 1 if accumulate else 0,
+                                                 ws.data_ptr(), ws_bytes, torch.cuda.current_stream().cuda_stream)
+        _lib.check(st, "sk_sparse_adjoint_wide_rows")
+
     def _adjoint_device(self, b):
         import torch
 

@@ -85,3 +85,17 @@ def rel_err(x, ref) -> float:
     x = np.asarray(x, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     return float(np.linalg.norm(x - ref) / max(np.linalg.norm(ref), 1e-300))
+
+
+def nystrom_inputs():
+    """(tall 1024x300, wide 300x256, psd 512x512, probe 512x3) for the Nystrom golden fixtures."""
+    rng = np.random.default_rng(2508)
+    u1, _ = np.linalg.qr(rng.standard_normal((1024, 40)))
+    v1, _ = np.linalg.qr(rng.standard_normal((300, 40)))
+    agn = (u1 * (0.7 ** np.arange(40))) @ v1.T
+    aw = agn[:256].T.copy()
+    q, _ = np.linalg.qr(rng.standard_normal((512, 512)))
+    apsd = (q * (0.8 ** np.arange(512))) @ q.T
+    apsd = (apsd + apsd.T) / 2
+    probe = rng.standard_normal((512, 3))
+    return agn, aw, apsd, probe

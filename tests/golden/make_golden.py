@@ -122,6 +122,31 @@ def small_fixtures() -> dict:
     out["sas_A"] = al
     out["sas_b"] = bl
     out["sas_x"] = sketch_and_solve(al, bl, SparseUniformTM(3000, 200, 8, seed=9))
+    # generalized Nystrom (rand_nla.py:191-275) and psd Nystrom (rand_nla.py:152-188); inputs are
+    # rebuilt by nystrom_inputs() in the tests, approximations stored as products with probes
+    from sketchkit.rand_nla import gen_nystrom_outer, gen_nystrom_svd, nystrom_psd
+    from sketchkit.sketch import GaussianTM
+
+    sys.path[:0] = [os.path.dirname(HERE), os.path.dirname(os.path.dirname(HERE))]  # tests/, repo root
+    from _cases import nystrom_inputs
+
+    agn, aw, apsd, probe = nystrom_inputs()
+    for name, (om, ps) in {
+        "gn_su": (SparseUniformTM(300, 20, 4, seed=21), SparseUniformTM(1024, 30, 4, seed=22)),
+        "gn_rtt": (SparseRttTM(300, 20, 2, "dct", seed=23), SparseUniformTM(1024, 30, 8, seed=24)),
+    }.items():
+        fo = gen_nystrom_outer(agn, 20, 30, om, ps)
+        out[f"{name}_outer_probe"] = fo.f @ (fo.g.conj().T @ probe[:300])
+        fs = gen_nystrom_svd(agn, 20, 30, om, ps)
+        out[f"{name}_svd_sigma"] = fs.sigma
+        out[f"{name}_svd_probe"] = (fs.u * fs.sigma) @ (fs.v.conj().T @ probe[:300])
+    # wide input: processed through the adjoint (rand_nla.py:222-226, 271-273)
+    fo = gen_nystrom_outer(aw, 20, 30, SparseUniformTM(256, 20, 4, seed=25), SparseUniformTM(300, 30, 4, seed=26))
+    out["gn_wide_outer_probe"] = fo.f @ (fo.g.conj().T @ probe[:256])
+    for name, tm in (("nys_su", SparseUniformTM(512, 30, 4, seed=27)), ("nys_gauss", GaussianTM(512, 30, seed=28))):
+        fe = nystrom_psd(apsd, 30, tm)
+        out[f"{name}_lam"] = fe.lam
+        out[f"{name}_probe"] = (fe.u * fe.lam) @ (fe.u.conj().T @ probe)
     return out
 
 
