@@ -228,7 +228,8 @@ WPlan wide_plan(int64_t d, int64_t m, int64_t k, int32_t seg_cap) {
   pl.nslices = (int)((m + W_COLS - 1) / W_COLS);
   const int64_t roles = (int64_t)pl.ngroups * pl.nslices;
   int64_t pieces = (4 * (int64_t)sm_count() + roles - 1) / roles;
-  if (pieces > pl.nchunks) pieces = pl.nchunks;
+  // at least 8 chunks per piece: the ring must fill, and every piece adds a k x m partial
+  if (pieces > (pl.nchunks + 7) / 8) pieces = (pl.nchunks + 7) / 8;
   if (pieces < 1) pieces = 1;
   pl.chunks_per_piece = (int)((pl.nchunks + pieces - 1) / pieces);
   pl.npieces = (pl.nchunks + pl.chunks_per_piece - 1) / pl.chunks_per_piece;

@@ -17,6 +17,7 @@
 // Butterfly order does not matter (the per-bit butterflies commute); natural Hadamard order as in
 // the reference (`top = y0 + y1`, `bot = y0 - y1`).
 //
+// Small rows (d = 2^L, 32 <= d <= 512): one warp per row (shuffle butterflies).
 // Other sizes (d = 2^L, row fits shared memory): one CTA per row, row in shared memory.
 #include <stdlib.h>
 
@@ -443,6 +444,108 @@ __global__ void srtt_wht_simple(const T* __restrict__ A, int64_t n, int64_t d, i
   }
 }
 
+// Small rows (d = 2^L, 5 <= L <= 9): one warp per row, V = d/32 consecutive values per lane.
+// In-register butterflies over the low log2(V) index bits, shuffle butterflies over the 5 lane
+// bits, then the warp's transformed row goes to a private shared-memory buffer for the sampled
+// gather (coalesced row loads, one HBM pass, no CTA barrier).
+template <typename T, int L, bool SIGNS, bool VEC>
+__global__ void __launch_bounds__(256)
+    srtt_wht_warp(const T* __restrict__ A, int64_t n, int64_t lda, const T* __restrict__ dvals,
+                  const int32_t* __restrict__ samp, int xi, int k, T scale, T* __restrict__ Y, int64_t ldy) {
+  constexpr int D = 1 << L, V = D / 32, NV = 16 / sizeof(T);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T* buf = reinterpret_cast<T*>(smem_raw) + warp * D;
+  T dv[V];
+  uint32_t dmask = 0;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    dv[v] = dvals[lane * V + v];
+    if (dv[v] < T(0)) dmask |= 1u << v;
+  }
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; row < n; row += wstride) {
+    const T* a = A + row * lda + lane * V;
+    T x[V];
+    if constexpr (VEC && (V % NV) == 0) {
+#pragma unroll
+      for (int q = 0; q < V / NV; ++q) {
+        T tmp[NV];
+        if constexpr (sizeof(T) == 4) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(a) + q);
+          tmp[0] = f.x; tmp[1] = f.y; tmp[2] = f.z; tmp[3] = f.w;
+        } else {
+          const double2 f = __ldg(reinterpret_cast<const double2*>(a) + q);
+          tmp[0] = f.x; tmp[1] = f.y;
+        }
+#pragma unroll
+        for (int c = 0; c < NV; ++c) x[q * NV + c] = tmp[c];
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) x[v] = __ldg(a + v);
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) x[v] = SIGNS ? flip_if(x[v], (dmask >> v) & 1u) : x[v] * dv[v];
+#pragma unroll
+    for (int h = 1; h < V; h <<= 1)
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        if ((v & h) == 0) butterfly(x[v], x[v | h]);
+#pragma unroll
+    for (int h = 1; h < 32; h <<= 1) {
+      const bool bottom = (lane & h) != 0;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const T o = __shfl_xor_sync(0xffffffffu, x[v], h);
+        x[v] = bottom ? o - x[v] : x[v] + o;
+      }
+    }
+    __syncwarp();  // previous row's gather is done with buf
+#pragma unroll
+    for (int v = 0; v < V; ++v) buf[lane * V + v] = x[v];
+    __syncwarp();
+    T* y = Y + row * ldy;
+    for (int c = lane; c < k; c += 32) {
+      T acc = T(0);
+      for (int u = 0; u < xi; ++u) {
+        const uint32_t e = (uint32_t)__ldg(samp + (int64_t)c * xi + u);
+        acc += flip_if(buf[e & 0x7fffffffu], e >> 31);
+      }
+      y[c] = acc * scale;
+    }
+  }
+}
+
+template <typename T, int L, bool SIGNS>
+int launch_warp(const T* A, int64_t n, int64_t lda, const T* dv, const int32_t* samp, int xi, int k, double scale,
+                T* Y, int64_t ldy, bool vec, cudaStream_t s) {
+  const size_t smem = sizeof(T) * ((size_t)8 << L);
+  auto kern = vec ? srtt_wht_warp<T, L, SIGNS, true> : srtt_wht_warp<T, L, SIGNS, false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)sm_count() * per_sm;
+  const int64_t need = (n + 7) / 8;
+  if (grid > need) grid = need;
+  kern<<<(unsigned)grid, 256, smem, s>>>(A, n, lda, dv, samp, xi, k, (T)scale, Y, ldy);
+  return check_launch("sk_srtt_right(warp)");
+}
+
+template <typename T, bool SIGNS>
+int dispatch_warp(int L, const T* A, int64_t n, int64_t lda, const T* dv, const int32_t* samp, int xi, int k,
+                  double scale, T* Y, int64_t ldy, bool vec, cudaStream_t s) {
+  switch (L) {
+    case 5: return launch_warp<T, 5, SIGNS>(A, n, lda, dv, samp, xi, k, scale, Y, ldy, vec, s);
+    case 6: return launch_warp<T, 6, SIGNS>(A, n, lda, dv, samp, xi, k, scale, Y, ldy, vec, s);
+    case 7: return launch_warp<T, 7, SIGNS>(A, n, lda, dv, samp, xi, k, scale, Y, ldy, vec, s);
+    case 8: return launch_warp<T, 8, SIGNS>(A, n, lda, dv, samp, xi, k, scale, Y, ldy, vec, s);
+    case 9: return launch_warp<T, 9, SIGNS>(A, n, lda, dv, samp, xi, k, scale, Y, ldy, vec, s);
+    default: return fail(SK_EUNSUPPORTED, "sk_srtt_right: no warp WHT for this length");
+  }
+}
+
 template <typename T, int L, bool SIGNS>
 int launch_fast(const T* A, int64_t n, int64_t lda, const T* dv, const int32_t* samp, int xi, int k,
                 double scale, T* Y, int64_t ldy, cudaStream_t s) {
@@ -504,6 +607,12 @@ int run(const void* A_, int64_t n, int64_t d, int64_t lda, const void* dv_, bool
     // Rademacher diagonals take the sign-mask path; any other diagonal multiplies.
     return pm1 ? dispatch_L<T, true>(L, A, n, lda, dv, samp, xi, (int)k, scale, Y, ldy, s)
                : dispatch_L<T, false>(L, A, n, lda, dv, samp, xi, (int)k, scale, Y, ldy, s);
+  }
+  if (L >= 5 && L <= 9 && (int64_t(1) << L) == d) {
+    const bool dv_aligned = (reinterpret_cast<uintptr_t>(dv) & 15) == 0;
+    const bool vec = aligned && dv_aligned;
+    return pm1 ? dispatch_warp<T, true>(L, A, n, lda, dv, samp, xi, (int)k, scale, Y, ldy, vec, s)
+               : dispatch_warp<T, false>(L, A, n, lda, dv, samp, xi, (int)k, scale, Y, ldy, vec, s);
   }
   const size_t smem = sizeof(T) * (size_t)d;
   if (smem > 200 * 1024) return fail(SK_EUNSUPPORTED, "sk_srtt_right: row does not fit shared memory");

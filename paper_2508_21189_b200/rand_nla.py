@@ -267,20 +267,22 @@ def _rank_of(s) -> int:
     return 0 if s.numel() == 0 or float(s[0]) == 0.0 else int((s > DEFAULT_RANK_TOL * s[0]).sum())
 
 
-def two_sided_sketch(a, tm_omega, tm_psi, *, block_bytes: int = 64 << 20):
-    """Y = A Omega (n x k) and X = A^* Psi (d x p) with ONE pass of A through HBM.
+def two_sided_sketch(a, tm_omega, tm_psi, *, one_pass: bool = False, block_bytes: int = 64 << 20):
+    """Y = A Omega (n x k) and X = A^* Psi (d x p) for the generalized Nystrom drivers.
 
-    For a float32 device A and a sparse-sign Psi (the register-accumulator adjoint kernel), A is
-    streamed in row blocks of about `block_bytes` (multiples of 128 rows) that stay resident in the
-    126 MB L2: the right kernel reads a block from DRAM and the adjoint kernel re-reads it from L2,
-    accumulating Psi[rows]^T A[rows] into X^*. Other operand / family combinations fall back to two
-    passes (the same results). Returns device tensors in A's precision.
+    one_pass=True: for a float32 device A and a sparse-sign Psi, A is streamed in
+    row blocks of about `block_bytes` (multiples of 128 rows) that stay resident in the 126 MB L2:
+    the right kernel reads a block from DRAM and the adjoint kernel re-reads it from L2,
+    accumulating Psi[rows]^T A[rows] into X^*. Measured (tools/two_sided_probe.py, A 2M x 512 f32):
+    two passes 7.1 ms; one pass 9.8 ms at 64 MB blocks, 7.5 ms at 1 GB — the adjoint is issue-bound
+    and each block costs two host-side launches, so the default is two passes (same results).
+    Returns device tensors in A's precision.
     """
     import torch
 
     A, _ = _as_device_2d(a)
     n, d = A.shape
-    fused = (A.is_cuda and A.dtype == torch.float32 and hasattr(tm_psi, "adjoint_rows")
+    fused = (one_pass and A.is_cuda and A.dtype == torch.float32 and hasattr(tm_psi, "adjoint_rows")
              and tm_psi.adjoint_path(A) == "wide")
     if not fused:
         return tm_omega.apply_right(A), tm_psi.apply_adjoint(A).conj().T

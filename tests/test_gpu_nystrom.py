@@ -60,7 +60,7 @@ def test_two_sided_sketch_one_pass(cuda):
     a = torch.randn(n, d, device=cuda)
     om = skb.SparseRttTM(d, k, 1, "wht", seed=1)
     ps = skb.SparseUniformTM(n, p, 8, seed=2)
-    y, x = rn.two_sided_sketch(a, om, ps, block_bytes=1 << 20)  # 512-row blocks
+    y, x = rn.two_sided_sketch(a, om, ps, one_pass=True, block_bytes=1 << 20)  # 512-row blocks
     assert y.shape == (n, k) and x.shape == (d, p)
     y_ref = om.apply_right(a).double()
     x_ref = ps.apply_adjoint(a).double().T

@@ -93,7 +93,8 @@ def test_identity_input_equals_materialize(cuda):
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
 @pytest.mark.parametrize("d,k,xi,n", [(8192, 512, 1, 70), (1024, 100, 3, 9), (2048, 64, 2, 5), (4096, 256, 1, 3),
-                                      (16384, 128, 2, 4), (256, 64, 1, 7), (32, 12, 4, 2)])
+                                      (16384, 128, 2, 4), (256, 64, 1, 7), (32, 12, 4, 2), (512, 64, 2, 301),
+                                      (64, 16, 3, 9), (128, 128, 1, 33), (16, 8, 2, 5)])
 def test_srtt_wht_vs_oracle(d, k, xi, n, dt, cuda):
     rng = np.random.default_rng(d * 3 + xi)
     a = (rng.standard_normal((n, d)) / np.arange(1, d + 1)).astype(dt)
@@ -104,8 +105,9 @@ def test_srtt_wht_vs_oracle(d, k, xi, n, dt, cuda):
     assert rel_err(y, ref) <= TOL[dt]
 
 
-def test_srtt_uniform_diagonal(cuda):
-    d, k, xi = 8192, 64, 2
+@pytest.mark.parametrize("d", [8192, 512, 64])
+def test_srtt_uniform_diagonal(d, cuda):
+    k, xi = 64, 2
     rng = np.random.default_rng(1)
     a = rng.standard_normal((6, d))
     tm = skb.SparseRttTM(d, k, xi, "wht", diagonal="uniform_symmetric", seed=4)
