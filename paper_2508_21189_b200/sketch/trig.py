@@ -50,6 +50,49 @@ def _identity_sampler(d: int):
     return srtt_sampler_encode(np.arange(d)[:, None], np.zeros((d, 1), bool))
 
 
+_SEG_L = 12  # segment length 2^12 for the two-level transform of long rows
+
+
+def _large_rows(d: int, dtype) -> bool:
+    """Rows longer than the single-pass kernels take (float32 d > 2^14, float64 d > 2^13)."""
+    import torch
+
+    return d > ((1 << 14) if dtype == torch.float32 else (1 << 13))
+
+
+def _wht_segments(x):
+    """Unnormalised WHT of every length-2^12 segment of the rows of a contiguous device tensor."""
+    n, d = x.shape
+    seg = 1 << _SEG_L
+    z = _srtt_native(x.reshape(-1, seg), np.ones(seg), _identity_sampler(seg), 1, seg, 1.0, pm1=True)
+    return z.view(n, d // seg, seg)
+
+
+def _hadamard_signs(rows_hi, d1: int, device, dtype):
+    """(-1)^popcount(r & a) for r in rows_hi, a < d1: the H_{d1} rows the sampled outputs need."""
+    import torch
+
+    a = torch.arange(d1, device=device)
+    bits = torch.bitwise_and(rows_hi[:, None], a[None, :])
+    par = torch.zeros_like(bits)
+    while bool(bits.any()):
+        par ^= bits & 1
+        bits = bits >> 1
+    return (1 - 2 * par).to(dtype)
+
+
+def _wht_rows_large(x):
+    """Unnormalised WHT of long rows: H_d = H_{d/2^12} (x) H_{2^12} (index j = 2^12 a + b) — the
+    segment transforms run in the K3 kernel, the short outer transform as an exact +-1 contraction."""
+    import torch
+
+    n, d = x.shape
+    z = _wht_segments(x.contiguous())
+    d1 = z.shape[1]
+    h = _hadamard_signs(torch.arange(d1, device=x.device), d1, x.device, x.dtype)
+    return torch.einsum("ra,nab->nrb", h, z).reshape(n, d)
+
+
 def wht(x, axis: int = 0):
     """Walsh-Hadamard transform with 1/sqrt(d) normalisation (self-inverse), computed on the GPU.
 
@@ -71,12 +114,18 @@ def wht(x, axis: int = 0):
         t = torch.movedim(x, axis, -1)
         lead = t.shape[:-1]
         op = to_operand(t.reshape(-1, d), allow_vector=False, complex_ok=False)
-        y = _srtt_native(op.tensor, np.ones(d), _identity_sampler(d), 1, d, 1.0 / np.sqrt(d), pm1=True)
+        if _large_rows(d, op.tensor.dtype):
+            y = _wht_rows_large(op.tensor) / np.sqrt(d)
+        else:
+            y = _srtt_native(op.tensor, np.ones(d), _identity_sampler(d), 1, d, 1.0 / np.sqrt(d), pm1=True)
         return torch.movedim(from_result(y, op).reshape(*lead, d), -1, axis)
     t = np.moveaxis(np.asarray(x, dtype=np.float64), axis, -1)
     lead = t.shape[:-1]
     op = to_operand(np.ascontiguousarray(t.reshape(-1, d)), allow_vector=False, complex_ok=False)
-    y = _srtt_native(op.tensor, np.ones(d), _identity_sampler(d), 1, d, 1.0 / np.sqrt(d), pm1=True)
+    if _large_rows(d, op.tensor.dtype):
+        y = _wht_rows_large(op.tensor) / np.sqrt(d)
+    else:
+        y = _srtt_native(op.tensor, np.ones(d), _identity_sampler(d), 1, d, 1.0 / np.sqrt(d), pm1=True)
     return np.moveaxis(from_result(y, op).reshape(*lead, d), -1, axis)
 
 
@@ -259,7 +308,34 @@ class SparseRttTM(TestMatrix):
             pm1 = bool(np.all(np.abs(dvals) == 1.0))
             self._device_cache[key] = (dv, samp, (1.0 / np.sqrt(self.d)) * mag, pm1)
         dv, samp, scale, pm1 = self._device_cache[key]
+        if _large_rows(self.d, a.dtype):
+            return self._large_right(a, dv, scale)
         return _srtt_native(a, dv, samp, self.xi, self.k, scale, pm1)
+
+    def _large_right(self, a, dv, scale):
+        """Long rows: D, segment WHTs (K3), then only the sampled outputs of the outer transform:
+        Y[:, j] = sum_a H_{d1}[j >> 12, a] Z[:, a, j & 4095] for the k*xi sampled j."""
+        import torch
+
+        key = ("srtt_large", a.device, a.dtype)
+        if key not in self._device_cache:
+            _, sampler = self._parts()
+            rows, neg, mag = sampler.column_draws()
+            j = torch.from_numpy(np.ascontiguousarray(rows.reshape(-1))).to(a.device)
+            d1 = self.d >> _SEG_L
+            hs = _hadamard_signs(j >> _SEG_L, d1, a.device, a.dtype)  # (k xi) x d1
+            sgn = torch.from_numpy(np.where(neg, -1.0, 1.0).reshape(self.k, self.xi)).to(a.device, a.dtype)
+            self._device_cache[key] = (j & ((1 << _SEG_L) - 1), hs, sgn)
+        jlo, hs, sgn = self._device_cache[key]
+        n = a.shape[0]
+        y = torch.empty((n, self.k), dtype=a.dtype, device=a.device)
+        step = max(1, (256 << 20) // (self.d * a.element_size()))
+        for r0 in range(0, n, step):
+            z = _wht_segments((a[r0:r0 + step] * dv).contiguous())  # m x d1 x 4096
+            zs = z[:, :, jlo]                                      # m x d1 x (k xi)
+            yj = torch.einsum("mak,ka->mk", zs, hs)
+            y[r0:r0 + step] = (yj.view(-1, self.k, self.xi) * sgn).sum(-1) * scale
+        return y
 
     def redraw(self, seed: int) -> "SparseRttTM":
         return SparseRttTM(self.d, self.k, self.xi, self.transform, diagonal=self.diagonal, field=self.field,

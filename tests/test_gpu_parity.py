@@ -94,7 +94,8 @@ def test_identity_input_equals_materialize(cuda):
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
 @pytest.mark.parametrize("d,k,xi,n", [(8192, 512, 1, 70), (1024, 100, 3, 9), (2048, 64, 2, 5), (4096, 256, 1, 3),
                                       (16384, 128, 2, 4), (256, 64, 1, 7), (32, 12, 4, 2), (512, 64, 2, 301),
-                                      (64, 16, 3, 9), (128, 128, 1, 33), (16, 8, 2, 5)])
+                                      (64, 16, 3, 9), (128, 128, 1, 33), (16, 8, 2, 5), (32768, 300, 2, 5),
+                                      (65536, 64, 1, 3)])
 def test_srtt_wht_vs_oracle(d, k, xi, n, dt, cuda):
     rng = np.random.default_rng(d * 3 + xi)
     a = (rng.standard_normal((n, d)) / np.arange(1, d + 1)).astype(dt)
@@ -115,8 +116,9 @@ def test_srtt_uniform_diagonal(d, cuda):
     assert rel_err(tm.apply_right(a), orc.srtt_right(dv, samp, a, "wht")) <= 1e-12
 
 
-def test_wht_function(cuda):
-    x = np.random.default_rng(0).standard_normal((16, 3))
+@pytest.mark.parametrize("d", [16, 8192, 32768])
+def test_wht_function(d, cuda):
+    x = np.random.default_rng(0).standard_normal((d, 3))
     y = skb.wht(x)
     assert rel_err(np.asarray(y), orc.wht_rows(x.T).T) <= 1e-13
     assert rel_err(np.asarray(skb.wht(np.asarray(y))), x) <= 1e-13
