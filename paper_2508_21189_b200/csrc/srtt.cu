@@ -24,7 +24,7 @@
 #include "common.cuh"
 
 namespace skb {
-int launch_srtt_tc(const float* A, int64_t n, int64_t lda, const float* dv, const int32_t* samp, int xi, int k,
+int launch_srtt_tc(int L, const float* A, int64_t n, int64_t lda, const float* dv, const int32_t* samp, int xi, int k,
                    double scale, float* Y, int64_t ldy, cudaStream_t s);
 namespace {
 
@@ -592,11 +592,15 @@ int run(const void* A_, int64_t n, int64_t d, int64_t lda, const void* dv_, bool
   const bool aligned = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % (16 / sizeof(T)) == 0);
   if constexpr (sizeof(T) == 4) {
     const bool dv_aligned = (reinterpret_cast<uintptr_t>(dv) & 15) == 0;
-    if (pm1 && aligned && dv_aligned && L >= 12 && L <= 14) {
+    if (pm1 && aligned && dv_aligned && L >= 11 && L <= 14) {
       const float* Af = reinterpret_cast<const float*>(A);
       const float* dvf = reinterpret_cast<const float*>(dv);
       float* Yf = reinterpret_cast<float*>(Y);
-      if (L == 13 && srtt_tc_enabled()) return launch_srtt_tc(Af, n, lda, dvf, samp, xi, (int)k, scale, Yf, ldy, s);
+      // tensor cores for d = 4096, 8192 (at d = 2048 the per-row epilogue and gather dominate: the
+      // CUDA-core kernel is faster, 40 % vs 32 % of HBM)
+      if (L >= 12 && L <= 13 && srtt_tc_enabled())
+        return launch_srtt_tc(L, Af, n, lda, dvf, samp, xi, (int)k, scale, Yf, ldy, s);
+      if (L == 11) return dispatch_L<float, true>(L, A, n, lda, dv, samp, xi, (int)k, scale, Y, ldy, s);
       if (L == 12) return launch_wide<12>(Af, n, lda, dvf, samp, xi, (int)k, scale, Yf, ldy, s);
       if (L == 13) return launch_wide<13>(Af, n, lda, dvf, samp, xi, (int)k, scale, Yf, ldy, s);
       return launch_wide<14>(Af, n, lda, dvf, samp, xi, (int)k, scale, Yf, ldy, s);

@@ -32,11 +32,19 @@ namespace {
 
 using namespace sm100;
 
-constexpr int TC_D = 8192;
-constexpr int TC_ROW_BYTES = TC_D * 4;        // 32 KB
-constexpr int TC_SLOTS = 5;                   // row ring: 5 x 32 KB in flight per SM
-constexpr int TC_ACC = 4;                     // TMEM accumulators of 64 columns (after H's 64)
-constexpr int TC_TMEM_COLS = 512;             // H_128 (64) + 4 x 64 accumulators, power of two
+// Shape of the kernel for d = 2^L (11 <= L <= 13): NA = d / 128 a-rows per row of A.
+template <int L>
+struct TcCfg {
+  static constexpr int D = 1 << L;
+  static constexpr int NA = D / 128;                 // N of the per-row MMAs, points of the register WHT
+  static constexpr int ROW_BYTES = D * 4;
+  static constexpr int TB = NA * 128;                // one hi/lo K-half operand tile (bytes)
+  static constexpr int SLOTS = L == 13 ? 5 : (L == 12 ? 10 : 16);  // row ring depth (shared memory)
+  static constexpr int NG = D / 512;                 // 4-float groups per converter thread per row
+  static_assert(NA >= 16 && NA <= 64, "tile shape");
+};
+constexpr int TC_ACC = 4;                     // TMEM accumulators of NA columns (after H's 64)
+constexpr int TC_TMEM_COLS = 512;             // H_128 (64) + 4 accumulators, power of two
 constexpr int TC_SAMP_REGS = 8;               // sampler entries per epilogue thread kept in registers
 constexpr int TC_THREADS = 512;               // WG0: producer/MMA/alloc | WG1 converters | WG2,3 epilogue
 
@@ -62,9 +70,10 @@ __device__ __forceinline__ void maxnreg_inc() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
 }
 
-__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
+template <int NA>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[NA]) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < NA / 16; ++q) {
     uint32_t (&t)[16] = *reinterpret_cast<uint32_t(*)[16]>(&r[16 * q]);
     tmem_ld16(taddr + 16 * q, t);
   }
@@ -99,9 +108,12 @@ __device__ __forceinline__ uint32_t sw128_off(int n, int k) {
   return (uint32_t)n * 128u + ((((uint32_t)k >> 3) ^ ((uint32_t)n & 7u)) << 4) + (((uint32_t)k & 7u) << 1);
 }
 
+template <int L>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     srtt_wht_tc(const float* __restrict__ A, int64_t n, int64_t lda, const float* __restrict__ dvals,
                 const int32_t* __restrict__ samp, int xi, int k, float scale, float* __restrict__ Y, int64_t ldy) {
+  using C = TcCfg<L>;
+  constexpr int TC_SLOTS = C::SLOTS, TC_ROW_BYTES = C::ROW_BYTES, NA = C::NA, TB = C::TB, NG = C::NG;
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
   uint8_t* rbuf = smem;                                               // TC_SLOTS row slots x 32 KB
@@ -169,22 +181,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     } else if (warp == 1 && lane == 0) {
       // ------------------------------------------------------------ MMA issuer
-      const uint32_t idesc = idesc_bf16_f32(128, 64);
+      const uint32_t idesc = idesc_bf16_f32(128, NA);
       int s = 0, buf = 0;
       uint32_t ph = 0, tph = 0;
       for (int64_t row = blockIdx.x; row < n; row += gridDim.x) {
         mbar_wait(&t_empty[buf], tph ^ 1);
         mbar_wait(&r_conv[s], ph);
         tc_fence_after();
-        const uint32_t d = tmem + 64 + buf * 64;
+        const uint32_t d = tmem + 64 + buf * NA;
         const uint32_t rb = smem_u32(rbuf + s * TC_ROW_BYTES);
 #pragma unroll
         for (int kh = 0; kh < 2; ++kh) {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const uint32_t ta = tmem + (uint32_t)(kh * 32 + kk * 8);  // K step of 16 = 8 columns
-            const uint64_t dbh = sdesc_kmajor_sw128(rb + kh * 8192 + kk * 32);
-            const uint64_t dbl = sdesc_kmajor_sw128(rb + 16384 + kh * 8192 + kk * 32);
+            const uint64_t dbh = sdesc_kmajor_sw128(rb + kh * TB + kk * 32);
+            const uint64_t dbl = sdesc_kmajor_sw128(rb + 2 * TB + kh * TB + kk * 32);
             umma_bf16_ts(d, ta, dbh, idesc, (kh | kk) ? 1u : 0u);
             umma_bf16_ts(d, ta, dbl, idesc, 1u);
           }
@@ -198,15 +210,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else if (warp < 8) {
     maxnreg_inc<152>();
     // ------------------------------------------------------------ converters (128 threads)
-    // Each row is converted in place into [hi K0 | hi K1 | lo K0 | lo K1], each an 8 KB K-major
-    // SWIZZLE_128B tile of 64 rows a x 64 columns b. Thread ct owns 16 groups of 4 floats
+    // Each row is converted in place into [hi K0 | hi K1 | lo K0 | lo K1], each a K-major
+    // SWIZZLE_128B tile of NA rows a x 64 columns b. Thread ct owns NG groups of 4 floats
     // q = ct + 128 i: a = q >> 5, b = 4 (q & 31). Reads are 16-byte contiguous across lanes; writes
     // are 8-byte halves of 16-byte chunks, each half-warp one 128-byte line. D is applied after
     // the split as an XOR on the packed bf16 pairs (round-to-nearest is sign symmetric).
     const int ct = tid - 128;
-    uint32_t dm[32];
+    uint32_t dm[2 * NG];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < NG; ++i) {
       const int q = ct + 128 * i;
       const int j0 = (q >> 5) * 128 + 4 * (q & 31);
       const float4 dv = __ldg(reinterpret_cast<const float4*>(dvals + j0));
@@ -218,21 +230,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     for (int64_t row = blockIdx.x; row < n; row += gridDim.x) {
       mbar_wait(&r_tma[s], ph);
       const uint32_t rsa = smem_u32(rbuf + s * TC_ROW_BYTES);
-      float4 v[16];
+      float4 v[NG];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = lds128(rsa + (uint32_t)(ct + 128 * i) * 16u);
+      for (int i = 0; i < NG; ++i) v[i] = lds128(rsa + (uint32_t)(ct + 128 * i) * 16u);
       asm volatile("bar.sync 1, 128;" ::: "memory");  // all fp32 reads of the row before in-place writes
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
+      for (int i = 0; i < NG; ++i) {
         const int q = ct + 128 * i;
         const int a = q >> 5, b4 = q & 31;
         const uint32_t h01 = cvt_bf16x2(v[i].y, v[i].x), h23 = cvt_bf16x2(v[i].w, v[i].z);
         const uint32_t l01 = cvt_bf16x2(v[i].y - __uint_as_float(h01 & 0xffff0000u), v[i].x - __uint_as_float(h01 << 16));
         const uint32_t l23 = cvt_bf16x2(v[i].w - __uint_as_float(h23 & 0xffff0000u), v[i].z - __uint_as_float(h23 << 16));
-        const uint32_t off = (uint32_t)(b4 >> 4) * 8192u + (uint32_t)a * 128u +
+        const uint32_t off = (uint32_t)(b4 >> 4) * (uint32_t)TB + (uint32_t)a * 128u +
                              (((((uint32_t)b4 & 15u) >> 1) ^ ((uint32_t)a & 7u)) << 4) + (((uint32_t)b4 & 1u) << 3);
         sts64(rsa + off, h01 ^ dm[2 * i], h23 ^ dm[2 * i + 1]);
-        sts64(rsa + 16384u + off, l01 ^ dm[2 * i], l23 ^ dm[2 * i + 1]);
+        sts64(rsa + 2u * TB + off, l01 ^ dm[2 * i], l23 ^ dm[2 * i + 1]);
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -260,26 +272,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     for (int64_t row = blockIdx.x + ew * (int64_t)gridDim.x; row < n; row += 2 * (int64_t)gridDim.x) {
       mbar_wait(&t_full[buf], tph);
       tc_fence_after();
-      uint32_t z[64];
-      tmem_ld64(tmem + ((uint32_t)(32 * lg) << 16) + 64 + buf * 64, z);
+      uint32_t z[NA];
+      tmem_ld_cols<NA>(tmem + ((uint32_t)(32 * lg) << 16) + 64 + buf * NA, z);
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&t_empty[buf]);
       buf += 2;
       if (buf >= TC_ACC) { buf -= TC_ACC; tph ^= 1; }
-      // 64-point WHT over a (register index): a-bit 0 inside pairs, a-bits 1..5 on packed pairs
-      u64 p[32];
+      // NA-point WHT over a (register index): a-bit 0 inside pairs, the other a-bits on packed pairs
+      u64 p[NA / 2];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
+      for (int i = 0; i < NA / 2; ++i) {
         const float x0 = __uint_as_float(z[2 * i]), x1 = __uint_as_float(z[2 * i + 1]);
         const float s0 = x0 + x1, d0 = x0 - x1;
         asm("mov.b64 %0, {%1, %2};" : "=l"(p[i]) : "f"(s0), "f"(d0));
       }
 #pragma unroll
-      for (int h = 1; h < 32; h <<= 1) {
+      for (int h = 1; h < NA / 2; h <<= 1) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
+        for (int i = 0; i < NA / 2; ++i) {
           if ((i & h) == 0) {
             const u64 s0 = f2add_(p[i], p[i | h]);
             const u64 d0 = f2sub_(p[i], p[i | h]);
@@ -290,7 +302,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       asm volatile("bar.sync %0, 128;" ::"r"(2 + ew) : "memory");  // previous gather done with ybuf
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
+      for (int i = 0; i < NA / 2; ++i) {
         float lo, hi;
         asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(p[i]));
         ybuf[(2 * i) * 128 + bp] = lo;
@@ -325,16 +337,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 }
 
 
+template <int L>
+int launch_tc_t(const float* A, int64_t n, int64_t lda, const float* dv, const int32_t* samp, int xi, int k,
+                double scale, float* Y, int64_t ldy, cudaStream_t s) {
+  using C = TcCfg<L>;
+  const int grid = (int)(n < sm_count() ? n : sm_count());
+  const size_t smem = 1024 + (size_t)(C::SLOTS + 2) * C::ROW_BYTES + 8 * (3 * C::SLOTS + 2 * TC_ACC + 1);
+  cudaFuncSetAttribute(srtt_wht_tc<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  srtt_wht_tc<L><<<grid, TC_THREADS, smem, s>>>(A, n, lda, dv, samp, xi, k, (float)scale, Y, ldy);
+  return check_launch("sk_srtt_right(tc)");
+}
+
 }  // namespace
 
-// Launcher used by sk_srtt_right (srtt.cu) for float32, d = 8192, +-1 diagonal.
-int launch_srtt_tc(const float* A, int64_t n, int64_t lda, const float* dv, const int32_t* samp, int xi, int k,
+// Launcher used by sk_srtt_right (srtt.cu) for float32, d = 2^L with 11 <= L <= 13, +-1 diagonal.
+int launch_srtt_tc(int L, const float* A, int64_t n, int64_t lda, const float* dv, const int32_t* samp, int xi, int k,
                    double scale, float* Y, int64_t ldy, cudaStream_t s) {
-  const int grid = (int)(n < sm_count() ? n : sm_count());
-  const size_t smem = 1024 + TC_SLOTS * TC_ROW_BYTES + 2 * TC_ROW_BYTES + 256;
-  cudaFuncSetAttribute(srtt_wht_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  srtt_wht_tc<<<grid, TC_THREADS, smem, s>>>(A, n, lda, dv, samp, xi, k, (float)scale, Y, ldy);
-  return check_launch("sk_srtt_right(tc)");
+  if (L == 13) return launch_tc_t<13>(A, n, lda, dv, samp, xi, k, scale, Y, ldy, s);
+  if (L == 12) return launch_tc_t<12>(A, n, lda, dv, samp, xi, k, scale, Y, ldy, s);
+  if (L == 11) return launch_tc_t<11>(A, n, lda, dv, samp, xi, k, scale, Y, ldy, s);
+  return fail(SK_EUNSUPPORTED, "sk_srtt_right(tc): no tensor-core variant for this length");
 }
 
 }  // namespace skb

@@ -191,11 +191,12 @@ def test_srtt_tc_row_counts_and_strides(n, cuda):
         assert rel_err(y.cpu().numpy(), tm.apply_right(a.contiguous()).cpu().numpy()) <= 1e-5
 
 
-def test_srtt_tc_matches_cuda_core_kernel(cuda, monkeypatch):
+@pytest.mark.parametrize("d", [2048, 4096, 8192])
+def test_srtt_tc_matches_cuda_core_kernel(d, cuda, monkeypatch):
     import torch
 
-    tm = skb.SparseRttTM(8192, 512, 3, "wht", seed=9)
-    a = torch.randn(1000, 8192, device=cuda)
+    tm = skb.SparseRttTM(d, 512, 3, "wht", seed=9)
+    a = torch.randn(1000, d, device=cuda)
     y_tc = tm.apply_right(a).double()
     monkeypatch.setenv("SKETCH_B200_SRTT", "regs")
     y_cc = tm.apply_right(a).double()
