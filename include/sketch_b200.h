@@ -77,6 +77,17 @@ SK_API int sk_sparse_right(int dtype, const void* A, int64_t n, int64_t d, int64
                            int64_t k, double scale, void* Y, int64_t ldy, void* stream);
 
 /*
+ * K1s — Y[n,k] = scale * A * Omega for a sparse A in CSR (int64 indptr[n+1], int32 indices, values
+ * of `dtype`) and a sparse-sign Omega given by rows: int32 indptr[d+1] and int32 entries
+ * `c | neg << 31` (magnitude folded into `scale`). A is never densified. Replaces
+ * `_SparseTM.apply_right` for SciPy-sparse A (src/sketch/sparse.py:63-66); the adjoint of a sparse
+ * B (sparse.py:68-71) is this on B^T. Sums are accumulated with atomics (order not reproducible).
+ */
+SK_API int sk_sparse_right_csr(int dtype, int64_t n, int64_t d, const int64_t* a_indptr, const int32_t* a_indices,
+                               const void* a_values, const int32_t* omega_indptr, const int32_t* omega_entries,
+                               int64_t k, double scale, void* Y, int64_t ldy, void* stream);
+
+/*
  * K2 — SA[k,m] = scale * Omega[d,k]^T * A[d,m] (accumulate != 0: SA += ...).
  * Replaces `_SparseTM.apply_adjoint` = `self.matrix.conj().T @ b` (src/sketch/sparse.py:68-78).
  * Workspace of sk_sparse_adjoint_workspace_bytes(...) bytes (may be 0 -> pass NULL).

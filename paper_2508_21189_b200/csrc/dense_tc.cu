@@ -52,9 +52,6 @@ struct TcParams {
   int mtiles;
 };
 
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 
 template <int N>
 __device__ __forceinline__ void setmaxnreg_dec() {

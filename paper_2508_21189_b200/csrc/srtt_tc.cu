@@ -103,11 +103,6 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
       "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
 }
 
-// byte offset of bf16 element (row n, k in [0,64)) inside a K-major SWIZZLE_128B tile
-__device__ __forceinline__ uint32_t sw128_off(int n, int k) {
-  return (uint32_t)n * 128u + ((((uint32_t)k >> 3) ^ ((uint32_t)n & 7u)) << 4) + (((uint32_t)k & 7u) << 1);
-}
-
 template <int L>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     srtt_wht_tc(const float* __restrict__ A, int64_t n, int64_t lda, const float* __restrict__ dvals,

@@ -212,6 +212,50 @@ class _SignSparseTM(TestMatrix):
                    and b.stride(1) == 1 and b.shape[1] >= 1)
         return "wide" if (wide_ok and forced != "gather") else "gather"
 
+    def _sparse_input_ok(self) -> bool:
+        return self._sign_form() is not None
+
+    def _omega_rows_on(self, device):
+        """Omega by rows for K1s: int32 indptr[d+1], int32 entries c | neg << 31 (cached)."""
+        key = ("omega_rows", device)
+        if key not in self._device_cache:
+            import torch
+
+            rows, cols, neg, mag = self._sign_form()
+            order = np.argsort(rows, kind="stable") if np.any(np.diff(rows) < 0) else slice(None)
+            r, c, g = rows[order], cols[order], neg[order]
+            ptr = np.zeros(self.d + 1, np.int64)
+            np.cumsum(np.bincount(r, minlength=self.d), out=ptr[1:])
+            ent = (c.astype(np.int64) | (g.astype(np.int64) << 31)).astype(np.uint32).view(np.int32)
+            self._device_cache[key] = (torch.from_numpy(ptr.astype(np.int32)).to(device),
+                                       torch.from_numpy(np.ascontiguousarray(ent)).to(device), mag)
+        return self._device_cache[key]
+
+    def _right_sparse_input(self, a):
+        """A Omega for a SciPy-sparse A without densifying A (reference sparse.py:63-66)."""
+        import scipy.sparse as sp
+        import torch
+
+        from .._device import require_cuda
+
+        require_cuda()
+        a = sp.csr_array(a)
+        if np.iscomplexobj(a.data):
+            raise NotImplementedError("complex sparse A: densify it first")
+        dev = torch.device("cuda", torch.cuda.current_device())
+        optr, oent, mag = self._omega_rows_on(dev)
+        aptr = torch.from_numpy(a.indptr.astype(np.int64)).to(dev)
+        aidx = torch.from_numpy(a.indices.astype(np.int32)).to(dev)
+        aval = torch.from_numpy(a.data.astype(np.float64)).to(dev)
+        n = a.shape[0]
+        y = torch.empty((n, self.k), dtype=torch.float64, device=dev)
+        lib = _lib.load()
+        st = lib.sk_sparse_right_csr(_lib.SK_F64, n, self.d, aptr.data_ptr(), aidx.data_ptr(), aval.data_ptr(),
+                                     optr.data_ptr(), oent.data_ptr(), self.k, mag, y.data_ptr(), y.stride(0),
+                                     torch.cuda.current_stream().cuda_stream)
+        _lib.check(st, "sk_sparse_right_csr")
+        return y.cpu().numpy()
+
     def adjoint_rows(self, b_rows, r0: int, r1: int, out, accumulate: bool) -> None:
         """out (+)= Omega[r0:r1]^T b_rows for a float32 device block b_rows = B[r0:r1] (K2w).
 

@@ -69,6 +69,14 @@ class _Shaped:
         self.shape = shape
 
 
+def _is_scipy_sparse(x) -> bool:
+    try:
+        import scipy.sparse as sp
+    except ImportError:  # pragma: no cover
+        return False
+    return sp.issparse(x)
+
+
 class TestMatrix(ABC):
     """Abstract random sketching operator Omega in F^{d x k}, applied on the GPU."""
 
@@ -112,6 +120,8 @@ class TestMatrix(ABC):
         if len(shape) != 2:
             raise ValueError(f"apply_right needs a 2-d A, got shape {shape}")
         self._check_right(_Shaped(shape))
+        if _is_scipy_sparse(a) and self._sparse_input_ok():
+            return self._right_sparse_input(a)
         host, kind = _device.host_tensor_of(a) if not hasattr(a, "toarray") else (None, None)
         if host is not None and not host.is_complex() and \
                 host.numel() * host.element_size() >= _device.PIPELINE_MIN_BYTES:
@@ -128,8 +138,18 @@ class TestMatrix(ABC):
         if len(shape) not in (1, 2):
             raise ValueError(f"apply_adjoint needs a 1-d or 2-d B, got shape {shape}")
         self._check_adjoint(_Shaped(shape if len(shape) == 2 else (shape[0], 1)))
+        if _is_scipy_sparse(b) and len(shape) == 2 and self._sparse_input_ok():
+            # Omega^T B = (B^T Omega)^T with B^T in CSR: the sparse-input row kernel
+            return np.ascontiguousarray(self._right_sparse_input(b.T.tocsr()).T)
         op = to_operand(b, allow_vector=True)
         return from_result(self._adjoint_device(op.tensor), op)
+
+    def _sparse_input_ok(self) -> bool:
+        """Families that apply SciPy-sparse input without densifying it (sparse sign: K1s)."""
+        return False
+
+    def _right_sparse_input(self, a):
+        raise NotImplementedError
 
     def _right_device(self, a):
         """Dense device GEMM with the materialized Omega (cuBLAS); families override with kernels."""
