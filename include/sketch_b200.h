@@ -88,6 +88,15 @@ SK_API int sk_sparse_right_csr(int dtype, int64_t n, int64_t d, const int64_t* a
                                int64_t k, double scale, void* Y, int64_t ldy, void* stream);
 
 /*
+ * Device NumPy Philox stream: out[i] = 32-bit output number (first + i) of a fresh
+ * numpy.random.Philox generator with 256-bit counter `counter4` and 128-bit key `key2` (HOST
+ * arrays, from `bit_generator.state`); `first` a multiple of 8, `out` 16-byte aligned device memory.
+ * Lets test matrices be drawn on the GPU bit-identically to the reference (src/core/rng.py:18-70).
+ */
+SK_API int sk_philox_u32(const uint64_t* key2, const uint64_t* counter4, uint64_t first, int64_t count,
+                         uint32_t* out, void* stream);
+
+/*
  * K2 — SA[k,m] = scale * Omega[d,k]^T * A[d,m] (accumulate != 0: SA += ...).
  * Replaces `_SparseTM.apply_adjoint` = `self.matrix.conj().T @ b` (src/sketch/sparse.py:68-78).
  * Workspace of sk_sparse_adjoint_workspace_bytes(...) bytes (may be 0 -> pass NULL).

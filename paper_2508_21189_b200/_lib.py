@@ -38,6 +38,7 @@ SIGNATURES = {
                                  _c_i64, _c_dbl, _c_p, _c_i64, _c_p]),
     "sk_sparse_right_csr": (_c_int, [_c_int, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_dbl, _c_p, _c_i64,
                                      _c_p]),
+    "sk_philox_u32": (_c_int, [_c_p, _c_p, ctypes.c_uint64, _c_i64, _c_p, _c_p]),
     "sk_sparse_adjoint_chunk_rows": (_c_int, [_c_int, _c_i64, _c_i64]),
     "sk_sparse_adjoint_workspace_bytes": (_c_size, [_c_int, _c_i64, _c_i64, _c_i64]),
     "sk_sparse_adjoint": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, ctypes.c_int32, _c_p,

@@ -15,6 +15,7 @@ import ctypes
 import numpy as np
 
 from .. import _lib
+from ..devrng import DevicePhilox, device_draws_enabled
 from .encode import ENT_PAD, PTR_PAD, bcsc_encode, bcsc_segments
 from .tensorcore import bt_from_triplets, dense_right_tc
 from .testmatrix import TestMatrix, entry_sample
@@ -357,6 +358,13 @@ class SparseStackTM(_SignSparseTM):
 
     def _draw(self):
         rng = self._rng("entries")
+        if self.distribution == "real_rademacher" and device_draws_enabled(self.d * self.zeta):
+            import torch
+
+            g = DevicePhilox(rng, torch.device("cuda", torch.cuda.current_device()))
+            buckets = g.integers(self.block_size, (self.d, self.zeta)).cpu().numpy()
+            signs = (g.integers(2, (self.d, self.zeta)) * 2 - 1).cpu().numpy().astype(np.float64)
+            return self._assemble(signs, buckets)
         buckets = rng.integers(0, self.block_size, size=(self.d, self.zeta))
         signs = entry_sample(self.distribution, rng, (self.d, self.zeta))
         return self._assemble(signs, buckets)
@@ -377,11 +385,29 @@ class SparseUniformTM(_SignSparseTM):
 
     def _draw(self):
         rng = self._rng("entries")
+        if device_draws_enabled(self.d * self.zeta):
+            drawn = self._draw_device(rng)
+            if drawn is not None:
+                return drawn
         cols = sample_without_replacement(rng, self.d, self.zeta, self.k)
         cols.sort(axis=1)
         signs = rng.integers(0, 2, size=(self.d, self.zeta)) * 2.0 - 1.0
         vals = (signs / np.sqrt(self.zeta)).astype(self.dtype).ravel()
         return np.repeat(np.arange(self.d), self.zeta), cols.ravel().astype(np.int64), vals
+
+    def _draw_device(self, rng):
+        """The same draws on the GPU (devrng): column sets, sort, then the sign draws."""
+        import torch
+
+        g = DevicePhilox(rng, torch.device("cuda", torch.cuda.current_device()))
+        cols = g.sample_without_replacement(self.d, self.zeta, self.k)
+        if cols is None:  # permutation regime: host generator
+            return None
+        cols = torch.sort(cols, dim=1).values
+        neg = g.integers(2, (self.d, self.zeta)) == 0
+        mag = 1.0 / np.sqrt(self.zeta)
+        vals = np.where(neg.cpu().numpy().ravel(), -mag, mag).astype(self.dtype)
+        return np.repeat(np.arange(self.d), self.zeta), cols.cpu().numpy().ravel(), vals
 
     def redraw(self, seed: int) -> "SparseUniformTM":
         return SparseUniformTM(self.d, self.k, self.zeta, field=self.field, seed=seed)
