@@ -151,6 +151,19 @@ SK_API int sk_srtt_right(int dtype, const void* A, int64_t n, int64_t d, int64_t
                   int64_t ldy, void* stream);
 
 /*
+ * Long SRTT rows: Z[r, 8192a : 8192(a+1)] = H_8192 (D[8192a : ...] o A[r, same]), unnormalised,
+ * for every segment a < d / 8192 (float32, d a multiple of 8192, D exactly +-1, 16-byte aligned).
+ * The tcgen05 SRTT kernel in segment mode; the caller finishes H_d = H_{d/8192} (x) H_8192 on the
+ * outputs it needs.
+ */
+SK_API int sk_wht_segments_f32(const float* A, int64_t n, int64_t d, int64_t lda, const float* dvals, float* Z,
+                               int64_t ldz, void* stream);
+/* ... and the sampled outputs of the outer transform: Y[r, c] = scale * sum_x sign * (H_d x)_j with
+ * H_d = H_{d/8192} (x) H_8192 applied to the segment transforms Z (sampler as in sk_srtt_right). */
+SK_API int sk_srtt_outer_f32(const float* Z, int64_t n, int64_t d, int64_t ldz, const int32_t* samp, int32_t xi,
+                             int64_t k, double scale, float* Y, int64_t ldy, void* stream);
+
+/*
  * K-TC — Y[n,k] = scale * A[n,d] * B[d,k] on the tcgen05 tensor cores, float32 A split in-kernel
  * into bf16 hi + lo, fp32 accumulation in TMEM.  B is given transposed and pre-converted: Bt_hi
  * (k x d bf16, row stride ldb) and optionally Bt_lo (the bf16 residual of B; NULL when B is exact in

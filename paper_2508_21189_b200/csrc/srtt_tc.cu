@@ -103,10 +103,16 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
       "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
 }
 
-template <int L>
+// FULL = false: sampled SRTT rows (the sketch). FULL = true: segment mode for rows longer than d:
+// the operand is n rows of `period` segments of d floats (segment row r = (r / period, r % period),
+// source A + (r / period) * lda + (r % period) * d); the CTA's segments all share r % period (the
+// grid is a multiple of `period`), so its D slice is dvals + (blockIdx.x % period) * d; the
+// transformed segment is written whole to Y (row r / period, offset (r % period) * d), unscaled.
+template <int L, bool FULL>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     srtt_wht_tc(const float* __restrict__ A, int64_t n, int64_t lda, const float* __restrict__ dvals,
-                const int32_t* __restrict__ samp, int xi, int k, float scale, float* __restrict__ Y, int64_t ldy) {
+                const int32_t* __restrict__ samp, int xi, int k, float scale, float* __restrict__ Y, int64_t ldy,
+                int period) {
   using C = TcCfg<L>;
   constexpr int TC_SLOTS = C::SLOTS, TC_ROW_BYTES = C::ROW_BYTES, NA = C::NA, TB = C::TB, NG = C::NG;
   extern __shared__ uint8_t smem_dyn[];
@@ -171,7 +177,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int64_t row = blockIdx.x; row < n; row += gridDim.x) {
         mbar_wait(&r_empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&r_tma[s], TC_ROW_BYTES);
-        bulk_g2s(rbuf + s * TC_ROW_BYTES, A + row * lda, TC_ROW_BYTES, &r_tma[s]);
+        const float* src = FULL ? A + (row / period) * lda + (row % period) * C::D : A + row * lda;
+        bulk_g2s(rbuf + s * TC_ROW_BYTES, src, TC_ROW_BYTES, &r_tma[s]);
         if (++s == TC_SLOTS) { s = 0; ph ^= 1; }
       }
     } else if (warp == 1 && lane == 0) {
@@ -211,6 +218,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // are 8-byte halves of 16-byte chunks, each half-warp one 128-byte line. D is applied after
     // the split as an XOR on the packed bf16 pairs (round-to-nearest is sign symmetric).
     const int ct = tid - 128;
+    if (FULL) dvals += (int64_t)(blockIdx.x % period) * C::D;
     uint32_t dm[2 * NG];
 #pragma unroll
     for (int i = 0; i < NG; ++i) {
@@ -255,7 +263,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int bp = 32 * lg + lane;  // b' = TMEM lane
     const int et = tid & 127;
     float* ybuf = ybufs + ew * (TC_ROW_BYTES / 4);
-    const bool fast = (xi == 1 && k <= 128 * TC_SAMP_REGS);
+    const bool fast = !FULL && (xi == 1 && k <= 128 * TC_SAMP_REGS);
     uint32_t se[TC_SAMP_REGS];      // sampler entries c = et + 128 j (xi = 1)
 #pragma unroll
     for (int j = 0; j < TC_SAMP_REGS; ++j) {
@@ -294,6 +302,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             p[i | h] = d0;
           }
         }
+      }
+      if constexpr (FULL) {
+        // whole transformed segment: Y[a'][b'] -> y[a' * 128 + b'], 128 consecutive floats per a'
+        float* y = Y + (row / period) * ldy + (row % period) * C::D + bp;
+#pragma unroll
+        for (int i = 0; i < NA / 2; ++i) {
+          float lo, hi;
+          asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(p[i]));
+          y[(2 * i) * 128] = lo;
+          y[(2 * i + 1) * 128] = hi;
+        }
+        continue;
       }
       asm volatile("bar.sync %0, 128;" ::"r"(2 + ew) : "memory");  // previous gather done with ybuf
 #pragma unroll
@@ -338,8 +358,8 @@ int launch_tc_t(const float* A, int64_t n, int64_t lda, const float* dv, const i
   using C = TcCfg<L>;
   const int grid = (int)(n < sm_count() ? n : sm_count());
   const size_t smem = 1024 + (size_t)(C::SLOTS + 2) * C::ROW_BYTES + 8 * (3 * C::SLOTS + 2 * TC_ACC + 1);
-  cudaFuncSetAttribute(srtt_wht_tc<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  srtt_wht_tc<L><<<grid, TC_THREADS, smem, s>>>(A, n, lda, dv, samp, xi, k, (float)scale, Y, ldy);
+  cudaFuncSetAttribute(srtt_wht_tc<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  srtt_wht_tc<L, false><<<grid, TC_THREADS, smem, s>>>(A, n, lda, dv, samp, xi, k, (float)scale, Y, ldy, 1);
   return check_launch("sk_srtt_right(tc)");
 }
 
@@ -355,3 +375,75 @@ int launch_srtt_tc(int L, const float* A, int64_t n, int64_t lda, const float* d
 }
 
 }  // namespace skb
+
+// Segment transforms of long rows: Z[r, a*8192 : (a+1)*8192] = H_8192 (D[a*8192 : ...] o A[r, same]),
+// unnormalised, for a < d / 8192 (d a multiple of 8192, D exactly +-1).
+extern "C" int sk_wht_segments_f32(const float* A, int64_t n, int64_t d, int64_t lda, const float* dvals, float* Z,
+                                   int64_t ldz, void* stream) {
+  using namespace skb;
+  constexpr int L = 13;
+  using C = TcCfg<L>;
+  if (n < 0 || d < C::D || (d % C::D) || lda < d || ldz < d)
+    return fail(SK_EINVAL, "sk_wht_segments_f32: d must be a multiple of 8192 (lda, ldz >= d)");
+  if (n == 0) return SK_OK;
+  if (!A || !dvals || !Z) return fail(SK_EINVAL, "sk_wht_segments_f32: null pointer");
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (lda & 3) || (reinterpret_cast<uintptr_t>(dvals) & 15))
+    return fail(SK_EUNSUPPORTED, "sk_wht_segments_f32: A and D must be 16-byte aligned with lda % 4 == 0");
+  const int64_t period = d / C::D, rows = n * period;
+  if (period > (1 << 20)) return fail(SK_EINVAL, "sk_wht_segments_f32: too many segments per row");
+  // the grid is a multiple of the period so every CTA keeps one D slice
+  int64_t grid = sm_count() / period * period;
+  if (grid < period) grid = period;
+  if (grid > rows) grid = rows;
+  const size_t smem = 1024 + (size_t)(C::SLOTS + 2) * C::ROW_BYTES + 8 * (3 * C::SLOTS + 2 * TC_ACC + 1);
+  cudaFuncSetAttribute(srtt_wht_tc<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  srtt_wht_tc<L, true><<<(unsigned)grid, TC_THREADS, smem, as_stream(stream)>>>(A, rows, lda, dvals, nullptr, 1, 1,
+                                                                                1.f, Z, ldz, (int)period);
+  return check_launch("sk_wht_segments_f32");
+}
+
+namespace skb {
+namespace {
+// Outer transform of long rows, only at the sampled outputs: for sampler entry j = row | neg << 31,
+// Y_j = sum_a (-1)^popc((j >> 13) & a) Z[a * 8192 + (j & 8191)], a < period; then
+// out[c] = scale * sum_x sign * Y_{j(c, x)}. One thread per (row, c); the Z row is L2-resident.
+__global__ void srtt_outer_kernel(const float* __restrict__ Z, int64_t n, int64_t ldz, int period,
+                                  const int32_t* __restrict__ samp, int xi, int k, float scale, float* __restrict__ Y,
+                                  int64_t ldy) {
+  const int64_t total = n * (int64_t)k;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = idx / k;
+    const int c = (int)(idx % k);
+    const float* z = Z + row * ldz;
+    float acc = 0.f;
+    for (int x = 0; x < xi; ++x) {
+      const uint32_t e = (uint32_t)__ldg(samp + (int64_t)c * xi + x);
+      const uint32_t j = e & 0x7fffffffu, hi = j >> 13, lo = j & 8191u;
+      float v = 0.f;
+      for (int a = 0; a < period; ++a) {
+        const float t = __ldg(z + (int64_t)a * 8192 + lo);
+        v += (__popc(hi & (uint32_t)a) & 1) ? -t : t;
+      }
+      acc += flip_if(v, e >> 31);
+    }
+    Y[row * ldy + c] = acc * scale;
+  }
+}
+}  // namespace
+}  // namespace skb
+
+extern "C" int sk_srtt_outer_f32(const float* Z, int64_t n, int64_t d, int64_t ldz, const int32_t* samp, int32_t xi,
+                                 int64_t k, double scale, float* Y, int64_t ldy, void* stream) {
+  using namespace skb;
+  if (n < 0 || d < 8192 || (d % 8192) || ldz < d || k < 1 || xi < 1 || ldy < k)
+    return fail(SK_EINVAL, "sk_srtt_outer_f32: bad shape (d a multiple of 8192)");
+  if (n == 0) return SK_OK;
+  if (!Z || !samp || !Y) return fail(SK_EINVAL, "sk_srtt_outer_f32: null pointer");
+  const int64_t total = n * k;
+  int64_t grid = (total + 255) / 256;
+  if (grid > 64 * (int64_t)sm_count()) grid = 64 * (int64_t)sm_count();
+  srtt_outer_kernel<<<(unsigned)grid, 256, 0, as_stream(stream)>>>(Z, n, ldz, (int)(d / 8192), samp, xi, (int)k,
+                                                                   (float)scale, Y, ldy);
+  return check_launch("sk_srtt_outer_f32");
+}

@@ -309,8 +309,36 @@ class SparseRttTM(TestMatrix):
             self._device_cache[key] = (dv, samp, (1.0 / np.sqrt(self.d)) * mag, pm1)
         dv, samp, scale, pm1 = self._device_cache[key]
         if _large_rows(self.d, a.dtype):
+            import torch
+
+            if (a.dtype == torch.float32 and pm1 and self.d % 8192 == 0 and a.data_ptr() % 16 == 0
+                    and a.stride(0) % 4 == 0 and a.stride(1) == 1):
+                return self._large_right_tc(a, dv, samp, scale)
             return self._large_right(a, dv, scale)
         return _srtt_native(a, dv, samp, self.xi, self.k, scale, pm1)
+
+    def _large_right_tc(self, a, dv, samp, scale):
+        """float32, +-1 D, d a multiple of 8192: segment transforms on the tcgen05 kernel
+        (sk_wht_segments_f32), then the sampled outputs of the outer H_{d/8192} (sk_srtt_outer_f32)."""
+        import torch
+
+        n = a.shape[0]
+        y = torch.empty((n, self.k), dtype=a.dtype, device=a.device)
+        step = max(1, (512 << 20) // (self.d * 4))  # scratch of at most 512 MB per batch
+        z = torch.empty((min(n, step), self.d), dtype=torch.float32, device=a.device)
+        lib = _lib.load()
+        stream = torch.cuda.current_stream().cuda_stream
+        for r0 in range(0, n, step):
+            blk = a[r0:r0 + step]
+            m = blk.shape[0]
+            with torch.cuda.device(a.device):
+                st = lib.sk_wht_segments_f32(blk.data_ptr(), m, self.d, blk.stride(0), dv.data_ptr(), z.data_ptr(),
+                                             z.stride(0), stream)
+                _lib.check(st, "sk_wht_segments_f32")
+                st = lib.sk_srtt_outer_f32(z.data_ptr(), m, self.d, z.stride(0), samp.data_ptr(), self.xi, self.k,
+                                           scale, y[r0:r0 + m].data_ptr(), y.stride(0), stream)
+                _lib.check(st, "sk_srtt_outer_f32")
+        return y
 
     def _large_right(self, a, dv, scale):
         """Long rows: D, segment WHTs (K3), then only the sampled outputs of the outer transform:
