@@ -5,7 +5,7 @@
 // once, row-tile by row-tile, and every output element is a register accumulator:
 //
 //   CTA   = 32 rows of A (one per lane) x a block of CB = W*CPW output columns.
-//   warp  = CPW output columns c (c = cb0 + warp + W*j); lane = row.
+//   warp  = CPW consecutive output columns c (c = cb0 + warp*CPW + j); lane = row.
 //   chunk = R consecutive columns of A (rows of Omega) staged in shared memory, XOR-swizzled so
 //           that (a) 16-byte vector stores of a row segment and (b) the gather pattern "32 lanes
 //           = 32 rows, same column r" are both bank-conflict free.
@@ -194,13 +194,17 @@ __global__ void __launch_bounds__(W * 32, 1)
     __syncthreads();
     if (h + 1 < nchunks) load_chunk(h + 1);
 
+    // warp w owns the CPW consecutive columns cb0 + w * CPW + j: their CPW + 1 offsets are adjacent
+    const int64_t cw = cb0 + (int64_t)warp * CPW;
+    int bounds[CPW + 1];
+#pragma unroll
+    for (int j = 0; j <= CPW; ++j) bounds[j] = (cw + j <= k) ? P((int64_t)h * k + cw + j) : 0;
 #pragma unroll
     for (int j = 0; j < CPW; ++j) {
-      const int64_t c = cb0 + warp + (int64_t)W * j;
       int lo = 0, hi = 0;
-      if (c < k) {
-        lo = P((int64_t)h * k + c);
-        hi = P((int64_t)h * k + c + 1);
+      if (cw + j < k) {
+        lo = bounds[j];
+        hi = bounds[j + 1];
       }
       T s0 = T(0), s1 = T(0);
       int e = lo;
@@ -234,7 +238,7 @@ __global__ void __launch_bounds__(W * 32, 1)
   constexpr int YS = CB + 1;
   T* Ys = As;
 #pragma unroll
-  for (int j = 0; j < CPW; ++j) Ys[lane * YS + warp + W * j] = acc[j] * scale;
+  for (int j = 0; j < CPW; ++j) Ys[lane * YS + warp * CPW + j] = acc[j] * scale;
   __syncthreads();
   for (int idx = tid; idx < kRowsPerTile * CB; idx += NT) {
     const int i = idx / CB, cl = idx % CB;
