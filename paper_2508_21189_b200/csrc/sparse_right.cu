@@ -103,16 +103,26 @@ __global__ void __launch_bounds__(W * 32, 1)
   V4 pre[VEC ? VPT : 1];
   T pres[VEC ? 1 : SPT];
 
+  // VEC: vector j of a thread is row tid / VEC_PER_ROW + j * (NT / VEC_PER_ROW), column (tid % VEC_PER_ROW) * NV
+  // of the chunk: one base pointer and a row-validity mask per thread, 64-bit adds per chunk.
+  static_assert(!VEC || NT % VEC_PER_ROW == 0, "prefetch mapping");
+  constexpr int ROWS_PER_PASS = VEC ? NT / VEC_PER_ROW : 1;
+  const int64_t vrow0 = row0 + tid / VEC_PER_ROW;
+  const int64_t vcol = (int64_t)(tid % VEC_PER_ROW) * NV;
+  const T* vbase = A + vrow0 * lda + vcol;
+  uint32_t vrows_ok = 0;
+#pragma unroll
+  for (int j = 0; j < (VEC ? VPT : 1); ++j)
+    if (vrow0 + (int64_t)j * ROWS_PER_PASS < n) vrows_ok |= 1u << j;
   auto load_chunk = [&](int h) {
     const int64_t c0 = (int64_t)h * R;
     if constexpr (VEC) {
+      const bool col_ok = vcol + c0 < d;
+      const T* p = vbase + c0;
 #pragma unroll
       for (int j = 0; j < VPT; ++j) {
-        const int q = tid + j * NT;
-        const int i = q / VEC_PER_ROW, cv = q % VEC_PER_ROW;
-        const int64_t row = row0 + i, col = c0 + (int64_t)cv * NV;
-        if (row < n && col < d) {
-          pre[j] = ld_stream(reinterpret_cast<const V4*>(A + row * lda + col));
+        if (col_ok && ((vrows_ok >> j) & 1u)) {
+          pre[j] = ld_stream(reinterpret_cast<const V4*>(p + (int64_t)j * ROWS_PER_PASS * lda));
         } else {
           pre[j] = V4{};
         }
