@@ -140,31 +140,31 @@ __global__ void __launch_bounds__(W * 32, 1)
   // every prefetch vector of a thread lies in rows of the same residue mod NV (NT is a multiple of
   // NV * VEC_PER_ROW), so the in-vector permutation is one warp-uniform choice per chunk
   static_assert(!VEC || (NT / VEC_PER_ROW) % NV == 0, "row residue per thread");
-  auto store_vecs = [&](auto key_c) {
+  auto store_vecs = [&](T* dst, auto key_c) {
     constexpr int KEY = decltype(key_c)::value;
 #pragma unroll
     for (int j = 0; j < VPT; ++j) {
       const int q = tid + j * NT;
       const int i = q / VEC_PER_ROW, cv = q % VEC_PER_ROW;
       const int blk = (cv * NV) ^ (i & 31 & ~(NV - 1));
-      *reinterpret_cast<V4*>(As + i * R + blk) = xor_perm(pre[j], KEY);
+      *reinterpret_cast<V4*>(dst + i * R + blk) = xor_perm(pre[j], KEY);
     }
   };
-  auto store_chunk = [&]() {
+  auto store_chunk = [&](T* dst) {
     if constexpr (VEC) {
       const int key = (tid / VEC_PER_ROW) & (NV - 1);
-      if (key == 0) store_vecs(std::integral_constant<int, 0>{});
-      else if (key == 1) store_vecs(std::integral_constant<int, 1>{});
+      if (key == 0) store_vecs(dst, std::integral_constant<int, 0>{});
+      else if (key == 1) store_vecs(dst, std::integral_constant<int, 1>{});
       else if constexpr (NV == 4) {
-        if (key == 2) store_vecs(std::integral_constant<int, 2>{});
-        else store_vecs(std::integral_constant<int, 3>{});
+        if (key == 2) store_vecs(dst, std::integral_constant<int, 2>{});
+        else store_vecs(dst, std::integral_constant<int, 3>{});
       }
     } else {
 #pragma unroll
       for (int j = 0; j < SPT; ++j) {
         const int q = tid + j * NT;
         const int i = q / R, cc = q % R;
-        As[i * R + (cc ^ (i & 31))] = pres[j];
+        dst[i * R + (cc ^ (i & 31))] = pres[j];
       }
     }
   };
@@ -191,18 +191,22 @@ __global__ void __launch_bounds__(W * 32, 1)
       ent_s[i] = (uint16_t)(((e >> 1) << SH) | ((e & 1u) << 15));
     }
   }
-  const uint32_t tile_s = (uint32_t)__cvta_generic_to_shared(smem_raw);
+  const uint32_t tile_s0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
   const uint32_t lxor = ((uint32_t)lane << 11) | ((uint32_t)lane << SH);
   auto P = [&](int64_t i) -> int { return OMS ? ptr_s[i] : __ldg(ptr + i); };
   auto E = [&](int i) -> uint32_t { return OMS ? (uint32_t)ent_s[i] : (uint32_t)__ldg(ent + i); };
 
-  const T* my_row = As + lane * R;
+  // two staged tiles: chunk h lives in As + (h & 1) * TILE; the next chunk is stored into the other
+  // tile right after this one is consumed, so one barrier per chunk separates the two
+  constexpr int TILE = kRowsPerTile * R;
   load_chunk(0);
+  store_chunk(As);
+  if (nchunks > 1) load_chunk(1);
+  __syncthreads();
   for (int h = 0; h < nchunks; ++h) {
-    __syncthreads();
-    store_chunk();
-    __syncthreads();
-    if (h + 1 < nchunks) load_chunk(h + 1);
+    T* const cur = As + (h & 1) * TILE;
+    const T* my_row = cur + lane * R;
+    const uint32_t tile_s = tile_s0 + (uint32_t)((h & 1) * TILE * sizeof(T));
 
     // warp w owns the CPW consecutive columns cb0 + w * CPW + j: their CPW + 1 offsets are adjacent
     const int64_t cw = cb0 + (int64_t)warp * CPW;
@@ -241,6 +245,11 @@ __global__ void __launch_bounds__(W * 32, 1)
       }
       acc[j] += s0 + s1;
     }
+    if (h + 1 < nchunks) {
+      store_chunk(As + ((h + 1) & 1) * TILE);
+      if (h + 2 < nchunks) load_chunk(h + 2);
+    }
+    __syncthreads();
   }
 
   // Epilogue: stage the 32 x CB tile through shared memory, then coalesced row stores.
@@ -270,7 +279,7 @@ int launch_t(const T* A, int64_t n, int64_t d, int64_t lda, const int32_t* ptr, 
   constexpr int R = chunk_rows_for<T>();
   constexpr int CB = kWarps * CPW;
   const int nchunks = (int)((d + R - 1) / R);
-  const size_t tile_bytes = (size_t)kRowsPerTile * R * sizeof(T);
+  const size_t tile_bytes = 2 * (size_t)kRowsPerTile * R * sizeof(T);  // double-buffered tile
   const size_t ys_bytes = (size_t)kRowsPerTile * (CB + 1) * sizeof(T);
   const size_t base = ((tile_bytes > ys_bytes ? tile_bytes : ys_bytes) + 15) & ~(size_t)15;
   // the whole encoding of a small Omega is staged in shared memory (nnz supplied by the caller)
