@@ -14,6 +14,8 @@
 //   one is consumed, so HBM reads overlap the shared-memory gathers.
 //
 // Bytes per launch (algorithmic): n*d*sizeof(T) read + n*k*sizeof(T) written.
+#include <stdlib.h>
+
 #include <type_traits>
 
 #include "common.cuh"
