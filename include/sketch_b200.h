@@ -164,6 +164,15 @@ SK_API int sk_srtt_outer_f32(const float* Z, int64_t n, int64_t d, int64_t ldz, 
                              int64_t k, double scale, float* Y, int64_t ldy, void* stream);
 
 /*
+ * DCT-III rows via one real inverse FFT: V[r, k] = tw_k (A[r, k] w_k - i A[r, N-k] w_{N-k}) for
+ * k <= N/2 (A[r, N] = 0), interleaved complex of `dtype` with row stride ldv (in reals, >= N + 2);
+ * tw = exp(i pi k / 2N) interleaved. irfft(V, N) then gives x_{2n} = v_n, x_{2n+1} = v_{N-1-n}.
+ * Serves SparseRttTM with the DCT transform (src/sketch/rtt.py:129-140). N even.
+ */
+SK_API int sk_dct3_prep(int dtype, const void* A, int64_t n, int64_t N, int64_t lda, const void* w, const void* tw,
+                        void* V, int64_t ldv, void* stream);
+
+/*
  * K-TC — Y[n,k] = scale * A[n,d] * B[d,k] on the tcgen05 tensor cores, float32 A split in-kernel
  * into bf16 hi + lo, fp32 accumulation in TMEM.  B is given transposed and pre-converted: Bt_hi
  * (k x d bf16, row stride ldb) and optionally Bt_lo (the bf16 residual of B; NULL when B is exact in
