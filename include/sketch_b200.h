@@ -173,6 +173,17 @@ SK_API int sk_dct3_prep(int dtype, const void* A, int64_t n, int64_t N, int64_t 
                         void* V, int64_t ldv, void* stream);
 
 /*
+ * Mixed-precision matrix-vector products for sketch-and-precondition LSQR: float32 A read once,
+ * float64 vectors and accumulation. y = A v; z = A^T u (deterministic ordered reduction; workspace
+ * of sk_gemv_t_f32_f64_workspace_bytes(n, d) bytes).
+ */
+SK_API int sk_gemv_f32_f64(const float* A, int64_t n, int64_t d, int64_t lda, const double* v, double* y,
+                           void* stream);
+SK_API size_t sk_gemv_t_f32_f64_workspace_bytes(int64_t n, int64_t d);
+SK_API int sk_gemv_t_f32_f64(const float* A, int64_t n, int64_t d, int64_t lda, const double* u, double* z,
+                             double* ws, size_t ws_bytes, void* stream);
+
+/*
  * K-TC — Y[n,k] = scale * A[n,d] * B[d,k] on the tcgen05 tensor cores, float32 A split in-kernel
  * into bf16 hi + lo, fp32 accumulation in TMEM.  B is given transposed and pre-converted: Bt_hi
  * (k x d bf16, row stride ldb) and optionally Bt_lo (the bf16 residual of B; NULL when B is exact in

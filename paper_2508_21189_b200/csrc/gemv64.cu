@@ -1,0 +1,194 @@
+// Mixed-precision matrix-vector products for sketch-and-precondition LSQR (config 4 downstream):
+// float32 A streamed once from HBM, float64 vectors and float64 accumulation (LSQR's residuals go
+// below float32 epsilon). Replaces the widen-then-GEMV form (an f64 copy of every row block:
+// 5x the HBM traffic of reading A once).
+//   sk_gemv_f32_f64   : y = A v            (warp per row, v in shared memory)
+//   sk_gemv_t_f32_f64 : z = A^T u          (thread per column over a row range, ordered float64
+//                                           reduction of the per-range partials: deterministic)
+#include "common.cuh"
+
+namespace skb {
+namespace {
+
+constexpr int GV_THREADS = 256;
+
+__global__ void __launch_bounds__(GV_THREADS)
+    gemv_rows(const float* __restrict__ A, int64_t n, int64_t d, int64_t lda, const double* __restrict__ v,
+              double* __restrict__ y, bool vec) {
+  extern __shared__ double vs[];
+  for (int64_t c = threadIdx.x; c < d; c += GV_THREADS) vs[c] = v[c];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t wstride = (int64_t)gridDim.x * (GV_THREADS / 32);
+  for (int64_t r = (int64_t)blockIdx.x * (GV_THREADS / 32) + warp; r < n; r += wstride) {
+    const float* a = A + r * lda;
+    double acc0 = 0.0, acc1 = 0.0;
+    if (vec) {
+      int64_t c = 4 * lane;
+      for (; c + 128 < d; c += 256) {  // two independent 16-byte loads in flight per lane
+        const float4 x = __ldg(reinterpret_cast<const float4*>(a + c));
+        const float4 x2 = __ldg(reinterpret_cast<const float4*>(a + c + 128));
+        acc0 = fma((double)x.x, vs[c], acc0);
+        acc0 = fma((double)x.y, vs[c + 1], acc0);
+        acc0 = fma((double)x.z, vs[c + 2], acc0);
+        acc0 = fma((double)x.w, vs[c + 3], acc0);
+        acc1 = fma((double)x2.x, vs[c + 128], acc1);
+        acc1 = fma((double)x2.y, vs[c + 129], acc1);
+        acc1 = fma((double)x2.z, vs[c + 130], acc1);
+        acc1 = fma((double)x2.w, vs[c + 131], acc1);
+      }
+      if (c < d) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(a + c));
+        acc0 = fma((double)x.x, vs[c], acc0);
+        acc0 = fma((double)x.y, vs[c + 1], acc0);
+        acc0 = fma((double)x.z, vs[c + 2], acc0);
+        acc0 = fma((double)x.w, vs[c + 3], acc0);
+      }
+    } else {
+      for (int64_t c = lane; c < d; c += 32) acc0 = fma((double)__ldg(a + c), vs[c], acc0);
+    }
+    double acc = acc0 + acc1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) y[r] = acc;
+  }
+}
+
+// thread = 4 consecutive columns (one 16-byte load per row) over a range of rows, 4 rows in flight
+__global__ void __launch_bounds__(GV_THREADS)
+    gemv_cols_partial(const float* __restrict__ A, int64_t n, int64_t d, int64_t lda, const double* __restrict__ u,
+                      int64_t rows_per_split, double* __restrict__ part, bool vec) {
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_split;
+  const int64_t r1 = min(n, r0 + rows_per_split);
+  if (c >= d) return;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (vec) {
+    int64_t r = r0;
+    for (; r + 4 <= r1; r += 4) {
+      float4 x[4];
+      double w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        x[q] = __ldg(reinterpret_cast<const float4*>(A + (r + q) * lda + c));
+        w[q] = __ldg(u + r + q);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc[0] = fma((double)x[q].x, w[q], acc[0]);
+        acc[1] = fma((double)x[q].y, w[q], acc[1]);
+        acc[2] = fma((double)x[q].z, w[q], acc[2]);
+        acc[3] = fma((double)x[q].w, w[q], acc[3]);
+      }
+    }
+    for (; r < r1; ++r) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(A + r * lda + c));
+      const double w = __ldg(u + r);
+      acc[0] = fma((double)x.x, w, acc[0]);
+      acc[1] = fma((double)x.y, w, acc[1]);
+      acc[2] = fma((double)x.z, w, acc[2]);
+      acc[3] = fma((double)x.w, w, acc[3]);
+    }
+  } else {
+    for (int64_t r = r0; r < r1; ++r) {
+      const double w = __ldg(u + r);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (c + q < d) acc[q] = fma((double)__ldg(A + r * lda + c + q), w, acc[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (c + q < d) part[(int64_t)blockIdx.y * d + c + q] = acc[q];
+}
+
+// block = 32 columns x 32 warps: warp w sums splits w, w + 32, ... (4 loads in flight), then the 32
+// warp sums are added in a fixed order (deterministic)
+constexpr int RS_WARPS = 32;
+__global__ void __launch_bounds__(RS_WARPS * 32)
+    reduce_splits(const double* __restrict__ part, int nsplit, int64_t d, double* __restrict__ z) {
+  __shared__ double sums[RS_WARPS][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 32 + lane;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if (c < d) {
+    int i = warp;
+    for (; i + 3 * RS_WARPS < nsplit; i += 4 * RS_WARPS) {
+      s0 += part[(int64_t)i * d + c];
+      s1 += part[(int64_t)(i + RS_WARPS) * d + c];
+      s2 += part[(int64_t)(i + 2 * RS_WARPS) * d + c];
+      s3 += part[(int64_t)(i + 3 * RS_WARPS) * d + c];
+    }
+    for (; i < nsplit; i += RS_WARPS) s0 += part[(int64_t)i * d + c];
+  }
+  sums[warp][lane] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (warp == 0 && c < d) {
+    double s = 0.0;
+#pragma unroll 8
+    for (int w = 0; w < RS_WARPS; ++w) s += sums[w][lane];
+    z[c] = s;
+  }
+}
+
+// threads per column block: one per 4 columns, a warp multiple, at most GV_THREADS
+int t_threads(int64_t d) {
+  const int64_t t = ((d + 3) / 4 + 31) / 32 * 32;
+  return (int)(t < GV_THREADS ? t : GV_THREADS);
+}
+int64_t t_colblocks(int64_t d) { return (d + 4 * t_threads(d) - 1) / (4 * t_threads(d)); }
+
+int t_splits(int64_t n, int64_t d) {
+  const int64_t colblocks = t_colblocks(d);
+  int64_t s = (16 * (int64_t)sm_count() + colblocks - 1) / colblocks;
+  if (s > n) s = n;
+  if (s < 1) s = 1;
+  return (int)s;
+}
+
+}  // namespace
+}  // namespace skb
+
+extern "C" int sk_gemv_f32_f64(const float* A, int64_t n, int64_t d, int64_t lda, const double* v, double* y,
+                               void* stream) {
+  using namespace skb;
+  if (n < 0 || d < 1 || lda < d) return fail(SK_EINVAL, "sk_gemv_f32_f64: bad shape");
+  if (n == 0) return SK_OK;
+  if (!A || !v || !y) return fail(SK_EINVAL, "sk_gemv_f32_f64: null pointer");
+  const size_t smem = (size_t)d * sizeof(double);
+  if (smem > 200 * 1024) return fail(SK_EUNSUPPORTED, "sk_gemv_f32_f64: d too large for the shared vector");
+  const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 4 == 0) && (d % 4 == 0);
+  cudaFuncSetAttribute(gemv_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int64_t grid = (n + 7) / 8;
+  if (grid > 16 * (int64_t)sm_count()) grid = 16 * (int64_t)sm_count();
+  gemv_rows<<<(unsigned)grid, GV_THREADS, smem, as_stream(stream)>>>(A, n, d, lda, v, y, vec);
+  return check_launch("sk_gemv_f32_f64");
+}
+
+extern "C" size_t sk_gemv_t_f32_f64_workspace_bytes(int64_t n, int64_t d) {
+  if (n < 1 || d < 1) return 0;
+  return (size_t)skb::t_splits(n, d) * d * sizeof(double);
+}
+
+extern "C" int sk_gemv_t_f32_f64(const float* A, int64_t n, int64_t d, int64_t lda, const double* u, double* z,
+                                 double* ws, size_t ws_bytes, void* stream) {
+  using namespace skb;
+  if (n < 0 || d < 1 || lda < d) return fail(SK_EINVAL, "sk_gemv_t_f32_f64: bad shape");
+  if (!A || !u || !z) return fail(SK_EINVAL, "sk_gemv_t_f32_f64: null pointer");
+  cudaStream_t s = as_stream(stream);
+  if (n == 0) {
+    cudaMemsetAsync(z, 0, (size_t)d * sizeof(double), s);
+    return check_launch("sk_gemv_t_f32_f64");
+  }
+  const int nsplit = t_splits(n, d);
+  if (!ws || ws_bytes < (size_t)nsplit * d * sizeof(double))
+    return fail(SK_EINVAL, "sk_gemv_t_f32_f64: workspace too small");
+  const int64_t rows_per_split = (n + nsplit - 1) / nsplit;
+  const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 4 == 0) && (d % 4 == 0);
+  dim3 grid((unsigned)t_colblocks(d), (unsigned)nsplit);
+  gemv_cols_partial<<<grid, t_threads(d), 0, s>>>(A, n, d, lda, u, rows_per_split, ws, vec);
+  int st = check_launch("sk_gemv_t_f32_f64");
+  if (st != SK_OK) return st;
+  reduce_splits<<<(unsigned)((d + 31) / 32), RS_WARPS * 32, 0, s>>>(ws, nsplit, d, z);
+  return check_launch("sk_gemv_t_f32_f64(reduce)");
+}

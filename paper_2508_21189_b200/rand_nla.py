@@ -483,26 +483,46 @@ def nystrom_psd(a, k: int, tm, *, max_shift_retries: int = 3) -> EigFactorizatio
 
 
 def _matvec_blocks(A, v, block_rows):
-    """A @ v in float64 (float32 A is widened block by block: LSQR needs residuals below fp32 eps)."""
+    """A @ v in float64 (LSQR needs residuals below fp32 eps): float32 A streams once through the
+    mixed-precision kernel (sk_gemv_f32_f64); float64 A uses cuBLAS."""
     import torch
 
     if A.dtype == torch.float64:
         return A @ v
+    from . import _lib
+
+    v = v.to(torch.float64).contiguous()
     out = torch.empty(A.shape[0], dtype=torch.float64, device=A.device)
-    for r0 in range(0, A.shape[0], block_rows):
-        out[r0:r0 + block_rows] = A[r0:r0 + block_rows].double() @ v
+    if A.stride(1) != 1:
+        A = A.contiguous()
+    lib = _lib.load()
+    with torch.cuda.device(A.device):
+        st = lib.sk_gemv_f32_f64(A.data_ptr(), A.shape[0], A.shape[1], A.stride(0), v.data_ptr(), out.data_ptr(),
+                                 torch.cuda.current_stream().cuda_stream)
+    _lib.check(st, "sk_gemv_f32_f64")
     return out
 
 
 def _rmatvec_blocks(A, u, block_rows):
-    """A^T @ u in float64, accumulated across row blocks."""
+    """A^T @ u in float64 (sk_gemv_t_f32_f64 for float32 A: one pass, ordered float64 reduction)."""
     import torch
 
     if A.dtype == torch.float64:
         return A.T @ u
-    out = torch.zeros(A.shape[1], dtype=torch.float64, device=A.device)
-    for r0 in range(0, A.shape[0], block_rows):
-        out += A[r0:r0 + block_rows].double().T @ u[r0:r0 + block_rows]
+    from . import _lib
+
+    u = u.to(torch.float64).contiguous()
+    if A.stride(1) != 1:
+        A = A.contiguous()
+    n, d = A.shape
+    out = torch.empty(d, dtype=torch.float64, device=A.device)
+    lib = _lib.load()
+    ws_bytes = lib.sk_gemv_t_f32_f64_workspace_bytes(n, d)
+    ws = torch.empty(max(ws_bytes, 8) // 8, dtype=torch.float64, device=A.device)
+    with torch.cuda.device(A.device):
+        st = lib.sk_gemv_t_f32_f64(A.data_ptr(), n, d, A.stride(0), u.data_ptr(), out.data_ptr(), ws.data_ptr(),
+                                   ws_bytes, torch.cuda.current_stream().cuda_stream)
+    _lib.check(st, "sk_gemv_t_f32_f64")
     return out
 
 
@@ -571,7 +591,8 @@ def sketch_precondition_lsqr(a, b, tm_psi, *, atol: float = 1e-6, btol: float = 
         v /= alpha
     w = v.clone()
     phibar, rhobar = beta, alpha
-    anorm2, ddnorm = 0.0, 0.0
+    anorm2 = 0.0
+    ddnorm = torch.zeros((), dtype=torch.float64, device=A.device)  # read once at the end (no sync)
     istop, itn = 0, 0
     r1norm, arnorm = beta, alpha * beta
     if arnorm == 0:
@@ -595,7 +616,7 @@ def sketch_precondition_lsqr(a, b, tm_psi, *, atol: float = 1e-6, btol: float = 
         phibar = sn * phibar
         tau = sn * phi
         x += (phi / rho) * w
-        ddnorm += float((w ** 2).sum()) / (rho * rho)
+        ddnorm += (w ** 2).sum() / (rho * rho)
         w = v - (theta / rho) * w
         anorm = np.sqrt(anorm2)
         r1norm = phibar
@@ -610,5 +631,5 @@ def sketch_precondition_lsqr(a, b, tm_psi, *, atol: float = 1e-6, btol: float = 
         if btol > 0 and test1 <= btol + atol * anorm * float(torch.linalg.norm(x)) / bnorm:
             istop = 1
             break
-    acond = float(np.sqrt(anorm2) * np.sqrt(ddnorm))
+    acond = float(np.sqrt(anorm2) * np.sqrt(float(ddnorm)))
     return LsqrResult(_back(rinv(x), kind), istop, itn, float(r1norm), float(arnorm), acond, t_sketch, float(test2))

@@ -79,3 +79,22 @@ def test_lsqr_vs_scipy(dt, cuda):
     r_ref = np.linalg.norm(a.astype(np.float64) @ ref - b) / np.linalg.norm(b)
     assert abs(r_gpu - r_ref) <= 1e-4 * r_ref
     assert res.itn < 60  # preconditioned: few iterations
+
+
+@pytest.mark.parametrize("n,d", [(100000, 512), (3001, 37), (5, 1000), (70000, 130)])
+def test_mixed_precision_gemv(n, d, cuda):
+    """float32 A read once, float64 vectors / accumulation (LSQR matvecs)."""
+    import torch
+
+    from paper_2508_21189_b200.rand_nla import _matvec_blocks, _rmatvec_blocks
+
+    g = torch.Generator(device=cuda).manual_seed(n + d)
+    big = torch.randn(n, d + 3, device=cuda, generator=g)
+    for a in (big[:, :d].contiguous(), big[:, 1:d + 1]):  # aligned and strided / misaligned
+        v = torch.randn(d, dtype=torch.float64, device=cuda, generator=g)
+        u = torch.randn(n, dtype=torch.float64, device=cuda, generator=g)
+        a64 = a.double()
+        y = _matvec_blocks(a, v, 1 << 16)
+        z = _rmatvec_blocks(a, u, 1 << 16)
+        assert float((y - a64 @ v).norm() / (a64 @ v).norm()) <= 1e-14
+        assert float((z - a64.T @ u).norm() / (a64.T @ u).norm()) <= 1e-13
