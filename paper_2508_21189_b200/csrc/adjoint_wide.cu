@@ -227,10 +227,22 @@ WPlan wide_plan(int64_t d, int64_t m, int64_t k, int32_t seg_cap) {
   pl.ngroups = (int)((k + W_CG - 1) / W_CG);
   pl.nslices = (int)((m + W_COLS - 1) / W_COLS);
   const int64_t roles = (int64_t)pl.ngroups * pl.nslices;
-  int64_t pieces = (4 * (int64_t)sm_count() + roles - 1) / roles;
+  // one CTA per SM: about 4 waves, with the piece count that fills the last wave best (config 4:
+  // 32 roles x 37 pieces = 8 full waves instead of 32 x 19 = 4.1)
+  const int64_t sms = sm_count();
+  const int64_t pmin = (4 * sms + roles - 1) / roles;
   // at least 8 chunks per piece: the ring must fill, and every piece adds a k x m partial
-  if (pieces > (pl.nchunks + 7) / 8) pieces = (pl.nchunks + 7) / 8;
-  if (pieces < 1) pieces = 1;
+  const int64_t pcap = std::max<int64_t>(1, (pl.nchunks + 7) / 8);
+  int64_t pieces = std::min(pmin, pcap);
+  double best = 0.0;
+  for (int64_t q = pieces; q <= std::min(2 * pmin, pcap); ++q) {
+    const int64_t ctas = roles * q;
+    const double fill = (double)ctas / (double)(((ctas + sms - 1) / sms) * sms);
+    if (fill > best + 1e-9) {
+      best = fill;
+      pieces = q;
+    }
+  }
   pl.chunks_per_piece = (int)((pl.nchunks + pieces - 1) / pieces);
   pl.npieces = (pl.nchunks + pl.chunks_per_piece - 1) / pl.chunks_per_piece;
   pl.stage_bytes = (W_TILE + (uint32_t)seg_cap * 2u + 1023u) & ~1023u;
