@@ -268,6 +268,245 @@ __global__ void __launch_bounds__(W * 32, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Persistent form (used whenever the CTA's share of Omega fits in shared memory, e.g. config 1).
+// One CTA per SM, fixed column block cb = blockIdx.x % ncb, row tiles blockIdx.x / ncb + i * (grid /
+// ncb). Omega's entries for the column block are staged once per CTA as 32-bit words
+// (local_r << SH) | (neg << 31), each column's list starting at an even slot so pairs come in one
+// 8-byte broadcast load, with per-(chunk, column) start offsets (bit 0 = odd count). The
+// double-buffered chunk stream runs across tile boundaries; a finished tile's accumulators go
+// straight from registers to Y (lane = row, CPW consecutive columns).
+template <typename T>
+__device__ __forceinline__ T xor_sign(T v, uint32_t u);
+template <>
+__device__ __forceinline__ float xor_sign<float>(float v, uint32_t u) {
+  return __uint_as_float(__float_as_uint(v) ^ (u & 0x80000000u));
+}
+template <>
+__device__ __forceinline__ double xor_sign<double>(double v, uint32_t u) {
+  return __hiloint2double(__double2hiint(v) ^ (int)(u & 0x80000000u), __double2loint(v));
+}
+__device__ __forceinline__ uint2 lds_u2(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u1(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ int4 lds_i4(uint32_t addr) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
+template <int CB>
+constexpr int lp_stride() {
+  return CB + 4;  // CB + 1 offsets per chunk, padded to a 16-byte multiple
+}
+
+template <typename T, int W, int CPW, int R>
+__global__ void __launch_bounds__(W * 32, 1)
+    sparse_right_persistent(const T* __restrict__ A, int64_t n, int64_t d, int64_t lda, const int32_t* __restrict__ ptr,
+                            const uint16_t* __restrict__ ent, int64_t k, int nchunks, int ncb, int64_t ntiles,
+                            uint32_t lp_off, uint32_t ent_off, T scale, T* __restrict__ Y, int64_t ldy) {
+  using V4 = typename VecOf<T>::type;
+  constexpr int NV = VecOf<T>::n;
+  constexpr int NT = W * 32;
+  constexpr int VEC_PER_ROW = R / NV;
+  constexpr int VPT = kRowsPerTile * VEC_PER_ROW / NT;
+  constexpr int ROWS_PER_PASS = NT / VEC_PER_ROW;
+  constexpr int CB = W * CPW;
+  constexpr int LPS = lp_stride<CB>();
+  constexpr int TILE = kRowsPerTile * R;
+  constexpr uint32_t SH = sizeof(T) == 8 ? 3u : 2u;
+  constexpr uint32_t RMASK = (uint32_t)(R - 1) << SH;
+  static_assert(R * sizeof(T) == 2048, "row stride of the staged tile");
+  static_assert(NT % VEC_PER_ROW == 0 && (NT / VEC_PER_ROW) % NV == 0, "prefetch mapping");
+  static_assert(CPW % 4 == 0, "vector loads of the column offsets");
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* As = reinterpret_cast<T*>(smem_raw);
+  int32_t* lp = reinterpret_cast<int32_t*>(smem_raw + lp_off);
+  uint32_t* lent = reinterpret_cast<uint32_t*>(smem_raw + ent_off);
+  __shared__ int32_t warp_tot[W];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cb = (int)(blockIdx.x % (unsigned)ncb);
+  const int64_t nper = gridDim.x / ncb;
+  const int64_t first_tile = blockIdx.x / ncb;
+  const int64_t c0 = (int64_t)cb * CB;
+
+  // ---- stage Omega's column block: padded counts, block-wide exclusive scan, offsets, entries
+  {
+    const int items = nchunks * CB;
+    const int per = (items + NT - 1) / NT;
+    const int i0 = min(items, tid * per), i1 = min(items, i0 + per);
+    auto count = [&](int i) -> int {
+      const int h = i / CB, j = i % CB;
+      const int64_t c = c0 + j;
+      if (c >= k) return 0;
+      return __ldg(ptr + (int64_t)h * k + c + 1) - __ldg(ptr + (int64_t)h * k + c);
+    };
+    int mine = 0;
+    for (int i = i0; i < i1; ++i) {
+      const int c = count(i);
+      mine += c + (c & 1);
+    }
+    // exclusive scan of the per-thread sums
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    int base = 0;
+    for (int w = 0; w < warp; ++w) base += warp_tot[w];
+    int run = base + incl - mine;
+    for (int i = i0; i < i1; ++i) {
+      const int h = i / CB, j = i % CB;
+      const int c = count(i);
+      lp[h * LPS + j] = run | (c & 1);
+      if (c > 0) {
+        const int64_t g0 = __ldg(ptr + (int64_t)h * k + c0 + j);
+        for (int q = 0; q < c; ++q) {
+          const uint32_t e = __ldg(ent + g0 + q);
+          lent[run + q] = ((e >> 1) << SH) | ((e & 1u) << 31);
+        }
+      }
+      run += c + (c & 1);
+      if (j == CB - 1) lp[h * LPS + CB] = run;  // end of chunk h's lists
+    }
+  }
+
+  // ---- chunk stream over this CTA's tiles (cursors advance incrementally: no divisions)
+  const int64_t my_tiles = first_tile < ntiles ? (ntiles - first_tile + nper - 1) / nper : 0;
+  const int64_t steps = my_tiles * nchunks;
+  const int vr = tid / VEC_PER_ROW;
+  const int vcol = (tid % VEC_PER_ROW) * NV;
+  V4 pre[VPT];
+  // loader cursor: tile lt, chunk lh; per-tile base pointer and row-validity mask
+  int64_t lt = first_tile;
+  int lh = 0;
+  const T* lbase = nullptr;
+  uint32_t lrows = 0;
+  auto set_tile = [&]() {
+    const int64_t r = lt * kRowsPerTile + vr;
+    lbase = A + r * lda + vcol;
+    lrows = 0;
+#pragma unroll
+    for (int j = 0; j < VPT; ++j)
+      if (r + (int64_t)j * ROWS_PER_PASS < n) lrows |= 1u << j;
+  };
+  auto load_next = [&]() {
+    // rows past n and columns past d keep stale values: only lanes of invalid rows read them,
+    // and Omega never references columns >= d
+    const T* p = lbase + (int64_t)lh * R;
+    const bool col_ok = (int64_t)lh * R + vcol < d;
+#pragma unroll
+    for (int j = 0; j < VPT; ++j)
+      if (col_ok && ((lrows >> j) & 1u)) pre[j] = ld_stream(reinterpret_cast<const V4*>(p + (int64_t)j * ROWS_PER_PASS * lda));
+    if (++lh == nchunks) {
+      lh = 0;
+      lt += nper;
+      set_tile();
+    }
+  };
+  auto store_vecs = [&](T* dst, auto key_c) {
+    constexpr int KEY = decltype(key_c)::value;
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      const int q = tid + j * NT;
+      const int i = q / VEC_PER_ROW, cv = q % VEC_PER_ROW;
+      const int blk = (cv * NV) ^ (i & 31 & ~(NV - 1));
+      *reinterpret_cast<V4*>(dst + i * R + blk) = xor_perm(pre[j], KEY);
+    }
+  };
+  auto store_step = [&](T* dst) {
+    const int key = vr & (NV - 1);
+    if (key == 0) store_vecs(dst, std::integral_constant<int, 0>{});
+    else if (key == 1) store_vecs(dst, std::integral_constant<int, 1>{});
+    else if constexpr (NV == 4) {
+      if (key == 2) store_vecs(dst, std::integral_constant<int, 2>{});
+      else store_vecs(dst, std::integral_constant<int, 3>{});
+    }
+  };
+
+  if (steps > 0) {
+    set_tile();
+    load_next();
+    store_step(As);
+    if (steps > 1) load_next();
+  }
+  __syncthreads();
+
+  const uint32_t tile_s0 = (uint32_t)__cvta_generic_to_shared(smem_raw);
+  const uint32_t lp_s = (uint32_t)__cvta_generic_to_shared(lp) + 4u * (uint32_t)(warp * CPW);
+  const uint32_t ent_s = (uint32_t)__cvta_generic_to_shared(lent);
+  const uint32_t lxor = ((uint32_t)lane << 11) | ((uint32_t)lane << SH);
+  T acc[CPW];
+#pragma unroll
+  for (int j = 0; j < CPW; ++j) acc[j] = T(0);
+
+  int h = 0;
+  int64_t ct = first_tile;  // compute cursor
+  for (int64_t st = 0; st < steps; ++st) {
+    const uint32_t tile_s = tile_s0 + ((uint32_t)st & 1u) * (uint32_t)(TILE * sizeof(T));
+    int bnd[CPW + 4];
+    const uint32_t lp_h = lp_s + 4u * (uint32_t)(h * LPS);
+#pragma unroll
+    for (int q = 0; q < CPW + 4; q += 4) {
+      const int4 b4 = lds_i4(lp_h + 4u * (uint32_t)q);
+      bnd[q] = b4.x;
+      bnd[q + 1] = b4.y;
+      bnd[q + 2] = b4.z;
+      bnd[q + 3] = b4.w;
+    }
+#pragma unroll
+    for (int j = 0; j < CPW; ++j) {
+      const int e0 = bnd[j] & ~1;
+      const int e1 = (bnd[j + 1] & ~1) - (bnd[j] & 1);
+      T s0 = T(0), s1 = T(0);
+      int e = e0;
+#pragma unroll 1
+      for (; e + 2 <= e1; e += 2) {
+        const uint2 u = lds_u2(ent_s + 4u * (uint32_t)e);
+        s0 += xor_sign(lds_t<T>(tile_s + ((u.x & RMASK) ^ lxor)), u.x);
+        s1 += xor_sign(lds_t<T>(tile_s + ((u.y & RMASK) ^ lxor)), u.y);
+      }
+      if (e < e1) {
+        const uint32_t u = lds_u1(ent_s + 4u * (uint32_t)e);
+        s0 += xor_sign(lds_t<T>(tile_s + ((u & RMASK) ^ lxor)), u);
+      }
+      acc[j] += s0 + s1;
+    }
+    if (++h == nchunks) {
+      // tile done: scaled accumulators straight to Y, then restart
+      h = 0;
+      const int64_t row = ct * kRowsPerTile + lane;
+      const int64_t cw = c0 + (int64_t)warp * CPW;
+      if (row < n) {
+        T* y = Y + row * ldy + cw;
+#pragma unroll
+        for (int j = 0; j < CPW; ++j)
+          if (cw + j < k) y[j] = acc[j] * scale;
+      }
+#pragma unroll
+      for (int j = 0; j < CPW; ++j) acc[j] = T(0);
+      ct += nper;
+    }
+    if (st + 1 < steps) {
+      store_step(As + ((st + 1) & 1) * TILE);
+      if (st + 2 < steps) load_next();
+    }
+    __syncthreads();
+  }
+}
+
 constexpr int kWarps = 16;
 
 template <typename T>
@@ -289,6 +528,34 @@ int launch_t(const T* A, int64_t n, int64_t d, int64_t lda, const int32_t* ptr, 
   const size_t ptr_bytes = (size_t)((nptr + 3) & ~3) * 4;
   const size_t oms_bytes = nnz > 0 ? ptr_bytes + (size_t)nnz * 2 : (size_t)1 << 30;
   const unsigned grid = (unsigned)(((n + kRowsPerTile - 1) / kRowsPerTile) * ((k + CB - 1) / CB));
+  // persistent form when the column block's lists fit beside the two tiles (bound: every list
+  // padded by one slot)
+  {
+    constexpr int LPS = lp_stride<CB>();
+    const size_t lp_bytes = (size_t)nchunks * LPS * 4;
+    const size_t ent_bytes = nnz > 0 ? ((size_t)nnz + (size_t)nchunks * CB + 3) / 4 * 16 : (size_t)1 << 30;
+    const size_t smem = tile_bytes + lp_bytes + ent_bytes;
+    const char* ov = getenv("SKETCH_B200_K1_CLASSIC");
+    const bool off = ov && ov[0] == '1';
+    if (VEC && !off && smem <= 220 * 1024) {
+      // 32 warps x CPW / 2 columns (same column block): twice the warps to hide the shared-load chains
+      constexpr int W2 = (CPW >= 8) ? 2 * kWarps : kWarps;
+      constexpr int CPW2 = (CPW >= 8) ? CPW / 2 : CPW;
+      static_assert(W2 * CPW2 == CB, "column block");
+      auto kern = sparse_right_persistent<T, W2, CPW2, R>;
+      const int nthreads = W2 * 32;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const int ncb = (int)((k + CB - 1) / CB);
+      const int64_t ntiles = (n + kRowsPerTile - 1) / kRowsPerTile;
+      int64_t per_cb = sm_count() / ncb;
+      if (per_cb < 1) per_cb = 1;
+      if (per_cb > ntiles) per_cb = ntiles;
+      kern<<<(unsigned)(per_cb * ncb), nthreads, smem, s>>>(A, n, d, lda, ptr, ent, k, nchunks, ncb, ntiles,
+                                                           (uint32_t)tile_bytes, (uint32_t)(tile_bytes + lp_bytes),
+                                                           (T)scale, Y, ldy);
+      return check_launch("sk_sparse_right");
+    }
+  }
   if (base + oms_bytes <= 200 * 1024) {
     const size_t smem = base + oms_bytes;
     auto kern = sparse_right_kernel<T, kWarps, CPW, R, VEC, true>;

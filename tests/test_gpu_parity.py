@@ -55,6 +55,26 @@ def test_sparse_right_vs_oracle(d, k, zeta, n, dt, cuda):
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("d,k,zeta,n", [(4096, 256, 4, 10007), (2048, 200, 8, 4900), (1536, 72, 2, 6001)])
+def test_sparse_right_many_row_tiles(d, k, zeta, n, dt, cuda, monkeypatch):
+    """Several row tiles per persistent CTA (chunk stream across tile boundaries, ragged last tile,
+    k not a multiple of the column block), and the persistent form equal to the classic one."""
+    import torch
+
+    rng = np.random.default_rng(n)
+    a = rng.standard_normal((n, d)).astype(dt)
+    tm = skb.SparseUniformTM(d, k, zeta, seed=11)
+    at = _t(a, cuda, dt)
+    y = tm.apply_right(at).cpu().numpy()
+    ref = orc.csr_right(orc.sparse_uniform_csr(d, k, zeta, 11), a)
+    assert rel_err(y, ref) <= TOL[dt]
+    monkeypatch.setenv("SKETCH_B200_K1_CLASSIC", "1")
+    y2 = tm.apply_right(at)
+    torch.cuda.synchronize()
+    assert rel_err(y2.cpu().numpy(), y) <= (1e-15 if dt == np.float64 else 1e-6)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
 @pytest.mark.parametrize("d,k,zeta,m", [(4096, 2048, 8, 40), (20000, 256, 8, 512), (1000, 300, 5, 1), (777, 64, 3, 33)])
 def test_sparse_adjoint_vs_oracle(d, k, zeta, m, dt, cuda):
     rng = np.random.default_rng(d + m)
