@@ -55,7 +55,7 @@ def _cfg1(torch, dev, rank):
     tm = SparseUniformTM(d, k, 4, seed=0)
     g = torch.Generator(device=dev).manual_seed(2000 + rank)
     a = torch.randn(n, d, dtype=torch.float64, device=dev, generator=g)
-    return dict(name="cfg1", tm=tm, a=a, n=n, d=d, k=k, launches=1, kernel="sparse_right_kernel",
+    return dict(name="cfg1", tm=tm, a=a, n=n, d=d, k=k, launches=1, kernel="sparse_right_persistent",
                 workload="cfg1 sparse sign Y=A*Omega: A 16384x4096 f64, zeta=4, k=256", op="right")
 
 
@@ -348,7 +348,8 @@ def measure(torch, w, steps, warmup, world, rank, dev, with_e2e, clocks_idx):
         el, h2d, d2h = time_e2e(torch, w, e_steps, world, dev)
         res["e2e"] = {"value": world * a_bytes * e_steps / el / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
                       "d2h_bytes_per_step": d2h, "steps": e_steps,
-                      "path": "tm.apply_right(pinned host torch tensor) -> host tensor (H2D+kernel+D2H)"}
+                      "path": f"tm.{'apply_adjoint' if w['op'] == 'adjoint' else 'apply_right'}(pinned host torch tensor)"
+                              " -> host tensor (H2D+kernel+D2H)"}
     return res
 
 
@@ -408,6 +409,7 @@ def main(argv=None):
                 others[name] = {"error": f"{type(exc).__name__}: {exc}"}
 
     if rank == 0:
+        a_gib = w["n"] * w["d"] * esize / 2**30
         out = {
             "metric": METRIC,
             "value": m["value"],
@@ -423,7 +425,7 @@ def main(argv=None):
             "data": "synthetic",
             "config": {"workload": w["workload"], "rows_per_gpu": w["n"], "d": w["d"], "k": w["k"],
                        "parallelism": f"row blocks over {world} GPU(s), no data-path collective",
-                       "l2": "input 2 GiB per step > 126 MB L2: no flush between steps"},
+                       "l2": f"input {a_gib:.1f} GiB per step > 126 MB L2: no flush between steps"},
             "pct_hbm_peak": 100.0 * m["achieved_gbs"] / peak,
             "roofline": {"bound": "hbm", "achieved": m["achieved_gbs"], "peak": peak, "unit": "GB/s",
                          "frac": m["achieved_gbs"] / peak, "traffic": _traffic(args.config),
