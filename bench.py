@@ -39,11 +39,12 @@ def _cfg2(torch, dev, rank):
     from paper_2508_21189_b200.sketch import SparseRttTM
 
     n, d, k = 65536, 8192, 512
-    tm = SparseRttTM(d, k, 1, "wht", seed=0)
+    make = lambda: SparseRttTM(d, k, 1, "wht", seed=0)  # noqa: E731
+    tm = make()
     g = torch.Generator(device=dev).manual_seed(1000 + rank)
     a = torch.randn(n, d, dtype=torch.float32, device=dev, generator=g)
     a /= torch.arange(1, d + 1, dtype=torch.float32, device=dev)  # sigma_j = 1/j
-    return dict(name="cfg2", tm=tm, a=a, n=n, d=d, k=k, launches=1, kernel="srtt_wht_tc",
+    return dict(name="cfg2", tm=tm, make=make, a=a, n=n, d=d, k=k, launches=1, kernel="srtt_wht_tc",
                 workload="cfg2 SRTT sketch Y=A*D*H*S: A 65536x8192 f32 (sigma_j=1/j), WHT d=8192, k=512, xi=1",
                 op="right")
 
@@ -52,10 +53,11 @@ def _cfg1(torch, dev, rank):
     from paper_2508_21189_b200.sketch import SparseUniformTM
 
     n, d, k = 16384, 4096, 256
-    tm = SparseUniformTM(d, k, 4, seed=0)
+    make = lambda: SparseUniformTM(d, k, 4, seed=0)  # noqa: E731
+    tm = make()
     g = torch.Generator(device=dev).manual_seed(2000 + rank)
     a = torch.randn(n, d, dtype=torch.float64, device=dev, generator=g)
-    return dict(name="cfg1", tm=tm, a=a, n=n, d=d, k=k, launches=1, kernel="sparse_right_persistent",
+    return dict(name="cfg1", tm=tm, make=make, a=a, n=n, d=d, k=k, launches=1, kernel="sparse_right_persistent",
                 workload="cfg1 sparse sign Y=A*Omega: A 16384x4096 f64, zeta=4, k=256", op="right")
 
 
@@ -63,10 +65,11 @@ def _cfg3(torch, dev, rank):
     from paper_2508_21189_b200.sketch import SparseUniformTM
 
     n, d, k = 131072, 16384, 200
-    tm = SparseUniformTM(d, k, 8, seed=0)
+    make = lambda: SparseUniformTM(d, k, 8, seed=0)  # noqa: E731
+    tm = make()
     g = torch.Generator(device=dev).manual_seed(3000 + rank)
     a = torch.randn(n, d, dtype=torch.float32, device=dev, generator=g)
-    return dict(name="cfg3", tm=tm, a=a, n=n, d=d, k=k, launches=1, kernel="dense_tc (sparse sign as bf16 Omega^T)",
+    return dict(name="cfg3", tm=tm, make=make, a=a, n=n, d=d, k=k, launches=1, kernel="dense_tc (sparse sign as bf16 Omega^T)",
                 workload="cfg3 RSVD sketch Y=A*Omega: A 131072x16384 f32 (iid input for throughput), zeta=8, k=200",
                 op="right")
 
@@ -75,10 +78,11 @@ def _cfg4(torch, dev, rank):
     from paper_2508_21189_b200.sketch import SparseUniformTM
 
     n, d, k = 4194304, 512, 2048
-    tm = SparseUniformTM(n, k, 8, seed=0)
+    make = lambda: SparseUniformTM(n, k, 8, seed=0)  # noqa: E731
+    tm = make()
     g = torch.Generator(device=dev).manual_seed(4000 + rank)
     a = torch.randn(n, d, dtype=torch.float32, device=dev, generator=g)
-    return dict(name="cfg4", tm=tm, a=a, n=n, d=d, k=k, launches=2, kernel="sparse_adjoint_wide",
+    return dict(name="cfg4", tm=tm, make=make, a=a, n=n, d=d, k=k, launches=2, kernel="sparse_adjoint_wide",
                 workload="cfg4 SA sketch: S (2048 x 4194304, zeta=8) applied to A 4194304x512 f32", op="adjoint")
 
 
@@ -86,10 +90,11 @@ def _cfg5(torch, dev, rank):
     from paper_2508_21189_b200.sketch import KhatriRaoTM
 
     n, d, k = 16384, 65536, 512
-    tm = KhatriRaoTM(256, 2, k, "real_rademacher", seed=0)
+    make = lambda: KhatriRaoTM(256, 2, k, "real_rademacher", seed=0)  # noqa: E731
+    tm = make()
     g = torch.Generator(device=dev).manual_seed(5000 + rank)
     a = torch.randn(n, d, dtype=torch.float32, device=dev, generator=g)
-    return dict(name="cfg5", tm=tm, a=a, n=n, d=d, k=k, launches=None, kernel="dense_tc (Khatri-Rao Omega^T in bf16)",
+    return dict(name="cfg5", tm=tm, make=make, a=a, n=n, d=d, k=k, launches=None, kernel="dense_tc (Khatri-Rao Omega^T in bf16)",
                 workload="cfg5 Khatri-Rao sketch: A 16384x65536 f32, ell=2, d0=256, k=512", op="right")
 
 
@@ -247,6 +252,20 @@ def time_device(torch, w, steps, warmup, world, dev):
     return total, per
 
 
+def time_setup(torch, w, steady_s):
+    """Operator construction + device encoding/upload, reported apart from the apply:
+    a fresh operator's first apply on the step's input minus one steady apply."""
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    tm = w["make"]()
+    y = (tm.apply_right if w["op"] == "right" else tm.apply_adjoint)(w["a"])
+    torch.cuda.synchronize()
+    first = time.perf_counter() - t0
+    del y, tm
+    return {"ms": max(0.0, first - steady_s) * 1e3, "first_call_ms": first * 1e3,
+            "what": "constructor draws + device encoding and upload of Omega (first apply minus a steady apply)"}
+
+
 def time_e2e(torch, w, steps, world, dev):
     """Through the public API with pinned HOST buffers: H2D of A, kernel, D2H of Y, every step."""
     a_host = torch.empty(w["a"].shape, dtype=w["a"].dtype, pin_memory=True)
@@ -343,6 +362,7 @@ def measure(torch, w, steps, warmup, world, rank, dev, with_e2e, clocks_idx):
         "achieved_gbs": alg_bytes / mean_step / 1e9,
         "clocks": cs.summary(),
     }
+    res["omega_setup"] = time_setup(torch, w, mean_step)
     if with_e2e:
         e_steps = max(1, min(steps, 5))
         el, h2d, d2h = time_e2e(torch, w, e_steps, world, dev)
@@ -402,7 +422,8 @@ def main(argv=None):
                 others[name] = {"workload": ow["workload"], "value_gbs": om["value"], "ms_per_step": om["ms_per_step"],
                                 "dtype": "f32" if oes == 4 else "f64", "kernel": ow["kernel"],
                                 "pct_hbm_peak": 100.0 * om["achieved_gbs"] / peak,
-                                "roofline_achieved_gbs": om["achieved_gbs"], "alg_bytes": om["alg_bytes"]}
+                                "roofline_achieved_gbs": om["achieved_gbs"], "alg_bytes": om["alg_bytes"],
+                                "omega_setup_ms": om["omega_setup"]["ms"]}
                 del ow
                 torch.cuda.empty_cache()
             except Exception as exc:  # report, never hide
@@ -435,6 +456,7 @@ def main(argv=None):
             "e2e": m["e2e"],
             "gpu_launches": (launches * args.steps) if launches else None,
             "clocks": m["clocks"],
+            "omega_setup": m["omega_setup"],
             "others": others,
         }
         print(json.dumps(out))
