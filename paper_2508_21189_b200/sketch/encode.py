@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["bcsc_encode", "bcsc_decode", "bcsc_segments", "srtt_sampler_encode", "sign_bits"]
+__all__ = ["bcsc_encode", "bcsc_decode", "bcsc_segments", "srtt_sampler_encode", "sign_bits", "wide_encode_device"]
 
 ADJ_GROUP = 1024  # output rows per CTA group of the adjoint fast path (sparse_adjoint.cu V2_CG)
 PTR_PAD = 1028    # ints the fast path may read past the pointer array
@@ -90,3 +90,58 @@ def sign_bits(neg) -> np.ndarray:
     if pad:
         neg = np.concatenate([neg, np.zeros(pad, bool)])
     return np.packbits(neg.reshape(-1, 32), axis=1, bitorder="little").view("<u4").astype(np.uint32).ravel()
+
+
+# K2w segment layout (adjoint_wide.cu): rows of Omega in chunks of 128, output columns in groups of
+# 256 = 16 warps x 16; a segment = 24-uint16 header (17 warp offsets) + per-warp entry lists
+# (row_in_chunk << 9) | (neg << 4) | (c mod 16), each padded to a multiple of 4 with no-op 32.
+WIDE_R, WIDE_CG, WIDE_CPW, WIDE_WARPS, WIDE_HDR, WIDE_NOOP = 128, 256, 16, 16, 24, 32
+
+
+def wide_encode_device(cols, neg, zeta: int, d: int, k: int):
+    """K2w encoding built on the GPU from device draws (rows implicit: entry e is row e // zeta).
+
+    Same bytes as the host encoder `sk_sparse_adjoint_wide_encode` fed the same entries in
+    row-major order: a stable sort by (segment, warp) keeps each list in entry order.
+    Returns (enc int16 device tensor, seg_off int64 device tensor, seg_cap).
+    """
+    import torch
+
+    dev = cols.device
+    c = cols.reshape(-1).to(torch.int64)
+    g = neg.reshape(-1).to(torch.int64)
+    nnz = c.numel()
+    r = torch.arange(nnz, device=dev, dtype=torch.int64) // zeta
+    nchunks, ngroups = -(-d // WIDE_R), -(-k // WIDE_CG)
+    nseg = nchunks * ngroups
+    if nnz and (int(c.min()) < 0 or int(c.max()) >= k):
+        raise ValueError("column index out of range")
+    key = ((r // WIDE_R) * ngroups + c // WIDE_CG) * WIDE_WARPS + (c % WIDE_CG) // WIDE_CPW
+    cnt = torch.bincount(key, minlength=nseg * WIDE_WARPS)
+    padded = ((cnt + 3) // 4 * 4).view(nseg, WIDE_WARPS)
+    n_seg = padded.sum(1)
+    if nseg and int(n_seg.max()) > 65535:
+        raise ValueError("K2w segment over 65535 entries")
+    seg_len = WIDE_HDR + (n_seg + 7) // 8 * 8
+    seg_off = torch.zeros(nseg + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(seg_len, 0, out=seg_off[1:])
+    total = int(seg_off[-1])
+    warp_off = padded.cumsum(1) - padded  # exclusive, within the segment's entry area
+    enc = torch.full((total,), WIDE_NOOP, dtype=torch.int32, device=dev)
+    hdr = torch.zeros(nseg, WIDE_HDR, dtype=torch.int32, device=dev)
+    hdr[:, :WIDE_WARPS] = warp_off.to(torch.int32)
+    hdr[:, WIDE_WARPS] = n_seg.to(torch.int32)
+    idx = seg_off[:-1, None] + torch.arange(WIDE_HDR, device=dev)[None, :]
+    enc[idx.reshape(-1)] = hdr.reshape(-1)
+    # rank of each entry inside its (segment, warp) list, in entry order
+    order = torch.sort(key, stable=True).indices
+    start = torch.cumsum(cnt, 0) - cnt
+    rank = torch.empty_like(key)
+    rank[order] = torch.arange(nnz, device=dev, dtype=torch.int64) - start[key[order]]
+    sg = key // WIDE_WARPS
+    pos = seg_off[sg] + WIDE_HDR + warp_off.reshape(-1)[key] + rank
+    code = ((r % WIDE_R) << 9) | (g << 4) | (c % WIDE_CPW)
+    enc[pos] = code.to(torch.int32)
+    enc16 = torch.where(enc >= 32768, enc - 65536, enc).to(torch.int16)
+    cap = int(seg_len.max()) if nseg else WIDE_HDR
+    return enc16, seg_off, cap

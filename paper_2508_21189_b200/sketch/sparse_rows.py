@@ -16,7 +16,7 @@ import numpy as np
 
 from .. import _lib
 from ..devrng import DevicePhilox, device_draws_enabled
-from .encode import ENT_PAD, PTR_PAD, bcsc_encode, bcsc_segments
+from .encode import ENT_PAD, PTR_PAD, bcsc_encode, bcsc_segments, wide_encode_device
 from .tensorcore import bt_from_triplets, dense_right_tc
 from .testmatrix import TestMatrix, entry_sample
 
@@ -100,6 +100,15 @@ class _SignSparseTM(TestMatrix):
         self._sign_cache = res
         return res
 
+    def _signed_real(self) -> bool:
+        """Every value is +-magnitude in the real field (the native sparse kernels apply)."""
+        return self._sign_form() is not None
+
+    def _device_sign_form(self, device):
+        """(cols (d, zeta), neg (d, zeta), magnitude) as device tensors when the draws live on the
+        GPU (rows implicit), else None."""
+        return None
+
     def _bcsc_on(self, device, kind: str, dtype_code: int):
         key = ("bcsc", kind, device, dtype_code)
         if key not in self._device_cache:
@@ -175,11 +184,18 @@ class _SignSparseTM(TestMatrix):
         return y
 
     def _adjoint_wide_on(self, device):
-        """K2w encoding (sk_sparse_adjoint_wide_encode), built once on the host and cached on `device`."""
+        """K2w encoding, cached on `device`: built on the GPU from device draws (wide_encode_device),
+        else on the host (sk_sparse_adjoint_wide_encode) and uploaded."""
         key = ("adjw", device)
         if key not in self._device_cache:
             import torch
 
+            dform = self._device_sign_form(device)
+            if dform is not None:
+                cols, neg, mag = dform
+                enc, seg_off, cap = wide_encode_device(cols, neg, cols.shape[1], self.d, self.k)
+                self._device_cache[key] = (enc, seg_off, cap, mag)
+                return self._device_cache[key]
             lib = _lib.load()
             rows, cols, neg, mag = self._sign_form()
             rows = np.ascontiguousarray(rows, dtype=np.int64)
@@ -206,7 +222,7 @@ class _SignSparseTM(TestMatrix):
 
         import torch
 
-        if self._sign_form() is None or b.dtype not in (torch.float32, torch.float64):
+        if not self._signed_real() or b.dtype not in (torch.float32, torch.float64):
             return "dense"
         forced = os.environ.get("SKETCH_B200_SPARSE_ADJOINT", "auto")
         wide_ok = (b.dtype == torch.float32 and b.data_ptr() % 16 == 0 and b.stride(0) % 4 == 0
@@ -384,30 +400,46 @@ class SparseUniformTM(_SignSparseTM):
         self.zeta = int(zeta)
 
     def _draw(self):
+        dd = self._device_draw()
+        if dd is not None:
+            cols, neg = dd
+            mag = 1.0 / np.sqrt(self.zeta)
+            vals = np.where(neg.cpu().numpy().ravel(), -mag, mag).astype(self.dtype)
+            return np.repeat(np.arange(self.d), self.zeta), cols.cpu().numpy().ravel(), vals
         rng = self._rng("entries")
-        if device_draws_enabled(self.d * self.zeta):
-            drawn = self._draw_device(rng)
-            if drawn is not None:
-                return drawn
         cols = sample_without_replacement(rng, self.d, self.zeta, self.k)
         cols.sort(axis=1)
         signs = rng.integers(0, 2, size=(self.d, self.zeta)) * 2.0 - 1.0
         vals = (signs / np.sqrt(self.zeta)).astype(self.dtype).ravel()
         return np.repeat(np.arange(self.d), self.zeta), cols.ravel().astype(np.int64), vals
 
-    def _draw_device(self, rng):
-        """The same draws on the GPU (devrng): column sets, sort, then the sign draws."""
-        import torch
+    def _device_draw(self):
+        """(cols (d, zeta) int64 sorted per row, neg (d, zeta) bool) drawn on the GPU (devrng), cached;
+        None when the host generator draws (small operators, permutation regime, no GPU)."""
+        if "_dev_draw" in self.__dict__:
+            return self._dev_draw
+        res = None
+        if device_draws_enabled(self.d * self.zeta):
+            import torch
 
-        g = DevicePhilox(rng, torch.device("cuda", torch.cuda.current_device()))
-        cols = g.sample_without_replacement(self.d, self.zeta, self.k)
-        if cols is None:  # permutation regime: host generator
+            g = DevicePhilox(self._rng("entries"), torch.device("cuda", torch.cuda.current_device()))
+            cols = g.sample_without_replacement(self.d, self.zeta, self.k)
+            if cols is not None:
+                cols = torch.sort(cols, dim=1).values
+                res = (cols, g.integers(2, (self.d, self.zeta)) == 0)
+        self._dev_draw = res
+        return res
+
+    def _signed_real(self) -> bool:
+        if self.field == "real" and self._coo is None and self._device_draw() is not None:
+            return True  # +-1/sqrt(zeta) by construction; no host copy of the draws needed
+        return super()._signed_real()
+
+    def _device_sign_form(self, device):
+        if self.field != "real" or self._device_draw() is None:
             return None
-        cols = torch.sort(cols, dim=1).values
-        neg = g.integers(2, (self.d, self.zeta)) == 0
-        mag = 1.0 / np.sqrt(self.zeta)
-        vals = np.where(neg.cpu().numpy().ravel(), -mag, mag).astype(self.dtype)
-        return np.repeat(np.arange(self.d), self.zeta), cols.cpu().numpy().ravel(), vals
+        cols, neg = self._device_draw()
+        return cols.to(device), neg.to(device), 1.0 / np.sqrt(self.zeta)
 
     def redraw(self, seed: int) -> "SparseUniformTM":
         return SparseUniformTM(self.d, self.k, self.zeta, field=self.field, seed=seed)

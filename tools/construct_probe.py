@@ -1,4 +1,4 @@
-"""Config-4 operator construction: host NumPy draws vs device draws (devrng), then the K2w encoding."""
+"""Config-4 operator setup: host draws + host K2w encoding vs device draws + device encoding."""
 import os
 import sys
 import time
@@ -8,15 +8,21 @@ import torch  # noqa: E402
 
 from paper_2508_21189_b200 import sketch as skb  # noqa: E402
 
-torch.zeros(1, device="cuda")
+dev = torch.device("cuda", 0)
+torch.zeros(1, device=dev)
 for mode in ("1", "0"):
     os.environ["SKETCH_B200_HOST_RNG"] = mode
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     tm = skb.SparseUniformTM(4194304, 2048, 8, seed=0)
-    tm._triplets()
+    if mode == "1":
+        tm._triplets()
+    else:
+        tm._device_draw()
     torch.cuda.synchronize()
     t1 = time.perf_counter()
-    tm._adjoint_wide_on(torch.device("cuda", 0))
+    tm._adjoint_wide_on(dev)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
-    print(f"{'host' if mode == '1' else 'device'} draws: {t1 - t0:.3f} s; wide encoding + upload: {t2 - t1:.3f} s")
+    print(f"{'host' if mode == '1' else 'device'} draws: {t1 - t0:.3f} s; K2w encoding on the "
+          f"{'host + upload' if mode == '1' else 'device'}: {t2 - t1:.3f} s")
