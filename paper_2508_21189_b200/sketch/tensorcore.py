@@ -86,7 +86,7 @@ def dense_right_tc(a, bt_hi, bt_lo, k: int, scale: float):
     if n == 0:
         return y
     lib = _lib.load()
-    stream = torch.cuda.current_stream().cuda_stream
+    stream = torch.cuda.current_stream(a.device).cuda_stream  # the operand's device, not the current one
     ldb = bt_hi.stride(0)
     ws_bytes = lib.sk_dense_tc_workspace_bytes(n, d, k, 1 if bt_lo is not None else 0)
     ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=a.device)

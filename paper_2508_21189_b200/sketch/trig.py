@@ -391,7 +391,7 @@ class SparseRttTM(TestMatrix):
         step = max(1, (512 << 20) // (self.d * 4))  # scratch of at most 512 MB per batch
         z = torch.empty((min(n, step), self.d), dtype=torch.float32, device=a.device)
         lib = _lib.load()
-        stream = torch.cuda.current_stream().cuda_stream
+        stream = torch.cuda.current_stream(a.device).cuda_stream
         for r0 in range(0, n, step):
             blk = a[r0:r0 + step]
             m = blk.shape[0]
