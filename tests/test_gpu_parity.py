@@ -221,3 +221,40 @@ def test_srtt_tc_matches_cuda_core_kernel(d, cuda, monkeypatch):
     monkeypatch.setenv("SKETCH_B200_SRTT", "regs")
     y_cc = tm.apply_right(a).double()
     assert float((y_tc - y_cc).norm() / y_cc.norm()) <= 1e-5
+
+
+def _families():
+    return [skb.SparseUniformTM(512, 48, 4, seed=1), skb.SparseStackTM(512, 4, 12, seed=2),
+            skb.SparseIIDTM(512, 40, 3.0, seed=3), skb.SparseColTM(512, 30, 2, seed=4),
+            skb.SparseRttTM(512, 32, 2, "wht", seed=5), skb.SparseRttTM(512, 32, 2, "dct", seed=6),
+            skb.KhatriRaoTM(8, 3, 24, "real_rademacher", seed=7), skb.GaussianTM(512, 20, seed=8)]
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_edge_shapes_every_family(dt, cuda):
+    """Empty, single-row, 1-D and strided (non-contiguous) operands on every family, host and
+    device, against the materialized Omega."""
+    import torch
+
+    rng = np.random.default_rng(0)
+    for tm in _families():
+        om = tm.materialize()
+        tol = 1e-12 if dt == np.float64 else 1e-5
+        # empty operands keep their shapes
+        assert tm.apply_right(np.zeros((0, tm.d), dt)).shape == (0, tm.k)
+        assert tm.apply_adjoint(np.zeros((tm.d, 0), dt)).shape == (tm.k, 0)
+        z = tm.apply_right(torch.zeros((0, tm.d), dtype=torch.float64 if dt == np.float64 else torch.float32,
+                                       device=cuda))
+        assert tuple(z.shape) == (0, tm.k)
+        # one row, and a 1-D adjoint operand (squeezed like the reference, base.py:86-91)
+        a1 = rng.standard_normal((1, tm.d)).astype(dt)
+        assert rel_err(tm.apply_right(a1), a1.astype(np.float64) @ om) <= tol
+        v = rng.standard_normal(tm.d).astype(dt)
+        got = tm.apply_adjoint(v)
+        assert got.shape == (tm.k,) and rel_err(got, om.T @ v.astype(np.float64)) <= tol
+        # strided device operands (a column slice and a transposed view)
+        big = torch.as_tensor(rng.standard_normal((9, 2 * tm.d)).astype(dt)).to(cuda)
+        sl = big[:, ::2]
+        assert rel_err(tm.apply_right(sl).cpu().numpy(), sl.cpu().double().numpy() @ om) <= tol
+        bt = torch.as_tensor(rng.standard_normal((7, tm.d)).astype(dt)).to(cuda).T
+        assert rel_err(tm.apply_adjoint(bt).cpu().numpy(), om.T @ bt.cpu().double().numpy()) <= tol
