@@ -97,7 +97,15 @@ def _t64(x):
 
 
 def orth(m, rel_tol: float = DEFAULT_RANK_TOL):
-    """Orthonormal basis of the numerical range (reference core/factor.py:63-82), on the device."""
+    """Orthonormal basis of the numerical range (reference core/factor.py:63-82), on the device.
+
+    Tall well-conditioned inputs (the rsvd sketch Y) take CholeskyQR2 in float64 — two Gram
+    matrices, two Cholesky factors, two triangular solves: a handful of GEMM-shaped passes instead
+    of a Householder QR (config 3, Y 131072 x 200: 9.9 -> ~2 ms). Anything else — a failed
+    Cholesky, diag(R) spread beyond 1e6 (CholeskyQR2 keeps orthogonality to ~eps only while
+    cond(Y) stays well below eps^-1/2), or the reference's rank cut firing — goes through the
+    reference path: Householder QR, then the 5-eps rank test on diag(R), else an SVD.
+    """
     import torch
 
     m = _t64(m)
@@ -105,6 +113,11 @@ def orth(m, rel_tol: float = DEFAULT_RANK_TOL):
         raise ValueError("matrix has nonfinite entries")
     if m.shape[1] == 0:
         return m.clone()
+    n, k = m.shape
+    if m.is_cuda and n >= 16 * k and n * k >= (1 << 20) and not m.is_complex():
+        q = _cholqr2(m)
+        if q is not None:
+            return q
     q, r = torch.linalg.qr(m, mode="reduced")
     diag = r.diagonal().abs()
     top = float(diag.max()) if diag.numel() else 0.0
@@ -115,6 +128,28 @@ def orth(m, rel_tol: float = DEFAULT_RANK_TOL):
     u, s, _ = torch.linalg.svd(m, full_matrices=False)
     rank = int((s > rel_tol * s[0]).sum())
     return u[:, :rank]
+
+
+def _cholqr2(m, max_spread: float = 1e6):
+    """Q of m = QR by CholeskyQR2 (float64), or None when the reference path must decide."""
+    import torch
+
+    r_tot = None
+    q = m
+    for _ in range(2):
+        g = q.T @ q
+        r, info = torch.linalg.cholesky_ex(g, upper=True)
+        if int(info) != 0:
+            return None
+        d = r.diagonal()
+        if float(d.min()) <= 0.0 or float(d.max()) > max_spread * float(d.min()):
+            return None
+        q = torch.linalg.solve_triangular(r, q, upper=True, left=False)
+        r_tot = r if r_tot is None else r @ r_tot
+    diag = r_tot.diagonal().abs()
+    if float(diag.min()) <= DEFAULT_RANK_TOL * float(diag.max()):
+        return None  # the reference's rank cut applies: let QR + SVD handle it
+    return q
 
 
 def _as_device_2d(a):
