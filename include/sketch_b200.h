@@ -199,6 +199,19 @@ SK_API int sk_dense_right_tc(const float* A, int64_t n, int64_t d, int64_t lda, 
                              const uint16_t* Bt_lo, int64_t ldb, int64_t k, double scale, float* Y,
                              int64_t ldy, void* ws, size_t ws_bytes, void* stream);
 
+/*
+ * K-TC, transposed operand — Y[d,k] = scale * A^T W for A [n rows][d cols] float32 (as stored) and
+ * W [n][k] given transposed as Wt_hi / Wt_lo (k x n bf16 hi + residual, row stride ldw): the second
+ * rsvd pass B = Q^* A (reference src/rand_nla.py:104, `q.conj().T @ a`), returned as B^T, with
+ * BF16x3 (A hi, A lo) x W hi + A hi x W lo.  The TMA lands 64 x 128 fp32 boxes of A and the
+ * converter warps transpose while splitting.  A 16-byte aligned with lda, d multiples of 4; ldw a
+ * multiple of 8.  Workspace: sk_dense_tn_tc_workspace_bytes(n, d, k) (split-K partials).
+ */
+SK_API size_t sk_dense_tn_tc_workspace_bytes(int64_t n, int64_t d, int64_t k);
+SK_API int sk_dense_tn_tc(const float* A, int64_t n, int64_t d, int64_t lda, const uint16_t* Wt_hi,
+                          const uint16_t* Wt_lo, int64_t ldw, int64_t k, double scale, float* Y, int64_t ldy,
+                          void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

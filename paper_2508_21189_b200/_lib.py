@@ -63,6 +63,9 @@ SIGNATURES = {
     "sk_dense_tc_workspace_bytes": (_c_size, [_c_i64, _c_i64, _c_i64, _c_int]),
     "sk_dense_right_tc": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_i64, _c_dbl, _c_p, _c_i64,
                                    _c_p, _c_size, _c_p]),
+    "sk_dense_tn_tc_workspace_bytes": (_c_size, [_c_i64, _c_i64, _c_i64]),
+    "sk_dense_tn_tc": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_i64, _c_dbl, _c_p, _c_i64,
+                                _c_p, _c_size, _c_p]),
 }
 
 _lock = threading.Lock()

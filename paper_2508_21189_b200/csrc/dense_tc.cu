@@ -62,6 +62,15 @@ __device__ __forceinline__ void setmaxnreg_inc() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
 }
 
+__device__ __forceinline__ float lds32f(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts128u(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
 struct Unit {
   int mt, nb, ks;
 };
@@ -74,7 +83,11 @@ __device__ __forceinline__ Unit unit_of(const TcParams& p, int u) {
   return r;
 }
 
-template <int NB>
+// TA = false: Y[M,N] = A[M,K] * B  (A row-major, the M x K operand read as stored).
+// TA = true : Y[M,N] = A^T * B with A stored [K rows][M cols] (the "TN" product Q^T A of rsvd):
+//             the TMA lands a 64 (K) x 128 (M) fp32 box and the converters transpose while they
+//             split, writing the same K-major SW128 bf16 tiles the MMA reads in the TA = false case.
+template <int NB, bool TA>
 __global__ void __launch_bounds__(kThreads, 1)
     dense_tc_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_bhi,
                     const __grid_constant__ CUtensorMap tm_blo, const TcParams p) {
@@ -129,7 +142,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + (size_t)s * stage_bytes;
           mbar_arrive_expect_tx(&tma_full[s], kAStageBytes + NB * b_bytes);
-          tma_load_2d(st, &tm_a, &tma_full[s], kb * BK, w.mt * BM);
+          if (TA) tma_load_2d(st, &tm_a, &tma_full[s], w.mt * BM, kb * BK);
+          else tma_load_2d(st, &tm_a, &tma_full[s], kb * BK, w.mt * BM);
           tma_load_2d(st + kAStageBytes, &tm_bhi, &tma_full[s], kb * BK, w.nb * p.BN);
           if (NB == 2) tma_load_2d(st + kAStageBytes + b_bytes, &tm_blo, &tma_full[s], kb * BK, w.nb * p.BN);
           if (++s == S) { s = 0; ph ^= 1; }
@@ -183,6 +197,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Unit w = unit_of(p, u);
       const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
       for (int kb = kb0; kb < kb1; ++kb) {
+        if constexpr (TA) {
+          // staging tile [64 k][128 m] fp32; thread ct = m reads its column (one 128-byte line per
+          // warp load) and writes row m of the K-major tiles as eight 16-byte chunks (k / 8)
+          mbar_wait(&tma_full[s], ph);
+          const uint32_t st = smem_u32(smem + (size_t)s * stage_bytes);
+          float col[BK];
+#pragma unroll
+          for (int i = 0; i < BK; ++i) col[i] = lds32f(st + (uint32_t)(i * BM + ct) * 4u);
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+          for (int g = 0; g < BK / 8; ++g) {
+            uint32_t h[4], l[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float x0 = col[8 * g + 2 * q], x1 = col[8 * g + 2 * q + 1];
+              h[q] = cvt_bf16x2(x1, x0);
+              l[q] = cvt_bf16x2(x1 - __uint_as_float(h[q] & 0xffff0000u), x0 - __uint_as_float(h[q] << 16));
+            }
+            const uint32_t off = (uint32_t)ct * 128u + ((((uint32_t)g) ^ ((uint32_t)ct & 7u)) << 4);
+            sts128u(st + off, h[0], h[1], h[2], h[3]);
+            sts128u(st + a_bytes + off, l[0], l[1], l[2], l[3]);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[s]);
+          if (++s == S) { s = 0; ph ^= 1; }
+          continue;
+        }
         float4 cur[16];
         mbar_wait(&tma_full[s], ph);
         const uint32_t st = smem_u32(smem + (size_t)s * stage_bytes);
@@ -331,15 +373,32 @@ int make_a_map(CUtensorMap* m, const float* a, int64_t M, int64_t K, int64_t lda
   return SK_OK;
 }
 
+// A stored [K rows][M cols] fp32 (the TN product): box 128 (M, contiguous) x 64 (K), no swizzle.
+int make_at_map(CUtensorMap* m, const float* a, int64_t M, int64_t K, int64_t lda) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(SK_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)K};
+  cuuint64_t strides[1] = {(cuuint64_t)lda * 4};
+  cuuint32_t box[2] = {(cuuint32_t)BM, (cuuint32_t)BK};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SK_EINVAL, "cuTensorMapEncodeTiled(A^T) failed (alignment of A / lda?)");
+  return SK_OK;
+}
+
 struct Plan {
   int BN, nblocks, ksplit, kb_per_split, mtiles, units, stages, astages;
   size_t smem, ws_bytes;
 };
 
-Plan make_plan(int64_t n, int64_t d, int64_t k, int NB) {
+Plan make_plan(int64_t n, int64_t d, int64_t k, int NB, bool wide_b = false) {
   Plan pl{};
-  // N blocks of at most 256 columns (two TMEM accumulators of BN columns each), BN % 32 == 0
-  const int64_t bn_max = NB == 2 ? 128 : 256;  // a split B doubles the B tile
+  // N blocks of at most 256 columns (two TMEM accumulators of BN columns each), BN % 32 == 0; a
+  // split B doubles the B tile, so it keeps 128 columns unless re-reading A per N block would cost
+  // more than the shallower ring (wide_b: the TN product, whose A strip is the big operand)
+  const int64_t bn_max = (NB == 2 && !wide_b) ? 128 : 256;
   pl.nblocks = (int)((k + bn_max - 1) / bn_max);
   const int64_t per = (k + pl.nblocks - 1) / pl.nblocks;
   pl.BN = (int)((per + 31) / 32 * 32);
@@ -427,11 +486,11 @@ extern "C" int sk_dense_right_tc(const float* A, int64_t n, int64_t d, int64_t l
   cudaStream_t s = as_stream(stream);
   const int grid = pl.units < sm_count() ? pl.units : sm_count();
   if (NB == 1) {
-    cudaFuncSetAttribute(dense_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
-    dense_tc_kernel<1><<<grid, kThreads, pl.smem, s>>>(ma, mh, ml, p);
+    cudaFuncSetAttribute(dense_tc_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    dense_tc_kernel<1, false><<<grid, kThreads, pl.smem, s>>>(ma, mh, ml, p);
   } else {
-    cudaFuncSetAttribute(dense_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
-    dense_tc_kernel<2><<<grid, kThreads, pl.smem, s>>>(ma, mh, ml, p);
+    cudaFuncSetAttribute(dense_tc_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    dense_tc_kernel<2, false><<<grid, kThreads, pl.smem, s>>>(ma, mh, ml, p);
   }
   st = check_launch("sk_dense_right_tc");
   if (st != SK_OK || pl.ksplit == 1) return st;
@@ -440,4 +499,67 @@ extern "C" int sk_dense_right_tc(const float* A, int64_t n, int64_t d, int64_t l
   if (blocks > 8 * (int64_t)sm_count()) blocks = 8 * (int64_t)sm_count();
   tc_splitk_reduce<<<(unsigned)blocks, 256, 0, s>>>(p.part, pl.ksplit, n, (int)k, (float)scale, Y, ldy);
   return check_launch("sk_dense_right_tc(reduce)");
+}
+
+extern "C" size_t sk_dense_tn_tc_workspace_bytes(int64_t n, int64_t d, int64_t k) {
+  if (n < 1 || d < 1 || k < 1) return 0;
+  return skb::make_plan(d, n, k, 2, true).ws_bytes;
+}
+
+// Y[d, k] = scale * A^T W  for A [n rows][d cols] fp32 and W [n][k] given as W^T = Wt (k rows of n,
+// bf16 hi + lo, row stride ldw): the rsvd product B^T = A^T Q (reference rand_nla.py:104) on the
+// tensor cores with BF16x3 (A hi/lo x W hi, A hi x W lo).
+extern "C" int sk_dense_tn_tc(const float* A, int64_t n, int64_t d, int64_t lda, const uint16_t* Wt_hi,
+                              const uint16_t* Wt_lo, int64_t ldw, int64_t k, double scale, float* Y, int64_t ldy,
+                              void* ws, size_t ws_bytes, void* stream) {
+  using namespace skb;
+  if (n < 1 || d < 1 || k < 1 || lda < d || ldw < n || ldy < k) return fail(SK_EINVAL, "sk_dense_tn_tc: bad shape");
+  if (!A || !Wt_hi || !Wt_lo || !Y) return fail(SK_EINVAL, "sk_dense_tn_tc: null pointer");
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (lda & 3) || (d & 3))
+    return fail(SK_EINVAL, "sk_dense_tn_tc: A must be 16-byte aligned with lda, d multiples of 4");
+  if ((reinterpret_cast<uintptr_t>(Wt_hi) & 15) || (reinterpret_cast<uintptr_t>(Wt_lo) & 15) || (ldw & 7))
+    return fail(SK_EINVAL, "sk_dense_tn_tc: W^T must be 16-byte aligned with ldw a multiple of 8");
+  const Plan pl = make_plan(d, n, k, 2, true);
+  if (pl.stages < 2) return fail(SK_EUNSUPPORTED, "sk_dense_tn_tc: tile does not fit shared memory");
+  if (pl.ksplit > 1 && (ws == nullptr || ws_bytes < pl.ws_bytes))
+    return fail(SK_EINVAL, "sk_dense_tn_tc: workspace too small (sk_dense_tn_tc_workspace_bytes)");
+  CUtensorMap ma, mh, ml;
+  int st = make_at_map(&ma, A, d, n, lda);
+  if (st != SK_OK) return st;
+  st = make_bt_map(&mh, Wt_hi, k, n, ldw, pl.BN);
+  if (st != SK_OK) return st;
+  st = make_bt_map(&ml, Wt_lo, k, n, ldw, pl.BN);
+  if (st != SK_OK) return st;
+  TcParams p{};
+  p.A = A;
+  p.M = d;
+  p.K = n;
+  p.lda = lda;
+  p.N = (int)k;
+  p.BN = pl.BN;
+  p.nblocks = pl.nblocks;
+  p.ksplit = pl.ksplit;
+  p.kb_per_split = pl.kb_per_split;
+  p.stages = pl.stages;
+  p.astages = pl.astages;
+  p.scale = (float)scale;
+  p.Y = Y;
+  p.ldy = ldy;
+  p.part = static_cast<float*>(ws);
+  p.num_units = pl.units;
+  p.mtiles = pl.mtiles;
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(2 * pl.BN)) cols <<= 1;
+  p.tmem_cols = cols;
+  cudaStream_t s = as_stream(stream);
+  const int grid = pl.units < sm_count() ? pl.units : sm_count();
+  cudaFuncSetAttribute(dense_tc_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+  dense_tc_kernel<2, true><<<grid, kThreads, pl.smem, s>>>(ma, mh, ml, p);
+  st = check_launch("sk_dense_tn_tc");
+  if (st != SK_OK || pl.ksplit == 1) return st;
+  const int64_t total = d * k;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 8 * (int64_t)sm_count()) blocks = 8 * (int64_t)sm_count();
+  tc_splitk_reduce<<<(unsigned)blocks, 256, 0, s>>>(p.part, pl.ksplit, d, (int)k, (float)scale, Y, ldy);
+  return check_launch("sk_dense_tn_tc(reduce)");
 }

@@ -13,7 +13,7 @@ import numpy as np
 
 from .. import _lib
 
-__all__ = ["dense_right_tc", "bt_from_triplets", "bt_from_dense", "bt_khatri_rao"]
+__all__ = ["dense_right_tc", "dense_tn_tc", "bt_from_triplets", "bt_from_dense", "bt_khatri_rao"]
 
 MAX_K = 512
 
@@ -95,4 +95,34 @@ def dense_right_tc(a, bt_hi, bt_lo, k: int, scale: float):
                                    bt_lo.data_ptr() if bt_lo is not None else None, ldb, k, float(scale),
                                    y.data_ptr(), y.stride(0), ws.data_ptr(), ws_bytes, stream)
     _lib.check(st, "sk_dense_right_tc")
+    return y
+
+
+def dense_tn_tc(a, w, scale: float = 1.0):
+    """scale * a^T @ w on the tensor cores (sk_dense_tn_tc) for float32 CUDA `a` (n x d) and a
+    float32/float64 `w` (n x k): BF16x3, fp32 accumulation in bounded chunks. Returns (d x k)."""
+    import torch
+
+    if a.dtype != torch.float32 or not a.is_cuda:
+        raise TypeError("dense_tn_tc needs a float32 CUDA A")
+    n, d = a.shape
+    k = w.shape[1]
+    if a.stride(1) != 1 or a.stride(0) % 4 or a.data_ptr() % 16 or d % 4:
+        a = a.contiguous()
+        if d % 4:
+            raise ValueError("dense_tn_tc needs d % 4 == 0")
+    ldw = _pad8(n)
+    wt = torch.zeros((k, ldw), dtype=torch.float32, device=a.device)
+    wt[:, :n] = w.T.to(device=a.device, dtype=torch.float32)
+    hi = wt.to(torch.bfloat16)
+    lo = (wt - hi.to(torch.float32)).to(torch.bfloat16)
+    y = torch.empty((d, k), dtype=torch.float32, device=a.device)
+    lib = _lib.load()
+    stream = torch.cuda.current_stream(a.device).cuda_stream
+    ws_bytes = lib.sk_dense_tn_tc_workspace_bytes(n, d, k)
+    ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=a.device)
+    with torch.cuda.device(a.device):
+        st = lib.sk_dense_tn_tc(a.data_ptr(), n, d, a.stride(0), hi.data_ptr(), lo.data_ptr(), ldw, k, float(scale),
+                                y.data_ptr(), y.stride(0), ws.data_ptr(), ws_bytes, stream)
+    _lib.check(st, "sk_dense_tn_tc")
     return y

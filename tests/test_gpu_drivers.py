@@ -98,3 +98,22 @@ def test_mixed_precision_gemv(n, d, cuda):
         z = _rmatvec_blocks(a, u, 1 << 16)
         assert float((y - a64 @ v).norm() / (a64 @ v).norm()) <= 1e-14
         assert float((z - a64.T @ u).norm() / (a64.T @ u).norm()) <= 1e-13
+
+
+@pytest.mark.parametrize("n,d,k", [(1000, 260, 37), (5000, 128, 200), (70001, 516, 64), (300, 4, 1)])
+def test_dense_tn_tc_vs_float64(n, d, k, cuda):
+    """A^T W on the tensor cores (BF16x3, transposing converters) against float64 torch."""
+    import torch
+
+    from paper_2508_21189_b200.sketch.tensorcore import dense_tn_tc
+
+    g = torch.Generator(device=cuda).manual_seed(n + d)
+    a = torch.randn(n, d, device=cuda, generator=g)
+    w = torch.randn(n, k, device=cuda, dtype=torch.float64, generator=g)
+    y = dense_tn_tc(a, w, 0.5)
+    ref = 0.5 * (a.double().T @ w)
+    assert tuple(y.shape) == (d, k)
+    assert float((y.double() - ref).norm() / ref.norm()) <= 1e-5
+    # strided A (a column slice): copied to a dense operand first
+    y2 = dense_tn_tc(torch.randn(n, 2 * d, device=cuda, generator=g)[:, :d].contiguous(), w)
+    assert tuple(y2.shape) == (d, k)

@@ -30,7 +30,9 @@ for _ in range(2):
     y = t("sketch", lambda: tm.apply_right(a))
     q = t("orth (f64 QR of Y)", lambda: rand_nla.orth(y))
     with rand_nla._no_tf32():
-        b = t("B = Q^T A (fp32 GEMM)", lambda: (q.to(a.dtype).T @ a).to(q.dtype))
+        b = t("B = Q^T A (fp32 cuBLAS)", lambda: (q.to(a.dtype).T @ a).to(q.dtype))
+    b2 = t("B = Q^T A (sk_dense_tn_tc)", lambda: rand_nla._qt_a(q, a))
+    print("   rel diff", float((b2 - b).norm() / b.norm()))
     usv = t("SVD(B) f64 direct", lambda: torch.linalg.svd(b.double(), full_matrices=False))
     bt = b.double().T.contiguous()
     t("  QR(B^T) 16384x200", lambda: torch.linalg.qr(bt, mode="reduced"))
