@@ -34,6 +34,7 @@ for _ in range(2):
     b2 = t("B = Q^T A (sk_dense_tn_tc)", lambda: rand_nla._qt_a(q, a))
     print("   rel diff", float((b2 - b).norm() / b.norm()))
     usv = t("SVD(B) f64 direct", lambda: torch.linalg.svd(b.double(), full_matrices=False))
+    t("SVD(B) f64 gesvdj", lambda: torch.linalg.svd(b.double(), full_matrices=False, driver="gesvdj"))
     bt = b.double().T.contiguous()
     t("  QR(B^T) 16384x200", lambda: torch.linalg.qr(bt, mode="reduced"))
     rr = torch.randn(200, 200, device=dev, dtype=torch.float64)
