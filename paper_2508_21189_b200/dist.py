@@ -77,12 +77,11 @@ def sharded_rsvd(a_local, k: int, tm, group=None):
     """Randomized SVD of a row-sharded A: returns (U_g, sigma, V) with U_g this rank's rows."""
     import torch
 
-    from .rand_nla import SvdFactorization, _no_tf32
+    from .rand_nla import SvdFactorization, _qt_a
 
     y = tm.apply_right(a_local)
     q = cholesky_qr2(y, group)
-    with _no_tf32():
-        b = (q.to(a_local.dtype).T @ a_local).to(torch.float64)
+    b = _qt_a(q, a_local).to(torch.float64)  # this rank's Q_g^T A_g (tensor cores for float32 CUDA)
     allreduce_sum(b, group)
     u, s, vh = torch.linalg.svd(b, full_matrices=False)
     return SvdFactorization(q @ u, s, vh.T)
