@@ -131,6 +131,17 @@ SK_API size_t sk_sparse_adjoint_wide_workspace_bytes(int64_t d, int64_t m, int64
 SK_API int sk_sparse_adjoint_wide(const float* A, int64_t d, int64_t m, int64_t lda, const uint16_t* enc,
                                   const int64_t* seg_off, int32_t seg_cap, int64_t k, double scale, float* SA,
                                   int64_t ldsa, int accumulate, void* ws, size_t ws_bytes, void* stream);
+
+/* float64 K2w (the reference's dtype): the same encoding and layout with 64-column slices (two
+ * float64 columns per lane, 16-byte loads) and float64 accumulation. A 16-byte aligned, lda even. */
+SK_API size_t sk_sparse_adjoint_wide_workspace_bytes_f64(int64_t d, int64_t m, int64_t k);
+SK_API int sk_sparse_adjoint_wide_f64(const double* A, int64_t d, int64_t m, int64_t lda, const uint16_t* enc,
+                                      const int64_t* seg_off, int32_t seg_cap, int64_t k, double scale, double* SA,
+                                      int64_t ldsa, int accumulate, void* ws, size_t ws_bytes, void* stream);
+SK_API int sk_sparse_adjoint_wide_rows_f64(const double* A, int64_t d, int64_t r0, int64_t r1, int64_t m,
+                                           int64_t lda, const uint16_t* enc, const int64_t* seg_off, int32_t seg_cap,
+                                           int64_t k, double scale, double* SA, int64_t ldsa, int accumulate, void* ws,
+                                           size_t ws_bytes, void* stream);
 /* The same for the row block [r0, r1) of Omega (r0 % 128 == 0): A points at row r0 of the operand
  * and holds r1 - r0 rows; SA (+)= scale * Omega[r0:r1]^T * A. Lets a caller stream A through L2 in
  * row blocks and chain other kernels on each block (two-sided sketches). Workspace:

@@ -31,19 +31,25 @@ namespace skb {
 // defined in sparse_adjoint.cu: part[p][k][m] summed over p in order (float64), scaled, stored to SA
 int adjoint_reduce_f32(const float* part, int npieces, int64_t k, int64_t m, double scale, float* SA, int64_t ldsa,
                        int accumulate, cudaStream_t s);
+int adjoint_reduce_f64(const double* part, int npieces, int64_t k, int64_t m, double scale, double* SA, int64_t ldsa,
+                       int accumulate, cudaStream_t s);
 
 namespace {
 
 using namespace sm100;
 
 constexpr int W_R = 128;                 // rows per chunk
-constexpr int W_COLS = 128;              // columns per CTA slice (4 per lane)
+constexpr int W_ROW_BYTES = 512;         // bytes of a tile row: 128 float32 or 64 float64 columns (16 per lane)
 constexpr int W_WARPS = 16;
 constexpr int W_CPW = 16;                // output rows per warp
 constexpr int W_CG = W_WARPS * W_CPW;    // output rows per CTA (group)
 constexpr int W_HDR = 24;                // header uint16s: 17 warp offsets, padded to 48 bytes
 constexpr int W_STAGES = 3;
-constexpr uint32_t W_TILE = W_R * W_COLS * 4;  // 64 KB
+constexpr uint32_t W_TILE = W_R * W_ROW_BYTES;  // 64 KB
+template <typename T>
+constexpr int w_cols() {
+  return W_ROW_BYTES / (int)sizeof(T);  // columns per CTA slice
+}
 
 typedef unsigned long long u64;
 
@@ -70,7 +76,7 @@ struct WParams {
   uint32_t stage_bytes;
   const uint16_t* enc;
   const int64_t* seg_off;  // [nchunks * ngroups + 1], uint16 units
-  float* part;             // [npieces][k][m]
+  void* part;              // [npieces][k][m] of the element type
 };
 
 // Dispatch one entry: index j = (neg << 4) | (c mod 16) selects acc[c mod 16] +=/-= v (four columns
@@ -117,12 +123,55 @@ struct WParams {
       : "+l"(acc[0]), "+l"(acc[1]), "+l"(acc[2]), "+l"(acc[3]), "+l"(acc[4]), "+l"(acc[5]), "+l"(acc[6]), "+l"(acc[7]), "+l"(acc[8]), "+l"(acc[9]), "+l"(acc[10]), "+l"(acc[11]), "+l"(acc[12]), "+l"(acc[13]), "+l"(acc[14]), "+l"(acc[15]), "+l"(acc[16]), "+l"(acc[17]), "+l"(acc[18]), "+l"(acc[19]), "+l"(acc[20]), "+l"(acc[21]), "+l"(acc[22]), "+l"(acc[23]), "+l"(acc[24]), "+l"(acc[25]), "+l"(acc[26]), "+l"(acc[27]), "+l"(acc[28]), "+l"(acc[29]), "+l"(acc[30]), "+l"(acc[31]) \
       : "l"(V0), "l"(V1), "r"(JJ))
 
+// float64 variant: each packed pair register holds one double (two columns per lane)
+#define SKB_W_DISPATCH64(V0, V1, JJ) \
+  asm volatile( \
+      "{\n\t" \
+      "T_%=: .branchtargets A0_%=, A1_%=, A2_%=, A3_%=, A4_%=, A5_%=, A6_%=, A7_%=, A8_%=, A9_%=, A10_%=, A11_%=, A12_%=, A13_%=, A14_%=, A15_%=, S0_%=, S1_%=, S2_%=, S3_%=, S4_%=, S5_%=, S6_%=, S7_%=, S8_%=, S9_%=, S10_%=, S11_%=, S12_%=, S13_%=, S14_%=, S15_%=, D_%=;\n\t" \
+      "brx.idx.uni %34, T_%=;\n\t" \
+      "A0_%=: add.rn.f64 %0, %0, %32;\n\tadd.rn.f64 %1, %1, %33;\n\tbra.uni D_%=;\n\t" \
+      "A1_%=: add.rn.f64 %2, %2, %32;\n\tadd.rn.f64 %3, %3, %33;\n\tbra.uni D_%=;\n\t" \
+      "A2_%=: add.rn.f64 %4, %4, %32;\n\tadd.rn.f64 %5, %5, %33;\n\tbra.uni D_%=;\n\t" \
+      "A3_%=: add.rn.f64 %6, %6, %32;\n\tadd.rn.f64 %7, %7, %33;\n\tbra.uni D_%=;\n\t" \
+      "A4_%=: add.rn.f64 %8, %8, %32;\n\tadd.rn.f64 %9, %9, %33;\n\tbra.uni D_%=;\n\t" \
+      "A5_%=: add.rn.f64 %10, %10, %32;\n\tadd.rn.f64 %11, %11, %33;\n\tbra.uni D_%=;\n\t" \
+      "A6_%=: add.rn.f64 %12, %12, %32;\n\tadd.rn.f64 %13, %13, %33;\n\tbra.uni D_%=;\n\t" \
+      "A7_%=: add.rn.f64 %14, %14, %32;\n\tadd.rn.f64 %15, %15, %33;\n\tbra.uni D_%=;\n\t" \
+      "A8_%=: add.rn.f64 %16, %16, %32;\n\tadd.rn.f64 %17, %17, %33;\n\tbra.uni D_%=;\n\t" \
+      "A9_%=: add.rn.f64 %18, %18, %32;\n\tadd.rn.f64 %19, %19, %33;\n\tbra.uni D_%=;\n\t" \
+      "A10_%=: add.rn.f64 %20, %20, %32;\n\tadd.rn.f64 %21, %21, %33;\n\tbra.uni D_%=;\n\t" \
+      "A11_%=: add.rn.f64 %22, %22, %32;\n\tadd.rn.f64 %23, %23, %33;\n\tbra.uni D_%=;\n\t" \
+      "A12_%=: add.rn.f64 %24, %24, %32;\n\tadd.rn.f64 %25, %25, %33;\n\tbra.uni D_%=;\n\t" \
+      "A13_%=: add.rn.f64 %26, %26, %32;\n\tadd.rn.f64 %27, %27, %33;\n\tbra.uni D_%=;\n\t" \
+      "A14_%=: add.rn.f64 %28, %28, %32;\n\tadd.rn.f64 %29, %29, %33;\n\tbra.uni D_%=;\n\t" \
+      "A15_%=: add.rn.f64 %30, %30, %32;\n\tadd.rn.f64 %31, %31, %33;\n\tbra.uni D_%=;\n\t" \
+      "S0_%=: sub.rn.f64 %0, %0, %32;\n\tsub.rn.f64 %1, %1, %33;\n\tbra.uni D_%=;\n\t" \
+      "S1_%=: sub.rn.f64 %2, %2, %32;\n\tsub.rn.f64 %3, %3, %33;\n\tbra.uni D_%=;\n\t" \
+      "S2_%=: sub.rn.f64 %4, %4, %32;\n\tsub.rn.f64 %5, %5, %33;\n\tbra.uni D_%=;\n\t" \
+      "S3_%=: sub.rn.f64 %6, %6, %32;\n\tsub.rn.f64 %7, %7, %33;\n\tbra.uni D_%=;\n\t" \
+      "S4_%=: sub.rn.f64 %8, %8, %32;\n\tsub.rn.f64 %9, %9, %33;\n\tbra.uni D_%=;\n\t" \
+      "S5_%=: sub.rn.f64 %10, %10, %32;\n\tsub.rn.f64 %11, %11, %33;\n\tbra.uni D_%=;\n\t" \
+      "S6_%=: sub.rn.f64 %12, %12, %32;\n\tsub.rn.f64 %13, %13, %33;\n\tbra.uni D_%=;\n\t" \
+      "S7_%=: sub.rn.f64 %14, %14, %32;\n\tsub.rn.f64 %15, %15, %33;\n\tbra.uni D_%=;\n\t" \
+      "S8_%=: sub.rn.f64 %16, %16, %32;\n\tsub.rn.f64 %17, %17, %33;\n\tbra.uni D_%=;\n\t" \
+      "S9_%=: sub.rn.f64 %18, %18, %32;\n\tsub.rn.f64 %19, %19, %33;\n\tbra.uni D_%=;\n\t" \
+      "S10_%=: sub.rn.f64 %20, %20, %32;\n\tsub.rn.f64 %21, %21, %33;\n\tbra.uni D_%=;\n\t" \
+      "S11_%=: sub.rn.f64 %22, %22, %32;\n\tsub.rn.f64 %23, %23, %33;\n\tbra.uni D_%=;\n\t" \
+      "S12_%=: sub.rn.f64 %24, %24, %32;\n\tsub.rn.f64 %25, %25, %33;\n\tbra.uni D_%=;\n\t" \
+      "S13_%=: sub.rn.f64 %26, %26, %32;\n\tsub.rn.f64 %27, %27, %33;\n\tbra.uni D_%=;\n\t" \
+      "S14_%=: sub.rn.f64 %28, %28, %32;\n\tsub.rn.f64 %29, %29, %33;\n\tbra.uni D_%=;\n\t" \
+      "S15_%=: sub.rn.f64 %30, %30, %32;\n\tsub.rn.f64 %31, %31, %33;\n\tbra.uni D_%=;\n\t" \
+      "D_%=:\n\t}" \
+      : "+l"(acc[0]), "+l"(acc[1]), "+l"(acc[2]), "+l"(acc[3]), "+l"(acc[4]), "+l"(acc[5]), "+l"(acc[6]), "+l"(acc[7]), "+l"(acc[8]), "+l"(acc[9]), "+l"(acc[10]), "+l"(acc[11]), "+l"(acc[12]), "+l"(acc[13]), "+l"(acc[14]), "+l"(acc[15]), "+l"(acc[16]), "+l"(acc[17]), "+l"(acc[18]), "+l"(acc[19]), "+l"(acc[20]), "+l"(acc[21]), "+l"(acc[22]), "+l"(acc[23]), "+l"(acc[24]), "+l"(acc[25]), "+l"(acc[26]), "+l"(acc[27]), "+l"(acc[28]), "+l"(acc[29]), "+l"(acc[30]), "+l"(acc[31]) \
+      : "l"(V0), "l"(V1), "r"(JJ))
+
 // Walk entries [a, b) of this warp (a, b multiples of 4): four entries per uniform 8-byte shared
 // load; their four row values (16 bytes per lane) are loaded before the four dispatches.
 __device__ __forceinline__ void lds128u(uint32_t addr, u64& x, u64& y) {
   asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(addr));
 }
 
+template <typename T>
 __device__ __forceinline__ void walk(u64 (&acc)[2 * W_CPW], uint32_t tile_lane, uint32_t ent, int a, int b) {
   for (int e = a; e < b; e += 4) {
     const u64 q = lds64(ent + 2u * (uint32_t)e);
@@ -134,15 +183,24 @@ __device__ __forceinline__ void walk(u64 (&acc)[2 * W_CPW], uint32_t tile_lane, 
     lds128u(tile_lane + (u2 & 0xfe00u), a2, b2);
     lds128u(tile_lane + (u3 & 0xfe00u), a3, b3);
     const uint32_t j0 = u0 & 63u, j1 = u1 & 63u, j2 = u2 & 63u, j3 = u3 & 63u;
-    SKB_W_DISPATCH(a0, b0, j0);
-    SKB_W_DISPATCH(a1, b1, j1);
-    SKB_W_DISPATCH(a2, b2, j2);
-    SKB_W_DISPATCH(a3, b3, j3);
+    if constexpr (sizeof(T) == 4) {
+      SKB_W_DISPATCH(a0, b0, j0);
+      SKB_W_DISPATCH(a1, b1, j1);
+      SKB_W_DISPATCH(a2, b2, j2);
+      SKB_W_DISPATCH(a3, b3, j3);
+    } else {
+      SKB_W_DISPATCH64(a0, b0, j0);
+      SKB_W_DISPATCH64(a1, b1, j1);
+      SKB_W_DISPATCH64(a2, b2, j2);
+      SKB_W_DISPATCH64(a3, b3, j3);
+    }
   }
 }
 
+template <typename T>
 __global__ void __launch_bounds__((W_WARPS + 1) * 32, 1)
     sparse_adjoint_wide(const __grid_constant__ CUtensorMap tm, const WParams p) {
+  constexpr int W_COLS = w_cols<T>();
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + W_STAGES * p.stage_bytes);
@@ -192,23 +250,31 @@ __global__ void __launch_bounds__((W_WARPS + 1) * 32, 1)
     const uint32_t st = smem_u32(smem + (size_t)s * p.stage_bytes);
     const uint32_t hdr = st + W_TILE;
     const int a = (int)lds_u16(hdr + 2u * warp), b = (int)lds_u16(hdr + 2u * warp + 2u);
-    walk(acc, st + 16u * lane, hdr + 2u * W_HDR, a, b);
+    walk<T>(acc, st + 16u * lane, hdr + 2u * W_HDR, a, b);
     __syncwarp();
     if (lane == 0) mbar_arrive(&consumed[s]);
   }
 
   {
-    const int64_t col = (int64_t)slice * W_COLS + 4 * lane;
-    float* out = p.part + (int64_t)piece * p.k * p.m;
+    constexpr int CPL = 16 / (int)sizeof(T);  // columns per lane
+    const int64_t col = (int64_t)slice * W_COLS + CPL * lane;
+    T* out = static_cast<T*>(p.part) + (int64_t)piece * p.k * p.m;
 #pragma unroll
     for (int j = 0; j < W_CPW; ++j) {
       const int64_t c = (int64_t)g * W_CG + warp * W_CPW + j;
       if (c < p.k) {
-        const float v[4] = {__uint_as_float((uint32_t)acc[2 * j]), __uint_as_float((uint32_t)(acc[2 * j] >> 32)),
-                            __uint_as_float((uint32_t)acc[2 * j + 1]),
-                            __uint_as_float((uint32_t)(acc[2 * j + 1] >> 32))};
+        T v[CPL];
+        if constexpr (sizeof(T) == 4) {
+          v[0] = __uint_as_float((uint32_t)acc[2 * j]);
+          v[1] = __uint_as_float((uint32_t)(acc[2 * j] >> 32));
+          v[2] = __uint_as_float((uint32_t)acc[2 * j + 1]);
+          v[3] = __uint_as_float((uint32_t)(acc[2 * j + 1] >> 32));
+        } else {
+          v[0] = __longlong_as_double((long long)acc[2 * j]);
+          v[1] = __longlong_as_double((long long)acc[2 * j + 1]);
+        }
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < CPL; ++q)
           if (col + q < p.m) out[c * p.m + col + q] = v[q];
       }
     }
@@ -221,11 +287,11 @@ struct WPlan {
   size_t smem, ws_bytes;
 };
 
-WPlan wide_plan(int64_t d, int64_t m, int64_t k, int32_t seg_cap) {
+WPlan wide_plan(int64_t d, int64_t m, int64_t k, int32_t seg_cap, int cols = 128, int esize = 4) {
   WPlan pl{};
   pl.nchunks = (int)((d + W_R - 1) / W_R);
   pl.ngroups = (int)((k + W_CG - 1) / W_CG);
-  pl.nslices = (int)((m + W_COLS - 1) / W_COLS);
+  pl.nslices = (int)((m + cols - 1) / cols);
   const int64_t roles = (int64_t)pl.ngroups * pl.nslices;
   // one CTA per SM: about 4 waves, with the piece count that fills the last wave best (config 4:
   // 32 roles x 37 pieces = 8 full waves instead of 32 x 19 = 4.1)
@@ -247,7 +313,7 @@ WPlan wide_plan(int64_t d, int64_t m, int64_t k, int32_t seg_cap) {
   pl.npieces = (pl.nchunks + pl.chunks_per_piece - 1) / pl.chunks_per_piece;
   pl.stage_bytes = (W_TILE + (uint32_t)seg_cap * 2u + 1023u) & ~1023u;
   pl.smem = 1024 + (size_t)W_STAGES * pl.stage_bytes + 2 * W_STAGES * 8;
-  pl.ws_bytes = (size_t)pl.npieces * k * m * sizeof(float);
+  pl.ws_bytes = (size_t)pl.npieces * k * m * esize;
   return pl;
 }
 
@@ -312,37 +378,37 @@ extern "C" int64_t sk_sparse_adjoint_wide_segments(int64_t d, int64_t k) {
   return ((d + W_R - 1) / W_R) * ((k + W_CG - 1) / W_CG) + 1;
 }
 
-extern "C" size_t sk_sparse_adjoint_wide_workspace_bytes(int64_t d, int64_t m, int64_t k) {
-  if (d < 1 || m < 1 || k < 1) return 0;
-  return wide_plan(d, m, k, 0).ws_bytes;
-}
+namespace skb {
+namespace {
 
-extern "C" int sk_sparse_adjoint_wide_rows(const float* A, int64_t d, int64_t r0, int64_t r1, int64_t m,
-                                           int64_t lda, const uint16_t* enc, const int64_t* seg_off, int32_t seg_cap,
-                                           int64_t k, double scale, float* SA, int64_t ldsa, int accumulate, void* ws,
-                                           size_t ws_bytes, void* stream) {
+template <typename T>
+int wide_rows_t(const T* A, int64_t d, int64_t r0, int64_t r1, int64_t m, int64_t lda, const uint16_t* enc,
+                const int64_t* seg_off, int32_t seg_cap, int64_t k, double scale, T* SA, int64_t ldsa, int accumulate,
+                void* ws, size_t ws_bytes, void* stream) {
+  constexpr int COLS = w_cols<T>();
+  constexpr int64_t LDA_Q = 16 / (int64_t)sizeof(T);  // 16-byte row alignment
   if (d < 1 || m < 0 || k < 1 || lda < m || ldsa < m || seg_cap < W_HDR)
     return fail(SK_EINVAL, "sk_sparse_adjoint_wide: bad shape/leading dimension");
   if (r0 < 0 || r1 > d || r0 >= r1 || (r0 % W_R) != 0)
     return fail(SK_EINVAL, "sk_sparse_adjoint_wide: row block must be [r0, r1) within [0, d) with r0 % 128 == 0");
   if (m == 0) return SK_OK;
   if (!A || !SA || !enc || !seg_off) return fail(SK_EINVAL, "sk_sparse_adjoint_wide: null pointer");
-  if ((reinterpret_cast<uintptr_t>(A) & 15) || (lda & 3))
-    return fail(SK_EUNSUPPORTED, "sk_sparse_adjoint_wide: A must be 16-byte aligned with lda % 4 == 0");
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (lda % LDA_Q))
+    return fail(SK_EUNSUPPORTED, "sk_sparse_adjoint_wide: A must be 16-byte aligned with 16-byte rows");
   const int64_t rows = r1 - r0;
-  const WPlan pl = wide_plan(rows, m, k, seg_cap);
+  const WPlan pl = wide_plan(rows, m, k, seg_cap, COLS, (int)sizeof(T));
   if (pl.smem > 227 * 1024) return fail(SK_EUNSUPPORTED, "sk_sparse_adjoint_wide: segment capacity too large");
   if (ws_bytes < pl.ws_bytes || !ws) return fail(SK_EINVAL, "sk_sparse_adjoint_wide: workspace too small");
   sm100::EncodeTiledFnT fn = sm100::encode_tiled_fn();
   if (!fn) return fail(SK_ECUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap tm;
   cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)lda * 4};
-  cuuint32_t box[2] = {(cuuint32_t)W_COLS, (cuuint32_t)W_R};
+  cuuint64_t strides[1] = {(cuuint64_t)lda * sizeof(T)};
+  cuuint32_t box[2] = {(cuuint32_t)COLS, (cuuint32_t)W_R};
   cuuint32_t estr[2] = {1, 1};
-  if (fn(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(A), dims, strides, box, estr,
-         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  if (fn(&tm, dt, 2, const_cast<T*>(A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return fail(SK_EINVAL, "sk_sparse_adjoint_wide: cannot describe A for TMA");
   WParams p{};
   p.d = rows;
@@ -357,14 +423,46 @@ extern "C" int sk_sparse_adjoint_wide_rows(const float* A, int64_t d, int64_t r0
   p.stage_bytes = pl.stage_bytes;
   p.enc = enc;
   p.seg_off = seg_off;
-  p.part = static_cast<float*>(ws);
+  p.part = ws;
   cudaStream_t s = as_stream(stream);
-  cudaFuncSetAttribute(sparse_adjoint_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
-  sparse_adjoint_wide<<<dim3((unsigned)pl.ngroups, (unsigned)pl.nslices, (unsigned)pl.npieces), (W_WARPS + 1) * 32,
-                        pl.smem, s>>>(tm, p);
+  cudaFuncSetAttribute(sparse_adjoint_wide<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+  sparse_adjoint_wide<T><<<dim3((unsigned)pl.ngroups, (unsigned)pl.nslices, (unsigned)pl.npieces),
+                           (W_WARPS + 1) * 32, pl.smem, s>>>(tm, p);
   int st = check_launch("sk_sparse_adjoint_wide");
   if (st != SK_OK) return st;
-  return adjoint_reduce_f32(p.part, pl.npieces, k, m, scale, SA, ldsa, accumulate, s);
+  if constexpr (sizeof(T) == 4)
+    return adjoint_reduce_f32(static_cast<const float*>(ws), pl.npieces, k, m, scale, SA, ldsa, accumulate, s);
+  else
+    return adjoint_reduce_f64(static_cast<const double*>(ws), pl.npieces, k, m, scale, SA, ldsa, accumulate, s);
+}
+
+}  // namespace
+}  // namespace skb
+
+extern "C" size_t sk_sparse_adjoint_wide_workspace_bytes(int64_t d, int64_t m, int64_t k) {
+  if (d < 1 || m < 1 || k < 1) return 0;
+  return wide_plan(d, m, k, 0).ws_bytes;
+}
+
+extern "C" size_t sk_sparse_adjoint_wide_workspace_bytes_f64(int64_t d, int64_t m, int64_t k) {
+  if (d < 1 || m < 1 || k < 1) return 0;
+  return wide_plan(d, m, k, 0, w_cols<double>(), 8).ws_bytes;
+}
+
+extern "C" int sk_sparse_adjoint_wide_rows(const float* A, int64_t d, int64_t r0, int64_t r1, int64_t m,
+                                           int64_t lda, const uint16_t* enc, const int64_t* seg_off, int32_t seg_cap,
+                                           int64_t k, double scale, float* SA, int64_t ldsa, int accumulate, void* ws,
+                                           size_t ws_bytes, void* stream) {
+  return wide_rows_t<float>(A, d, r0, r1, m, lda, enc, seg_off, seg_cap, k, scale, SA, ldsa, accumulate, ws, ws_bytes,
+                            stream);
+}
+
+extern "C" int sk_sparse_adjoint_wide_rows_f64(const double* A, int64_t d, int64_t r0, int64_t r1, int64_t m,
+                                               int64_t lda, const uint16_t* enc, const int64_t* seg_off,
+                                               int32_t seg_cap, int64_t k, double scale, double* SA, int64_t ldsa,
+                                               int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  return wide_rows_t<double>(A, d, r0, r1, m, lda, enc, seg_off, seg_cap, k, scale, SA, ldsa, accumulate, ws,
+                             ws_bytes, stream);
 }
 
 extern "C" int sk_sparse_adjoint_wide(const float* A, int64_t d, int64_t m, int64_t lda, const uint16_t* enc,
@@ -372,4 +470,11 @@ extern "C" int sk_sparse_adjoint_wide(const float* A, int64_t d, int64_t m, int6
                                       int64_t ldsa, int accumulate, void* ws, size_t ws_bytes, void* stream) {
   return sk_sparse_adjoint_wide_rows(A, d, 0, d, m, lda, enc, seg_off, seg_cap, k, scale, SA, ldsa, accumulate, ws,
                                      ws_bytes, stream);
+}
+
+extern "C" int sk_sparse_adjoint_wide_f64(const double* A, int64_t d, int64_t m, int64_t lda, const uint16_t* enc,
+                                          const int64_t* seg_off, int32_t seg_cap, int64_t k, double scale, double* SA,
+                                          int64_t ldsa, int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  return sk_sparse_adjoint_wide_rows_f64(A, d, 0, d, m, lda, enc, seg_off, seg_cap, k, scale, SA, ldsa, accumulate,
+                                         ws, ws_bytes, stream);
 }

@@ -493,6 +493,15 @@ int adjoint_reduce_f32(const float* part, int npieces, int64_t k, int64_t m, dou
   return check_launch("sk_sparse_adjoint(reduce)");
 }
 
+int adjoint_reduce_f64(const double* part, int npieces, int64_t k, int64_t m, double scale, double* SA, int64_t ldsa,
+                       int accumulate, cudaStream_t s) {
+  const int64_t total = k * m;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 8 * (int64_t)sm_count()) blocks = 8 * (int64_t)sm_count();
+  adjoint_reduce<double><<<(unsigned)blocks, 256, 0, s>>>(part, npieces, k * m, m, k, m, scale, SA, ldsa, accumulate);
+  return check_launch("sk_sparse_adjoint(reduce)");
+}
+
 }  // namespace skb
 
 extern "C" int sk_sparse_adjoint_chunk_rows(int dtype, int64_t d, int64_t k) {

@@ -217,7 +217,7 @@ class _SignSparseTM(TestMatrix):
         return self._device_cache[key]
 
     def adjoint_path(self, b) -> str:
-        """Kernel used by apply_adjoint: 'wide' (K2w, float32), 'gather' (K2) or 'dense'."""
+        """Kernel used by apply_adjoint: 'wide' (K2w, float32 / float64), 'gather' (K2) or 'dense'."""
         import os
 
         import torch
@@ -225,8 +225,8 @@ class _SignSparseTM(TestMatrix):
         if not self._signed_real() or b.dtype not in (torch.float32, torch.float64):
             return "dense"
         forced = os.environ.get("SKETCH_B200_SPARSE_ADJOINT", "auto")
-        wide_ok = (b.dtype == torch.float32 and b.data_ptr() % 16 == 0 and b.stride(0) % 4 == 0
-                   and b.stride(1) == 1 and b.shape[1] >= 1)
+        per16 = 16 // b.element_size()  # 16-byte rows for the TMA tiles
+        wide_ok = (b.data_ptr() % 16 == 0 and b.stride(0) % per16 == 0 and b.stride(1) == 1 and b.shape[1] >= 1)
         return "wide" if (wide_ok and forced != "gather") else "gather"
 
     def _sparse_input_ok(self) -> bool:
@@ -282,14 +282,17 @@ class _SignSparseTM(TestMatrix):
         import torch
 
         if self.adjoint_path(b_rows) != "wide":
-            raise NotImplementedError("adjoint_rows needs an aligned float32 device block (wide path)")
+            raise NotImplementedError("adjoint_rows needs an aligned float32 or float64 device block (wide path)")
         enc, seg_off, cap, mag = self._adjoint_wide_on(b_rows.device)
         m = b_rows.shape[1]
         lib = _lib.load()
-        ws_bytes = lib.sk_sparse_adjoint_wide_workspace_bytes(r1 - r0, m, self.k)
+        f64 = b_rows.dtype == torch.float64
+        ws_bytes = (lib.sk_sparse_adjoint_wide_workspace_bytes_f64 if f64 else
+                    lib.sk_sparse_adjoint_wide_workspace_bytes)(r1 - r0, m, self.k)
         ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=b_rows.device)
+        fn = lib.sk_sparse_adjoint_wide_rows_f64 if f64 else lib.sk_sparse_adjoint_wide_rows
         with torch.cuda.device(b_rows.device):
-            st = lib.sk_sparse_adjoint_wide_rows(b_rows.data_ptr(), self.d, r0, r1, m, b_rows.stride(0),
+            st = fn(b_rows.data_ptr(), self.d, r0, r1, m, b_rows.stride(0),
                                                  enc.data_ptr(), seg_off.data_ptr(), cap, self.k, mag,
                                                  out.data_ptr(), out.stride(0), 1 if accumulate else 0,
                                                  ws.data_ptr(), ws_bytes, torch.cuda.current_stream().cuda_stream)
@@ -306,10 +309,13 @@ class _SignSparseTM(TestMatrix):
             m = b.shape[1]
             out = torch.empty((self.k, m), dtype=b.dtype, device=b.device)
             lib = _lib.load()
-            ws_bytes = lib.sk_sparse_adjoint_wide_workspace_bytes(self.d, m, self.k)
+            f64 = b.dtype == torch.float64
+            ws_bytes = (lib.sk_sparse_adjoint_wide_workspace_bytes_f64 if f64 else
+                        lib.sk_sparse_adjoint_wide_workspace_bytes)(self.d, m, self.k)
             ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=b.device)
+            fn = lib.sk_sparse_adjoint_wide_f64 if f64 else lib.sk_sparse_adjoint_wide
             with torch.cuda.device(b.device):
-                st = lib.sk_sparse_adjoint_wide(b.data_ptr(), self.d, m, b.stride(0), enc.data_ptr(), seg_off.data_ptr(),
+                st = fn(b.data_ptr(), self.d, m, b.stride(0), enc.data_ptr(), seg_off.data_ptr(),
                                                 cap, self.k, mag, out.data_ptr(), out.stride(0), 0, ws.data_ptr(),
                                                 ws_bytes, torch.cuda.current_stream().cuda_stream)
             _lib.check(st, "sk_sparse_adjoint_wide")
