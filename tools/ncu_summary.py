@@ -1,43 +1,35 @@
-"""Summarise an .ncu-rep: key throughput metrics, DRAM traffic, top stall reasons."""
+"""One-page summary of an .ncu-rep (first kernel): key metrics, stall mix, hottest SASS."""
 import csv
 import io
 import subprocess
 import sys
 
-WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
-        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "launch__registers_per_thread", "launch__occupancy_limit_registers", "launch__grid_size", "launch__block_size",
-        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread", "launch__grid_size",
+        "launch__block_size", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
-        "smsp__inst_executed.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
-        "sm__cycles_elapsed.avg.per_second", "lts__t_bytes.sum", "smsp__thread_inst_executed_per_inst_executed.ratio"]
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "smsp__inst_executed.sum", "sm__cycles_elapsed.avg.per_second"]
 
 
-def raw(rep):
+def main(rep, top=12):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, units = rows[0], rows[1]
-    return [(hdr, units, r) for r in rows[2:]]
-
-
-def main(rep):
-    for hdr, units, r in raw(rep):
-        name = r[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
-        print("kernel:", name[:120])
-        d = dict(zip(hdr, r))
-        u = dict(zip(hdr, units))
-        for k in WANT:
-            if k in d:
-                print(f"  {k:75s} {d[k]:>16s} {u.get(k, '')}")
-        stalls = [(k, float(v)) for k, v in d.items()
-                  if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")
-                  and v not in ("", "n/a")]
-        stalls.sort(key=lambda kv: -kv[1])
-        print("  top stalls (warps per issue-active cycle):")
-        for k, v in stalls[:8]:
-            print(f"    {k[len('smsp__average_warps_issue_stalled_'):-len('_per_issue_active.ratio')]:30s} {v:.3f}")
+    h, units, v = rows[0], rows[1], rows[2]
+    print("kernel:", v[h.index("Kernel Name")][:110])
+    for k in KEYS:
+        if k in h:
+            print(f"  {k:80s} {v[h.index(k)]} {units[h.index(k)]}")
+    st = [(float(v[i] or 0), h[i][len("smsp__pcsamp_warps_issue_stalled_"):]) for i in range(len(h))
+          if h[i].startswith("smsp__pcsamp_warps_issue_stalled_") and not h[i].endswith("not_issued")]
+    tot = sum(x for x, _ in st) or 1.0
+    print("  stall mix (share of pc samples):")
+    for x, n in sorted(st, reverse=True)[:8]:
+        print(f"    {n:30s} {100 * x / tot:5.1f} %")
+    hot = subprocess.run([sys.executable, "tools/ncu_hot.py", rep, str(top)], capture_output=True, text=True).stdout
+    print("\ntop SASS by stall samples:\n" + hot)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 12)
