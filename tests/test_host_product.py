@@ -177,3 +177,18 @@ def test_bcsc_segments():
             e0, cnt = seg[h, g]
             lo, hi = ptr[h * k + g * 1024], ptr[h * k + min(k, (g + 1) * 1024)]
             assert e0 % 8 == 0 and cnt % 8 == 0 and e0 <= lo and e0 + cnt >= hi and cnt <= cap
+
+
+def test_redraw_determinism():
+    """redraw(seed) is the same operator as a fresh construction with that seed, every family
+    (reference pkg/tests/test_sketch.py:82-85 checks the same contract)."""
+    fams = [skb.SparseUniformTM(64, 12, 3, seed=1), skb.SparseStackTM(64, 3, 5, seed=1),
+            skb.SparseIIDTM(64, 12, 2.0, seed=1), skb.SparseColTM(64, 12, 2, seed=1),
+            skb.SparseRttTM(64, 12, 2, "wht", seed=1), skb.SparseRttTM(64, 12, 2, "dct", seed=1),
+            skb.KhatriRaoTM(4, 3, 12, "real_rademacher", seed=1), skb.GaussianTM(64, 12, seed=1)]
+    for tm in fams:
+        a, b = tm.redraw(7), tm.redraw(7)
+        assert type(a) is type(tm) and (a.d, a.k) == (tm.d, tm.k) and a.seed == 7
+        assert np.array_equal(a.materialize(), b.materialize())
+        assert not np.array_equal(a.materialize(), tm.materialize())
+        assert np.array_equal(tm.materialize(), tm.materialize())
