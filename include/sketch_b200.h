@@ -142,6 +142,19 @@ SK_API int sk_sparse_adjoint_wide_rows_f64(const double* A, int64_t d, int64_t r
                                            int64_t lda, const uint16_t* enc, const int64_t* seg_off, int32_t seg_cap,
                                            int64_t k, double scale, double* SA, int64_t ldsa, int accumulate, void* ws,
                                            size_t ws_bytes, void* stream);
+
+/*
+ * K2g — the same adjoint by row gathers (float32 / float64): S = Omega^T given in CSR by target row
+ * (ent: for output row q the A rows j it sums, ascending, as j | neg << 31; off[q][p]: start of
+ * row piece p in q's list, npieces + 1 per row, pieces of sk_sparse_adjoint_gather_pieces() rows).
+ * One warp per (piece, output row, 1 KB column block) sums its rows fetched with TMA row gathers;
+ * pieces are handed out in order so A streams from DRAM once. A 16-byte aligned with 16-byte rows.
+ */
+SK_API int64_t sk_sparse_adjoint_gather_pieces(int dtype, int64_t d, int64_t m, int64_t k, int64_t* piece_rows);
+SK_API size_t sk_sparse_adjoint_gather_workspace_bytes(int dtype, int64_t d, int64_t m, int64_t k);
+SK_API int sk_sparse_adjoint_gather(int dtype, const void* A, int64_t d, int64_t m, int64_t lda, const int32_t* ent,
+                                    const int64_t* off, int64_t k, double scale, void* SA, int64_t ldsa,
+                                    int accumulate, void* ws, size_t ws_bytes, void* stream);
 /* The same for the row block [r0, r1) of Omega (r0 % 128 == 0): A points at row r0 of the operand
  * and holds r1 - r0 rows; SA (+)= scale * Omega[r0:r1]^T * A. Lets a caller stream A through L2 in
  * row blocks and chain other kernels on each block (two-sided sketches). Workspace:

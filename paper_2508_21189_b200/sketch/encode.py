@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["bcsc_encode", "bcsc_decode", "bcsc_segments", "srtt_sampler_encode", "sign_bits", "wide_encode_device"]
+__all__ = ["bcsc_encode", "bcsc_decode", "bcsc_segments", "srtt_sampler_encode", "sign_bits", "wide_encode_device", "gather_encode"]
 
 ADJ_GROUP = 1024  # output rows per CTA group of the adjoint fast path (sparse_adjoint.cu V2_CG)
 PTR_PAD = 1028    # ints the fast path may read past the pointer array
@@ -145,3 +145,26 @@ def wide_encode_device(cols, neg, zeta: int, d: int, k: int):
     enc16 = torch.where(enc >= 32768, enc - 65536, enc).to(torch.int16)
     cap = int(seg_len.max()) if nseg else WIDE_HDR
     return enc16, seg_off, cap
+
+
+def gather_encode(rows, cols, neg, d: int, k: int, piece_rows: int, device):
+    """K2g encoding (adjoint_gather.cu): S = Omega^T in CSR by target row — for output row q the A
+    rows j it sums, ascending, as int32 words j | neg << 31 — and off[q][p], the start of row piece
+    p (rows [p * piece_rows, ...)) inside q's list. Built with torch ops on `device`.
+    Returns (ent int32 tensor, off int64 tensor [k, npieces + 1])."""
+    import torch
+
+    j = torch.as_tensor(rows, device=device).reshape(-1).to(torch.int64)
+    q = torch.as_tensor(cols, device=device).reshape(-1).to(torch.int64)
+    g = torch.as_tensor(neg, device=device).reshape(-1).to(torch.int64)
+    if d >= 2**31:
+        raise ValueError("K2g needs d < 2^31")
+    key = q * d + j
+    skey, order = torch.sort(key)
+    word = j[order] | (g[order] << 31)
+    ent = torch.where(word >= 2**31, word - 2**32, word).to(torch.int32)
+    npieces = -(-d // piece_rows)
+    bounds = (torch.arange(k, device=device, dtype=torch.int64)[:, None] * d
+              + torch.clamp(torch.arange(npieces + 1, device=device, dtype=torch.int64) * piece_rows, max=d)[None, :])
+    off = torch.searchsorted(skey, bounds.reshape(-1)).reshape(k, npieces + 1).to(torch.int64)
+    return ent.contiguous(), off.contiguous()

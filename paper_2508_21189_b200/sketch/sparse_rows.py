@@ -16,7 +16,7 @@ import numpy as np
 
 from .. import _lib
 from ..devrng import DevicePhilox, device_draws_enabled
-from .encode import ENT_PAD, PTR_PAD, bcsc_encode, bcsc_segments, wide_encode_device
+from .encode import ENT_PAD, PTR_PAD, bcsc_encode, bcsc_segments, gather_encode, wide_encode_device
 from .tensorcore import bt_from_triplets, dense_right_tc
 from .testmatrix import TestMatrix, entry_sample
 
@@ -216,6 +216,31 @@ class _SignSparseTM(TestMatrix):
                                        torch.from_numpy(seg_off).to(device), int(cap.value), mag)
         return self._device_cache[key]
 
+    def _adjoint_gather_on(self, device, dtype_code: int, m: int):
+        """K2g encoding (CSR of S by target row + piece offsets), built with torch ops on `device`."""
+        import ctypes as _ct
+
+        lib = _lib.load()
+        prows = _ct.c_int64(0)
+        npieces = int(lib.sk_sparse_adjoint_gather_pieces(dtype_code, self.d, m, self.k, _ct.byref(prows)))
+        _lib.check(min(npieces, 0), "sk_sparse_adjoint_gather_pieces")
+        key = ("adjg", device, int(prows.value))
+        if key not in self._device_cache:
+            import torch
+
+            dform = self._device_sign_form(device)
+            if dform is not None:
+                cols, neg, mag = dform
+                z = cols.shape[1]
+                rows = torch.arange(self.d, device=device).repeat_interleave(z)
+                ent, off = gather_encode(rows, cols.reshape(-1), neg.reshape(-1), self.d, self.k, int(prows.value),
+                                         device)
+            else:
+                rows, cols, neg, mag = self._sign_form()
+                ent, off = gather_encode(rows, cols, neg, self.d, self.k, int(prows.value), device)
+            self._device_cache[key] = (ent, off, mag)
+        return self._device_cache[key]
+
     def adjoint_path(self, b) -> str:
         """Kernel used by apply_adjoint: 'wide' (K2w, float32 / float64), 'gather' (K2) or 'dense'."""
         import os
@@ -227,6 +252,8 @@ class _SignSparseTM(TestMatrix):
         forced = os.environ.get("SKETCH_B200_SPARSE_ADJOINT", "auto")
         per16 = 16 // b.element_size()  # 16-byte rows for the TMA tiles
         wide_ok = (b.data_ptr() % 16 == 0 and b.stride(0) % per16 == 0 and b.stride(1) == 1 and b.shape[1] >= 1)
+        if forced == "rowgather" and wide_ok:
+            return "rowgather"
         return "wide" if (wide_ok and forced != "gather") else "gather"
 
     def _sparse_input_ok(self) -> bool:
@@ -304,6 +331,20 @@ class _SignSparseTM(TestMatrix):
         path = self.adjoint_path(b)
         if path == "dense":
             return super()._adjoint_device(b)
+        if path == "rowgather":
+            code = _lib.SK_F32 if b.dtype == torch.float32 else _lib.SK_F64
+            m = b.shape[1]
+            ent, off, mag = self._adjoint_gather_on(b.device, code, m)
+            out = torch.empty((self.k, m), dtype=b.dtype, device=b.device)
+            lib = _lib.load()
+            ws_bytes = lib.sk_sparse_adjoint_gather_workspace_bytes(code, self.d, m, self.k)
+            ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=b.device)
+            with torch.cuda.device(b.device):
+                st = lib.sk_sparse_adjoint_gather(code, b.data_ptr(), self.d, m, b.stride(0), ent.data_ptr(),
+                                                  off.data_ptr(), self.k, mag, out.data_ptr(), out.stride(0), 0,
+                                                  ws.data_ptr(), ws_bytes, torch.cuda.current_stream().cuda_stream)
+            _lib.check(st, "sk_sparse_adjoint_gather")
+            return out
         if path == "wide":
             enc, seg_off, cap, mag = self._adjoint_wide_on(b.device)
             m = b.shape[1]

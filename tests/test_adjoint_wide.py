@@ -146,3 +146,22 @@ def test_device_encoding_on_gpu(cuda):
     assert np.array_equal(enc_dev.cpu().numpy().view(np.uint16), enc)
     ref = orc.csr_adjoint(orc.sparse_uniform_csr(d, k, zeta, 12), b.cpu().double().numpy())
     assert rel_err(y.cpu().numpy(), ref) <= 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("d,k,zeta,m", [(70000, 2048, 8, 68), (1000, 300, 5, 512), (129, 513, 3, 260),
+                                        (40000, 64, 2, 1000)])
+def test_rowgather_vs_oracle(d, k, zeta, m, dt, cuda, monkeypatch):
+    """K2g (TMA row gathers, one warp per target row / column block / row piece) against the oracle."""
+    import torch
+
+    monkeypatch.setenv("SKETCH_B200_SPARSE_ADJOINT", "rowgather")
+    tm = skb.SparseUniformTM(d, k, zeta, seed=7)
+    rng = np.random.default_rng(d + m)
+    b = rng.standard_normal((d, m)).astype(dt)
+    bt = torch.as_tensor(b).to(cuda)
+    assert tm.adjoint_path(bt) == "rowgather"
+    y = tm.apply_adjoint(bt).cpu().numpy()
+    ref = orc.csr_adjoint(orc.sparse_uniform_csr(d, k, zeta, 7), b)
+    assert rel_err(y, ref) <= (1e-5 if dt == np.float32 else 1e-12)
