@@ -82,7 +82,7 @@ def _cfg4(torch, dev, rank):
     tm = make()
     g = torch.Generator(device=dev).manual_seed(4000 + rank)
     a = torch.randn(n, d, dtype=torch.float32, device=dev, generator=g)
-    return dict(name="cfg4", tm=tm, make=make, a=a, n=n, d=d, k=k, launches=2, kernel="sparse_adjoint_wide",
+    return dict(name="cfg4", tm=tm, make=make, a=a, n=n, d=d, k=k, launches=2, kernel="sparse_adjoint_gather",
                 workload="cfg4 SA sketch: S (2048 x 4194304, zeta=8) applied to A 4194304x512 f32", op="adjoint")
 
 

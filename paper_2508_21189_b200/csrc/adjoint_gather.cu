@@ -80,17 +80,17 @@ __device__ __forceinline__ void lds128(uint32_t addr, u64& x, u64& y) {
   asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(addr));
 }
 
-// acc (+)= sgn * v on packed pairs: float32 pairs (f32x2) or one float64 per register
+// acc += v * s on packed pairs: float32 pairs times {s, s} (fma.rn.f32x2) or one float64 times s
 template <typename T>
-__device__ __forceinline__ void add_signed(u64& acc, u64 v, uint32_t neg) {
+__device__ __forceinline__ void fma_signed(u64& acc, u64 v, uint32_t s32, u64 s64) {
   if constexpr (sizeof(T) == 4) {
-    const u64 m = neg ? 0x8000000080000000ull : 0ull;
-    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(v ^ m));
+    asm("{\n\t.reg .b64 ss;\n\tmov.b64 ss, {%2, %2};\n\tfma.rn.f32x2 %0, %1, ss, %0;\n\t}" : "+l"(acc) : "l"(v), "r"(s32));
   } else {
-    const u64 m = neg ? 0x8000000000000000ull : 0ull;
-    asm("add.rn.f64 %0, %0, %1;" : "+l"(acc) : "l"(v ^ m));
+    asm("fma.rn.f64 %0, %1, %2, %0;" : "+l"(acc) : "l"(v), "l"(s64));
   }
 }
+
+constexpr int G_ENT = 512;  // entries of a unit staged in the warp's shared buffer at a time
 
 template <typename T>
 __global__ void __launch_bounds__(G_WARPS * 32, 1)
@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(G_WARPS * 32, 1)
   constexpr int W = g_cols<T>();
   extern __shared__ __align__(1024) uint8_t smem_dyn[];
   uint8_t* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)G_WARPS * G_STAGES * G_STAGE_BYTES);
+  uint32_t* ebuf_all = reinterpret_cast<uint32_t*>(smem + (size_t)G_WARPS * G_STAGES * G_STAGE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ebuf_all + G_WARPS * G_ENT);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0)
@@ -109,7 +110,10 @@ __global__ void __launch_bounds__(G_WARPS * 32, 1)
 
   const uint32_t ring = smem_u32(smem + (size_t)warp * G_STAGES * G_STAGE_BYTES);
   const uint32_t bar0 = smem_u32(&bars[warp * G_STAGES]);
-  uint32_t gc = 0;  // gathers issued by this warp so far (stage = gc % S, phase = (gc / S) & 1)
+  uint32_t* ebuf = ebuf_all + warp * G_ENT;
+  const uint32_t ebuf_s = smem_u32(ebuf);
+  // ring position of the next gather to issue / to consume (stage, phase) — no divisions
+  uint32_t is = 0, ip = 0, cs = 0, cp = 0;
   const int64_t kh = p.k * p.nhalves;
 
   for (;;) {
@@ -118,51 +122,58 @@ __global__ void __launch_bounds__(G_WARPS * 32, 1)
     u = __shfl_sync(0xffffffffu, u, 0);
     if (u >= p.nunits) break;
     const int piece = (int)(u / kh);
-    const int64_t rest = u % kh;
+    const int64_t rest = u - (int64_t)piece * kh;
     const int64_t q = rest / p.nhalves;
-    const int h = (int)(rest % p.nhalves);
-    const int64_t e0 = p.off[q * (p.npieces + 1) + piece], e1 = p.off[q * (p.npieces + 1) + piece + 1];
-    const int L = (int)(e1 - e0);
-    const int G = (L + 3) >> 2;
+    const int h = (int)(rest - q * p.nhalves);
+    const int64_t eb = p.off[q * (p.npieces + 1) + piece], ee = p.off[q * (p.npieces + 1) + piece + 1];
     const int col = h * W;
-    const int32_t* ent = p.ent + e0;
 
-    // issue gather g of this unit (rows e0 + 4g .. +3; a short last group repeats its last row)
-    auto issue = [&](int g, uint32_t slot) {
-      const int b = 4 * g;
-      const int last = L - 1;
-      const int r0 = ent[min(b, last)] & 0x7fffffff, r1 = ent[min(b + 1, last)] & 0x7fffffff;
-      const int r2 = ent[min(b + 2, last)] & 0x7fffffff, r3 = ent[min(b + 3, last)] & 0x7fffffff;
-      const uint32_t s = slot % G_STAGES;
-      arrive_tx(bar0 + 8u * s, G_STAGE_BYTES);
-      gather4(ring + s * G_STAGE_BYTES, &tm, bar0 + 8u * s, col, r0, r1, r2, r3);
-    };
-    if (lane == 0)
-      for (int g = 0; g < G && g < G_STAGES; ++g) issue(g, gc + g);
-
-    u64 a0 = 0ull, a1 = 0ull, b0 = 0ull, b1 = 0ull;  // lane's columns: [4 lane, +4) and [W/2 + 4 lane, +4) (f32)
-    for (int g = 0; g < G; ++g) {
-      const uint32_t slot = gc + g, s = slot % G_STAGES;
-      wait_parity(bar0 + 8u * s, (slot / G_STAGES) & 1u);
-      const uint32_t base = ring + s * G_STAGE_BYTES + 16u * lane;
-      const int nrow = min(4, L - 4 * g);
+    u64 a0 = 0ull, a1 = 0ull, b0 = 0ull, b1 = 0ull;
+    for (int64_t e0 = eb; e0 < ee; e0 += G_ENT) {
+      const int L = (int)min((int64_t)G_ENT, ee - e0);
+      // stage the block's entries (coalesced), padded to a multiple of 4 with the last row
+      const int Lp = (L + 3) & ~3;
+      for (int i = lane; i < Lp; i += 32) ebuf[i] = (uint32_t)p.ent[e0 + min(i, L - 1)];
+      __syncwarp();
+      const int G = Lp >> 2;
+      auto issue = [&](int g) {
+        uint32_t w0, w1, w2, w3;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                     : "r"(ebuf_s + 16u * (uint32_t)g));
+        arrive_tx(bar0 + 8u * is, G_STAGE_BYTES);
+        gather4(ring + is * G_STAGE_BYTES, &tm, bar0 + 8u * is, col, (int)(w0 & 0x7fffffffu), (int)(w1 & 0x7fffffffu),
+                (int)(w2 & 0x7fffffffu), (int)(w3 & 0x7fffffffu));
+        if (++is == G_STAGES) { is = 0; ip ^= 1u; }
+      };
+      if (lane == 0)
+        for (int g = 0; g < G && g < G_STAGES; ++g) issue(g);
+      for (int g = 0; g < G; ++g) {
+        wait_parity(bar0 + 8u * cs, cp);
+        uint32_t w[4];
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                     : "r"(ebuf_s + 16u * (uint32_t)g));
+        const uint32_t base = ring + cs * G_STAGE_BYTES + 16u * lane;
+        const int nrow = L - 4 * g;  // >= 4 except in the last group
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        if (t < nrow) {
-          const uint32_t neg = (uint32_t)ent[4 * g + t] >> 31;
-          u64 x0, x1, y0, y1;
-          lds128(base + t * G_ROW_BYTES, x0, x1);
-          lds128(base + t * G_ROW_BYTES + G_ROW_BYTES / 2, y0, y1);
-          add_signed<T>(a0, x0, neg);
-          add_signed<T>(a1, x1, neg);
-          add_signed<T>(b0, y0, neg);
-          add_signed<T>(b1, y1, neg);
+        for (int t = 0; t < 4; ++t) {
+          if (t < nrow) {
+            const uint32_t s32 = 0x3F800000u | (w[t] & 0x80000000u);                          // +-1.0f
+            const u64 s64 = (u64)(0x3FF00000u | (w[t] & 0x80000000u)) << 32;                   // +-1.0
+            u64 x0, x1, y0, y1;
+            lds128(base + t * G_ROW_BYTES, x0, x1);
+            lds128(base + t * G_ROW_BYTES + G_ROW_BYTES / 2, y0, y1);
+            fma_signed<T>(a0, x0, s32, s64);
+            fma_signed<T>(a1, x1, s32, s64);
+            fma_signed<T>(b0, y0, s32, s64);
+            fma_signed<T>(b1, y1, s32, s64);
+          }
         }
+        __syncwarp();  // every lane has read the stage before it is refilled
+        if (++cs == G_STAGES) { cs = 0; cp ^= 1u; }
+        if (lane == 0 && g + G_STAGES < G) issue(g + G_STAGES);
       }
-      __syncwarp();  // every lane has read stage s before it is refilled
-      if (lane == 0 && g + G_STAGES < G) issue(g + G_STAGES, slot + G_STAGES);
+      __syncwarp();  // the entry buffer is reused by the next block
     }
-    gc += (uint32_t)G;
 
     // unit partial: part[piece][q][col ...]
     T* out = static_cast<T*>(p.part) + ((int64_t)piece * p.k + q) * p.m;
@@ -202,14 +213,14 @@ template <typename T>
 GPlan gather_plan(int64_t d, int64_t m, int64_t k) {
   GPlan pl{};
   pl.nhalves = (int)((m + g_cols<T>() - 1) / g_cols<T>());
-  // pieces of ~32 MB of A: resident warps (148 x 16) cover about one piece of units at a time
+  // pieces of ~64 MB of A: resident warps (148 x 16) work inside one or two pieces at a time
   const int64_t row_bytes = m * (int64_t)sizeof(T);
-  int64_t prows = std::max<int64_t>(1024, ((int64_t)32 << 20) / std::max<int64_t>(1, row_bytes));
+  int64_t prows = std::max<int64_t>(1024, ((int64_t)64 << 20) / std::max<int64_t>(1, row_bytes));
   if (prows > d) prows = d;
   pl.prows = prows;
   pl.npieces = (int)((d + prows - 1) / prows);
   pl.nunits = (int64_t)pl.npieces * k * pl.nhalves;
-  pl.smem = 1024 + (size_t)G_WARPS * G_STAGES * G_STAGE_BYTES + (size_t)G_WARPS * G_STAGES * 8;
+  pl.smem = 1024 + (size_t)G_WARPS * G_STAGES * G_STAGE_BYTES + (size_t)G_WARPS * G_ENT * 4 + (size_t)G_WARPS * G_STAGES * 8;
   pl.part_bytes = (size_t)pl.npieces * k * m * sizeof(T);
   return pl;
 }

@@ -331,7 +331,7 @@ def two_sided_sketch(a, tm_omega, tm_psi, *, one_pass: bool = False, block_bytes
     A, _ = _as_device_2d(a)
     n, d = A.shape
     fused = (one_pass and A.is_cuda and A.dtype == torch.float32 and hasattr(tm_psi, "adjoint_rows")
-             and tm_psi.adjoint_path(A) == "wide")
+             and tm_psi.adjoint_path(A) in ("wide", "rowgather"))
     if not fused:
         return tm_omega.apply_right(A), tm_psi.apply_adjoint(A).conj().T
     rows = max(128, (block_bytes // (d * 4)) // 128 * 128)

@@ -241,8 +241,14 @@ class _SignSparseTM(TestMatrix):
             self._device_cache[key] = (ent, off, mag)
         return self._device_cache[key]
 
+    def _tma_rows_ok(self, b) -> bool:
+        """16-byte aligned rows with unit column stride: the TMA-fed adjoints (K2g, K2w) apply."""
+        per16 = 16 // b.element_size()
+        return b.data_ptr() % 16 == 0 and b.stride(0) % per16 == 0 and b.stride(1) == 1 and b.shape[1] >= 1
+
     def adjoint_path(self, b) -> str:
-        """Kernel used by apply_adjoint: 'wide' (K2w, float32 / float64), 'gather' (K2) or 'dense'."""
+        """Kernel used by apply_adjoint: 'rowgather' (K2g, default for aligned float32 / float64),
+        'wide' (K2w), 'gather' (K2, any layout) or 'dense'. SKETCH_B200_SPARSE_ADJOINT picks one."""
         import os
 
         import torch
@@ -250,11 +256,9 @@ class _SignSparseTM(TestMatrix):
         if not self._signed_real() or b.dtype not in (torch.float32, torch.float64):
             return "dense"
         forced = os.environ.get("SKETCH_B200_SPARSE_ADJOINT", "auto")
-        per16 = 16 // b.element_size()  # 16-byte rows for the TMA tiles
-        wide_ok = (b.data_ptr() % 16 == 0 and b.stride(0) % per16 == 0 and b.stride(1) == 1 and b.shape[1] >= 1)
-        if forced == "rowgather" and wide_ok:
-            return "rowgather"
-        return "wide" if (wide_ok and forced != "gather") else "gather"
+        if forced == "gather" or not self._tma_rows_ok(b):
+            return "gather"
+        return "wide" if forced == "wide" else "rowgather"
 
     def _sparse_input_ok(self) -> bool:
         return self._sign_form() is not None
@@ -308,7 +312,7 @@ class _SignSparseTM(TestMatrix):
         """
         import torch
 
-        if self.adjoint_path(b_rows) != "wide":
+        if self.adjoint_path(b_rows) == "gather" or not self._tma_rows_ok(b_rows):
             raise NotImplementedError("adjoint_rows needs an aligned float32 or float64 device block (wide path)")
         enc, seg_off, cap, mag = self._adjoint_wide_on(b_rows.device)
         m = b_rows.shape[1]

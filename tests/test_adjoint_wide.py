@@ -69,9 +69,10 @@ def test_encoder_rejects_bad_indices():
 @pytest.mark.parametrize("d,k,zeta,m", [(4096, 2048, 8, 512), (20000, 1300, 8, 100), (1000, 300, 5, 4),
                                         (129, 513, 3, 64), (70000, 2048, 8, 68)])
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
-def test_wide_vs_oracle(d, k, zeta, m, dt, cuda):
+def test_wide_vs_oracle(d, k, zeta, m, dt, cuda, monkeypatch):
     import torch
 
+    monkeypatch.setenv("SKETCH_B200_SPARSE_ADJOINT", "wide")
     tm = skb.SparseUniformTM(d, k, zeta, seed=7)
     rng = np.random.default_rng(d + m)
     b = rng.standard_normal((d, m)).astype(dt)
@@ -84,13 +85,16 @@ def test_wide_vs_oracle(d, k, zeta, m, dt, cuda):
 
 
 @pytest.mark.gpu
-def test_wide_variable_row_counts(cuda):
-    """SparseIID: rows carry 0..many nonzeros; the encoder pads each warp list independently."""
+@pytest.mark.parametrize("path", ["wide", "rowgather"])
+def test_wide_variable_row_counts(path, cuda, monkeypatch):
+    """SparseIID: rows carry 0..many nonzeros (K2w pads each warp list independently; K2g lists
+    have any length per target row)."""
     import torch
 
+    monkeypatch.setenv("SKETCH_B200_SPARSE_ADJOINT", path)
     tm = skb.SparseIIDTM(3000, 700, 6.0, seed=3)
     b = torch.randn(3000, 96, device=cuda)
-    assert tm.adjoint_path(b) == "wide"
+    assert tm.adjoint_path(b) == path
     ref = tm.materialize().T @ b.cpu().double().numpy()
     assert rel_err(tm.apply_adjoint(b).cpu().numpy(), ref) <= 1e-5
 
@@ -102,8 +106,12 @@ def test_wide_matches_gather_path(dtype, cuda, monkeypatch):
 
     tm = skb.SparseStackTM(8192, 8, 64, seed=1)
     b = torch.randn(8192, 256, device=cuda, dtype=getattr(torch, dtype))
+    assert tm.adjoint_path(b) == "rowgather"
+    rowg = tm.apply_adjoint(b).double()
+    monkeypatch.setenv("SKETCH_B200_SPARSE_ADJOINT", "wide")
     assert tm.adjoint_path(b) == "wide"
     wide = tm.apply_adjoint(b).double()
+    assert float((wide - rowg).norm() / rowg.norm()) <= (1e-6 if dtype == "float32" else 1e-14)
     monkeypatch.setenv("SKETCH_B200_SPARSE_ADJOINT", "gather")
     assert tm.adjoint_path(b) == "gather"
     gather = tm.apply_adjoint(b).double()
@@ -129,11 +137,12 @@ def test_device_encoder_matches_host(d, k, zeta):
 
 
 @pytest.mark.gpu
-def test_device_encoding_on_gpu(cuda):
+def test_device_encoding_on_gpu(cuda, monkeypatch):
     """Device-drawn operator: the adjoint builds its K2w encoding on the GPU without a host copy
     of the draws, byte-identical to the host encoder, and matches the oracle."""
     import torch
 
+    monkeypatch.setenv("SKETCH_B200_SPARSE_ADJOINT", "wide")
     d, k, zeta, m = 200003, 2048, 8, 40
     tm = skb.SparseUniformTM(d, k, zeta, seed=12)
     b = torch.randn(d, m, device=cuda)
