@@ -20,6 +20,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -215,7 +216,9 @@ GPlan gather_plan(int64_t d, int64_t m, int64_t k) {
   pl.nhalves = (int)((m + g_cols<T>() - 1) / g_cols<T>());
   // pieces of ~64 MB of A: resident warps (148 x 16) work inside one or two pieces at a time
   const int64_t row_bytes = m * (int64_t)sizeof(T);
-  int64_t prows = std::max<int64_t>(1024, ((int64_t)64 << 20) / std::max<int64_t>(1, row_bytes));
+  int64_t piece_mb = 64;
+  if (const char* e = getenv("SKETCH_B200_K2G_PIECE_MB")) piece_mb = std::max(1, atoi(e));
+  int64_t prows = std::max<int64_t>(1024, (piece_mb << 20) / std::max<int64_t>(1, row_bytes));
   if (prows > d) prows = d;
   pl.prows = prows;
   pl.npieces = (int)((d + prows - 1) / prows);
