@@ -196,10 +196,11 @@ __global__ void __launch_bounds__(G_WARPS * 32, 1)
       vb[1] = __longlong_as_double((long long)b1);
     }
     const int64_t ca = col + CPL * lane, cb = col + W / 2 + CPL * lane;
+    // streaming stores: the partials are read once by the reduction, keep L2 for the A pieces
 #pragma unroll
     for (int i = 0; i < CPL; ++i) {
-      if (ca + i < p.m) out[ca + i] = va[i];
-      if (cb + i < p.m) out[cb + i] = vb[i];
+      if (ca + i < p.m) __stcs(out + ca + i, va[i]);
+      if (cb + i < p.m) __stcs(out + cb + i, vb[i]);
     }
   }
 }
