@@ -174,3 +174,33 @@ def test_rowgather_vs_oracle(d, k, zeta, m, dt, cuda, monkeypatch):
     y = tm.apply_adjoint(bt).cpu().numpy()
     ref = orc.csr_adjoint(orc.sparse_uniform_csr(d, k, zeta, 7), b)
     assert rel_err(y, ref) <= (1e-5 if dt == np.float32 else 1e-12)
+
+
+@pytest.mark.gpu
+def test_adjoint_paths_randomized(cuda):
+    """Random shapes, families and dtypes through the default adjoint path (K2g when aligned,
+    K2 otherwise) against the materialized Omega."""
+    import torch
+
+    rng = np.random.default_rng(2024)
+    for trial in range(24):
+        d = int(rng.integers(1, 60000))
+        k = int(rng.integers(1, 2600))
+        m = int(rng.integers(1, 700))
+        dt = torch.float32 if trial % 2 else torch.float64
+        fam = trial % 4
+        if fam == 0:
+            tm = skb.SparseUniformTM(d, k, int(rng.integers(1, min(k, 8) + 1)), seed=trial)
+        elif fam == 1:
+            z = int(rng.integers(1, 5))
+            tm = skb.SparseStackTM(d, z, max(1, k // z), seed=trial)
+        elif fam == 2:
+            tm = skb.SparseIIDTM(d, k, float(rng.uniform(0.5, min(k, 6))), seed=trial)
+        else:
+            tm = skb.SparseColTM(d, k, int(rng.integers(1, min(d, 4) + 1)), seed=trial)
+        b = torch.randn(d, m, device=cuda, dtype=dt)
+        y = tm.apply_adjoint(b).double().cpu().numpy()
+        om = tm.materialize()
+        ref = om.T @ b.double().cpu().numpy()
+        tol = 1e-5 if dt == torch.float32 else 1e-12
+        assert rel_err(y, ref) <= tol, (trial, type(tm).__name__, d, tm.k, m, tm.adjoint_path(b))

@@ -258,3 +258,35 @@ def test_edge_shapes_every_family(dt, cuda):
         assert rel_err(tm.apply_right(sl).cpu().numpy(), sl.cpu().double().numpy() @ om) <= tol
         bt = torch.as_tensor(rng.standard_normal((7, tm.d)).astype(dt)).to(cuda).T
         assert rel_err(tm.apply_adjoint(bt).cpu().numpy(), om.T @ bt.cpu().double().numpy()) <= tol
+
+
+def test_right_paths_randomized(cuda):
+    """Random shapes, families and dtypes through the default right-apply paths (K1 persistent /
+    classic, tensor-core dense form, SRTT, Khatri-Rao) against the materialized Omega."""
+    import torch
+
+    rng = np.random.default_rng(7)
+    for trial in range(20):
+        n = int(rng.integers(1, 3000))
+        dt = torch.float32 if trial % 2 else torch.float64
+        fam = trial % 5
+        if fam == 0:
+            d, k = int(rng.integers(1, 9000)), int(rng.integers(1, 700))
+            tm = skb.SparseUniformTM(d, k, int(rng.integers(1, min(k, 8) + 1)), seed=trial)
+        elif fam == 1:
+            d = int(rng.integers(1, 9000))
+            z = int(rng.integers(1, 5))
+            tm = skb.SparseStackTM(d, z, int(rng.integers(1, 150)), seed=trial)
+        elif fam == 2:
+            d = 2 ** int(rng.integers(3, 14))
+            tm = skb.SparseRttTM(d, int(rng.integers(1, min(d, 600) + 1)), int(rng.integers(1, 3)), "wht", seed=trial)
+        elif fam == 3:
+            d0 = int(rng.integers(2, 40))
+            tm = skb.KhatriRaoTM(d0, 2, int(rng.integers(1, 300)), "real_rademacher", seed=trial)
+        else:
+            tm = skb.SparseColTM(int(rng.integers(2, 5000)), int(rng.integers(1, 400)), 2, seed=trial)
+        a = torch.randn(n, tm.d, device=cuda, dtype=dt)
+        y = tm.apply_right(a).double().cpu().numpy()
+        ref = a.double().cpu().numpy() @ tm.materialize()
+        tol = 1e-5 if dt == torch.float32 else 1e-12
+        assert rel_err(y, ref) <= tol, (trial, type(tm).__name__, n, tm.d, tm.k)
