@@ -82,6 +82,8 @@ def _cfg4(torch, dev, rank):
     tm = make()
     g = torch.Generator(device=dev).manual_seed(4000 + rank)
     a = torch.randn(n, d, dtype=torch.float32, device=dev, generator=g)
+    # rows scaled by 1 + Pareto(1.5) weights (coherent rows, as the config states; inverse CDF)
+    a *= (torch.rand(n, 1, device=dev, generator=g).clamp_min(1e-12) ** (-1.0 / 1.5))
     return dict(name="cfg4", tm=tm, make=make, a=a, n=n, d=d, k=k, launches=2, kernel="sparse_adjoint_gather",
                 workload="cfg4 SA sketch: S (2048 x 4194304, zeta=8) applied to A 4194304x512 f32", op="adjoint")
 
@@ -252,6 +254,34 @@ def time_device(torch, w, steps, warmup, world, dev):
     return total, per
 
 
+def _downstream(torch, w, dev):
+    """The config's downstream pipeline on the same input (warm, wall clock around a synchronized
+    call): config 3 rsvd (sketch, orth, Q^T A, SVD), config 4 sketch-and-precondition LSQR."""
+    from paper_2508_21189_b200 import rand_nla
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = fn()
+        torch.cuda.synchronize()
+        return out, (time.perf_counter() - t0) * 1e3
+
+    if w["name"] == "cfg3":
+        _, ms = timed(lambda: rand_nla.rsvd(w["a"], w["k"], w["tm"]))
+        return {"rsvd_ms": ms, "what": "rank-200 rsvd of A (sketch, CholeskyQR2, Q^T A on the tensor cores, SVD)"}
+    if w["name"] == "cfg4":
+        a = w["a"]
+        g = torch.Generator(device=dev).manual_seed(4444)
+        x0 = torch.randn(a.shape[1], device=dev, dtype=torch.float64, generator=g)
+        b = (rand_nla._matvec_blocks(a, x0, 0) + 1e-3 * torch.randn(a.shape[0], device=dev, dtype=torch.float64,
+                                                                      generator=g)).float()
+        res, ms = timed(lambda: rand_nla.sketch_precondition_lsqr(a, b, w["tm"], atol=1e-6, btol=0.0))
+        return {"lsqr_ms": ms, "iterations": res.itn, "istop": res.istop,
+                "what": "sketch-and-precondition LSQR to the 1e-6 normal-equation test (SA, QR(SA), LSQR on A R^-1)"}
+    return None
+
+
 def time_setup(torch, w, steady_s):
     """Operator construction + device encoding/upload, reported apart from the apply:
     a fresh operator's first apply on the step's input minus one steady apply."""
@@ -419,11 +449,14 @@ def main(argv=None):
                 ow = WORKLOADS[name](torch, dev, rank)
                 om = measure(torch, ow, 3, 3, 1, 0, dev, False, 0)
                 oes = ow["a"].element_size()
+                downstream = _downstream(torch, ow, dev)
                 others[name] = {"workload": ow["workload"], "value_gbs": om["value"], "ms_per_step": om["ms_per_step"],
                                 "dtype": "f32" if oes == 4 else "f64", "kernel": ow["kernel"],
                                 "pct_hbm_peak": 100.0 * om["achieved_gbs"] / peak,
                                 "roofline_achieved_gbs": om["achieved_gbs"], "alg_bytes": om["alg_bytes"],
                                 "omega_setup_ms": om["omega_setup"]["ms"]}
+                if downstream:
+                    others[name]["downstream"] = downstream
                 del ow
                 torch.cuda.empty_cache()
             except Exception as exc:  # report, never hide
