@@ -54,6 +54,53 @@ __global__ void __launch_bounds__(GV_THREADS)
   }
 }
 
+// d = 128 * NQ (NQ <= 4): each lane keeps its 4 * NQ entries of v in registers (no shared-memory
+// traffic per row) and loads its NQ 16-byte pieces of two rows at once (2 * NQ loads in flight)
+template <int NQ>
+__global__ void __launch_bounds__(GV_THREADS)
+    gemv_rows_reg(const float* __restrict__ A, int64_t n, int64_t lda, const double* __restrict__ v,
+                  double* __restrict__ y) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double vr[NQ][4];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) vr[q][c] = v[128 * q + 4 * lane + c];
+  const int64_t wstride = (int64_t)gridDim.x * (GV_THREADS / 32);
+  for (int64_t r = (int64_t)blockIdx.x * (GV_THREADS / 32) + warp; r < n; r += 2 * wstride) {
+    const int64_t r2 = r + wstride;
+    const bool two = r2 < n;
+    float4 x[NQ], x2[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      x[q] = __ldg(reinterpret_cast<const float4*>(A + r * lda + 128 * q + 4 * lane));
+      x2[q] = two ? __ldg(reinterpret_cast<const float4*>(A + r2 * lda + 128 * q + 4 * lane)) : make_float4(0, 0, 0, 0);
+    }
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      a0 = fma((double)x[q].x, vr[q][0], a0);
+      a1 = fma((double)x[q].y, vr[q][1], a1);
+      a0 = fma((double)x[q].z, vr[q][2], a0);
+      a1 = fma((double)x[q].w, vr[q][3], a1);
+      b0 = fma((double)x2[q].x, vr[q][0], b0);
+      b1 = fma((double)x2[q].y, vr[q][1], b1);
+      b0 = fma((double)x2[q].z, vr[q][2], b0);
+      b1 = fma((double)x2[q].w, vr[q][3], b1);
+    }
+    double sa = a0 + a1, sb = b0 + b1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      sa += __shfl_xor_sync(0xffffffffu, sa, o);
+      sb += __shfl_xor_sync(0xffffffffu, sb, o);
+    }
+    if (lane == 0) {
+      y[r] = sa;
+      if (two) y[r2] = sb;
+    }
+  }
+}
+
 // thread = 4 consecutive columns (one 16-byte load per row) over a range of rows, 4 rows in flight
 __global__ void __launch_bounds__(GV_THREADS)
     gemv_cols_partial(const float* __restrict__ A, int64_t n, int64_t d, int64_t lda, const double* __restrict__ u,
@@ -158,6 +205,19 @@ extern "C" int sk_gemv_f32_f64(const float* A, int64_t n, int64_t d, int64_t lda
   const size_t smem = (size_t)d * sizeof(double);
   if (smem > 200 * 1024) return fail(SK_EUNSUPPORTED, "sk_gemv_f32_f64: d too large for the shared vector");
   const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 4 == 0) && (d % 4 == 0);
+  if (vec && d % 128 == 0 && d <= 512) {
+    // one resident wave (64-register kernel: 4 CTAs of 256 threads per SM)
+    int64_t g = (n + 15) / 16;
+    if (g > 4 * (int64_t)sm_count()) g = 4 * (int64_t)sm_count();
+    cudaStream_t st = as_stream(stream);
+    switch (d / 128) {
+      case 1: gemv_rows_reg<1><<<(unsigned)g, GV_THREADS, 0, st>>>(A, n, lda, v, y); break;
+      case 2: gemv_rows_reg<2><<<(unsigned)g, GV_THREADS, 0, st>>>(A, n, lda, v, y); break;
+      case 3: gemv_rows_reg<3><<<(unsigned)g, GV_THREADS, 0, st>>>(A, n, lda, v, y); break;
+      default: gemv_rows_reg<4><<<(unsigned)g, GV_THREADS, 0, st>>>(A, n, lda, v, y); break;
+    }
+    return check_launch("sk_gemv_f32_f64");
+  }
   cudaFuncSetAttribute(gemv_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int64_t grid = (n + 7) / 8;
   if (grid > 16 * (int64_t)sm_count()) grid = 16 * (int64_t)sm_count();
