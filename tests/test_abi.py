@@ -42,3 +42,25 @@ def test_error_path_without_device():
     assert b"sk_sparse_right" in lib.sk_last_error()
     assert lib.sk_sparse_right_chunk_rows(0, 100, 10) == 512
     assert lib.sk_sparse_right_chunk_rows(7, 100, 10) == _lib.SK_EINVAL
+
+
+def test_argument_checks_without_device():
+    """Every new entry point rejects bad shapes / dtypes / pointers before touching the device."""
+    from paper_2508_21189_b200 import _lib
+
+    lib = _lib.load()
+    E = _lib.SK_EINVAL
+    # K2g: bad dtype, bad leading dimension, null pointers
+    assert lib.sk_sparse_adjoint_gather(7, None, 10, 4, 4, None, None, 3, 1.0, None, 4, 0, None, 0, None) == E
+    assert lib.sk_sparse_adjoint_gather(0, None, 10, 4, 2, None, None, 3, 1.0, None, 4, 0, None, 0, None) == E
+    assert lib.sk_sparse_adjoint_gather(0, None, 10, 4, 4, None, None, 3, 1.0, None, 4, 0, None, 0, None) == E
+    assert b"sk_sparse_adjoint_gather" in lib.sk_last_error()
+    assert lib.sk_sparse_adjoint_gather_pieces(0, 0, 4, 3, None) == E
+    assert lib.sk_sparse_adjoint_gather_workspace_bytes(0, 0, 4, 3) == 0
+    # K2w float64, TN product, mixed-precision GEMV
+    assert lib.sk_sparse_adjoint_wide_f64(None, 0, 4, 4, None, None, 24, 3, 1.0, None, 4, 0, None, 0, None) == E
+    assert lib.sk_dense_tn_tc(None, 0, 4, 4, None, None, 8, 3, 1.0, None, 3, None, 0, None) == E
+    assert lib.sk_dense_tn_tc(None, 8, 4, 4, None, None, 8, 3, 1.0, None, 3, None, 0, None) == E
+    assert lib.sk_gemv_f32_f64(None, 4, 0, 0, None, None, None) == E
+    assert lib.sk_gemv_t_f32_f64(None, 4, 4, 2, None, None, None, 0, None) == E
+    assert lib.sk_philox_u32(None, None, 0, 8, None, None) == E
