@@ -155,6 +155,11 @@ SK_API size_t sk_sparse_adjoint_gather_workspace_bytes(int dtype, int64_t d, int
 SK_API int sk_sparse_adjoint_gather(int dtype, const void* A, int64_t d, int64_t m, int64_t lda, const int32_t* ent,
                                     const int64_t* off, int64_t k, double scale, void* SA, int64_t ldsa,
                                     int accumulate, void* ws, size_t ws_bytes, void* stream);
+/* Narrow operands of the same adjoint (m <= 8 columns, any row stride ldb, e.g. a right-hand side
+ * vector): one warp per target row over the K2g encoding, float64 sums in a fixed order. */
+SK_API int sk_sparse_adjoint_narrow(int dtype, const void* B, int64_t d, int64_t m, int64_t ldb, const int32_t* ent,
+                                    const int64_t* off, int npieces, int64_t k, double scale, void* SA, int64_t ldsa,
+                                    void* stream);
 /* The same for the row block [r0, r1) of Omega (r0 % 128 == 0): A points at row r0 of the operand
  * and holds r1 - r0 rows; SA (+)= scale * Omega[r0:r1]^T * A. Lets a caller stream A through L2 in
  * row blocks and chain other kernels on each block (two-sided sketches). Workspace:

@@ -50,6 +50,8 @@ SIGNATURES = {
                                         _c_i64, _c_int, _c_p, _c_size, _c_p]),
     "sk_sparse_adjoint_wide_rows": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_p, ctypes.c_int32,
                                              _c_i64, _c_dbl, _c_p, _c_i64, _c_int, _c_p, _c_size, _c_p]),
+    "sk_sparse_adjoint_narrow": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_int, _c_i64, _c_dbl,
+                                          _c_p, _c_i64, _c_p]),
     "sk_sparse_adjoint_gather_pieces": (_c_i64, [_c_int, _c_i64, _c_i64, _c_i64, _c_p]),
     "sk_sparse_adjoint_gather_workspace_bytes": (_c_size, [_c_int, _c_i64, _c_i64, _c_i64]),
     "sk_sparse_adjoint_gather": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_dbl, _c_p,

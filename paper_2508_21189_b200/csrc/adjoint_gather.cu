@@ -205,6 +205,38 @@ __global__ void __launch_bounds__(G_WARPS * 32, 1)
   }
 }
 
+// Narrow operands (m <= 8 columns, any row stride, e.g. the right-hand side b of sketch-and-solve):
+// one warp per target row q walks q's whole list (all pieces) with the lanes striding over its
+// entries and gathering B[j, 0:m] (B stays L2-resident), float64 sums, a fixed-order warp tree.
+template <typename T, int M>
+__global__ void __launch_bounds__(256)
+    sparse_adjoint_narrow(const T* __restrict__ B, int64_t ldb, int m, const int32_t* __restrict__ ent,
+                          const int64_t* __restrict__ off, int npieces, int64_t k, double scale, T* __restrict__ SA,
+                          int64_t ldsa) {
+  const int lane = threadIdx.x & 31;
+  const int64_t q = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (q >= k) return;
+  const int64_t e0 = off[q * (npieces + 1)], e1 = off[q * (npieces + 1) + npieces];
+  double acc[M];
+#pragma unroll
+  for (int c = 0; c < M; ++c) acc[c] = 0.0;
+  for (int64_t e = e0 + lane; e < e1; e += 32) {
+    const uint32_t w = (uint32_t)__ldg(ent + e);
+    const T* row = B + (int64_t)(w & 0x7fffffffu) * ldb;
+    const double sg = (w >> 31) ? -1.0 : 1.0;
+#pragma unroll
+    for (int c = 0; c < M; ++c)
+      if (c < m) acc[c] = fma(sg, (double)__ldg(row + c), acc[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < M; ++c) {
+    double v = acc[c];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && c < m) SA[q * ldsa + c] = (T)(v * scale);
+  }
+}
+
 struct GPlan {
   int npieces, nhalves;
   int64_t prows, nunits;
@@ -309,4 +341,32 @@ extern "C" int sk_sparse_adjoint_gather(int dtype, const void* A, int64_t d, int
                              ldsa, accumulate, ws, ws_bytes, s);
   return gather_run<double>(static_cast<const double*>(A), d, m, lda, ent, off, k, scale, static_cast<double*>(SA),
                             ldsa, accumulate, ws, ws_bytes, s);
+}
+
+extern "C" int sk_sparse_adjoint_narrow(int dtype, const void* B, int64_t d, int64_t m, int64_t ldb, const int32_t* ent,
+                                        const int64_t* off, int npieces, int64_t k, double scale, void* SA,
+                                        int64_t ldsa, void* stream) {
+  if (d < 1 || m < 0 || m > 8 || k < 1 || npieces < 1 || ldb < m || ldsa < m)
+    return fail(SK_EINVAL, "sk_sparse_adjoint_narrow: bad shape (m <= 8)/leading dimension");
+  if (dtype != SK_F32 && dtype != SK_F64) return fail(SK_EINVAL, "sk_sparse_adjoint_narrow: bad dtype");
+  if (m == 0) return SK_OK;
+  if (!B || !SA || !ent || !off) return fail(SK_EINVAL, "sk_sparse_adjoint_narrow: null pointer");
+  cudaStream_t s = as_stream(stream);
+  const unsigned grid = (unsigned)((k + 7) / 8);
+  if (dtype == SK_F32) {
+    if (m == 1)
+      sparse_adjoint_narrow<float, 1><<<grid, 256, 0, s>>>(static_cast<const float*>(B), ldb, 1, ent, off, npieces, k,
+                                                            scale, static_cast<float*>(SA), ldsa);
+    else
+      sparse_adjoint_narrow<float, 8><<<grid, 256, 0, s>>>(static_cast<const float*>(B), ldb, (int)m, ent, off,
+                                                            npieces, k, scale, static_cast<float*>(SA), ldsa);
+  } else {
+    if (m == 1)
+      sparse_adjoint_narrow<double, 1><<<grid, 256, 0, s>>>(static_cast<const double*>(B), ldb, 1, ent, off, npieces,
+                                                             k, scale, static_cast<double*>(SA), ldsa);
+    else
+      sparse_adjoint_narrow<double, 8><<<grid, 256, 0, s>>>(static_cast<const double*>(B), ldb, (int)m, ent, off,
+                                                             npieces, k, scale, static_cast<double*>(SA), ldsa);
+  }
+  return check_launch("sk_sparse_adjoint_narrow");
 }

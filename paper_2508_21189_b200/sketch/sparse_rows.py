@@ -216,30 +216,52 @@ class _SignSparseTM(TestMatrix):
                                        torch.from_numpy(seg_off).to(device), int(cap.value), mag)
         return self._device_cache[key]
 
-    def _adjoint_gather_on(self, device, dtype_code: int, m: int):
-        """K2g encoding (CSR of S by target row + piece offsets), built with torch ops on `device`."""
-        import ctypes as _ct
-
-        lib = _lib.load()
-        prows = _ct.c_int64(0)
-        npieces = int(lib.sk_sparse_adjoint_gather_pieces(dtype_code, self.d, m, self.k, _ct.byref(prows)))
-        _lib.check(min(npieces, 0), "sk_sparse_adjoint_gather_pieces")
-        key = ("adjg", device, int(prows.value))
+    def _gather_csr_on(self, device):
+        """S = Omega^T in CSR by target row (K2g entry words + row pointers), built once per device
+        with torch ops (from the device draws when they exist)."""
+        key = ("adjg_csr", device)
         if key not in self._device_cache:
             import torch
 
             dform = self._device_sign_form(device)
             if dform is not None:
                 cols, neg, mag = dform
-                z = cols.shape[1]
-                rows = torch.arange(self.d, device=device).repeat_interleave(z)
-                ent, off = gather_encode(rows, cols.reshape(-1), neg.reshape(-1), self.d, self.k, int(prows.value),
-                                         device)
+                rows = torch.arange(self.d, device=device).repeat_interleave(cols.shape[1])
+                ent, off = gather_encode(rows, cols.reshape(-1), neg.reshape(-1), self.d, self.k, self.d, device)
             else:
                 rows, cols, neg, mag = self._sign_form()
-                ent, off = gather_encode(rows, cols, neg, self.d, self.k, int(prows.value), device)
-            self._device_cache[key] = (ent, off, mag)
+                ent, off = gather_encode(rows, cols, neg, self.d, self.k, self.d, device)
+            rowptr = torch.cat([off[:, 0], off[-1:, 1]])
+            self._device_cache[key] = (ent, rowptr, mag)
         return self._device_cache[key]
+
+    def _adjoint_gather_on(self, device, dtype_code: int, m: int):
+        """K2g encoding for the launch plan's row pieces: the CSR plus off[q][p] (start of piece p in
+        q's list). Piece offsets are derived from the one CSR per piece size (cached)."""
+        import ctypes as _ct
+
+        import torch
+
+        lib = _lib.load()
+        prows = _ct.c_int64(0)
+        npieces = int(lib.sk_sparse_adjoint_gather_pieces(dtype_code, self.d, m, self.k, _ct.byref(prows)))
+        _lib.check(min(npieces, 0), "sk_sparse_adjoint_gather_pieces")
+        ent, rowptr, mag = self._gather_csr_on(device)
+        prows = int(prows.value)
+        key = ("adjg_off", device, prows)
+        if key not in self._device_cache:
+            if npieces == 1:
+                off = torch.stack([rowptr[:-1], rowptr[1:]], dim=1).contiguous()
+            else:
+                counts = rowptr[1:] - rowptr[:-1]
+                q = torch.arange(self.k, device=device, dtype=torch.int64).repeat_interleave(counts)
+                skey = q * self.d + (ent.to(torch.int64) & 0x7FFFFFFF)
+                pstart = torch.clamp(torch.arange(npieces + 1, device=device, dtype=torch.int64) * prows, max=self.d)
+                bounds = torch.arange(self.k, device=device, dtype=torch.int64)[:, None] * self.d + pstart[None, :]
+                off = torch.searchsorted(skey, bounds.reshape(-1)).reshape(self.k, npieces + 1).contiguous()
+                del q, skey
+            self._device_cache[key] = off
+        return ent, self._device_cache[key], mag
 
     def _tma_rows_ok(self, b) -> bool:
         """16-byte aligned rows with unit column stride: the TMA-fed adjoints (K2g, K2w) apply."""
@@ -247,8 +269,9 @@ class _SignSparseTM(TestMatrix):
         return b.data_ptr() % 16 == 0 and b.stride(0) % per16 == 0 and b.stride(1) == 1 and b.shape[1] >= 1
 
     def adjoint_path(self, b) -> str:
-        """Kernel used by apply_adjoint: 'rowgather' (K2g, default for aligned float32 / float64),
-        'wide' (K2w), 'gather' (K2, any layout) or 'dense'. SKETCH_B200_SPARSE_ADJOINT picks one."""
+        """Kernel used by apply_adjoint: 'narrow' (m <= 8 columns), 'rowgather' (K2g, default for
+        aligned float32 / float64), 'wide' (K2w), 'gather' (K2, any layout) or 'dense'.
+        SKETCH_B200_SPARSE_ADJOINT picks one."""
         import os
 
         import torch
@@ -256,7 +279,11 @@ class _SignSparseTM(TestMatrix):
         if not self._signed_real() or b.dtype not in (torch.float32, torch.float64):
             return "dense"
         forced = os.environ.get("SKETCH_B200_SPARSE_ADJOINT", "auto")
-        if forced == "gather" or not self._tma_rows_ok(b):
+        if forced == "gather":
+            return "gather"
+        if forced == "auto" and b.dim() == 2 and 1 <= b.shape[1] <= 8 and (b.shape[1] == 1 or b.stride(1) == 1):
+            return "narrow"
+        if not self._tma_rows_ok(b):
             return "gather"
         return "wide" if forced == "wide" else "rowgather"
 
@@ -335,6 +362,18 @@ class _SignSparseTM(TestMatrix):
         path = self.adjoint_path(b)
         if path == "dense":
             return super()._adjoint_device(b)
+        if path == "narrow":
+            code = _lib.SK_F32 if b.dtype == torch.float32 else _lib.SK_F64
+            m = b.shape[1]
+            ent, off, mag = self._adjoint_gather_on(b.device, code, m)
+            out = torch.empty((self.k, m), dtype=b.dtype, device=b.device)
+            lib = _lib.load()
+            with torch.cuda.device(b.device):
+                st = lib.sk_sparse_adjoint_narrow(code, b.data_ptr(), self.d, m, b.stride(0), ent.data_ptr(),
+                                                  off.data_ptr(), off.shape[1] - 1, self.k, mag, out.data_ptr(),
+                                                  out.stride(0), torch.cuda.current_stream().cuda_stream)
+            _lib.check(st, "sk_sparse_adjoint_narrow")
+            return out
         if path == "rowgather":
             code = _lib.SK_F32 if b.dtype == torch.float32 else _lib.SK_F64
             m = b.shape[1]

@@ -204,3 +204,29 @@ def test_adjoint_paths_randomized(cuda):
         ref = om.T @ b.double().cpu().numpy()
         tol = 1e-5 if dt == torch.float32 else 1e-12
         assert rel_err(y, ref) <= tol, (trial, type(tm).__name__, d, tm.k, m, tm.adjoint_path(b))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_narrow_adjoint(dt, cuda):
+    """m <= 8 columns (right-hand sides): warp per target row over the K2g encoding."""
+    import torch
+
+    tm = skb.SparseUniformTM(50003, 700, 5, seed=9)
+    om = orc.sparse_uniform_csr(50003, 700, 5, 9)
+    rng = np.random.default_rng(1)
+    tol = 1e-5 if dt == np.float32 else 1e-12
+    for m in (1, 3, 8):
+        b = rng.standard_normal((50003, m)).astype(dt)
+        bt = torch.as_tensor(b).to(cuda)
+        assert tm.adjoint_path(bt) == "narrow"
+        assert rel_err(tm.apply_adjoint(bt).cpu().numpy(), orc.csr_adjoint(om, b)) <= tol
+    # 1-D vector (squeezed back), and a strided row view
+    v = rng.standard_normal(50003).astype(dt)
+    got = tm.apply_adjoint(torch.as_tensor(v).to(cuda))
+    assert tuple(got.shape) == (700,)
+    assert rel_err(got.cpu().numpy(), orc.csr_adjoint(om, v[:, None])[:, 0]) <= tol
+    big = torch.as_tensor(rng.standard_normal((50003, 10)).astype(dt)).to(cuda)
+    sl = big[:, 2:6]
+    assert tm.adjoint_path(sl) == "narrow"
+    assert rel_err(tm.apply_adjoint(sl).cpu().numpy(), orc.csr_adjoint(om, sl.cpu().numpy())) <= tol

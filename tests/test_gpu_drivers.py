@@ -117,3 +117,25 @@ def test_dense_tn_tc_vs_float64(n, d, k, cuda):
     # strided A (a column slice): copied to a dense operand first
     y2 = dense_tn_tc(torch.randn(n, 2 * d, device=cuda, generator=g)[:, :d].contiguous(), w)
     assert tuple(y2.shape) == (d, k)
+
+
+def test_truncated_pinv_qr_path(cuda):
+    """Well-conditioned tall systems take the QR solve, ill-conditioned / rank-deficient ones the
+    reference's SVD with the 5-eps cut; both agree with the float64 SVD pseudo-inverse."""
+    import torch
+
+    g = torch.Generator(device=cuda).manual_seed(3)
+    m = torch.randn(3000, 200, device=cuda, dtype=torch.float64, generator=g)
+    b = torch.randn(3000, 3, device=cuda, dtype=torch.float64, generator=g)
+    assert rand_nla._qr_solve_if_well_conditioned(m, b, rand_nla.DEFAULT_RANK_TOL) is not None
+    ref = torch.linalg.pinv(m) @ b
+    got = rand_nla.truncated_pinv_apply(m, b)
+    assert float((got - ref).norm() / ref.norm()) <= 1e-12
+    # exactly rank-deficient: the QR path must decline and the cut must apply
+    m2 = m.clone()
+    m2[:, 7] = m2[:, 3] * 2.0
+    assert rand_nla._qr_solve_if_well_conditioned(m2, b, rand_nla.DEFAULT_RANK_TOL) is None
+    u, s, vh = torch.linalg.svd(m2, full_matrices=False)
+    r = int((s > rand_nla.DEFAULT_RANK_TOL * s[0]).sum())
+    ref2 = vh[:r].T @ ((u[:, :r].T @ b) / s[:r, None])
+    assert float((rand_nla.truncated_pinv_apply(m2, b) - ref2).norm() / ref2.norm()) <= 1e-10
