@@ -112,7 +112,7 @@ struct Phase3 {
 };
 
 template <typename T, int L, bool SIGNS>
-__global__ void __launch_bounds__((1 << (L - 5)), (sizeof(T) == 4 ? (L <= 12 ? 3 : (L == 13 ? 2 : 1)) : (L <= 12 ? 2 : 1)))
+__global__ void __launch_bounds__((1 << (L - 5)), (sizeof(T) == 4 ? (L <= 12 ? 3 : (L == 13 ? 2 : 1)) : (L <= 12 ? 2 : (L == 13 ? 2 : 1))))
     srtt_wht_fast(const T* __restrict__ A, int64_t n, int64_t lda, const T* __restrict__ dvals,
                   const int32_t* __restrict__ samp, int xi, int k, T scale, T* __restrict__ Y,
                   int64_t ldy) {
