@@ -138,6 +138,7 @@ def pipelined_right(apply_dev, host, k: int):
     ev_free = [torch.cuda.Event() for _ in range(2)]
     ev_staged = [torch.cuda.Event() for _ in range(2)]
     used = [False, False]
+    keep = []
     for i, r0 in enumerate(range(0, n, rows)):
         b = i % 2
         m = min(rows, n - r0)
@@ -164,13 +165,16 @@ def pipelined_right(apply_dev, host, k: int):
         with torch.cuda.stream(s_d2h):
             s_d2h.wait_stream(s_cmp)
             y_host[r0:r0 + m].copy_(y, non_blocking=True)
-            y.record_stream(s_d2h)
+        # keep the chunk result alive until the end of the call instead of record_stream: blocks
+        # come back to the caching allocator only after the final synchronize, so steady-state
+        # calls reuse them (record_stream let the pool grow and occasionally hit cudaMalloc/cudaFree)
+        keep.append(y)
         used[b] = True
     for s in (s_h2d, s_cmp, s_d2h):
         outer.wait_stream(s)
-    for bb in bufs:
-        bb.record_stream(s_cmp)
     s_d2h.synchronize()
+    s_cmp.synchronize()
+    del keep
     if y_host is None:
         y_host = torch.empty((0, k), dtype=dt)
     return y_host
