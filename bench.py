@@ -307,15 +307,18 @@ def time_e2e(torch, w, steps, world, dev):
     torch.cuda.synchronize()
     _barrier(world)
     t0 = time.perf_counter()
+    marks = []
     for _ in range(steps):
-        y = _apply(w, a_host)
+        y = _apply(w, a_host)  # returns after the D2H of the step's result has completed
+        marks.append(time.perf_counter())
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
     el = _max_over_ranks(world, el, dev)
     h2d = a_host.numel() * a_host.element_size()
     d2h = y.numel() * y.element_size()
     del a_host
-    return el, h2d, d2h
+    step_ms = [1e3 * (b - a) for a, b in zip([t0] + marks[:-1], marks)]
+    return el, h2d, d2h, step_ms
 
 
 def cpu_reference_step(w, a_host, procs):
@@ -397,9 +400,9 @@ def measure(torch, w, steps, warmup, world, rank, dev, with_e2e, clocks_idx):
     res["omega_setup"] = time_setup(torch, w, mean_step)
     if with_e2e:
         e_steps = max(1, min(steps, 5))
-        el, h2d, d2h = time_e2e(torch, w, e_steps, world, dev)
+        el, h2d, d2h, step_ms = time_e2e(torch, w, e_steps, world, dev)
         res["e2e"] = {"value": world * a_bytes * e_steps / el / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
-                      "d2h_bytes_per_step": d2h, "steps": e_steps,
+                      "d2h_bytes_per_step": d2h, "steps": e_steps, "step_ms": [round(x, 2) for x in step_ms],
                       "path": f"tm.{'apply_adjoint' if w['op'] == 'adjoint' else 'apply_right'}(pinned host torch tensor)"
                               " -> host tensor (H2D+kernel+D2H)"}
     return res

@@ -113,6 +113,18 @@ def host_tensor_of(x):
     return torch.from_numpy(np.ascontiguousarray(arr)), "numpy"
 
 
+_STREAMS = {}
+
+
+def _pipeline_streams(dev):
+    """Three streams per device, created once: the caching allocator keeps per-stream pools, so
+    fresh streams every call would turn each chunk's output allocation into a cudaMalloc."""
+    key = dev.index
+    if key not in _STREAMS:
+        _STREAMS[key] = tuple(torch.cuda.Stream(dev) for _ in range(3))
+    return _STREAMS[key]
+
+
 def pipelined_right(apply_dev, host, k: int):
     """Row-chunked host -> device -> host pipeline for a row-independent right apply.
 
@@ -128,7 +140,7 @@ def pipelined_right(apply_dev, host, k: int):
     rows = max(1, min(n, PIPELINE_CHUNK_BYTES // max(1, d * esz)))
     pinned = host.is_pinned() and host.dtype == dt and host.is_contiguous()
     y_host = None
-    s_h2d, s_cmp, s_d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    s_h2d, s_cmp, s_d2h = _pipeline_streams(dev)
     outer = torch.cuda.current_stream(dev)
     for s in (s_h2d, s_cmp, s_d2h):
         s.wait_stream(outer)
