@@ -255,8 +255,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     setmaxnreg_inc<168>();
     // ---------------------------------------------------------------- reducers + output
     const int lg = warp & 3;                 // TMEM lane group
-    const int half = (warp - 8) >> 2;        // column half
-    const int bnh = p.BN >> 1;               // multiple of 16
+    const int half = (warp - 8) >> 2;        // column half: [0, bh0) and [bh0, BN), bh0 = 16-aligned
+    const int bh0 = ((p.BN >> 1) + 15) & ~15;
+    const int hoff = half * bh0;
+    const int bnh = half == 0 ? bh0 : p.BN - bh0;  // columns of this half (BN % 16 == 0)
     uint32_t chunk_seq = 0;
     for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
       const Unit w = unit_of(p, u);
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t buf = chunk_seq & 1, use = chunk_seq >> 1;
         mbar_wait(&acc_full[buf], use & 1);
         tc_fence_after();
-        const uint32_t base = tmem + ((uint32_t)(32 * lg) << 16) + buf * (uint32_t)p.BN + half * bnh;
+        const uint32_t base = tmem + ((uint32_t)(32 * lg) << 16) + buf * (uint32_t)p.BN + hoff;
 #pragma unroll
         for (int g = 0; g < kMaxBNH / 16; ++g) {
           if (g * 16 < bnh) {
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int64_t row = (int64_t)w.mt * BM + 32 * lg + lane;
       if (row < p.M) {
-        const int col0 = w.nb * p.BN + half * bnh;
+        const int col0 = w.nb * p.BN + hoff;
         float* out;
         float sc;
         if (p.ksplit == 1) {
@@ -395,13 +397,13 @@ struct Plan {
 
 Plan make_plan(int64_t n, int64_t d, int64_t k, int NB, bool wide_b = false) {
   Plan pl{};
-  // N blocks of at most 256 columns (two TMEM accumulators of BN columns each), BN % 32 == 0; a
+  // N blocks of at most 256 columns (two TMEM accumulators of BN columns each), BN % 16 == 0; a
   // split B doubles the B tile, so it keeps 128 columns unless re-reading A per N block would cost
   // more than the shallower ring (wide_b: the TN product, whose A strip is the big operand)
   const int64_t bn_max = (NB == 2 && !wide_b) ? 128 : 256;
   pl.nblocks = (int)((k + bn_max - 1) / bn_max);
   const int64_t per = (k + pl.nblocks - 1) / pl.nblocks;
-  pl.BN = (int)((per + 31) / 32 * 32);
+  pl.BN = (int)((per + 15) / 16 * 16);  // UMMA N (M = 128) is any multiple of 16
   pl.mtiles = (int)((n + BM - 1) / BM);
   const int nk = (int)((d + BK - 1) / BK);
   const int tiles = pl.mtiles * pl.nblocks;
