@@ -416,30 +416,17 @@ __global__ void __launch_bounds__(W * 32, 1)
       set_tile();
     }
   };
-  // byte offsets of this thread's vectors inside a staged tile (fixed for the whole kernel)
-  uint32_t soff[VPT];
-#pragma unroll
-  for (int j = 0; j < VPT; ++j) {
-    const int q = tid + j * NT;
-    const int i = q / VEC_PER_ROW, cv = q % VEC_PER_ROW;
-    soff[j] = (uint32_t)((i * R + ((cv * NV) ^ (i & 31 & ~(NV - 1)))) * sizeof(T));
-  }
-  const uint32_t as_s = (uint32_t)__cvta_generic_to_shared(As);
-  auto store_vecs = [&](uint32_t dst, auto key_c) {
+  auto store_vecs = [&](T* dst, auto key_c) {
     constexpr int KEY = decltype(key_c)::value;
 #pragma unroll
     for (int j = 0; j < VPT; ++j) {
-      const V4 v = xor_perm(pre[j], KEY);
-      if constexpr (sizeof(T) == 4) {
-        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + soff[j]), "f"(v.x), "f"(v.y), "f"(v.z),
-                     "f"(v.w)
-                     : "memory");
-      } else {
-        asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(dst + soff[j]), "d"(v.x), "d"(v.y) : "memory");
-      }
+      const int q = tid + j * NT;
+      const int i = q / VEC_PER_ROW, cv = q % VEC_PER_ROW;
+      const int blk = (cv * NV) ^ (i & 31 & ~(NV - 1));
+      *reinterpret_cast<V4*>(dst + i * R + blk) = xor_perm(pre[j], KEY);
     }
   };
-  auto store_step = [&](uint32_t dst) {
+  auto store_step = [&](T* dst) {
     const int key = vr & (NV - 1);
     if (key == 0) store_vecs(dst, std::integral_constant<int, 0>{});
     else if (key == 1) store_vecs(dst, std::integral_constant<int, 1>{});
@@ -452,7 +439,7 @@ __global__ void __launch_bounds__(W * 32, 1)
   if (steps > 0) {
     set_tile();
     load_next();
-    store_step(as_s);
+    store_step(As);
     if (steps > 1) load_next();
   }
   __syncthreads();
@@ -513,7 +500,7 @@ __global__ void __launch_bounds__(W * 32, 1)
       ct += nper;
     }
     if (st + 1 < steps) {
-      store_step(as_s + ((uint32_t)(st + 1) & 1u) * (uint32_t)(TILE * sizeof(T)));
+      store_step(As + ((st + 1) & 1) * TILE);
       if (st + 2 < steps) load_next();
     }
     __syncthreads();
