@@ -381,6 +381,54 @@ def run_reference(args):
     return 0
 
 
+def measure_sharded_sa(torch, world, rank, dev, steps=5, warmup=3):
+    """Config 4 SA over row shards with the NCCL all-reduce of the partials.
+
+    Strong scaling: the 4194304-row A is split into `world` row blocks; rank g holds its block
+    and the matching rows of Omega (`SparseRowBlockTM`), runs K2g on them and the 2048 x 512
+    float64 partials are summed by one all-reduce (`dist.sharded_adjoint`).  Timed on the device
+    (events on the launching stream, barrier on both sides, max over ranks), all-reduce included;
+    the all-reduce alone is timed the same way and reported apart.
+    """
+    from paper_2508_21189_b200 import dist as skd
+    from paper_2508_21189_b200.sketch import SparseUniformTM
+
+    n, d, k = 4194304, 512, 2048
+    r0, r1 = skd.row_range(n, world, rank)
+    tm = SparseUniformTM(n, k, 8, seed=0)
+    g = torch.Generator(device=dev).manual_seed(4000 + rank)
+    a = torch.randn(r1 - r0, d, dtype=torch.float32, device=dev, generator=g)
+    a *= (torch.rand(r1 - r0, 1, device=dev, generator=g).clamp_min(1e-12) ** (-1.0 / 1.5))
+    step = lambda: skd.sharded_adjoint(tm, a, r0)  # noqa: E731
+    part = step()  # builds the row block's device encoding (setup, untimed)
+
+    def timed(fn):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        _barrier(world)
+        torch.cuda.synchronize()
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            fn()
+        e1.record(st)
+        torch.cuda.synchronize()
+        _barrier(world)
+        return _max_over_ranks(world, e0.elapsed_time(e1) / 1e3 / steps, dev)
+
+    t_step = timed(step)
+    t_ar = timed(lambda: skd.allreduce_sum(part))
+    out = {"workload": f"cfg4 SA, A 4194304x512 f32 split into {world} row block(s), NCCL all-reduce of the "
+                       "2048x512 float64 partials", "scaling": "strong",
+           "value_gbs": n * d * 4 / t_step / 1e9, "ms_per_step": t_step * 1e3, "allreduce_ms": t_ar * 1e3,
+           "rows_per_gpu": r1 - r0, "allreduce_bytes": part.numel() * part.element_size()}
+    del a, part
+    torch.cuda.empty_cache()
+    return out
+
+
 def measure(torch, w, steps, warmup, world, rank, dev, with_e2e, clocks_idx):
     a = w["a"]
     esize = a.element_size()
@@ -417,6 +465,7 @@ def main(argv=None):
     ap.add_argument("--config", choices=sorted(WORKLOADS), default="cfg2")
     ap.add_argument("--others", default="cfg1,cfg3,cfg4,cfg5", help="extra configs measured at N=1 ('' = none)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (quick kernel experiments)")
+    ap.add_argument("--no-sharded", action="store_true", help="skip the sharded config-4 SA (NCCL all-reduce) leg")
     args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference(args)
@@ -446,9 +495,14 @@ def main(argv=None):
                "parity_rel_fro_err_vs_gpu": err}
 
     others = {}
+    del w["a"]
+    torch.cuda.empty_cache()
+    if not args.no_sharded:
+        try:  # the one path with a collective, at every N (strong scaling)
+            others["cfg4_sharded"] = measure_sharded_sa(torch, world, rank, dev)
+        except Exception as exc:  # report, never hide
+            others["cfg4_sharded"] = {"error": f"{type(exc).__name__}: {exc}"}
     if world == 1 and args.others:
-        del w["a"]
-        torch.cuda.empty_cache()
         for name in [s for s in args.others.split(",") if s and s != args.config]:
             try:
                 ow = WORKLOADS[name](torch, dev, rank)

@@ -581,6 +581,7 @@ int dispatch(const void* A_, int64_t n, int64_t d, int64_t lda, const int32_t* p
   // split the output columns over more CTAs when there are few row tiles (wave balance)
   const int64_t tiles = (n + kRowsPerTile - 1) / kRowsPerTile;
   if (tiles < 8 * (int64_t)sm_count() && need > 8) need = 8;
+  if (const char* ov = getenv("SKETCH_B200_K1_NEED")) need = atoi(ov);  // A/B experiments
   if (need <= 4) return vec ? launch_t<T, 4, true>(A, n, d, lda, ptr, ent, nnz, k, scale, Y, ldy, s)
                             : launch_t<T, 4, false>(A, n, d, lda, ptr, ent, nnz, k, scale, Y, ldy, s);
   if (need <= 8) return vec ? launch_t<T, 8, true>(A, n, d, lda, ptr, ent, nnz, k, scale, Y, ldy, s)

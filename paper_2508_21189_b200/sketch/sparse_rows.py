@@ -631,7 +631,12 @@ class SparseRowBlockTM(_SignSparseTM):
 
 
 def _row_block(self, r0: int, r1: int) -> SparseRowBlockTM:
-    return SparseRowBlockTM(self, r0, r1)
+    """Rows [r0, r1) as an operator; cached on the parent so repeated sharded calls reuse its encoding."""
+    cache = self.__dict__.setdefault("_row_blocks", {})
+    key = (int(r0), int(r1))
+    if key not in cache:
+        cache[key] = SparseRowBlockTM(self, r0, r1)
+    return cache[key]
 
 
 _SignSparseTM.row_block = _row_block
