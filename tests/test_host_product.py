@@ -192,3 +192,15 @@ def test_redraw_determinism():
         assert np.array_equal(a.materialize(), b.materialize())
         assert not np.array_equal(a.materialize(), tm.materialize())
         assert np.array_equal(tm.materialize(), tm.materialize())
+
+
+def test_row_blocks_cached_and_partition_rows():
+    """Row blocks of a sparse operator (multi-GPU shards) are cached per parent and their rows
+    concatenate to the parent's matrix exactly."""
+    tm = skb.SparseUniformTM(300, 40, 5, seed=3)
+    blocks = [tm.row_block(0, 128), tm.row_block(128, 300)]
+    assert tm.row_block(0, 128) is blocks[0] and tm.row_block(128, 300) is blocks[1]
+    assert blocks[0].row_offset == 0 and blocks[1].row_offset == 128
+    full = tm.materialize()
+    assert np.array_equal(np.vstack([b.materialize() for b in blocks]), full)
+    assert tm.redraw(3).row_block(0, 128) is not blocks[0]
