@@ -22,7 +22,11 @@
 //        (warp w: TMEM lane group w%4, column half (w-8)/4), final scale + store         (168 regs)
 // smem ring of `stages` x {A 32 KB (fp32 -> bf16 hi/lo in place), B_hi BN*128 B (, B_lo)}; mbarriers
 // tma_full/full/empty per stage and acc_full/acc_empty per TMEM accumulator.
+// With an exact B (NB = 1) and more than 128 rows the CTA-pair form below runs instead
+// (dense_tc_pair_kernel, tcgen05 cta_group::2): config 5 1.71 -> 1.59 ms, config 3 1.71 -> 1.55 ms.
 #include <cuda.h>
+
+#include <cstdio>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -316,6 +320,256 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------------------------ CTA pairs
+// The same engine on a CTA pair (cluster of 2 on one TPC, tcgen05 cta_group::2): one MMA of
+// M = 256 (128 rows of A from each CTA's shared memory) x N = BN, with B^T split by N — each CTA
+// stages only BN/2 rows of the B tile, and the pair's tensor cores share them. Per k-block of 64
+// and SM the shared-memory traffic drops from 224 KB (A fp32 32 + convert 64 + B 32 + MMA reads
+// 96) to 176 KB, the B-tile half also buys a fourth ring stage. The leader (rank 0) issues the
+// MMAs; both CTAs convert their own A rows and arrive on the leader's `full` barrier; commits
+// multicast to both CTAs' `empty` / `acc_full`; reducers of both CTAs release the leader's
+// `acc_empty`. Each CTA's TMEM holds its own 128 rows x BN of the pair's accumulator.
+// Cross-CTA arrives use the default (.cta) release, as CUTLASS's ClusterBarrier: a .release.cluster
+// arrive per stage from the converters cost 2.77 ms at config 5 (vs 1.59 ms).
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of `bar` in CTA `cta` of this cluster
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(sm100::smem_u32(p)), "r"(cta));
+  return r;
+}
+// remote arrive with the default (.release, .cta) semantics, as CUTLASS's ClusterBarrier::arrive: the
+// data it publishes is this CTA's own shared memory, read by this SM's half of the pair MMA
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive once on `bar` (same offset) in both CTAs of the pair when this thread's MMAs complete
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          sm100::smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    dense_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                         const TcParams p) {
+  extern __shared__ uint8_t smem_dyn[];
+  uint8_t* smem = smem_dyn + ((1024u - (sm100::smem_u32(smem_dyn) & 1023u)) & 1023u);
+  const uint32_t a_bytes = BM * 128;
+  const int bnh2 = p.BN >> 1;                      // B^T rows staged by each CTA
+  const uint32_t stage_bytes = kAStageBytes + (uint32_t)bnh2 * 128;
+  const int S = p.stages;
+  uint64_t* tma_full = reinterpret_cast<uint64_t*>(smem + (size_t)S * stage_bytes);
+  uint64_t* full = tma_full + S;       // leader: converted in both CTAs (8 converter warps)
+  uint64_t* empty = full + S;          // consumed by the pair MMA (multicast commit)
+  uint64_t* acc_full = empty + S;      // [2] (multicast commit)
+  uint64_t* acc_empty = acc_full + 2;  // [2] leader: drained by both CTAs (16 reducer warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&tma_full[s], 1);
+      mbar_init(&full[s], 8);  // leader: the converter warps of both CTAs
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 16);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&tm_a);
+    tma_prefetch_desc(&tm_b);
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sm100::smem_u32(tmem_slot)),
+                 "r"(p.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int nk = (int)((p.K + BK - 1) / BK);
+  const uint32_t full_leader = mapa_u32(full, 0);       // full[0] in the leader; + 8 s
+  const uint32_t acc_empty_leader = mapa_u32(acc_empty, 0);
+
+  if (warp < 4) {
+    setmaxnreg_dec<32>();
+    if (warp == 0 && lane == 0) {
+      // -------------------------------------------------------------- producer (this CTA's rows + B half)
+      int s = 0;
+      uint32_t ph = 0;
+      for (int u = pair; u < p.num_units; u += npairs) {
+        const Unit w = unit_of(p, u);
+        const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
+        const int row0 = (2 * w.mt + (int)rank) * BM;
+        const int brow0 = w.nb * p.BN + (int)rank * bnh2;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + (size_t)s * stage_bytes;
+          mbar_arrive_expect_tx(&tma_full[s], stage_bytes);
+          tma_load_2d(st, &tm_a, &tma_full[s], kb * BK, row0);
+          tma_load_2d(st + kAStageBytes, &tm_b, &tma_full[s], kb * BK, brow0);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+      }
+    } else if (warp == 1 && lane == 0 && rank == 0) {
+      // -------------------------------------------------------------- MMA issuer (leader only)
+      const uint32_t idesc = idesc_bf16_f32(2 * BM, p.BN);
+      int s = 0;
+      uint32_t ph = 0;
+      uint32_t chunk_seq = 0;
+      for (int u = pair; u < p.num_units; u += npairs) {
+        const Unit w = unit_of(p, u);
+        const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
+        for (int c0 = kb0; c0 < kb1; c0 += CHUNK_KB, ++chunk_seq) {
+          const uint32_t buf = chunk_seq & 1, use = chunk_seq >> 1;
+          mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + buf * (uint32_t)p.BN;
+          const int c1 = min(kb1, c0 + CHUNK_KB);
+          for (int kb = c0; kb < c1; ++kb) {
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            const uint32_t st = sm100::smem_u32(smem + (size_t)s * stage_bytes);
+            const uint32_t a_hi = st, a_lo = st + a_bytes, b = st + kAStageBytes;
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint64_t db = sdesc_kmajor_sw128(b + kk * 32);
+              umma_bf16_pair(d, sdesc_kmajor_sw128(a_hi + kk * 32), db, idesc, (kb > c0 || kk > 0) ? 1u : 0u);
+              umma_bf16_pair(d, sdesc_kmajor_sw128(a_lo + kk * 32), db, idesc, 1u);
+            }
+            umma_commit_pair(&empty[s]);
+            if (++s == S) { s = 0; ph ^= 1; }
+          }
+          umma_commit_pair(&acc_full[buf]);
+        }
+      }
+    }
+  } else if (warp < 8) {
+    setmaxnreg_dec<128>();
+    // -------------------------------------------------------------- A converters (as dense_tc_kernel)
+    const int ct = threadIdx.x - 128;
+    const int c4 = ct & 15;
+    const int rsub = ct >> 4;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int u = pair; u < p.num_units; u += npairs) {
+      const Unit w = unit_of(p, u);
+      const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        float4 cur[16];
+        mbar_wait(&tma_full[s], ph);
+        const uint32_t st = sm100::smem_u32(smem + (size_t)s * stage_bytes);
+        const uint32_t at = st + (rsub * BK + c4 * 4) * 4;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) cur[i] = lds128(at + i * 8 * BK * 4);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int r = rsub + 8 * i;
+          const float4 v = cur[i];
+          const uint32_t h01 = cvt_bf16x2(v.y, v.x), h23 = cvt_bf16x2(v.w, v.z);
+          const float l0 = v.x - __uint_as_float(h01 << 16), l1 = v.y - __uint_as_float(h01 & 0xffff0000u);
+          const float l2 = v.z - __uint_as_float(h23 << 16), l3 = v.w - __uint_as_float(h23 & 0xffff0000u);
+          const uint32_t lo01 = cvt_bf16x2(l1, l0), lo23 = cvt_bf16x2(l3, l2);
+          const uint32_t off = r * 128 + (((c4 >> 1) ^ (r & 7)) << 4) + ((c4 & 1) << 3);
+          sts64(st + off, h01, h23);
+          sts64(st + a_bytes + off, lo01, lo23);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(full_leader + 8u * (uint32_t)s);
+        if (++s == S) { s = 0; ph ^= 1; }
+      }
+    }
+  } else {
+    setmaxnreg_inc<168>();
+    // -------------------------------------------------------------- reducers + output (own 128 rows)
+    const int lg = warp & 3;
+    const int half = (warp - 8) >> 2;
+    const int bh0 = ((p.BN >> 1) + 15) & ~15;
+    const int hoff = half * bh0;
+    const int bnh = half == 0 ? bh0 : p.BN - bh0;
+    uint32_t chunk_seq = 0;
+    for (int u = pair; u < p.num_units; u += npairs) {
+      const Unit w = unit_of(p, u);
+      const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
+      float sum[kMaxBNH];
+#pragma unroll
+      for (int j = 0; j < kMaxBNH; ++j) sum[j] = 0.f;
+      for (int c0 = kb0; c0 < kb1; c0 += CHUNK_KB, ++chunk_seq) {
+        const uint32_t buf = chunk_seq & 1, use = chunk_seq >> 1;
+        mbar_wait(&acc_full[buf], use & 1);
+        tc_fence_after();
+        const uint32_t base = tmem + ((uint32_t)(32 * lg) << 16) + buf * (uint32_t)p.BN + hoff;
+#pragma unroll
+        for (int g = 0; g < kMaxBNH / 16; ++g) {
+          if (g * 16 < bnh) {
+            uint32_t r[16];
+            tmem_ld16(base + g * 16, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) sum[g * 16 + j] += __uint_as_float(r[j]);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(acc_empty_leader + 8u * buf);
+      }
+      const int64_t row = (int64_t)(2 * w.mt + (int)rank) * BM + 32 * lg + lane;
+      if (row < p.M) {
+        const int col0 = w.nb * p.BN + hoff;
+        float* out;
+        float sc;
+        if (p.ksplit == 1) {
+          out = p.Y + row * p.ldy + col0;
+          sc = p.scale;
+        } else {
+          out = p.part + ((int64_t)w.ks * p.M + row) * p.N + col0;
+          sc = 1.0f;
+        }
+#pragma unroll
+        for (int g = 0; g < kMaxBNH / 16; ++g) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int c = g * 16 + j;
+            if (c < bnh && col0 + c < p.N) out[c] = sum[c] * sc;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs done with the pair's TMEM
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
+  }
+}
+
 // Y = scale * sum_s part[s] (fixed order)
 __global__ void tc_splitk_reduce(const float* __restrict__ part, int ksplit, int64_t M, int N, float scale,
                                  float* __restrict__ Y, int64_t ldy) {
@@ -426,6 +680,40 @@ Plan make_plan(int64_t n, int64_t d, int64_t k, int NB, bool wide_b = false) {
   return pl;
 }
 
+// CTA-pair plan (NB == 1): units = (pair of M tiles, N block, K split), BN <= 256 (TMEM: two
+// accumulators of BN columns in each CTA), each CTA stages BN/2 rows of B^T per stage.
+Plan make_plan_pair(int64_t n, int64_t d, int64_t k) {
+  Plan pl{};
+  pl.nblocks = (int)((k + 255) / 256);
+  const int64_t per = (k + pl.nblocks - 1) / pl.nblocks;
+  pl.BN = (int)((per + 15) / 16 * 16);  // cta_group::2: N % 16 == 0, so each half is a multiple of 8 rows
+  pl.mtiles = (int)((n + 2 * BM - 1) / (2 * BM));  // M-tile pairs
+  const int nk = (int)((d + BK - 1) / BK);
+  const int tiles = pl.mtiles * pl.nblocks;
+  const int pairs = sm_count() / 2;
+  int ks = 1;
+  while (tiles * ks < 4 * pairs && (nk + 2 * ks - 1) / (2 * ks) >= 4 * CHUNK_KB) ks *= 2;
+  pl.kb_per_split = (nk + ks - 1) / ks;
+  pl.kb_per_split = (pl.kb_per_split + CHUNK_KB - 1) / CHUNK_KB * CHUNK_KB;
+  pl.ksplit = (nk + pl.kb_per_split - 1) / pl.kb_per_split;
+  pl.units = tiles * pl.ksplit;
+  const size_t stage_bytes = kAStageBytes + (size_t)(pl.BN / 2) * 128;
+  const size_t budget = 227 * 1024 - 1024 - 512;
+  int stages = (int)(budget / stage_bytes);
+  if (stages > 6) stages = 6;
+  pl.stages = stages;
+  pl.astages = 0;
+  pl.smem = 1024 + stages * stage_bytes + (3 * stages + 4) * 8 + 16;
+  pl.ws_bytes = pl.ksplit > 1 ? (size_t)pl.ksplit * n * k * sizeof(float) : 0;
+  return pl;
+}
+
+bool use_pair(int64_t n, int NB) {
+  if (NB != 1 || n <= BM) return false;
+  const char* e = getenv("SKETCH_B200_TC_PAIR");
+  return !(e && e[0] == '0');
+}
+
 }  // namespace
 }  // namespace skb
 
@@ -433,7 +721,9 @@ extern "C" int sk_dense_tc_supported(int64_t k) { return k >= 1 ? 1 : 0; }
 
 extern "C" size_t sk_dense_tc_workspace_bytes(int64_t n, int64_t d, int64_t k, int split_b) {
   if (n < 1 || d < 1 || k < 1) return 0;
-  return skb::make_plan(n, d, k, split_b ? 2 : 1).ws_bytes;
+  const size_t a = skb::make_plan(n, d, k, split_b ? 2 : 1).ws_bytes;
+  const size_t b = skb::use_pair(n, split_b ? 2 : 1) ? skb::make_plan_pair(n, d, k).ws_bytes : 0;
+  return a > b ? a : b;
 }
 
 extern "C" int sk_dense_right_tc(const float* A, int64_t n, int64_t d, int64_t lda, const uint16_t* Bt_hi,
@@ -449,6 +739,75 @@ extern "C" int sk_dense_right_tc(const float* A, int64_t n, int64_t d, int64_t l
   if ((reinterpret_cast<uintptr_t>(Bt_hi) & 15) || (ldb & 7) || (Bt_lo && (reinterpret_cast<uintptr_t>(Bt_lo) & 15)))
     return fail(SK_EINVAL, "sk_dense_right_tc: B^T must be 16-byte aligned with ldb a multiple of 8");
   const int NB = Bt_lo ? 2 : 1;
+  if (use_pair(n, NB)) {
+    const Plan pl = make_plan_pair(n, d, k);
+    if (pl.stages < 2) return fail(SK_EUNSUPPORTED, "sk_dense_right_tc: tile does not fit shared memory");
+    if (pl.ksplit > 1 && (ws == nullptr || ws_bytes < pl.ws_bytes))
+      return fail(SK_EINVAL, "sk_dense_right_tc: workspace too small (sk_dense_tc_workspace_bytes)");
+    CUtensorMap ma, mb;
+    int st = make_a_map(&ma, A, n, d, lda);
+    if (st != SK_OK) return st;
+    st = make_bt_map(&mb, Bt_hi, k, d, ldb, pl.BN / 2);
+    if (st != SK_OK) return st;
+    TcParams p{};
+    p.A = A;
+    p.M = n;
+    p.K = d;
+    p.lda = lda;
+    p.N = (int)k;
+    p.BN = pl.BN;
+    p.nblocks = pl.nblocks;
+    p.ksplit = pl.ksplit;
+    p.kb_per_split = pl.kb_per_split;
+    p.stages = pl.stages;
+    p.astages = 0;
+    p.scale = (float)scale;
+    p.Y = Y;
+    p.ldy = ldy;
+    p.part = static_cast<float*>(ws);
+    p.num_units = pl.units;
+    p.mtiles = pl.mtiles;
+    uint32_t cols = 32;
+    while (cols < (uint32_t)(2 * pl.BN)) cols <<= 1;
+    p.tmem_cols = cols;
+    cudaStream_t s = as_stream(stream);
+    cudaFuncSetAttribute(dense_tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(2 * (sm_count() / 2)));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    // persistent grid = the clusters that can be co-resident (GPCs with an odd SM count leave an
+    // SM without a partner, so this can be below sm_count() / 2)
+    static int max_clusters = 0;
+    if (max_clusters == 0) {
+      int mc = 0;
+      if (cudaOccupancyMaxActiveClusters(&mc, dense_tc_pair_kernel, &cfg) != cudaSuccess || mc < 1) {
+        cudaGetLastError();
+        mc = sm_count() / 2;
+      }
+      max_clusters = mc;
+      if (getenv("SKETCH_B200_TC_PAIR_VERBOSE")) fprintf(stderr, "dense_tc pair: %d co-resident clusters\n", mc);
+    }
+    const int npairs = pl.units < max_clusters ? pl.units : max_clusters;
+    cfg.gridDim = dim3((unsigned)(2 * npairs));
+    if (cudaLaunchKernelEx(&cfg, dense_tc_pair_kernel, ma, mb, p) != cudaSuccess)
+      return check_launch("sk_dense_right_tc(pair)");
+    st = check_launch("sk_dense_right_tc(pair)");
+    if (st != SK_OK || pl.ksplit == 1) return st;
+    const int64_t total = n * k;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 8 * (int64_t)sm_count()) blocks = 8 * (int64_t)sm_count();
+    tc_splitk_reduce<<<(unsigned)blocks, 256, 0, s>>>(p.part, pl.ksplit, n, (int)k, (float)scale, Y, ldy);
+    return check_launch("sk_dense_right_tc(reduce)");
+  }
   const Plan pl = make_plan(n, d, k, NB);
   if (pl.stages < 2) return fail(SK_EUNSUPPORTED, "sk_dense_right_tc: tile does not fit shared memory");
   if (pl.ksplit > 1 && (ws == nullptr || ws_bytes < pl.ws_bytes))
