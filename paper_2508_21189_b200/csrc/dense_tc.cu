@@ -368,14 +368,16 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
+template <int NB>
 __global__ void __launch_bounds__(kThreads, 1)
     dense_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-                         const TcParams p) {
+                         const __grid_constant__ CUtensorMap tm_blo, const TcParams p) {
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_dyn + ((1024u - (sm100::smem_u32(smem_dyn) & 1023u)) & 1023u);
   const uint32_t a_bytes = BM * 128;
   const int bnh2 = p.BN >> 1;                      // B^T rows staged by each CTA
-  const uint32_t stage_bytes = kAStageBytes + (uint32_t)bnh2 * 128;
+  const uint32_t bh_bytes = (uint32_t)bnh2 * 128;
+  const uint32_t stage_bytes = kAStageBytes + NB * bh_bytes;
   const int S = p.stages;
   uint64_t* tma_full = reinterpret_cast<uint64_t*>(smem + (size_t)S * stage_bytes);
   uint64_t* full = tma_full + S;       // leader: converted in both CTAs (8 converter warps)
@@ -400,6 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_mbar_init();
     tma_prefetch_desc(&tm_a);
     tma_prefetch_desc(&tm_b);
+    if (NB == 2) tma_prefetch_desc(&tm_blo);
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sm100::smem_u32(tmem_slot)),
@@ -432,6 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive_expect_tx(&tma_full[s], stage_bytes);
           tma_load_2d(st, &tm_a, &tma_full[s], kb * BK, row0);
           tma_load_2d(st + kAStageBytes, &tm_b, &tma_full[s], kb * BK, brow0);
+          if (NB == 2) tma_load_2d(st + kAStageBytes + bh_bytes, &tm_blo, &tma_full[s], kb * BK, brow0);
           if (++s == S) { s = 0; ph ^= 1; }
         }
       }
@@ -460,6 +464,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t db = sdesc_kmajor_sw128(b + kk * 32);
               umma_bf16_pair(d, sdesc_kmajor_sw128(a_hi + kk * 32), db, idesc, (kb > c0 || kk > 0) ? 1u : 0u);
               umma_bf16_pair(d, sdesc_kmajor_sw128(a_lo + kk * 32), db, idesc, 1u);
+              if (NB == 2)
+                umma_bf16_pair(d, sdesc_kmajor_sw128(a_hi + kk * 32), sdesc_kmajor_sw128(b + bh_bytes + kk * 32), idesc,
+                               1u);
             }
             umma_commit_pair(&empty[s]);
             if (++s == S) { s = 0; ph ^= 1; }
@@ -680,9 +687,9 @@ Plan make_plan(int64_t n, int64_t d, int64_t k, int NB, bool wide_b = false) {
   return pl;
 }
 
-// CTA-pair plan (NB == 1): units = (pair of M tiles, N block, K split), BN <= 256 (TMEM: two
+// CTA-pair plan: units = (pair of M tiles, N block, K split), BN <= 256 (TMEM: two
 // accumulators of BN columns in each CTA), each CTA stages BN/2 rows of B^T per stage.
-Plan make_plan_pair(int64_t n, int64_t d, int64_t k) {
+Plan make_plan_pair(int64_t n, int64_t d, int64_t k, int NB) {
   Plan pl{};
   pl.nblocks = (int)((k + 255) / 256);
   const int64_t per = (k + pl.nblocks - 1) / pl.nblocks;
@@ -697,7 +704,7 @@ Plan make_plan_pair(int64_t n, int64_t d, int64_t k) {
   pl.kb_per_split = (pl.kb_per_split + CHUNK_KB - 1) / CHUNK_KB * CHUNK_KB;
   pl.ksplit = (nk + pl.kb_per_split - 1) / pl.kb_per_split;
   pl.units = tiles * pl.ksplit;
-  const size_t stage_bytes = kAStageBytes + (size_t)(pl.BN / 2) * 128;
+  const size_t stage_bytes = kAStageBytes + (size_t)NB * (pl.BN / 2) * 128;
   const size_t budget = 227 * 1024 - 1024 - 512;
   int stages = (int)(budget / stage_bytes);
   if (stages > 6) stages = 6;
@@ -708,8 +715,8 @@ Plan make_plan_pair(int64_t n, int64_t d, int64_t k) {
   return pl;
 }
 
-bool use_pair(int64_t n, int NB) {
-  if (NB != 1 || n <= BM) return false;
+bool use_pair(int64_t n) {
+  if (n <= BM) return false;
   const char* e = getenv("SKETCH_B200_TC_PAIR");
   return !(e && e[0] == '0');
 }
@@ -722,7 +729,7 @@ extern "C" int sk_dense_tc_supported(int64_t k) { return k >= 1 ? 1 : 0; }
 extern "C" size_t sk_dense_tc_workspace_bytes(int64_t n, int64_t d, int64_t k, int split_b) {
   if (n < 1 || d < 1 || k < 1) return 0;
   const size_t a = skb::make_plan(n, d, k, split_b ? 2 : 1).ws_bytes;
-  const size_t b = skb::use_pair(n, split_b ? 2 : 1) ? skb::make_plan_pair(n, d, k).ws_bytes : 0;
+  const size_t b = skb::use_pair(n) ? skb::make_plan_pair(n, d, k, split_b ? 2 : 1).ws_bytes : 0;
   return a > b ? a : b;
 }
 
@@ -739,16 +746,22 @@ extern "C" int sk_dense_right_tc(const float* A, int64_t n, int64_t d, int64_t l
   if ((reinterpret_cast<uintptr_t>(Bt_hi) & 15) || (ldb & 7) || (Bt_lo && (reinterpret_cast<uintptr_t>(Bt_lo) & 15)))
     return fail(SK_EINVAL, "sk_dense_right_tc: B^T must be 16-byte aligned with ldb a multiple of 8");
   const int NB = Bt_lo ? 2 : 1;
-  if (use_pair(n, NB)) {
-    const Plan pl = make_plan_pair(n, d, k);
+  if (use_pair(n)) {
+    const Plan pl = make_plan_pair(n, d, k, NB);
     if (pl.stages < 2) return fail(SK_EUNSUPPORTED, "sk_dense_right_tc: tile does not fit shared memory");
     if (pl.ksplit > 1 && (ws == nullptr || ws_bytes < pl.ws_bytes))
       return fail(SK_EINVAL, "sk_dense_right_tc: workspace too small (sk_dense_tc_workspace_bytes)");
-    CUtensorMap ma, mb;
+    CUtensorMap ma, mb, mbl;
     int st = make_a_map(&ma, A, n, d, lda);
     if (st != SK_OK) return st;
     st = make_bt_map(&mb, Bt_hi, k, d, ldb, pl.BN / 2);
     if (st != SK_OK) return st;
+    if (NB == 2) {
+      st = make_bt_map(&mbl, Bt_lo, k, d, ldb, pl.BN / 2);
+      if (st != SK_OK) return st;
+    } else {
+      mbl = mb;
+    }
     TcParams p{};
     p.A = A;
     p.M = n;
@@ -771,7 +784,8 @@ extern "C" int sk_dense_right_tc(const float* A, int64_t n, int64_t d, int64_t l
     while (cols < (uint32_t)(2 * pl.BN)) cols <<= 1;
     p.tmem_cols = cols;
     cudaStream_t s = as_stream(stream);
-    cudaFuncSetAttribute(dense_tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    auto kern = NB == 2 ? dense_tc_pair_kernel<2> : dense_tc_pair_kernel<1>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(2 * (sm_count() / 2)));
     cfg.blockDim = dim3(kThreads);
@@ -786,10 +800,11 @@ extern "C" int sk_dense_right_tc(const float* A, int64_t n, int64_t d, int64_t l
     cfg.numAttrs = 1;
     // persistent grid = the clusters that can be co-resident (GPCs with an odd SM count leave an
     // SM without a partner, so this can be below sm_count() / 2)
-    static int max_clusters = 0;
+    static int max_clusters_nb[3] = {0, 0, 0};
+    int& max_clusters = max_clusters_nb[NB];
     if (max_clusters == 0) {
       int mc = 0;
-      if (cudaOccupancyMaxActiveClusters(&mc, dense_tc_pair_kernel, &cfg) != cudaSuccess || mc < 1) {
+      if (cudaOccupancyMaxActiveClusters(&mc, kern, &cfg) != cudaSuccess || mc < 1) {
         cudaGetLastError();
         mc = sm_count() / 2;
       }
@@ -798,7 +813,7 @@ extern "C" int sk_dense_right_tc(const float* A, int64_t n, int64_t d, int64_t l
     }
     const int npairs = pl.units < max_clusters ? pl.units : max_clusters;
     cfg.gridDim = dim3((unsigned)(2 * npairs));
-    if (cudaLaunchKernelEx(&cfg, dense_tc_pair_kernel, ma, mb, p) != cudaSuccess)
+    if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mbl, p) != cudaSuccess)
       return check_launch("sk_dense_right_tc(pair)");
     st = check_launch("sk_dense_right_tc(pair)");
     if (st != SK_OK || pl.ksplit == 1) return st;

@@ -4,5 +4,4 @@ run() { env "$@" python bench.py --config $CFG --others "" --no-cpu --no-sharded
 for CFG in cfg5 cfg3; do
   run SKETCH_B200_TC_PAIR=0
   run SKETCH_B200_TC_PAIR=1
-  run SKETCH_B200_TC_PAIR=1 SKETCH_B200_TC_PAIR_FWD=1
 done
