@@ -97,10 +97,26 @@ def _cfg5(torch, dev, rank):
     g = torch.Generator(device=dev).manual_seed(5000 + rank)
     a = torch.randn(n, d, dtype=torch.float32, device=dev, generator=g)
     return dict(name="cfg5", tm=tm, make=make, a=a, n=n, d=d, k=k, launches=None, kernel="dense_tc (Khatri-Rao Omega^T in bf16)",
+                flops=2.0 * n * d * k, flops_executed_x=2,
                 workload="cfg5 Khatri-Rao sketch: A 16384x65536 f32, ell=2, d0=256, k=512", op="right")
 
 
-WORKLOADS = {"cfg1": _cfg1, "cfg2": _cfg2, "cfg3": _cfg3, "cfg4": _cfg4, "cfg5": _cfg5}
+def _gauss(torch, dev, rank):
+    """Gaussian Omega at the config-3 sketch shape: the dense tcgen05 GEMM kept as the tensor-core
+    reference (north star); Omega's float64 draws split into bf16 hi + lo, A into hi + lo (BF16x3)."""
+    from paper_2508_21189_b200.sketch import GaussianTM
+
+    n, d, k = 131072, 16384, 200
+    make = lambda: GaussianTM(d, k, seed=0)  # noqa: E731
+    tm = make()
+    g = torch.Generator(device=dev).manual_seed(6000 + rank)
+    a = torch.randn(n, d, dtype=torch.float32, device=dev, generator=g)
+    return dict(name="gauss", tm=tm, make=make, a=a, n=n, d=d, k=k, launches=1,
+                kernel="dense_tc_pair_kernel<2> (Gaussian Omega, BF16x3)", flops=2.0 * n * d * k, flops_executed_x=3,
+                workload="Gaussian Y=A*Omega at the cfg3 shape: A 131072x16384 f32, k=200", op="right")
+
+
+WORKLOADS = {"cfg1": _cfg1, "cfg2": _cfg2, "cfg3": _cfg3, "cfg4": _cfg4, "cfg5": _cfg5, "gauss": _gauss}
 
 
 def _apply(w, x):
@@ -463,7 +479,7 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
     ap.add_argument("--config", choices=sorted(WORKLOADS), default="cfg2")
-    ap.add_argument("--others", default="cfg1,cfg3,cfg4,cfg5", help="extra configs measured at N=1 ('' = none)")
+    ap.add_argument("--others", default="cfg1,cfg3,cfg4,cfg5,gauss", help="extra configs measured at N=1 ('' = none)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (quick kernel experiments)")
     ap.add_argument("--no-sharded", action="store_true", help="skip the sharded config-4 SA (NCCL all-reduce) leg")
     args = ap.parse_args(argv)
@@ -502,6 +518,11 @@ def main(argv=None):
             others["cfg4_sharded"] = measure_sharded_sa(torch, world, rank, dev)
         except Exception as exc:  # report, never hide
             others["cfg4_sharded"] = {"error": f"{type(exc).__name__}: {exc}"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            bf16_sust = float(json.load(f)["bf16_tflops_sustained"])
+    except (OSError, KeyError, ValueError):
+        bf16_sust = None
     if world == 1 and args.others:
         for name in [s for s in args.others.split(",") if s and s != args.config]:
             try:
@@ -516,6 +537,12 @@ def main(argv=None):
                                 "omega_setup_ms": om["omega_setup"]["ms"]}
                 if downstream:
                     others[name]["downstream"] = downstream
+                if ow.get("flops"):
+                    tf = ow["flops"] / (om["kernel_ms"] / 1e3) / 1e12
+                    ex = tf * ow["flops_executed_x"]
+                    others[name]["tensor"] = {"useful_tflops": tf, "executed_tflops": ex,
+                                              "executed_frac_of_sustained_bf16": ex / bf16_sust if bf16_sust else None,
+                                              "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"}
                 del ow
                 torch.cuda.empty_cache()
             except Exception as exc:  # report, never hide
