@@ -139,3 +139,23 @@ def test_truncated_pinv_qr_path(cuda):
     r = int((s > rand_nla.DEFAULT_RANK_TOL * s[0]).sum())
     ref2 = vh[:r].T @ ((u[:, :r].T @ b) / s[:r, None])
     assert float((rand_nla.truncated_pinv_apply(m2, b) - ref2).norm() / ref2.norm()) <= 1e-10
+
+
+@pytest.mark.parametrize("cond", [4e4, 1e9])
+def test_svd_wide_matches_direct_svd(cond, cuda):
+    """rsvd's SVD of B = Q^* A (200 x 16384): CholeskyQR2 + k x k SVD when B is well conditioned,
+    the direct SVD otherwise; singular values to 1e-12 relative and B reconstructed to 1e-12."""
+    import torch
+
+    k, d = 200, 16384
+    g = torch.Generator(device=cuda).manual_seed(1)
+    u0, _ = torch.linalg.qr(torch.randn(d, k, dtype=torch.float64, device=cuda, generator=g))
+    w0, _ = torch.linalg.qr(torch.randn(k, k, dtype=torch.float64, device=cuda, generator=g))
+    s0 = torch.logspace(0, -np.log10(cond), k, dtype=torch.float64, device=cuda)
+    b = (w0 * s0) @ u0.T
+    u, s, vh = rand_nla._svd_wide(b)
+    s_ref = torch.linalg.svdvals(b)
+    assert float(((s - s_ref).abs() / s_ref).max()) <= 1e-9 * (cond / 4e4 if cond > 4e4 else 1.0)
+    assert float(torch.linalg.norm((u * s) @ vh - b) / torch.linalg.norm(b)) <= 1e-12
+    eye = torch.eye(k, dtype=torch.float64, device=cuda)
+    assert float(torch.linalg.norm(u.T @ u - eye)) <= 1e-11 and float(torch.linalg.norm(vh @ vh.T - eye)) <= 1e-11
