@@ -171,7 +171,10 @@ def _cholqr2_qr(m, max_spread: float = 1e6):
         d = r.diagonal()
         if float(d.min()) <= 0.0 or float(d.max()) > max_spread * float(d.min()):
             return None
-        q = torch.linalg.solve_triangular(r, q, upper=True, left=False)
+        # Q R^-1 as one GEMM with the explicit k x k inverse (cuBLAS trsm on a tall Q is ~3x slower:
+        # 1.26 vs 0.41 + 0.12 ms at 131072 x 200); the second pass restores orthogonality to ~eps
+        eye = torch.eye(r.shape[0], dtype=r.dtype, device=r.device)
+        q = q @ torch.linalg.solve_triangular(r, eye, upper=True)
         r_tot = r if r_tot is None else r @ r_tot
     diag = r_tot.diagonal().abs()
     if float(diag.min()) <= DEFAULT_RANK_TOL * float(diag.max()):
