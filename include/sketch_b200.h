@@ -211,6 +211,16 @@ SK_API int sk_gemv_f32_f64(const float* A, int64_t n, int64_t d, int64_t lda, co
 SK_API size_t sk_gemv_t_f32_f64_workspace_bytes(int64_t n, int64_t d);
 SK_API int sk_gemv_t_f32_f64(const float* A, int64_t n, int64_t d, int64_t lda, const double* u, double* z,
                              double* ws, size_t ws_bytes, void* stream);
+/*
+ * One LSQR bidiagonalisation step in a single pass over float32 A (d = 128 q <= 512, 16-byte
+ * aligned, lda % 4 == 0): u <- A v - alpha u in place, zb[0:d] = A^T u_new and zb[d] = ||u_new||^2
+ * (float64, deterministic). The LSQR iteration of sketch-and-precondition (new in this repository:
+ * the reference has only sketch_and_solve, rand_nla.py:278-297) otherwise reads A twice.
+ * Workspace: sk_lsqr_step_f32_f64_workspace_bytes(n, d) bytes.
+ */
+SK_API size_t sk_lsqr_step_f32_f64_workspace_bytes(int64_t n, int64_t d);
+SK_API int sk_lsqr_step_f32_f64(const float* A, int64_t n, int64_t d, int64_t lda, const double* v, double alpha,
+                                double* u, double* zb, double* ws, size_t ws_bytes, void* stream);
 
 /*
  * K-TC — Y[n,k] = scale * A[n,d] * B[d,k] on the tcgen05 tensor cores, float32 A split in-kernel

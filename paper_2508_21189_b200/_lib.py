@@ -71,6 +71,8 @@ SIGNATURES = {
     "sk_gemv_f32_f64": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p]),
     "sk_gemv_t_f32_f64_workspace_bytes": (_c_size, [_c_i64, _c_i64]),
     "sk_gemv_t_f32_f64": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_size, _c_p]),
+    "sk_lsqr_step_f32_f64_workspace_bytes": (_c_size, [_c_i64, _c_i64]),
+    "sk_lsqr_step_f32_f64": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_dbl, _c_p, _c_p, _c_p, _c_size, _c_p]),
     "sk_dense_tc_supported": (_c_int, [_c_i64]),
     "sk_dense_tc_workspace_bytes": (_c_size, [_c_i64, _c_i64, _c_i64, _c_int]),
     "sk_dense_right_tc": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_i64, _c_dbl, _c_p, _c_i64,

@@ -5,6 +5,8 @@
 //   sk_gemv_f32_f64   : y = A v            (warp per row, v in shared memory)
 //   sk_gemv_t_f32_f64 : z = A^T u          (thread per column over a row range, ordered float64
 //                                           reduction of the per-range partials: deterministic)
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace skb {
@@ -193,8 +195,252 @@ int t_splits(int64_t n, int64_t d) {
   return (int)s;
 }
 
+// One LSQR bidiagonalisation step in one pass over A (d = 128 * NQ):
+//   u[r] <- (A v)[r] - alpha * u[r]   (written back),   part[split] = (A^T u_new, ||u_new||^2)
+// Row r's update only needs row r of A, so the row that formed (A v)[r] is still in registers when
+// u_new[r] * A[r, :] is added to the lane's column partials: both products of an LSQR iteration
+// for one read of A (the two-kernel form reads it twice). Warps walk fixed row sets of the CTA's
+// row range, then the CTA sums its 8 warps in a fixed order (deterministic with reduce_splits).
+template <int NQ>
+__global__ void __launch_bounds__(GV_THREADS)
+    lsqr_step_rows(const float* __restrict__ A, int64_t n, int64_t lda, const double* __restrict__ v, double alpha,
+                   double* __restrict__ u, int64_t rows_per_split, double* __restrict__ part, int64_t dp) {
+  __shared__ double red[GV_THREADS / 32][4 * NQ * 32 + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double vr[NQ][4], zr[NQ][4];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      vr[q][c] = v[128 * q + 4 * lane + c];
+      zr[q][c] = 0.0;
+    }
+  double b2 = 0.0;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_split;
+  const int64_t r1 = min(n, r0 + rows_per_split);
+  constexpr int W = GV_THREADS / 32;
+  for (int64_t r = r0 + warp; r < r1; r += 2 * W) {
+    const int64_t r2 = r + W;
+    const bool two = r2 < r1;
+    float4 x[NQ], x2[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      x[q] = __ldg(reinterpret_cast<const float4*>(A + r * lda + 128 * q + 4 * lane));
+      x2[q] = two ? __ldg(reinterpret_cast<const float4*>(A + r2 * lda + 128 * q + 4 * lane)) : make_float4(0, 0, 0, 0);
+    }
+    const double ua = u[r], ub = two ? u[r2] : 0.0;
+    double xa[NQ][4], xb[NQ][4];
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      xa[q][0] = x[q].x; xa[q][1] = x[q].y; xa[q][2] = x[q].z; xa[q][3] = x[q].w;
+      xb[q][0] = x2[q].x; xb[q][1] = x2[q].y; xb[q][2] = x2[q].z; xb[q][3] = x2[q].w;
+      a0 = fma(xa[q][0], vr[q][0], a0);
+      a1 = fma(xa[q][1], vr[q][1], a1);
+      a0 = fma(xa[q][2], vr[q][2], a0);
+      a1 = fma(xa[q][3], vr[q][3], a1);
+      b0 = fma(xb[q][0], vr[q][0], b0);
+      b1 = fma(xb[q][1], vr[q][1], b1);
+      b0 = fma(xb[q][2], vr[q][2], b0);
+      b1 = fma(xb[q][3], vr[q][3], b1);
+    }
+    double sa = a0 + a1, sb = b0 + b1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      sa += __shfl_xor_sync(0xffffffffu, sa, o);
+      sb += __shfl_xor_sync(0xffffffffu, sb, o);
+    }
+    const double na = sa - alpha * ua, nb = two ? sb - alpha * ub : 0.0;
+    if (lane == 0) {
+      u[r] = na;
+      if (two) u[r2] = nb;
+      b2 = fma(na, na, b2);
+      b2 = fma(nb, nb, b2);
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) zr[q][c] = fma(nb, xb[q][c], fma(na, xa[q][c], zr[q][c]));
+  }
+  // CTA partial: warps in a fixed order
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) red[warp][128 * q + 4 * lane + c] = zr[q][c];
+  if (lane == 0) red[warp][4 * NQ * 32] = b2;
+  __syncthreads();
+  double* out = part + (int64_t)blockIdx.x * dp;
+  for (int c = threadIdx.x; c <= 4 * NQ * 32; c += GV_THREADS) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) s += red[w][c];
+    out[c] = s;
+  }
+}
+
+// Same step with the rows fed through a per-warp ring of bulk copies (cp.async.bulk, LS_SLOTS rows
+// in flight per warp, no registers held by loads in flight): 2 CTAs per SM at <= 128 registers.
+constexpr int LS_SLOTS = 4;
+template <int NQ>
+__global__ void __launch_bounds__(GV_THREADS, 2)
+    lsqr_step_ring(const float* __restrict__ A, int64_t n, int64_t lda, const double* __restrict__ v, double alpha,
+                   double* __restrict__ u, int64_t rows_per_split, double* __restrict__ part, int64_t dp) {
+  constexpr int W = GV_THREADS / 32;
+  constexpr uint32_t ROWB = 512u * NQ;  // bytes of one row (d = 128 NQ floats)
+  extern __shared__ __align__(128) unsigned char ls_smem[];
+  double* red = reinterpret_cast<double*>(ls_smem);  // reused after the row loop: [W][4 NQ 32 + 1]
+  unsigned char* ring = ls_smem;
+  __shared__ __align__(8) uint64_t bars[W][LS_SLOTS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_split;
+  const int64_t r1 = min(n, r0 + rows_per_split);
+  const int64_t nmine = r1 - r0 > warp ? (r1 - r0 - warp + W - 1) / W : 0;  // rows r0 + warp + W i
+  unsigned char* wring = ring + (size_t)warp * LS_SLOTS * ROWB;
+  const uint32_t wring_s = (uint32_t)__cvta_generic_to_shared(wring);
+  if (lane == 0) {
+    for (int s = 0; s < LS_SLOTS; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&bars[warp][s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  auto issue = [&](int64_t i) {  // row i of this warp into slot i % LS_SLOTS
+    const int s = (int)(i % LS_SLOTS);
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&bars[warp][s]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(ROWB) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     wring_s + (uint32_t)s * ROWB),
+                 "l"(A + (r0 + warp + (int64_t)W * i) * lda), "r"(ROWB), "r"(bar)
+                 : "memory");
+  };
+  if (lane == 0)
+    for (int64_t i = 0; i < nmine && i < LS_SLOTS; ++i) issue(i);
+  double vr[NQ][4], zr[NQ][4];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      vr[q][c] = v[128 * q + 4 * lane + c];
+      zr[q][c] = 0.0;
+    }
+  double b2 = 0.0;
+  for (int64_t i = 0; i < nmine; ++i) {
+    const int s = (int)(i % LS_SLOTS);
+    const uint32_t par = (uint32_t)((i / LS_SLOTS) & 1);
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&bars[warp][s]);
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tLSW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra LSW_%=;\n\t}" ::"r"(bar),
+        "r"(par)
+        : "memory");
+    const int64_t r = r0 + warp + (int64_t)W * i;
+    const double ur = u[r];
+    double x[NQ][4];
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      float4 f;
+      asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(f.x), "=f"(f.y), "=f"(f.z), "=f"(f.w)
+                   : "r"(wring_s + (uint32_t)s * ROWB + 512u * q + 16u * lane));
+      x[q][0] = f.x; x[q][1] = f.y; x[q][2] = f.z; x[q][3] = f.w;
+      a0 = fma(x[q][0], vr[q][0], a0);
+      a1 = fma(x[q][1], vr[q][1], a1);
+      a0 = fma(x[q][2], vr[q][2], a0);
+      a1 = fma(x[q][3], vr[q][3], a1);
+    }
+    double sa = a0 + a1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    // every lane's shared reads of slot s are complete (their values fed the reduction): refill it
+    if (lane == 0 && i + LS_SLOTS < nmine) issue(i + LS_SLOTS);
+    const double na = sa - alpha * ur;
+    if (lane == 0) {
+      u[r] = na;
+      b2 = fma(na, na, b2);
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) zr[q][c] = fma(na, x[q][c], zr[q][c]);
+  }
+  __syncthreads();  // all rings drained before the buffer is reused for the reduction
+  constexpr int RS = 4 * NQ * 32 + 1;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) red[warp * RS + 128 * q + 4 * lane + c] = zr[q][c];
+  if (lane == 0) red[warp * RS + 4 * NQ * 32] = b2;
+  __syncthreads();
+  double* out = part + (int64_t)blockIdx.x * dp;
+  for (int c = threadIdx.x; c < RS; c += GV_THREADS) {
+    double acc = 0.0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) acc += red[w * RS + c];
+    out[c] = acc;
+  }
+}
+
+int lsqr_splits(int64_t n) {
+  int64_t s = 4 * (int64_t)sm_count();  // one resident wave of 256-thread CTAs
+  if (s > n) s = n;
+  return (int)(s < 1 ? 1 : s);
+}
+
 }  // namespace
 }  // namespace skb
+
+extern "C" size_t sk_lsqr_step_f32_f64_workspace_bytes(int64_t n, int64_t d) {
+  if (n < 1 || d < 1) return 0;
+  return (size_t)skb::lsqr_splits(n) * (size_t)(d + 1) * sizeof(double);
+}
+
+// u <- A v - alpha u (in place); zb[0:d] = A^T u_new, zb[d] = ||u_new||^2 (float64, deterministic)
+extern "C" int sk_lsqr_step_f32_f64(const float* A, int64_t n, int64_t d, int64_t lda, const double* v, double alpha,
+                                    double* u, double* zb, double* ws, size_t ws_bytes, void* stream) {
+  using namespace skb;
+  if (n < 1 || d < 1 || lda < d) return fail(SK_EINVAL, "sk_lsqr_step_f32_f64: bad shape");
+  if (!A || !v || !u || !zb) return fail(SK_EINVAL, "sk_lsqr_step_f32_f64: null pointer");
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (lda % 4) || d % 128 || d > 512)
+    return fail(SK_EUNSUPPORTED, "sk_lsqr_step_f32_f64: needs 16-byte aligned A, lda % 4 == 0, d = 128 q <= 512");
+  const int nsplit = lsqr_splits(n);
+  if (!ws || ws_bytes < (size_t)nsplit * (size_t)(d + 1) * sizeof(double))
+    return fail(SK_EINVAL, "sk_lsqr_step_f32_f64: workspace too small");
+  const int64_t rps = (n + nsplit - 1) / nsplit;
+  cudaStream_t s = as_stream(stream);
+  const char* ev = getenv("SKETCH_B200_LSQR_RING");
+  if (!(ev && ev[0] == '0')) {
+    const size_t smem = (size_t)(GV_THREADS / 32) * LS_SLOTS * 512 * (d / 128);
+    int st = SK_OK;
+    switch (d / 128) {
+#define LS_CASE(Q)                                                                                             \
+  case Q:                                                                                                      \
+    cudaFuncSetAttribute(lsqr_step_ring<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
+    lsqr_step_ring<Q><<<(unsigned)nsplit, GV_THREADS, smem, s>>>(A, n, lda, v, alpha, u, rps, ws, d + 1);     \
+    break;
+      LS_CASE(1)
+      LS_CASE(2)
+      LS_CASE(3)
+      default:
+        LS_CASE(4)
+#undef LS_CASE
+    }
+    st = check_launch("sk_lsqr_step_f32_f64");
+    if (st != SK_OK) return st;
+    reduce_splits<<<(unsigned)((d + 1 + 31) / 32), RS_WARPS * 32, 0, s>>>(ws, nsplit, d + 1, zb);
+    return check_launch("sk_lsqr_step_f32_f64(reduce)");
+  }
+  switch (d / 128) {
+    case 1: lsqr_step_rows<1><<<(unsigned)nsplit, GV_THREADS, 0, s>>>(A, n, lda, v, alpha, u, rps, ws, d + 1); break;
+    case 2: lsqr_step_rows<2><<<(unsigned)nsplit, GV_THREADS, 0, s>>>(A, n, lda, v, alpha, u, rps, ws, d + 1); break;
+    case 3: lsqr_step_rows<3><<<(unsigned)nsplit, GV_THREADS, 0, s>>>(A, n, lda, v, alpha, u, rps, ws, d + 1); break;
+    default: lsqr_step_rows<4><<<(unsigned)nsplit, GV_THREADS, 0, s>>>(A, n, lda, v, alpha, u, rps, ws, d + 1); break;
+  }
+  int st = check_launch("sk_lsqr_step_f32_f64");
+  if (st != SK_OK) return st;
+  reduce_splits<<<(unsigned)((d + 1 + 31) / 32), RS_WARPS * 32, 0, s>>>(ws, nsplit, d + 1, zb);
+  return check_launch("sk_lsqr_step_f32_f64(reduce)");
+}
 
 extern "C" int sk_gemv_f32_f64(const float* A, int64_t n, int64_t d, int64_t lda, const double* v, double* y,
                                void* stream) {

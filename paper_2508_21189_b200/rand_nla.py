@@ -18,6 +18,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 
 from ._device import require_cuda, to_operand
@@ -614,6 +616,33 @@ def _matvec_blocks(A, v, block_rows):
     return out
 
 
+def _lsqr_fused_ok(A):
+    import torch
+
+    return (A.is_cuda and A.dtype == torch.float32 and A.stride(1) == 1 and A.shape[1] % 128 == 0
+            and A.shape[1] <= 512 and A.stride(0) % 4 == 0 and A.data_ptr() % 16 == 0 and A.shape[0] > 0)
+
+
+def _lsqr_step(A, v, alpha, u):
+    """u <- A v - alpha u (in place) and [A^T u_new, ||u_new||^2] in one pass over float32 A
+    (sk_lsqr_step_f32_f64): the fused bidiagonalisation step of sketch_precondition_lsqr."""
+    import torch
+
+    from . import _lib
+
+    n, d = A.shape
+    v = v.to(torch.float64).contiguous()
+    zb = torch.empty(d + 1, dtype=torch.float64, device=A.device)
+    lib = _lib.load()
+    ws_bytes = lib.sk_lsqr_step_f32_f64_workspace_bytes(n, d)
+    ws = torch.empty(max(ws_bytes, 8) // 8, dtype=torch.float64, device=A.device)
+    with torch.cuda.device(A.device):
+        st = lib.sk_lsqr_step_f32_f64(A.data_ptr(), n, d, A.stride(0), v.data_ptr(), float(alpha), u.data_ptr(),
+                                      zb.data_ptr(), ws.data_ptr(), ws_bytes, torch.cuda.current_stream().cuda_stream)
+    _lib.check(st, "sk_lsqr_step_f32_f64")
+    return zb
+
+
 def _rmatvec_blocks(A, u, block_rows):
     """A^T @ u in float64 (sk_gemv_t_f32_f64 for float32 A: one pass, ordered float64 reduction)."""
     import torch
@@ -708,17 +737,34 @@ def sketch_precondition_lsqr(a, b, tm_psi, *, atol: float = 1e-6, btol: float = 
     r1norm, arnorm = beta, alpha * beta
     if arnorm == 0:
         return LsqrResult(_back(rinv(x), kind), 0, 0, r1norm, 0.0, 0.0, t_sketch)
+    # float32 A with d = 128 q <= 512: u <- A R^-1 v - alpha u, A^T u and ||u||^2 in one pass over A
+    # (sk_lsqr_step_f32_f64), one all-reduce of [A^T u, ||u||^2] per iteration when distributed
+    fused = _lsqr_fused_ok(A) and os.environ.get("SKETCH_B200_LSQR_FUSED", "1") != "0"
+    if fused:
+        u = u.contiguous()
     while itn < iter_lim:
         itn += 1
-        u = mv(v) - alpha * u
-        beta = norm(u)
-        if beta > 0:
-            u /= beta
-            anorm2 += alpha * alpha + beta * beta
-            v = rmv(u) - beta * v
-            alpha = float(torch.linalg.norm(v))
-            if alpha > 0:
-                v /= alpha
+        if fused:
+            zb = _lsqr_step(A, rinv(v), alpha, u)
+            red(zb)
+            beta = float(zb[d].sqrt())
+            if beta > 0:
+                u /= beta
+                anorm2 += alpha * alpha + beta * beta
+                v = rinvt(zb[:d]) / beta - beta * v
+                alpha = float(torch.linalg.norm(v))
+                if alpha > 0:
+                    v /= alpha
+        else:
+            u = mv(v) - alpha * u
+            beta = norm(u)
+            if beta > 0:
+                u /= beta
+                anorm2 += alpha * alpha + beta * beta
+                v = rmv(u) - beta * v
+                alpha = float(torch.linalg.norm(v))
+                if alpha > 0:
+                    v /= alpha
         rho = float(np.hypot(rhobar, beta))
         cs, sn = rhobar / rho, beta / rho
         theta = sn * alpha

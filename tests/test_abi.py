@@ -63,4 +63,6 @@ def test_argument_checks_without_device():
     assert lib.sk_dense_tn_tc(None, 8, 4, 4, None, None, 8, 3, 1.0, None, 3, None, 0, None) == E
     assert lib.sk_gemv_f32_f64(None, 4, 0, 0, None, None, None) == E
     assert lib.sk_gemv_t_f32_f64(None, 4, 4, 2, None, None, None, 0, None) == E
+    assert lib.sk_lsqr_step_f32_f64(None, 4, 128, 128, None, 0.0, None, None, None, 0, None) == E
+    assert lib.sk_lsqr_step_f32_f64_workspace_bytes(0, 128) == 0
     assert lib.sk_philox_u32(None, None, 0, 8, None, None) == E

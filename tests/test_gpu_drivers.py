@@ -159,3 +159,47 @@ def test_svd_wide_matches_direct_svd(cond, cuda):
     assert float(torch.linalg.norm((u * s) @ vh - b) / torch.linalg.norm(b)) <= 1e-12
     eye = torch.eye(k, dtype=torch.float64, device=cuda)
     assert float(torch.linalg.norm(u.T @ u - eye)) <= 1e-11 and float(torch.linalg.norm(vh @ vh.T - eye)) <= 1e-11
+
+
+@pytest.mark.parametrize("n,d", [(100000, 512), (3001, 128), (7, 384), (70001, 256)])
+def test_lsqr_fused_step(n, d, cuda):
+    """One-pass LSQR step: u <- A v - alpha u, [A^T u_new, ||u_new||^2] against float64 torch."""
+    import torch
+
+    from paper_2508_21189_b200.rand_nla import _lsqr_fused_ok, _lsqr_step
+
+    g = torch.Generator(device=cuda).manual_seed(n + d)
+    a = torch.randn(n, d, device=cuda, generator=g)
+    assert _lsqr_fused_ok(a)
+    v = torch.randn(d, dtype=torch.float64, device=cuda, generator=g)
+    u = torch.randn(n, dtype=torch.float64, device=cuda, generator=g)
+    alpha = 0.37
+    a64 = a.double()
+    u_ref = a64 @ v - alpha * u
+    zb = _lsqr_step(a, v, alpha, u)
+    assert float((u - u_ref).norm() / u_ref.norm()) <= 1e-14
+    z_ref = a64.T @ u_ref
+    assert float((zb[:d] - z_ref).norm() / z_ref.norm()) <= 1e-13
+    assert abs(float(zb[d]) - float(u_ref @ u_ref)) <= 1e-13 * float(u_ref @ u_ref)
+    zb2 = _lsqr_step(a, v, alpha, u_ref.clone())  # deterministic: same inputs, same bits
+    zb3 = _lsqr_step(a, v, alpha, u_ref.clone())
+    assert torch.equal(zb2, zb3)
+
+
+def test_lsqr_fused_matches_two_pass(cuda, monkeypatch):
+    """float32 A, d = 256: the fused iteration and the two-kernel iteration reach the same solution."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    n, d = 200000, 256
+    w = 1.0 + rng.pareto(1.5, size=n)
+    a = torch.from_numpy((rng.standard_normal((n, d)) * w[:, None]).astype(np.float32)).to(cuda)
+    x0 = rng.standard_normal(d)
+    b = (a.double() @ torch.from_numpy(x0).to(cuda) + 1e-3 * torch.randn(n, dtype=torch.float64, device=cuda)).float()
+    tm = skb.SparseUniformTM(n, 1024, 8, seed=5)
+    r1 = rand_nla.sketch_precondition_lsqr(a, b, tm, atol=1e-10, btol=0.0)
+    monkeypatch.setenv("SKETCH_B200_LSQR_FUSED", "0")
+    r2 = rand_nla.sketch_precondition_lsqr(a, b, tm, atol=1e-10, btol=0.0)
+    x1, x2 = np.asarray(r1.x.cpu() if hasattr(r1.x, "cpu") else r1.x), np.asarray(r2.x.cpu() if hasattr(r2.x, "cpu") else r2.x)
+    assert r1.itn == r2.itn or abs(r1.itn - r2.itn) <= 2
+    assert np.linalg.norm(x1 - x2) <= 1e-8 * np.linalg.norm(x2)
