@@ -368,7 +368,7 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
-template <int NB>
+template <int NB, bool TA>
 __global__ void __launch_bounds__(kThreads, 1)
     dense_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                          const __grid_constant__ CUtensorMap tm_blo, const TcParams p) {
@@ -433,7 +433,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + (size_t)s * stage_bytes;
           mbar_arrive_expect_tx(&tma_full[s], stage_bytes);
-          tma_load_2d(st, &tm_a, &tma_full[s], kb * BK, row0);
+          if (TA) tma_load_2d(st, &tm_a, &tma_full[s], row0, kb * BK);
+          else tma_load_2d(st, &tm_a, &tma_full[s], kb * BK, row0);
           tma_load_2d(st + kAStageBytes, &tm_b, &tma_full[s], kb * BK, brow0);
           if (NB == 2) tma_load_2d(st + kAStageBytes + bh_bytes, &tm_blo, &tma_full[s], kb * BK, brow0);
           if (++s == S) { s = 0; ph ^= 1; }
@@ -487,6 +488,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Unit w = unit_of(p, u);
       const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
       for (int kb = kb0; kb < kb1; ++kb) {
+        if constexpr (TA) {  // transpose while splitting (as dense_tc_kernel<NB, true>)
+          mbar_wait(&tma_full[s], ph);
+          const uint32_t st = sm100::smem_u32(smem + (size_t)s * stage_bytes);
+          float col[BK];
+#pragma unroll
+          for (int i = 0; i < BK; ++i) col[i] = lds32f(st + (uint32_t)(i * BM + ct) * 4u);
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+          for (int g = 0; g < BK / 8; ++g) {
+            uint32_t h[4], l[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float x0 = col[8 * g + 2 * q], x1 = col[8 * g + 2 * q + 1];
+              h[q] = cvt_bf16x2(x1, x0);
+              l[q] = cvt_bf16x2(x1 - __uint_as_float(h[q] & 0xffff0000u), x0 - __uint_as_float(h[q] << 16));
+            }
+            const uint32_t off = (uint32_t)ct * 128u + ((((uint32_t)g) ^ ((uint32_t)ct & 7u)) << 4);
+            sts128u(st + off, h[0], h[1], h[2], h[3]);
+            sts128u(st + a_bytes + off, l[0], l[1], l[2], l[3]);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote(full_leader + 8u * (uint32_t)s);
+          if (++s == S) { s = 0; ph ^= 1; }
+          continue;
+        }
         float4 cur[16];
         mbar_wait(&tma_full[s], ph);
         const uint32_t st = sm100::smem_u32(smem + (size_t)s * stage_bytes);
@@ -721,6 +748,43 @@ bool use_pair(int64_t n) {
   return !(e && e[0] == '0');
 }
 
+// launch the CTA-pair engine: a persistent grid of the co-resident 2-CTA clusters
+int launch_pair(int NB, bool TA, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mbl, TcParams& p,
+                size_t smem, cudaStream_t s) {
+  using KernT = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams);
+  KernT kern = TA ? (NB == 2 ? dense_tc_pair_kernel<2, true> : dense_tc_pair_kernel<1, true>)
+                  : (NB == 2 ? dense_tc_pair_kernel<2, false> : dense_tc_pair_kernel<1, false>);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(2 * (sm_count() / 2)));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // persistent grid = the clusters that can be co-resident (GPCs with an odd SM count leave an
+  // SM without a partner, so this can be below sm_count() / 2)
+  static int max_clusters_v[4] = {0, 0, 0, 0};
+  int& max_clusters = max_clusters_v[(NB - 1) + 2 * (TA ? 1 : 0)];
+  if (max_clusters == 0) {
+    int mc = 0;
+    if (cudaOccupancyMaxActiveClusters(&mc, kern, &cfg) != cudaSuccess || mc < 1) {
+      cudaGetLastError();
+      mc = sm_count() / 2;
+    }
+    max_clusters = mc;
+    if (getenv("SKETCH_B200_TC_PAIR_VERBOSE")) fprintf(stderr, "dense_tc pair: %d co-resident clusters\n", mc);
+  }
+  const int npairs = p.num_units < max_clusters ? p.num_units : max_clusters;
+  cfg.gridDim = dim3((unsigned)(2 * npairs));
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb, mbl, p) == cudaSuccess ? SK_OK : SK_ECUDA;
+}
+
 }  // namespace
 }  // namespace skb
 
@@ -784,37 +848,7 @@ extern "C" int sk_dense_right_tc(const float* A, int64_t n, int64_t d, int64_t l
     while (cols < (uint32_t)(2 * pl.BN)) cols <<= 1;
     p.tmem_cols = cols;
     cudaStream_t s = as_stream(stream);
-    auto kern = NB == 2 ? dense_tc_pair_kernel<2> : dense_tc_pair_kernel<1>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)(2 * (sm_count() / 2)));
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = pl.smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    // persistent grid = the clusters that can be co-resident (GPCs with an odd SM count leave an
-    // SM without a partner, so this can be below sm_count() / 2)
-    static int max_clusters_nb[3] = {0, 0, 0};
-    int& max_clusters = max_clusters_nb[NB];
-    if (max_clusters == 0) {
-      int mc = 0;
-      if (cudaOccupancyMaxActiveClusters(&mc, kern, &cfg) != cudaSuccess || mc < 1) {
-        cudaGetLastError();
-        mc = sm_count() / 2;
-      }
-      max_clusters = mc;
-      if (getenv("SKETCH_B200_TC_PAIR_VERBOSE")) fprintf(stderr, "dense_tc pair: %d co-resident clusters\n", mc);
-    }
-    const int npairs = pl.units < max_clusters ? pl.units : max_clusters;
-    cfg.gridDim = dim3((unsigned)(2 * npairs));
-    if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mbl, p) != cudaSuccess)
-      return check_launch("sk_dense_right_tc(pair)");
+    if (launch_pair(NB, false, ma, mb, mbl, p, pl.smem, s) != SK_OK) return check_launch("sk_dense_right_tc(pair)");
     st = check_launch("sk_dense_right_tc(pair)");
     if (st != SK_OK || pl.ksplit == 1) return st;
     const int64_t total = n * k;
@@ -879,7 +913,9 @@ extern "C" int sk_dense_right_tc(const float* A, int64_t n, int64_t d, int64_t l
 
 extern "C" size_t sk_dense_tn_tc_workspace_bytes(int64_t n, int64_t d, int64_t k) {
   if (n < 1 || d < 1 || k < 1) return 0;
-  return skb::make_plan(d, n, k, 2, true).ws_bytes;
+  const size_t a = skb::make_plan(d, n, k, 2, true).ws_bytes;
+  const size_t b = skb::use_pair(d) ? skb::make_plan_pair(d, n, k, 2).ws_bytes : 0;
+  return a > b ? a : b;
 }
 
 // Y[d, k] = scale * A^T W  for A [n rows][d cols] fp32 and W [n][k] given as W^T = Wt (k rows of n,
@@ -895,6 +931,49 @@ extern "C" int sk_dense_tn_tc(const float* A, int64_t n, int64_t d, int64_t lda,
     return fail(SK_EINVAL, "sk_dense_tn_tc: A must be 16-byte aligned with lda, d multiples of 4");
   if ((reinterpret_cast<uintptr_t>(Wt_hi) & 15) || (reinterpret_cast<uintptr_t>(Wt_lo) & 15) || (ldw & 7))
     return fail(SK_EINVAL, "sk_dense_tn_tc: W^T must be 16-byte aligned with ldw a multiple of 8");
+  if (use_pair(d)) {  // CTA pairs (cta_group::2), B^T split by N between the pair
+    const Plan pl = make_plan_pair(d, n, k, 2);
+    if (pl.stages < 2) return fail(SK_EUNSUPPORTED, "sk_dense_tn_tc: tile does not fit shared memory");
+    if (pl.ksplit > 1 && (ws == nullptr || ws_bytes < pl.ws_bytes))
+      return fail(SK_EINVAL, "sk_dense_tn_tc: workspace too small (sk_dense_tn_tc_workspace_bytes)");
+    CUtensorMap ma, mh, ml;
+    int st = make_at_map(&ma, A, d, n, lda);
+    if (st != SK_OK) return st;
+    st = make_bt_map(&mh, Wt_hi, k, n, ldw, pl.BN / 2);
+    if (st != SK_OK) return st;
+    st = make_bt_map(&ml, Wt_lo, k, n, ldw, pl.BN / 2);
+    if (st != SK_OK) return st;
+    TcParams p{};
+    p.A = A;
+    p.M = d;
+    p.K = n;
+    p.lda = lda;
+    p.N = (int)k;
+    p.BN = pl.BN;
+    p.nblocks = pl.nblocks;
+    p.ksplit = pl.ksplit;
+    p.kb_per_split = pl.kb_per_split;
+    p.stages = pl.stages;
+    p.astages = 0;
+    p.scale = (float)scale;
+    p.Y = Y;
+    p.ldy = ldy;
+    p.part = static_cast<float*>(ws);
+    p.num_units = pl.units;
+    p.mtiles = pl.mtiles;
+    uint32_t cols = 32;
+    while (cols < (uint32_t)(2 * pl.BN)) cols <<= 1;
+    p.tmem_cols = cols;
+    cudaStream_t s = as_stream(stream);
+    if (launch_pair(2, true, ma, mh, ml, p, pl.smem, s) != SK_OK) return check_launch("sk_dense_tn_tc(pair)");
+    st = check_launch("sk_dense_tn_tc(pair)");
+    if (st != SK_OK || pl.ksplit == 1) return st;
+    const int64_t total = d * k;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 8 * (int64_t)sm_count()) blocks = 8 * (int64_t)sm_count();
+    tc_splitk_reduce<<<(unsigned)blocks, 256, 0, s>>>(p.part, pl.ksplit, d, (int)k, (float)scale, Y, ldy);
+    return check_launch("sk_dense_tn_tc(reduce)");
+  }
   const Plan pl = make_plan(d, n, k, 2, true);
   if (pl.stages < 2) return fail(SK_EUNSUPPORTED, "sk_dense_tn_tc: tile does not fit shared memory");
   if (pl.ksplit > 1 && (ws == nullptr || ws_bytes < pl.ws_bytes))
