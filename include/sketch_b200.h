@@ -24,7 +24,10 @@
  *   ent[ptr[h*k + c] .. ptr[h*k + c + 1]) are uint16 values (local_row << 1) | negative,
  *   ascending in local_row.  Values are +-1; the 1/sqrt(zeta) magnitude is `scale`.
  *   srtt sampler (SparseColTM, src/sketch/sparse.py:308-320): samp[c*xi + x] = row | (neg << 31).
- *   kr sign bits: bit (p*k + j) of f_neg is 1 where factor[p, j] == -1 (src/sketch/khatri_rao.py:46-59).
+ *   Khatri-Rao (src/sketch/khatri_rao.py:101-164) is passed as its factors, never as Omega: with
+ *   d = P * dl (the trailing factors span q < dl, the leading ones P), F = the Khatri-Rao product of
+ *   the trailing factors (dl x k) and W = that of the leading ones (P x k, all ones for one factor),
+ *   Omega[P*dl + q, j] = W[P, j] * F[q, j].  Config 5: F = factor 1 (256 x 512), W = factor 0.
  */
 #ifndef SKETCH_B200_H
 #define SKETCH_B200_H
@@ -250,6 +253,40 @@ SK_API size_t sk_dense_tn_tc_workspace_bytes(int64_t n, int64_t d, int64_t k);
 SK_API int sk_dense_tn_tc(const float* A, int64_t n, int64_t d, int64_t lda, const uint16_t* Wt_hi,
                           const uint16_t* Wt_lo, int64_t ldw, int64_t k, double scale, float* Y, int64_t ldy,
                           void* ws, size_t ws_bytes, void* stream);
+
+/*
+ * K4 — Khatri-Rao sketch without forming Omega: Y[n,k] = scale * sum_{P,q} A[i, P*dl+q] W[P,j] F[q,j].
+ * Replaces `KhatriRaoTM.apply_right` (src/sketch/khatri_rao.py:158-164, mode contractions of
+ * `_contract` :62-74; BASELINE config 5).  tcgen05 on CTA pairs: each pair keeps its N block of F^T
+ * resident in shared memory (Ft_hi: k x dl bf16, row stride ldf; Ft_lo its bf16 residual, NULL when F
+ * is exact, e.g. Rademacher), streams A once (float32 split to bf16 hi + lo), accumulates one P at a
+ * time in TMEM and folds it into registers scaled by W[P, :] (float32, row stride ldw).  A 16-byte
+ * aligned with lda, dl multiples of 4; q >= dl in a 64-wide k-block is zero-filled by the TMA.
+ * Workspace: sk_kr_workspace_bytes(n, P, dl, k, Ft_lo != NULL, 0).
+ */
+SK_API size_t sk_kr_workspace_bytes(int64_t n, int64_t P, int64_t dl, int64_t k, int split_f, int trans);
+SK_API int sk_kr_right(const float* A, int64_t n, int64_t P, int64_t dl, int64_t lda, const uint16_t* Ft_hi,
+                       const uint16_t* Ft_lo, int64_t ldf, const float* W, int64_t ldw, int64_t k, double scale,
+                       float* Y, int64_t ldy, void* ws, size_t ws_bytes, void* stream);
+/*
+ * K4 adjoint — X[k,m] = scale * Omega^T B for B [P*dl rows][m] float32 (row stride ldb), read in
+ * place (no transposed copy).  Replaces `KhatriRaoTM.apply_adjoint` (src/sketch/khatri_rao.py:147-156).
+ * Workspace: sk_kr_workspace_bytes(m, P, dl, k, Ft_lo != NULL, 1).
+ */
+SK_API int sk_kr_adjoint(const float* B, int64_t m, int64_t P, int64_t dl, int64_t ldb, const uint16_t* Ft_hi,
+                         const uint16_t* Ft_lo, int64_t ldf, const float* W, int64_t ldw, int64_t k, double scale,
+                         float* X, int64_t ldx, void* ws, size_t ws_bytes, void* stream);
+/*
+ * K4c — the same contractions on the CUDA cores for float64 (the reference's dtype; float64
+ * accumulation, parity 1e-12) and float32 shapes the tcgen05 form does not take.  F is dl x k
+ * (row stride ldf) and W is P x k (row stride ldw), both of `dtype`.  Adjoint: X[k,m] from B [P*dl][m].
+ */
+SK_API int sk_kr_right_cc(int dtype, const void* A, int64_t n, int64_t P, int64_t dl, int64_t lda, const void* F,
+                          int64_t ldf, const void* W, int64_t ldw, int64_t k, double scale, void* Y, int64_t ldy,
+                          void* stream);
+SK_API int sk_kr_adjoint_cc(int dtype, const void* B, int64_t m, int64_t P, int64_t dl, int64_t ldb, const void* F,
+                            int64_t ldf, const void* W, int64_t ldw, int64_t k, double scale, void* X, int64_t ldx,
+                            void* stream);
 
 #ifdef __cplusplus
 }

@@ -80,6 +80,15 @@ SIGNATURES = {
     "sk_dense_tn_tc_workspace_bytes": (_c_size, [_c_i64, _c_i64, _c_i64]),
     "sk_dense_tn_tc": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_i64, _c_dbl, _c_p, _c_i64,
                                 _c_p, _c_size, _c_p]),
+    "sk_kr_workspace_bytes": (_c_size, [_c_i64, _c_i64, _c_i64, _c_i64, _c_int, _c_int]),
+    "sk_kr_right": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_p, _c_i64, _c_i64, _c_dbl,
+                             _c_p, _c_i64, _c_p, _c_size, _c_p]),
+    "sk_kr_adjoint": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_p, _c_i64, _c_i64, _c_dbl,
+                               _c_p, _c_i64, _c_p, _c_size, _c_p]),
+    "sk_kr_right_cc": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_i64,
+                                _c_dbl, _c_p, _c_i64, _c_p]),
+    "sk_kr_adjoint_cc": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_i64,
+                                  _c_dbl, _c_p, _c_i64, _c_p]),
 }
 
 _lock = threading.Lock()

@@ -54,6 +54,15 @@ struct TcParams {
   float* part;     // ... or partial sums [ksplit][M][N] (ksplit > 1)
   int num_units;
   int mtiles;
+  // Khatri-Rao mode (dense_tc_pair_kernel<.., KR = true>): K = (P, q) with q < kr_dl fastest; the
+  // last factor F^T (k x dl bf16) is resident in shared memory, chunk = one P (kr_qb k-blocks of
+  // q), and a finished chunk is folded with the column weights W[P][col] (the product of the
+  // other factors' rows).
+  const float* kr_w;
+  int64_t kr_ldw;
+  int kr_qb;       // k-blocks per P (ceil(dl / 64); q >= dl is zero-filled by the 3-D TMA box)
+  int kr_ngroups;  // N blocks, one per group of pairs (each pair keeps one N block resident)
+  int out_t;       // write Y transposed: element (row, col) -> Y[col * ldy + row]
 };
 
 
@@ -73,6 +82,12 @@ __device__ __forceinline__ float lds32f(uint32_t addr) {
 }
 __device__ __forceinline__ void sts128u(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+__device__ __forceinline__ float4 ldg_nc_v4(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
 }
 
 struct Unit {
@@ -368,7 +383,43 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
-template <int NB, bool TA>
+// Persistent schedule of a pair. Dense: units u = pair, pair + npairs, ... decoded by unit_of. KR:
+// the pairs form kr_ngroups groups, group g keeps N block g resident and walks t = (mt, ks) with the
+// pairs of its group (pairs p and p + 1 work on the same A rows at the same time, so the second N
+// block's read of A is an L2 hit).
+struct PairSched {
+  int first, step, count, nb;
+};
+template <bool KR>
+__device__ __forceinline__ PairSched pair_sched(const TcParams& p, int pair, int npairs) {
+  PairSched s;
+  if constexpr (KR) {
+    s.nb = pair % p.kr_ngroups;
+    s.first = pair / p.kr_ngroups;
+    s.step = npairs / p.kr_ngroups;
+    s.count = p.mtiles * p.ksplit;
+  } else {
+    s.nb = 0;
+    s.first = pair;
+    s.step = npairs;
+    s.count = p.num_units;
+  }
+  return s;
+}
+template <bool KR>
+__device__ __forceinline__ Unit pair_unit(const TcParams& p, const PairSched& s, int t) {
+  if constexpr (KR) {
+    Unit r;
+    r.mt = t / p.ksplit;
+    r.ks = t % p.ksplit;
+    r.nb = s.nb;
+    return r;
+  } else {
+    return unit_of(p, t);
+  }
+}
+
+template <int NB, bool TA, bool KR>
 __global__ void __launch_bounds__(kThreads, 1)
     dense_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                          const __grid_constant__ CUtensorMap tm_blo, const TcParams p) {
@@ -377,18 +428,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t a_bytes = BM * 128;
   const int bnh2 = p.BN >> 1;                      // B^T rows staged by each CTA
   const uint32_t bh_bytes = (uint32_t)bnh2 * 128;
-  const uint32_t stage_bytes = kAStageBytes + NB * bh_bytes;
+  // dense: stage = {A, B half (, B_lo half)}; KR: stage = {A}, the B halves of all q blocks resident
+  const uint32_t stage_bytes = KR ? kAStageBytes : kAStageBytes + NB * bh_bytes;
   const int S = p.stages;
-  uint64_t* tma_full = reinterpret_cast<uint64_t*>(smem + (size_t)S * stage_bytes);
+  const int qb = KR ? p.kr_qb : 1;
+  uint8_t* resident = smem + (size_t)S * stage_bytes;  // KR: [NB][qb] tiles of bh_bytes
+  const uint32_t res_bytes = KR ? (uint32_t)NB * (uint32_t)qb * bh_bytes : 0u;
+  uint64_t* tma_full = reinterpret_cast<uint64_t*>(resident + res_bytes);
   uint64_t* full = tma_full + S;       // leader: converted in both CTAs (8 converter warps)
   uint64_t* empty = full + S;          // consumed by the pair MMA (multicast commit)
   uint64_t* acc_full = empty + S;      // [2] (multicast commit)
   uint64_t* acc_empty = acc_full + 2;  // [2] leader: drained by both CTAs (16 reducer warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* res_full = acc_empty + 2;  // KR: this CTA's resident B half has landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const PairSched sc = pair_sched<KR>(p, pair, npairs);
+  const int cqb = KR ? qb : CHUNK_KB;  // k-blocks per TMEM chunk
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&tma_full[s], 1);
@@ -399,6 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], 16);
     }
+    mbar_init(res_full, 1);
     fence_mbar_init();
     tma_prefetch_desc(&tm_a);
     tma_prefetch_desc(&tm_b);
@@ -414,18 +473,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int nk = (int)((p.K + BK - 1) / BK);
+  const int nk = (int)((p.K + BK - 1) / BK);  // KR: p.K = P * qb * 64 (q padded to whole k-blocks)
   const uint32_t full_leader = mapa_u32(full, 0);       // full[0] in the leader; + 8 s
   const uint32_t acc_empty_leader = mapa_u32(acc_empty, 0);
 
   if (warp < 4) {
-    setmaxnreg_dec<32>();
+    setmaxnreg_dec<48>();  // 128 x 48 + 128 x 128 + 256 x 168 = 64K registers
     if (warp == 0 && lane == 0) {
       // -------------------------------------------------------------- producer (this CTA's rows + B half)
+      if constexpr (KR) {  // resident B half of N block sc.nb: qb tiles of 64 (q) x bnh2 (columns)
+        const int brow0 = sc.nb * p.BN + (int)rank * bnh2;
+        mbar_arrive_expect_tx(res_full, res_bytes);
+        for (int q = 0; q < qb; ++q) {
+          tma_load_2d(resident + (size_t)q * bh_bytes, &tm_b, res_full, q * BK, brow0);
+          if (NB == 2) tma_load_2d(resident + (size_t)(qb + q) * bh_bytes, &tm_blo, res_full, q * BK, brow0);
+        }
+      }
       int s = 0;
       uint32_t ph = 0;
-      for (int u = pair; u < p.num_units; u += npairs) {
-        const Unit w = unit_of(p, u);
+      for (int t = sc.first; t < sc.count; t += sc.step) {
+        const Unit w = pair_unit<KR>(p, sc, t);
         const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
         const int row0 = (2 * w.mt + (int)rank) * BM;
         const int brow0 = w.nb * p.BN + (int)rank * bnh2;
@@ -433,10 +500,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + (size_t)s * stage_bytes;
           mbar_arrive_expect_tx(&tma_full[s], stage_bytes);
-          if (TA) tma_load_2d(st, &tm_a, &tma_full[s], row0, kb * BK);
-          else tma_load_2d(st, &tm_a, &tma_full[s], kb * BK, row0);
-          tma_load_2d(st + kAStageBytes, &tm_b, &tma_full[s], kb * BK, brow0);
-          if (NB == 2) tma_load_2d(st + kAStageBytes + bh_bytes, &tm_blo, &tma_full[s], kb * BK, brow0);
+          if constexpr (KR) {  // A as (q, P, row) [TA: (col, q, P)]; box 64 q x 1 P x 128, q >= dl zero-filled
+            const int P = kb / qb, q0 = (kb - P * qb) * BK;
+            if (TA) tma_load_3d(st, &tm_a, &tma_full[s], row0, q0, P);
+            else tma_load_3d(st, &tm_a, &tma_full[s], q0, P, row0);
+          } else {
+            if (TA) tma_load_2d(st, &tm_a, &tma_full[s], row0, kb * BK);
+            else tma_load_2d(st, &tm_a, &tma_full[s], kb * BK, row0);
+            tma_load_2d(st + kAStageBytes, &tm_b, &tma_full[s], kb * BK, brow0);
+            if (NB == 2) tma_load_2d(st + kAStageBytes + bh_bytes, &tm_blo, &tma_full[s], kb * BK, brow0);
+          }
           if (++s == S) { s = 0; ph ^= 1; }
         }
       }
@@ -446,28 +519,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       uint32_t chunk_seq = 0;
-      for (int u = pair; u < p.num_units; u += npairs) {
-        const Unit w = unit_of(p, u);
+      for (int t = sc.first; t < sc.count; t += sc.step) {
+        const Unit w = pair_unit<KR>(p, sc, t);
         const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
-        for (int c0 = kb0; c0 < kb1; c0 += CHUNK_KB, ++chunk_seq) {
+        for (int c0 = kb0; c0 < kb1; c0 += cqb, ++chunk_seq) {
           const uint32_t buf = chunk_seq & 1, use = chunk_seq >> 1;
           mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
           tc_fence_after();
           const uint32_t d = tmem + buf * (uint32_t)p.BN;
-          const int c1 = min(kb1, c0 + CHUNK_KB);
+          const int c1 = min(kb1, c0 + cqb);
           for (int kb = c0; kb < c1; ++kb) {
             mbar_wait(&full[s], ph);
             tc_fence_after();
             const uint32_t st = sm100::smem_u32(smem + (size_t)s * stage_bytes);
-            const uint32_t a_hi = st, a_lo = st + a_bytes, b = st + kAStageBytes;
+            const uint32_t a_hi = st, a_lo = st + a_bytes;
+            const uint32_t b = KR ? sm100::smem_u32(resident) + (uint32_t)(kb - c0) * bh_bytes : st + kAStageBytes;
+            const uint32_t blo = KR ? b + (uint32_t)qb * bh_bytes : b + bh_bytes;
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
               const uint64_t db = sdesc_kmajor_sw128(b + kk * 32);
               umma_bf16_pair(d, sdesc_kmajor_sw128(a_hi + kk * 32), db, idesc, (kb > c0 || kk > 0) ? 1u : 0u);
               umma_bf16_pair(d, sdesc_kmajor_sw128(a_lo + kk * 32), db, idesc, 1u);
               if (NB == 2)
-                umma_bf16_pair(d, sdesc_kmajor_sw128(a_hi + kk * 32), sdesc_kmajor_sw128(b + bh_bytes + kk * 32), idesc,
-                               1u);
+                umma_bf16_pair(d, sdesc_kmajor_sw128(a_hi + kk * 32), sdesc_kmajor_sw128(blo + kk * 32), idesc, 1u);
             }
             umma_commit_pair(&empty[s]);
             if (++s == S) { s = 0; ph ^= 1; }
@@ -482,10 +556,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ct = threadIdx.x - 128;
     const int c4 = ct & 15;
     const int rsub = ct >> 4;
+    // KR: the leader's first MMA reads both CTAs' resident B halves; it waits for every converter
+    // warp of both CTAs, so each CTA's converters first wait for their own CTA's resident half
+    if constexpr (KR) mbar_wait(res_full, 0);
     int s = 0;
     uint32_t ph = 0;
-    for (int u = pair; u < p.num_units; u += npairs) {
-      const Unit w = unit_of(p, u);
+    for (int t = sc.first; t < sc.count; t += sc.step) {
+      const Unit w = pair_unit<KR>(p, sc, t);
       const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
       for (int kb = kb0; kb < kb1; ++kb) {
         if constexpr (TA) {  // transpose while splitting (as dense_tc_kernel<NB, true>)
@@ -548,25 +625,42 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int hoff = half * bh0;
     const int bnh = half == 0 ? bh0 : p.BN - bh0;
     uint32_t chunk_seq = 0;
-    for (int u = pair; u < p.num_units; u += npairs) {
-      const Unit w = unit_of(p, u);
+    for (int t = sc.first; t < sc.count; t += sc.step) {
+      const Unit w = pair_unit<KR>(p, sc, t);
       const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
+      const int col0 = w.nb * p.BN + hoff;
       float sum[kMaxBNH];
 #pragma unroll
       for (int j = 0; j < kMaxBNH; ++j) sum[j] = 0.f;
-      for (int c0 = kb0; c0 < kb1; c0 += CHUNK_KB, ++chunk_seq) {
+      for (int c0 = kb0; c0 < kb1; c0 += cqb, ++chunk_seq) {
         const uint32_t buf = chunk_seq & 1, use = chunk_seq >> 1;
         mbar_wait(&acc_full[buf], use & 1);
         tc_fence_after();
         const uint32_t base = tmem + ((uint32_t)(32 * lg) << 16) + buf * (uint32_t)p.BN + hoff;
+        // KR: the chunk's column weights W[P][col0 ...] (the same address in every lane: broadcast)
+        const float4* wrow = nullptr;
+        if constexpr (KR) wrow = reinterpret_cast<const float4*>(p.kr_w + (int64_t)(c0 / qb) * p.kr_ldw + col0);
 #pragma unroll
         for (int g = 0; g < kMaxBNH / 16; ++g) {
           if (g * 16 < bnh) {
             uint32_t r[16];
             tmem_ld16(base + g * 16, r);
-            tmem_ld_wait();
+            if constexpr (KR) {
+              tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 16; ++j) sum[g * 16 + j] += __uint_as_float(r[j]);
+              for (int j = 0; j < 4; ++j) {
+                const float4 x = ldg_nc_v4(wrow + 4 * g + j);  // volatile: stays after the TMEM wait
+                float* sg = sum + g * 16 + 4 * j;
+                sg[0] = fmaf(x.x, __uint_as_float(r[4 * j]), sg[0]);
+                sg[1] = fmaf(x.y, __uint_as_float(r[4 * j + 1]), sg[1]);
+                sg[2] = fmaf(x.z, __uint_as_float(r[4 * j + 2]), sg[2]);
+                sg[3] = fmaf(x.w, __uint_as_float(r[4 * j + 3]), sg[3]);
+              }
+            } else {
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 16; ++j) sum[g * 16 + j] += __uint_as_float(r[j]);
+            }
           }
         }
         tc_fence_before();
@@ -575,22 +669,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int64_t row = (int64_t)(2 * w.mt + (int)rank) * BM + 32 * lg + lane;
       if (row < p.M) {
-        const int col0 = w.nb * p.BN + hoff;
         float* out;
-        float sc;
-        if (p.ksplit == 1) {
+        float sc2;
+        if (p.ksplit == 1 && !p.out_t) {
           out = p.Y + row * p.ldy + col0;
-          sc = p.scale;
-        } else {
+          sc2 = p.scale;
+        } else {  // partial sums (or a transposed result): tc_splitk_reduce forms Y
           out = p.part + ((int64_t)w.ks * p.M + row) * p.N + col0;
-          sc = 1.0f;
+          sc2 = 1.0f;
         }
 #pragma unroll
         for (int g = 0; g < kMaxBNH / 16; ++g) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int c = g * 16 + j;
-            if (c < bnh && col0 + c < p.N) out[c] = sum[c] * sc;
+            if (c < bnh && col0 + c < p.N) out[c] = sum[c] * sc2;
           }
         }
       }
@@ -604,15 +697,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// Y = scale * sum_s part[s] (fixed order)
+// Y = scale * sum_s part[s] (fixed order); out_t: element (r, c) -> Y[c * ldy + r]
 __global__ void tc_splitk_reduce(const float* __restrict__ part, int ksplit, int64_t M, int N, float scale,
-                                 float* __restrict__ Y, int64_t ldy) {
+                                 float* __restrict__ Y, int64_t ldy, int out_t = 0) {
   const int64_t total = M * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / N, c = i % N;
+    int64_t r, c;
+    if (out_t) {  // consecutive threads -> consecutive r (coalesced Y^T writes)
+      c = i / M;
+      r = i % M;
+    } else {
+      r = i / N;
+      c = i % N;
+    }
     float s = 0.f;
     for (int q = 0; q < ksplit; ++q) s += part[(q * M + r) * N + c];
-    Y[r * ldy + c] = s * scale;
+    if (out_t) Y[c * ldy + r] = s * scale;
+    else Y[r * ldy + c] = s * scale;
   }
 }
 
@@ -737,7 +838,7 @@ Plan make_plan_pair(int64_t n, int64_t d, int64_t k, int NB) {
   if (stages > 6) stages = 6;
   pl.stages = stages;
   pl.astages = 0;
-  pl.smem = 1024 + stages * stage_bytes + (3 * stages + 4) * 8 + 16;
+  pl.smem = 1024 + stages * stage_bytes + (3 * stages + 5) * 8 + 16;
   pl.ws_bytes = pl.ksplit > 1 ? (size_t)pl.ksplit * n * k * sizeof(float) : 0;
   return pl;
 }
@@ -752,8 +853,8 @@ bool use_pair(int64_t n) {
 int launch_pair(int NB, bool TA, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mbl, TcParams& p,
                 size_t smem, cudaStream_t s) {
   using KernT = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams);
-  KernT kern = TA ? (NB == 2 ? dense_tc_pair_kernel<2, true> : dense_tc_pair_kernel<1, true>)
-                  : (NB == 2 ? dense_tc_pair_kernel<2, false> : dense_tc_pair_kernel<1, false>);
+  KernT kern = TA ? (NB == 2 ? dense_tc_pair_kernel<2, true, false> : dense_tc_pair_kernel<1, true, false>)
+                  : (NB == 2 ? dense_tc_pair_kernel<2, false, false> : dense_tc_pair_kernel<1, false, false>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(2 * (sm_count() / 2)));
@@ -783,6 +884,220 @@ int launch_pair(int NB, bool TA, const CUtensorMap& ma, const CUtensorMap& mb, c
   const int npairs = p.num_units < max_clusters ? p.num_units : max_clusters;
   cfg.gridDim = dim3((unsigned)(2 * npairs));
   return cudaLaunchKernelEx(&cfg, kern, ma, mb, mbl, p) == cudaSuccess ? SK_OK : SK_ECUDA;
+}
+
+// ------------------------------------------------------------------------------------ Khatri-Rao
+// Y = scale * sum_P (A[:, P, :] F) * W[P, :] on the CTA-pair engine with F resident (KR = true).
+// A viewed as 3-D (q < dl, P, row) [TA: (col, q, P)], box 64 x 1 x 128: q >= dl is zero-filled,
+// so dl need not be a multiple of 64 (dl % 4 == 0 for the TMA strides).
+int make_a3_map(CUtensorMap* m, const float* a, int64_t rows, int64_t P, int64_t dl, int64_t lda, bool ta) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(SK_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3], strides[2];
+  cuuint32_t box[3];
+  if (!ta) {  // A [rows][P * dl]: (q, P, row)
+    dims[0] = (cuuint64_t)dl; dims[1] = (cuuint64_t)P; dims[2] = (cuuint64_t)rows;
+    strides[0] = (cuuint64_t)dl * 4; strides[1] = (cuuint64_t)lda * 4;
+    box[0] = BK; box[1] = 1; box[2] = BM;
+  } else {    // B [P * dl][rows]: (col, q, P)
+    dims[0] = (cuuint64_t)rows; dims[1] = (cuuint64_t)dl; dims[2] = (cuuint64_t)P;
+    strides[0] = (cuuint64_t)lda * 4; strides[1] = (cuuint64_t)dl * lda * 4;
+    box[0] = BM; box[1] = BK; box[2] = 1;
+  }
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(a), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SK_EINVAL, "cuTensorMapEncodeTiled(KR A) failed (alignment of A / lda / dl?)");
+  return SK_OK;
+}
+
+constexpr int kKrMaxCols = 2048;  // columns per launch (N blocks <= 8, one group of pairs per block)
+
+struct KrPlan {
+  int BN, nblocks, qb, ksplit, kb_per_split, mtiles, stages, npairs;
+  size_t smem, ws_bytes;
+};
+
+using KernT = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams);
+KernT kr_kernel(int NB, bool TA) {
+  return TA ? (NB == 2 ? dense_tc_pair_kernel<2, true, true> : dense_tc_pair_kernel<1, true, true>)
+            : (NB == 2 ? dense_tc_pair_kernel<2, false, true> : dense_tc_pair_kernel<1, false, true>);
+}
+
+// co-resident 2-CTA clusters of the KR kernel at this shared-memory size
+int kr_max_clusters(int NB, bool TA, size_t smem) {
+  KernT kern = kr_kernel(NB, TA);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(2 * (sm_count() / 2)));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int mc = 0;
+  if (cudaOccupancyMaxActiveClusters(&mc, kern, &cfg) != cudaSuccess || mc < 1) {
+    cudaGetLastError();
+    mc = sm_count() / 2;
+  }
+  return mc;
+}
+
+// kslab = columns of this launch (<= kKrMaxCols); maxc < 0: no device query (workspace sizing)
+bool make_plan_kr(KrPlan& pl, int64_t n, int64_t P, int64_t dl, int64_t kslab, int NB, int maxc, bool ta) {
+  pl = KrPlan{};
+  pl.qb = (int)((dl + BK - 1) / BK);
+  pl.nblocks = (int)((kslab + 255) / 256);
+  for (;;) {
+    const int64_t per = (kslab + pl.nblocks - 1) / pl.nblocks;
+    pl.BN = (int)((per + 15) / 16 * 16);
+    const size_t res = (size_t)NB * pl.qb * (pl.BN / 2) * 128;
+    if (res <= 160 * 1024) break;
+    if (pl.BN <= 32) return false;
+    pl.nblocks *= 2;
+  }
+  const size_t res = (size_t)NB * pl.qb * (pl.BN / 2) * 128;
+  const size_t budget = 227 * 1024 - 1024 - 512;
+  if (res + 2 * (size_t)kAStageBytes > budget) return false;
+  int stages = (int)((budget - res) / kAStageBytes);
+  if (stages > 6) stages = 6;
+  pl.stages = stages;
+  pl.smem = 1024 + (size_t)stages * kAStageBytes + res + (3 * stages + 5) * 8 + 16;
+  pl.mtiles = (int)((n + 2 * BM - 1) / (2 * BM));
+  const int mc = maxc > 0 ? maxc : sm_count() / 2;
+  const int gp = mc / pl.nblocks > 0 ? mc / pl.nblocks : 1;  // pairs per N-block group
+  int ks = 1;
+  while ((int64_t)pl.mtiles * ks < 4 * gp && P / (2 * ks) >= 2) ks *= 2;
+  const int64_t p_per = (P + ks - 1) / ks;
+  pl.kb_per_split = (int)(p_per * pl.qb);
+  pl.ksplit = (int)((P + p_per - 1) / p_per);
+  const int64_t work = (int64_t)pl.mtiles * pl.ksplit;
+  pl.npairs = (int)((work < gp ? work : gp) * pl.nblocks);
+  pl.ws_bytes = (pl.ksplit > 1 || ta) ? (size_t)pl.ksplit * n * kslab * sizeof(float) : 0;
+  return true;
+}
+
+size_t kr_workspace(int64_t n, int64_t P, int64_t dl, int64_t k, int NB, bool ta) {
+  size_t ws = 0;
+  for (int64_t c0 = 0; c0 < k; c0 += kKrMaxCols) {
+    const int64_t ks = k - c0 < kKrMaxCols ? k - c0 : kKrMaxCols;
+    KrPlan pl;
+    if (!make_plan_kr(pl, n, P, dl, ks, NB, -1, ta)) return 0;
+    // the real grid may have fewer pairs per group -> more K splits; size for the largest split count
+    KrPlan pl1;
+    make_plan_kr(pl1, n, P, dl, ks, NB, 2 * pl.nblocks, ta);
+    const size_t w = pl.ws_bytes > pl1.ws_bytes ? pl.ws_bytes : pl1.ws_bytes;
+    if (w > ws) ws = w;
+  }
+  return ws;
+}
+
+// rows: output rows (A rows, or B columns when TA); out: Y [rows][k] (ldy) or, when TA, X [k][rows]
+int kr_run(bool TA, const float* A, int64_t rows, int64_t P, int64_t dl, int64_t lda, const uint16_t* Ft_hi,
+           const uint16_t* Ft_lo, int64_t ldf, const float* W, int64_t ldw, int64_t k, double scale, float* Y,
+           int64_t ldy, void* ws, size_t ws_bytes, cudaStream_t s, const char* what) {
+  const int NB = Ft_lo ? 2 : 1;
+  CUtensorMap ma;
+  int st = make_a3_map(&ma, A, rows, P, dl, lda, TA);
+  if (st != SK_OK) return st;
+  for (int64_t c0 = 0; c0 < k; c0 += kKrMaxCols) {
+    const int64_t kslab = k - c0 < kKrMaxCols ? k - c0 : kKrMaxCols;
+    KrPlan pl;
+    if (!make_plan_kr(pl, rows, P, dl, kslab, NB, -1, TA))
+      return fail(SK_EUNSUPPORTED, std::string(what) + ": resident factor does not fit shared memory");
+    static int maxc_cache[4] = {0, 0, 0, 0};
+    static size_t maxc_smem[4] = {0, 0, 0, 0};
+    const int slot = (NB - 1) + 2 * (TA ? 1 : 0);
+    if (maxc_smem[slot] != pl.smem) {
+      maxc_cache[slot] = kr_max_clusters(NB, TA, pl.smem);
+      maxc_smem[slot] = pl.smem;
+    }
+    if (maxc_cache[slot] < pl.nblocks) return fail(SK_EUNSUPPORTED, std::string(what) + ": too few co-resident pairs");
+    make_plan_kr(pl, rows, P, dl, kslab, NB, maxc_cache[slot], TA);
+    if (pl.ws_bytes > 0 && (ws == nullptr || ws_bytes < pl.ws_bytes))
+      return fail(SK_EINVAL, std::string(what) + ": workspace too small (sk_kr_workspace_bytes)");
+    CUtensorMap mb, mbl;
+    st = make_bt_map(&mb, Ft_hi + c0 * ldf, kslab, dl, ldf, pl.BN / 2);
+    if (st != SK_OK) return st;
+    if (NB == 2) {
+      st = make_bt_map(&mbl, Ft_lo + c0 * ldf, kslab, dl, ldf, pl.BN / 2);
+      if (st != SK_OK) return st;
+    } else {
+      mbl = mb;
+    }
+    TcParams p{};
+    p.A = A;
+    p.M = rows;
+    p.K = P * (int64_t)pl.qb * BK;
+    p.lda = lda;
+    p.N = (int)kslab;
+    p.BN = pl.BN;
+    p.nblocks = pl.nblocks;
+    p.ksplit = pl.ksplit;
+    p.kb_per_split = pl.kb_per_split;
+    p.stages = pl.stages;
+    p.scale = (float)scale;
+    p.Y = TA ? Y + c0 * ldy : Y + c0;
+    p.ldy = ldy;
+    p.part = static_cast<float*>(ws);
+    p.num_units = pl.mtiles * pl.ksplit * pl.nblocks;
+    p.mtiles = pl.mtiles;
+    p.kr_w = W + c0;
+    p.kr_ldw = ldw;
+    p.kr_qb = pl.qb;
+    p.kr_ngroups = pl.nblocks;
+    p.out_t = TA ? 1 : 0;
+    uint32_t cols = 32;
+    while (cols < (uint32_t)(2 * pl.BN)) cols <<= 1;
+    p.tmem_cols = cols;
+    KernT kern = kr_kernel(NB, TA);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(2 * pl.npairs));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mbl, p) != cudaSuccess) return check_launch(what);
+    st = check_launch(what);
+    if (st != SK_OK) return st;
+    if (pl.ksplit > 1 || TA) {
+      const int64_t total = rows * kslab;
+      int64_t blocks = (total + 255) / 256;
+      if (blocks > 8 * (int64_t)sm_count()) blocks = 8 * (int64_t)sm_count();
+      tc_splitk_reduce<<<(unsigned)blocks, 256, 0, s>>>(p.part, pl.ksplit, rows, (int)kslab, (float)scale, p.Y, ldy,
+                                                       p.out_t);
+      st = check_launch(what);
+      if (st != SK_OK) return st;
+    }
+  }
+  return SK_OK;
+}
+
+int kr_check(const float* A, int64_t rows, int64_t P, int64_t dl, int64_t lda, int64_t minlda, const uint16_t* Ft_hi,
+             const uint16_t* Ft_lo, int64_t ldf, const float* W, int64_t ldw, int64_t k, const float* Y, int64_t ldy,
+             int64_t minldy, const char* what) {
+  if (rows < 0 || P < 1 || dl < 1 || k < 1 || lda < minlda || ldf < dl || ldw < k || ldy < minldy)
+    return fail(SK_EINVAL, std::string(what) + ": bad shape");
+  if (!A || !Ft_hi || !W || !Y) return fail(SK_EINVAL, std::string(what) + ": null pointer");
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (lda & 3) || (dl & 3))
+    return fail(SK_EINVAL, std::string(what) + ": A must be 16-byte aligned with lda, dl multiples of 4");
+  if ((reinterpret_cast<uintptr_t>(Ft_hi) & 15) || (ldf & 7) || (Ft_lo && (reinterpret_cast<uintptr_t>(Ft_lo) & 15)))
+    return fail(SK_EINVAL, std::string(what) + ": F^T must be 16-byte aligned with ldf a multiple of 8");
+  if ((reinterpret_cast<uintptr_t>(W) & 15) || (ldw & 3))
+    return fail(SK_EINVAL, std::string(what) + ": W must be 16-byte aligned with ldw a multiple of 4");
+  return SK_OK;
 }
 
 }  // namespace
@@ -1017,4 +1332,33 @@ extern "C" int sk_dense_tn_tc(const float* A, int64_t n, int64_t d, int64_t lda,
   if (blocks > 8 * (int64_t)sm_count()) blocks = 8 * (int64_t)sm_count();
   tc_splitk_reduce<<<(unsigned)blocks, 256, 0, s>>>(p.part, pl.ksplit, d, (int)k, (float)scale, Y, ldy);
   return check_launch("sk_dense_tn_tc(reduce)");
+}
+
+// ------------------------------------------------------------------------------------ Khatri-Rao C ABI
+// trans = 0: sk_kr_right with n rows; trans = 1: sk_kr_adjoint with n = m columns of B
+extern "C" size_t sk_kr_workspace_bytes(int64_t n, int64_t P, int64_t dl, int64_t k, int split_f, int trans) {
+  if (n < 1 || P < 1 || dl < 1 || k < 1) return 0;
+  return skb::kr_workspace(n, P, dl, k, split_f ? 2 : 1, trans != 0);
+}
+
+// Y[n, k] = scale * sum_{P, q} A[i, P * dl + q] * W[P, j] * F[q, j]   (Khatri-Rao, Omega never formed)
+extern "C" int sk_kr_right(const float* A, int64_t n, int64_t P, int64_t dl, int64_t lda, const uint16_t* Ft_hi,
+                           const uint16_t* Ft_lo, int64_t ldf, const float* W, int64_t ldw, int64_t k, double scale,
+                           float* Y, int64_t ldy, void* ws, size_t ws_bytes, void* stream) {
+  using namespace skb;
+  int st = kr_check(A, n, P, dl, lda, P * dl, Ft_hi, Ft_lo, ldf, W, ldw, k, Y, ldy, k, "sk_kr_right");
+  if (st != SK_OK || n == 0) return st;
+  return kr_run(false, A, n, P, dl, lda, Ft_hi, Ft_lo, ldf, W, ldw, k, scale, Y, ldy, ws, ws_bytes,
+                as_stream(stream), "sk_kr_right");
+}
+
+// X[k, m] = scale * Omega^T B for B [P * dl rows][m] (row stride ldb), read in place (no transposed copy)
+extern "C" int sk_kr_adjoint(const float* B, int64_t m, int64_t P, int64_t dl, int64_t ldb, const uint16_t* Ft_hi,
+                             const uint16_t* Ft_lo, int64_t ldf, const float* W, int64_t ldw, int64_t k,
+                             double scale, float* X, int64_t ldx, void* ws, size_t ws_bytes, void* stream) {
+  using namespace skb;
+  int st = kr_check(B, m, P, dl, ldb, m, Ft_hi, Ft_lo, ldf, W, ldw, k, X, ldx, m, "sk_kr_adjoint");
+  if (st != SK_OK || m == 0) return st;
+  return kr_run(true, B, m, P, dl, ldb, Ft_hi, Ft_lo, ldf, W, ldw, k, scale, X, ldx, ws, ws_bytes, as_stream(stream),
+                "sk_kr_adjoint");
 }

@@ -1,9 +1,9 @@
 """Dense tensor-core apply (K-TC, `sk_dense_right_tc`) and the device forms of Omega^T it consumes.
 
 The kernel computes Y = scale * A * B for float32 A with B supplied as B^T in bf16 (k x d, rows
-padded to a multiple of 8 elements).  +-1 matrices (sparse sign, Rademacher Khatri-Rao) are exact
-in bf16, so only A is split (hi + lo); general matrices (Gaussian, non-Rademacher factors) also
-pass the bf16 residual of B.  The kernel tiles N in blocks of <= 256 columns and splits K across
+padded to a multiple of 8 elements).  +-1 matrices (sparse sign) are exact in bf16, so only A is
+split (hi + lo); general matrices (Gaussian) also pass the bf16 residual of B.  Khatri-Rao has its
+own entry (sk_kr_right, sketch/kron.py) that never forms Omega.  The kernel tiles N in blocks of <= 256 columns and splits K across
 CTAs (workspace + ordered reduction) when there are too few row tiles to fill the GPU.
 """
 
@@ -13,7 +13,7 @@ import numpy as np
 
 from .. import _lib
 
-__all__ = ["dense_right_tc", "dense_tn_tc", "bt_from_triplets", "bt_from_dense", "bt_khatri_rao"]
+__all__ = ["dense_right_tc", "dense_tn_tc", "bt_from_triplets", "bt_from_dense"]
 
 MAX_K = 512
 
@@ -51,24 +51,6 @@ def bt_from_dense(omega: np.ndarray, device):
     if bool(torch.all(lo == 0).item()):
         return hi, None
     return hi, lo
-
-
-def bt_khatri_rao(factors: np.ndarray, device):
-    """Omega^T for a Khatri-Rao matrix: row j = f_0[:, j] (x) ... (x) f_{ell-1}[:, j] (factor 0 slowest)."""
-    import torch
-
-    f = torch.as_tensor(np.ascontiguousarray(factors), dtype=torch.float64, device=device)  # (ell, d0, k)
-    ell, d0, k = f.shape
-    rows = f[0].T  # (k, d0)
-    for i in range(1, ell):
-        rows = (rows[:, :, None] * f[i].T[:, None, :]).reshape(k, -1)
-    d = rows.shape[1]
-    ldb = _pad8(d)
-    om = torch.zeros((k, ldb), dtype=torch.float64, device=device)
-    om[:, :d] = rows
-    hi = om.to(torch.bfloat16)
-    lo = (om - hi.to(torch.float64)).to(torch.bfloat16)
-    return hi, (None if bool(torch.all(lo == 0).item()) else lo)
 
 
 def dense_right_tc(a, bt_hi, bt_lo, k: int, scale: float):

@@ -204,3 +204,21 @@ def test_row_blocks_cached_and_partition_rows():
     full = tm.materialize()
     assert np.array_equal(np.vstack([b.materialize() for b in blocks]), full)
     assert tm.redraw(3).row_block(0, 128) is not blocks[0]
+
+
+@pytest.mark.parametrize("d0,ell,k,base", [(256, 2, 512, "real_rademacher"), (16, 2, 48, "real_rademacher"),
+                                           (8, 3, 20, "real_gaussian"), (4, 4, 60, "real_rademacher"),
+                                           (5, 2, 7, "real_spherical"), (2, 5, 9, "real_rademacher")])
+def test_kr_factor_split_reproduces_omega(d0, ell, k, base):
+    """The device operands of the Khatri-Rao kernels: Omega[P*dl + q, j] = W[P, j] F[q, j] exactly
+    (W, F = Khatri-Rao products of the leading / trailing factors; Omega itself is never formed)."""
+    tm = skb.KhatriRaoTM(d0, ell, k, base, seed=3)
+    om = tm.materialize()
+    for tensor_cores in (True, False):
+        g = tm._kr_group(tensor_cores) or 1
+        w, f = tm._kr_split_arrays(g)
+        assert w.shape == (d0 ** (ell - g), k) and f.shape == (d0 ** g, k)
+        np.testing.assert_allclose((w[:, None, :] * f[None, :, :]).reshape(-1, k) / np.sqrt(k), om, rtol=1e-15,
+                                   atol=0)  # products regrouped: exact for +-1, 1 ulp otherwise
+    if (d0, ell) == (256, 2):
+        assert tm._kr_group(True) == 1  # config 5: F = factor 1, W = factor 0 (no Kronecker columns formed)
