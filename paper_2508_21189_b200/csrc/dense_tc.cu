@@ -27,6 +27,7 @@
 #include <cuda.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -54,15 +55,21 @@ struct TcParams {
   float* part;     // ... or partial sums [ksplit][M][N] (ksplit > 1)
   int num_units;
   int mtiles;
-  // Khatri-Rao mode (dense_tc_pair_kernel<.., KR = true>): K = (P, q) with q < kr_dl fastest; the
-  // last factor F^T (k x dl bf16) is resident in shared memory, chunk = one P (kr_qb k-blocks of
-  // q), and a finished chunk is folded with the column weights W[P][col] (the product of the
-  // other factors' rows).
+  // Khatri-Rao modes (dense_tc_pair_kernel<.., KR = 1 | 2>): K = (P, q) with q < dl fastest, A read
+  // through a 3-D map (q >= dl of a 64-wide k-block is zero-filled).
+  // KR = 1: F^T (k x dl bf16) resident in shared memory, chunk = one P (kr_qb k-blocks), a finished
+  //         chunk folded with the column weights W[P][col] (the product of the other factors' rows).
+  // KR = 2: +-1 factors; B tiles synthesised from sign bits: kr_fbits[j * kr_fwords + 2 qq (+1)] =
+  //         the 64 signs of F^T[j, 64 qq ..] (bit q % 32), kr_wbits[P * kr_wwords + j / 32] bit j % 32.
   const float* kr_w;
   int64_t kr_ldw;
-  int kr_qb;       // k-blocks per P (ceil(dl / 64); q >= dl is zero-filled by the 3-D TMA box)
-  int kr_ngroups;  // N blocks, one per group of pairs (each pair keeps one N block resident)
-  int out_t;       // write Y transposed: element (row, col) -> Y[col * ldy + row]
+  const uint32_t* kr_fbits;
+  int64_t kr_fwords;
+  const uint32_t* kr_wbits;
+  int64_t kr_wwords;
+  int kr_qb;       // k-blocks per P (ceil(dl / 64))
+  int kr_ngroups;  // N blocks, one per group of pairs (each pair keeps one N block)
+  int out_t;       // result transposed: element (row, col) -> Y[col * ldy + row] (through the reduce)
 };
 
 
@@ -384,16 +391,16 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
 }
 
 // Persistent schedule of a pair. Dense: units u = pair, pair + npairs, ... decoded by unit_of. KR:
-// the pairs form kr_ngroups groups, group g keeps N block g resident and walks t = (mt, ks) with the
-// pairs of its group (pairs p and p + 1 work on the same A rows at the same time, so the second N
-// block's read of A is an L2 hit).
+// the pairs form kr_ngroups groups, group g keeps N block g (its B source) and walks t = (mt, ks)
+// with the pairs of its group (pairs p and p + 1 work on the same A rows at the same time, so the
+// second N block's read of A is an L2 hit).
 struct PairSched {
   int first, step, count, nb;
 };
-template <bool KR>
+template <int KR>
 __device__ __forceinline__ PairSched pair_sched(const TcParams& p, int pair, int npairs) {
   PairSched s;
-  if constexpr (KR) {
+  if constexpr (KR != 0) {
     s.nb = pair % p.kr_ngroups;
     s.first = pair / p.kr_ngroups;
     s.step = npairs / p.kr_ngroups;
@@ -406,9 +413,9 @@ __device__ __forceinline__ PairSched pair_sched(const TcParams& p, int pair, int
   }
   return s;
 }
-template <bool KR>
+template <int KR>
 __device__ __forceinline__ Unit pair_unit(const TcParams& p, const PairSched& s, int t) {
-  if constexpr (KR) {
+  if constexpr (KR != 0) {
     Unit r;
     r.mt = t / p.ksplit;
     r.ks = t % p.ksplit;
@@ -419,7 +426,13 @@ __device__ __forceinline__ Unit pair_unit(const TcParams& p, const PairSched& s,
   }
 }
 
-template <int NB, bool TA, bool KR>
+// KR = 0: dense B^T streamed by TMA with A.
+// KR = 1: Khatri-Rao, general factors: F^T resident in shared memory (qb tiles per CTA half), one
+//         P per TMEM chunk, reducers fold each chunk scaled by W[P, :].
+// KR = 2: Khatri-Rao, +-1 factors: warps 2-3 synthesise each k-block's B tile (F^T sign-flipped by
+//         W[P, :]) in the stage from sign bits (F: 2 words per column and k-block; W: one bit per
+//         (P, column)); chunks of CHUNK_KB k-blocks as the dense engine.  Omega is never formed.
+template <int NB, bool TA, int KR>
 __global__ void __launch_bounds__(kThreads, 1)
     dense_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                          const __grid_constant__ CUtensorMap tm_blo, const TcParams p) {
@@ -428,29 +441,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t a_bytes = BM * 128;
   const int bnh2 = p.BN >> 1;                      // B^T rows staged by each CTA
   const uint32_t bh_bytes = (uint32_t)bnh2 * 128;
-  // dense: stage = {A, B half (, B_lo half)}; KR: stage = {A}, the B halves of all q blocks resident
-  const uint32_t stage_bytes = KR ? kAStageBytes : kAStageBytes + NB * bh_bytes;
+  // stage = {A, B half (, B_lo half)}; KR = 1: stage = {A}, the B halves of all q blocks resident
+  const uint32_t stage_bytes = KR == 1 ? kAStageBytes : kAStageBytes + NB * bh_bytes;
   const int S = p.stages;
   const int qb = KR ? p.kr_qb : 1;
-  uint8_t* resident = smem + (size_t)S * stage_bytes;  // KR: [NB][qb] tiles of bh_bytes
-  const uint32_t res_bytes = KR ? (uint32_t)NB * (uint32_t)qb * bh_bytes : 0u;
+  uint8_t* resident = smem + (size_t)S * stage_bytes;  // KR = 1: [NB][qb] tiles of bh_bytes
+  const uint32_t res_bytes = KR == 1 ? (uint32_t)NB * (uint32_t)qb * bh_bytes : 0u;
   uint64_t* tma_full = reinterpret_cast<uint64_t*>(resident + res_bytes);
-  uint64_t* full = tma_full + S;       // leader: converted in both CTAs (8 converter warps)
+  uint64_t* full = tma_full + S;       // leader: converted (and, KR = 2, synthesised) in both CTAs
   uint64_t* empty = full + S;          // consumed by the pair MMA (multicast commit)
   uint64_t* acc_full = empty + S;      // [2] (multicast commit)
   uint64_t* acc_empty = acc_full + 2;  // [2] leader: drained by both CTAs (16 reducer warps)
-  uint64_t* res_full = acc_empty + 2;  // KR: this CTA's resident B half has landed
+  uint64_t* res_full = acc_empty + 2;  // KR = 1: this CTA's resident B half has landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const PairSched sc = pair_sched<KR>(p, pair, npairs);
-  const int cqb = KR ? qb : CHUNK_KB;  // k-blocks per TMEM chunk
+  const int cqb = KR == 1 ? qb : CHUNK_KB;  // k-blocks per TMEM chunk
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&tma_full[s], 1);
-      mbar_init(&full[s], 8);  // leader: the converter warps of both CTAs
+      mbar_init(&full[s], KR == 2 ? 12 : 8);  // leader: converter (+ synthesis) warps of both CTAs
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -460,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(res_full, 1);
     fence_mbar_init();
     tma_prefetch_desc(&tm_a);
-    tma_prefetch_desc(&tm_b);
+    if (KR != 2) tma_prefetch_desc(&tm_b);
     if (NB == 2) tma_prefetch_desc(&tm_blo);
   }
   if (warp == 2) {
@@ -481,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     setmaxnreg_dec<48>();  // 128 x 48 + 128 x 128 + 256 x 168 = 64K registers
     if (warp == 0 && lane == 0) {
       // -------------------------------------------------------------- producer (this CTA's rows + B half)
-      if constexpr (KR) {  // resident B half of N block sc.nb: qb tiles of 64 (q) x bnh2 (columns)
+      if constexpr (KR == 1) {  // resident B half of N block sc.nb: qb tiles of 64 (q) x bnh2 (columns)
         const int brow0 = sc.nb * p.BN + (int)rank * bnh2;
         mbar_arrive_expect_tx(res_full, res_bytes);
         for (int q = 0; q < qb; ++q) {
@@ -489,6 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (NB == 2) tma_load_2d(resident + (size_t)(qb + q) * bh_bytes, &tm_blo, res_full, q * BK, brow0);
         }
       }
+      const uint32_t tx_bytes = KR == 0 ? stage_bytes : kAStageBytes;
       int s = 0;
       uint32_t ph = 0;
       for (int t = sc.first; t < sc.count; t += sc.step) {
@@ -499,8 +513,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + (size_t)s * stage_bytes;
-          mbar_arrive_expect_tx(&tma_full[s], stage_bytes);
-          if constexpr (KR) {  // A as (q, P, row) [TA: (col, q, P)]; box 64 q x 1 P x 128, q >= dl zero-filled
+          mbar_arrive_expect_tx(&tma_full[s], tx_bytes);
+          if constexpr (KR != 0) {  // A as (q, P, row) [TA: (col, q, P)]; box 64 q x 1 P x 128, q >= dl zero-filled
             const int P = kb / qb, q0 = (kb - P * qb) * BK;
             if (TA) tma_load_3d(st, &tm_a, &tma_full[s], row0, q0, P);
             else tma_load_3d(st, &tm_a, &tma_full[s], q0, P, row0);
@@ -533,8 +547,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const uint32_t st = sm100::smem_u32(smem + (size_t)s * stage_bytes);
             const uint32_t a_hi = st, a_lo = st + a_bytes;
-            const uint32_t b = KR ? sm100::smem_u32(resident) + (uint32_t)(kb - c0) * bh_bytes : st + kAStageBytes;
-            const uint32_t blo = KR ? b + (uint32_t)qb * bh_bytes : b + bh_bytes;
+            const uint32_t b = KR == 1 ? sm100::smem_u32(resident) + (uint32_t)(kb - c0) * bh_bytes : st + kAStageBytes;
+            const uint32_t blo = KR == 1 ? b + (uint32_t)qb * bh_bytes : b + bh_bytes;
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
               const uint64_t db = sdesc_kmajor_sw128(b + kk * 32);
@@ -549,6 +563,57 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma_commit_pair(&acc_full[buf]);
         }
       }
+    } else if (KR == 2 && warp >= 2) {
+      // -------------------------------------------------------------- B synthesis (KR = 2), warps 2-3
+      // tile row c (= column jg of Y) of k-block (P, qq): 64 bf16 +-1 = sign bits of F^T[jg, 64 qq ..]
+      // XOR W[P, jg]; 16-byte chunk ch (q = 8 ch .. 8 ch + 7) lands at (ch ^ (c & 7)) (SWIZZLE_128B)
+      const int st_id = threadIdx.x - 64;  // 0..63
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = sc.first; t < sc.count; t += sc.step) {
+        const Unit w = pair_unit<KR>(p, sc, t);
+        const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
+        const int jb = w.nb * p.BN + (int)rank * bnh2;  // first Y column of this CTA's B half
+        for (int kb = kb0; kb < kb1; ++kb) {
+          const int P = kb / qb, qq = kb - P * qb;
+          // sign words for this thread's rows (loaded before the stage is free)
+          uint32_t lo[2], hi[2];
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int c = st_id + 64 * i;
+            const int jg = jb + c;
+            lo[i] = hi[i] = 0u;
+            if (c < bnh2 && jg < p.N) {
+              const uint32_t wbit = (__ldg(p.kr_wbits + (int64_t)P * p.kr_wwords + (jg >> 5)) >> (jg & 31)) & 1u;
+              const uint32_t m = 0u - wbit;
+              const uint2 f = __ldg(reinterpret_cast<const uint2*>(p.kr_fbits + (int64_t)jg * p.kr_fwords) + qq);
+              lo[i] = f.x ^ m;
+              hi[i] = f.y ^ m;
+            }
+          }
+          mbar_wait(&empty[s], ph ^ 1);
+          const uint32_t bt = sm100::smem_u32(smem + (size_t)s * stage_bytes) + kAStageBytes;
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int c = st_id + 64 * i;
+            if (c < bnh2) {
+#pragma unroll
+              for (int ch = 0; ch < 8; ++ch) {
+                const uint32_t byte = ((ch < 4 ? lo[i] : hi[i]) >> (8 * (ch & 3))) & 0xffu;
+                uint32_t v[4];
+#pragma unroll
+                for (int pp = 0; pp < 4; ++pp)
+                  v[pp] = 0x3f803f80u | (((byte >> (2 * pp)) & 1u) << 15) | (((byte >> (2 * pp + 1)) & 1u) << 31);
+                sts128u(bt + (uint32_t)c * 128u + ((uint32_t)(ch ^ (c & 7)) << 4), v[0], v[1], v[2], v[3]);
+              }
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote(full_leader + 8u * (uint32_t)s);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+      }
     }
   } else if (warp < 8) {
     setmaxnreg_dec<128>();
@@ -556,9 +621,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ct = threadIdx.x - 128;
     const int c4 = ct & 15;
     const int rsub = ct >> 4;
-    // KR: the leader's first MMA reads both CTAs' resident B halves; it waits for every converter
+    // KR = 1: the leader's first MMA reads both CTAs' resident B halves; it waits for every converter
     // warp of both CTAs, so each CTA's converters first wait for their own CTA's resident half
-    if constexpr (KR) mbar_wait(res_full, 0);
+    if constexpr (KR == 1) mbar_wait(res_full, 0);
     int s = 0;
     uint32_t ph = 0;
     for (int t = sc.first; t < sc.count; t += sc.step) {
@@ -637,25 +702,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&acc_full[buf], use & 1);
         tc_fence_after();
         const uint32_t base = tmem + ((uint32_t)(32 * lg) << 16) + buf * (uint32_t)p.BN + hoff;
-        // KR: the chunk's column weights W[P][col0 ...] (the same address in every lane: broadcast)
+        // KR = 1: the chunk's column weights W[P][col0 ...] (the same address in every lane: broadcast)
         const float4* wrow = nullptr;
-        if constexpr (KR) wrow = reinterpret_cast<const float4*>(p.kr_w + (int64_t)(c0 / qb) * p.kr_ldw + col0);
+        if constexpr (KR == 1) wrow = reinterpret_cast<const float4*>(p.kr_w + (int64_t)(c0 / qb) * p.kr_ldw + col0);
 #pragma unroll
         for (int g = 0; g < kMaxBNH / 16; ++g) {
           if (g * 16 < bnh) {
             uint32_t r[16];
             tmem_ld16(base + g * 16, r);
-            if constexpr (KR) {
+            if constexpr (KR == 1) {
+              float wv[16];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {  // issued with the TMEM load, consumed after its wait
+                const float4 x = ldg_nc_v4(wrow + 4 * g + j);
+                wv[4 * j] = x.x;
+                wv[4 * j + 1] = x.y;
+                wv[4 * j + 2] = x.z;
+                wv[4 * j + 3] = x.w;
+              }
               tmem_ld_wait();
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const float4 x = ldg_nc_v4(wrow + 4 * g + j);  // volatile: stays after the TMEM wait
-                float* sg = sum + g * 16 + 4 * j;
-                sg[0] = fmaf(x.x, __uint_as_float(r[4 * j]), sg[0]);
-                sg[1] = fmaf(x.y, __uint_as_float(r[4 * j + 1]), sg[1]);
-                sg[2] = fmaf(x.z, __uint_as_float(r[4 * j + 2]), sg[2]);
-                sg[3] = fmaf(x.w, __uint_as_float(r[4 * j + 3]), sg[3]);
-              }
+              for (int j = 0; j < 16; ++j) sum[g * 16 + j] = fmaf(wv[j], __uint_as_float(r[j]), sum[g * 16 + j]);
             } else {
               tmem_ld_wait();
 #pragma unroll
@@ -853,8 +920,8 @@ bool use_pair(int64_t n) {
 int launch_pair(int NB, bool TA, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mbl, TcParams& p,
                 size_t smem, cudaStream_t s) {
   using KernT = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams);
-  KernT kern = TA ? (NB == 2 ? dense_tc_pair_kernel<2, true, false> : dense_tc_pair_kernel<1, true, false>)
-                  : (NB == 2 ? dense_tc_pair_kernel<2, false, false> : dense_tc_pair_kernel<1, false, false>);
+  KernT kern = TA ? (NB == 2 ? dense_tc_pair_kernel<2, true, 0> : dense_tc_pair_kernel<1, true, 0>)
+                  : (NB == 2 ? dense_tc_pair_kernel<2, false, 0> : dense_tc_pair_kernel<1, false, 0>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(2 * (sm_count() / 2)));
@@ -920,14 +987,15 @@ struct KrPlan {
 };
 
 using KernT = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams);
-KernT kr_kernel(int NB, bool TA) {
-  return TA ? (NB == 2 ? dense_tc_pair_kernel<2, true, true> : dense_tc_pair_kernel<1, true, true>)
-            : (NB == 2 ? dense_tc_pair_kernel<2, false, true> : dense_tc_pair_kernel<1, false, true>);
+// mode 1: resident F (general factors), mode 2: B synthesised from sign bits (+-1 factors)
+KernT kr_kernel(int NB, bool TA, int mode) {
+  if (mode == 2) return TA ? dense_tc_pair_kernel<1, true, 2> : dense_tc_pair_kernel<1, false, 2>;
+  return TA ? (NB == 2 ? dense_tc_pair_kernel<2, true, 1> : dense_tc_pair_kernel<1, true, 1>)
+            : (NB == 2 ? dense_tc_pair_kernel<2, false, 1> : dense_tc_pair_kernel<1, false, 1>);
 }
 
-// co-resident 2-CTA clusters of the KR kernel at this shared-memory size
-int kr_max_clusters(int NB, bool TA, size_t smem) {
-  KernT kern = kr_kernel(NB, TA);
+// co-resident 2-CTA clusters of a KR kernel at this shared-memory size
+int kr_max_clusters(KernT kern, size_t smem) {
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(2 * (sm_count() / 2)));
@@ -948,31 +1016,37 @@ int kr_max_clusters(int NB, bool TA, size_t smem) {
   return mc;
 }
 
-// kslab = columns of this launch (<= kKrMaxCols); maxc < 0: no device query (workspace sizing)
-bool make_plan_kr(KrPlan& pl, int64_t n, int64_t P, int64_t dl, int64_t kslab, int NB, int maxc, bool ta) {
+// kslab = columns of this launch (<= kKrMaxCols); maxc <= 0: no device query (workspace sizing)
+bool make_plan_kr(KrPlan& pl, int64_t n, int64_t P, int64_t dl, int64_t kslab, int NB, int mode, int maxc, bool ta) {
   pl = KrPlan{};
   pl.qb = (int)((dl + BK - 1) / BK);
   pl.nblocks = (int)((kslab + 255) / 256);
+  const size_t budget = 227 * 1024 - 1024 - 512;
+  size_t res = 0, stage = 0;
   for (;;) {
     const int64_t per = (kslab + pl.nblocks - 1) / pl.nblocks;
     pl.BN = (int)((per + 15) / 16 * 16);
-    const size_t res = (size_t)NB * pl.qb * (pl.BN / 2) * 128;
+    if (mode == 2) {  // stage = A + synthesised B half
+      stage = kAStageBytes + (size_t)(pl.BN / 2) * 128;
+      break;
+    }
+    res = (size_t)NB * pl.qb * (pl.BN / 2) * 128;
+    stage = kAStageBytes;
     if (res <= 160 * 1024) break;
     if (pl.BN <= 32) return false;
     pl.nblocks *= 2;
   }
-  const size_t res = (size_t)NB * pl.qb * (pl.BN / 2) * 128;
-  const size_t budget = 227 * 1024 - 1024 - 512;
-  if (res + 2 * (size_t)kAStageBytes > budget) return false;
-  int stages = (int)((budget - res) / kAStageBytes);
+  if (res + 2 * stage > budget) return false;
+  int stages = (int)((budget - res) / stage);
   if (stages > 6) stages = 6;
   pl.stages = stages;
-  pl.smem = 1024 + (size_t)stages * kAStageBytes + res + (3 * stages + 5) * 8 + 16;
+  pl.smem = 1024 + (size_t)stages * stage + res + (3 * stages + 5) * 8 + 16;
   pl.mtiles = (int)((n + 2 * BM - 1) / (2 * BM));
   const int mc = maxc > 0 ? maxc : sm_count() / 2;
   const int gp = mc / pl.nblocks > 0 ? mc / pl.nblocks : 1;  // pairs per N-block group
   int ks = 1;
-  while ((int64_t)pl.mtiles * ks < 4 * gp && P / (2 * ks) >= 2) ks *= 2;
+  while ((int64_t)pl.mtiles * ks < 4 * gp && P / (2 * ks) >= 2 && (mode != 2 || P * pl.qb / (2 * ks) >= CHUNK_KB))
+    ks *= 2;
   const int64_t p_per = (P + ks - 1) / ks;
   pl.kb_per_split = (int)(p_per * pl.qb);
   pl.ksplit = (int)((P + p_per - 1) / p_per);
@@ -982,53 +1056,72 @@ bool make_plan_kr(KrPlan& pl, int64_t n, int64_t P, int64_t dl, int64_t kslab, i
   return true;
 }
 
-size_t kr_workspace(int64_t n, int64_t P, int64_t dl, int64_t k, int NB, bool ta) {
+size_t kr_workspace(int64_t n, int64_t P, int64_t dl, int64_t k, int NB, int mode, bool ta) {
   size_t ws = 0;
   for (int64_t c0 = 0; c0 < k; c0 += kKrMaxCols) {
     const int64_t ks = k - c0 < kKrMaxCols ? k - c0 : kKrMaxCols;
-    KrPlan pl;
-    if (!make_plan_kr(pl, n, P, dl, ks, NB, -1, ta)) return 0;
-    // the real grid may have fewer pairs per group -> more K splits; size for the largest split count
-    KrPlan pl1;
-    make_plan_kr(pl1, n, P, dl, ks, NB, 2 * pl.nblocks, ta);
+    KrPlan pl, pl1;
+    if (!make_plan_kr(pl, n, P, dl, ks, NB, mode, -1, ta)) return 0;
+    // the real grid may hold fewer pairs per group (more K splits): size for 2 pairs per group too
+    make_plan_kr(pl1, n, P, dl, ks, NB, mode, 2 * pl.nblocks, ta);
     const size_t w = pl.ws_bytes > pl1.ws_bytes ? pl.ws_bytes : pl1.ws_bytes;
     if (w > ws) ws = w;
   }
   return ws;
 }
 
+struct KrOperands {
+  const uint16_t* ft_hi;  // mode 1: F^T bf16 (k x ldf) and residual (or null)
+  const uint16_t* ft_lo;
+  int64_t ldf;
+  const float* w;  // mode 1: W (P x ldw) float32
+  int64_t ldw;
+  const uint32_t* fbits;  // mode 2: sign bits (layouts in TcParams)
+  const uint32_t* wbits;
+};
+
 // rows: output rows (A rows, or B columns when TA); out: Y [rows][k] (ldy) or, when TA, X [k][rows]
-int kr_run(bool TA, const float* A, int64_t rows, int64_t P, int64_t dl, int64_t lda, const uint16_t* Ft_hi,
-           const uint16_t* Ft_lo, int64_t ldf, const float* W, int64_t ldw, int64_t k, double scale, float* Y,
-           int64_t ldy, void* ws, size_t ws_bytes, cudaStream_t s, const char* what) {
-  const int NB = Ft_lo ? 2 : 1;
+int kr_run(bool TA, int mode, const float* A, int64_t rows, int64_t P, int64_t dl, int64_t lda, const KrOperands& o,
+           int64_t k, double scale, float* Y, int64_t ldy, void* ws, size_t ws_bytes, cudaStream_t s, const char* what) {
+  const int NB = (mode == 1 && o.ft_lo) ? 2 : 1;
   CUtensorMap ma;
   int st = make_a3_map(&ma, A, rows, P, dl, lda, TA);
   if (st != SK_OK) return st;
+  KernT kern = kr_kernel(NB, TA, mode);
+  const int64_t fwords = 2 * ((dl + BK - 1) / BK), wwords = (k + 31) / 32;
   for (int64_t c0 = 0; c0 < k; c0 += kKrMaxCols) {
     const int64_t kslab = k - c0 < kKrMaxCols ? k - c0 : kKrMaxCols;
     KrPlan pl;
-    if (!make_plan_kr(pl, rows, P, dl, kslab, NB, -1, TA))
+    if (!make_plan_kr(pl, rows, P, dl, kslab, NB, mode, -1, TA))
       return fail(SK_EUNSUPPORTED, std::string(what) + ": resident factor does not fit shared memory");
-    static int maxc_cache[4] = {0, 0, 0, 0};
-    static size_t maxc_smem[4] = {0, 0, 0, 0};
-    const int slot = (NB - 1) + 2 * (TA ? 1 : 0);
-    if (maxc_smem[slot] != pl.smem) {
-      maxc_cache[slot] = kr_max_clusters(NB, TA, pl.smem);
+    static KernT maxc_kern[8] = {};
+    static size_t maxc_smem[8] = {};
+    static int maxc_val[8] = {};
+    int slot = 0;
+    while (slot < 7 && maxc_kern[slot] && !(maxc_kern[slot] == kern && maxc_smem[slot] == pl.smem)) ++slot;
+    if (maxc_kern[slot] != kern || maxc_smem[slot] != pl.smem) {
+      maxc_kern[slot] = kern;
       maxc_smem[slot] = pl.smem;
+      maxc_val[slot] = kr_max_clusters(kern, pl.smem);
     }
-    if (maxc_cache[slot] < pl.nblocks) return fail(SK_EUNSUPPORTED, std::string(what) + ": too few co-resident pairs");
-    make_plan_kr(pl, rows, P, dl, kslab, NB, maxc_cache[slot], TA);
+    const int maxc = maxc_val[slot];
+    if (maxc < pl.nblocks) return fail(SK_EUNSUPPORTED, std::string(what) + ": too few co-resident pairs");
+    make_plan_kr(pl, rows, P, dl, kslab, NB, mode, maxc, TA);
     if (pl.ws_bytes > 0 && (ws == nullptr || ws_bytes < pl.ws_bytes))
       return fail(SK_EINVAL, std::string(what) + ": workspace too small (sk_kr_workspace_bytes)");
     CUtensorMap mb, mbl;
-    st = make_bt_map(&mb, Ft_hi + c0 * ldf, kslab, dl, ldf, pl.BN / 2);
-    if (st != SK_OK) return st;
-    if (NB == 2) {
-      st = make_bt_map(&mbl, Ft_lo + c0 * ldf, kslab, dl, ldf, pl.BN / 2);
+    if (mode == 1) {
+      st = make_bt_map(&mb, o.ft_hi + c0 * o.ldf, kslab, dl, o.ldf, pl.BN / 2);
       if (st != SK_OK) return st;
+      if (NB == 2) {
+        st = make_bt_map(&mbl, o.ft_lo + c0 * o.ldf, kslab, dl, o.ldf, pl.BN / 2);
+        if (st != SK_OK) return st;
+      } else {
+        mbl = mb;
+      }
     } else {
-      mbl = mb;
+      mb = ma;  // unused (B is synthesised)
+      mbl = ma;
     }
     TcParams p{};
     p.A = A;
@@ -1047,15 +1140,21 @@ int kr_run(bool TA, const float* A, int64_t rows, int64_t P, int64_t dl, int64_t
     p.part = static_cast<float*>(ws);
     p.num_units = pl.mtiles * pl.ksplit * pl.nblocks;
     p.mtiles = pl.mtiles;
-    p.kr_w = W + c0;
-    p.kr_ldw = ldw;
+    if (mode == 1) {
+      p.kr_w = o.w + c0;
+      p.kr_ldw = o.ldw;
+    } else {
+      p.kr_fbits = o.fbits + c0 * fwords;  // c0 is a multiple of 32: whole words of W bits
+      p.kr_fwords = fwords;
+      p.kr_wbits = o.wbits + c0 / 32;
+      p.kr_wwords = wwords;
+    }
     p.kr_qb = pl.qb;
     p.kr_ngroups = pl.nblocks;
     p.out_t = TA ? 1 : 0;
     uint32_t cols = 32;
     while (cols < (uint32_t)(2 * pl.BN)) cols <<= 1;
     p.tmem_cols = cols;
-    KernT kern = kr_kernel(NB, TA);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(2 * pl.npairs));
@@ -1069,6 +1168,9 @@ int kr_run(bool TA, const float* A, int64_t rows, int64_t P, int64_t dl, int64_t
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (getenv("SKETCH_B200_TC_PAIR_VERBOSE"))
+      fprintf(stderr, "%s: mode %d BN %d nblocks %d ksplit %d kb/split %d stages %d pairs %d (max %d) smem %zu\n", what,
+              mode, pl.BN, pl.nblocks, pl.ksplit, pl.kb_per_split, pl.stages, pl.npairs, maxc, pl.smem);
     if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mbl, p) != cudaSuccess) return check_launch(what);
     st = check_launch(what);
     if (st != SK_OK) return st;
@@ -1085,14 +1187,19 @@ int kr_run(bool TA, const float* A, int64_t rows, int64_t P, int64_t dl, int64_t
   return SK_OK;
 }
 
-int kr_check(const float* A, int64_t rows, int64_t P, int64_t dl, int64_t lda, int64_t minlda, const uint16_t* Ft_hi,
-             const uint16_t* Ft_lo, int64_t ldf, const float* W, int64_t ldw, int64_t k, const float* Y, int64_t ldy,
-             int64_t minldy, const char* what) {
-  if (rows < 0 || P < 1 || dl < 1 || k < 1 || lda < minlda || ldf < dl || ldw < k || ldy < minldy)
+int kr_check(const float* A, int64_t rows, int64_t P, int64_t dl, int64_t lda, int64_t minlda, int64_t k,
+             const float* Y, int64_t ldy, int64_t minldy, const char* what) {
+  if (rows < 0 || P < 1 || dl < 1 || k < 1 || lda < minlda || ldy < minldy)
     return fail(SK_EINVAL, std::string(what) + ": bad shape");
-  if (!A || !Ft_hi || !W || !Y) return fail(SK_EINVAL, std::string(what) + ": null pointer");
+  if (!A || !Y) return fail(SK_EINVAL, std::string(what) + ": null pointer");
   if ((reinterpret_cast<uintptr_t>(A) & 15) || (lda & 3) || (dl & 3))
     return fail(SK_EINVAL, std::string(what) + ": A must be 16-byte aligned with lda, dl multiples of 4");
+  return SK_OK;
+}
+
+int kr_check_f(const uint16_t* Ft_hi, const uint16_t* Ft_lo, int64_t ldf, int64_t dl, const float* W, int64_t ldw,
+               int64_t k, const char* what) {
+  if (!Ft_hi || !W || ldf < dl || ldw < k) return fail(SK_EINVAL, std::string(what) + ": bad factor operands");
   if ((reinterpret_cast<uintptr_t>(Ft_hi) & 15) || (ldf & 7) || (Ft_lo && (reinterpret_cast<uintptr_t>(Ft_lo) & 15)))
     return fail(SK_EINVAL, std::string(what) + ": F^T must be 16-byte aligned with ldf a multiple of 8");
   if ((reinterpret_cast<uintptr_t>(W) & 15) || (ldw & 3))
@@ -1338,7 +1445,7 @@ extern "C" int sk_dense_tn_tc(const float* A, int64_t n, int64_t d, int64_t lda,
 // trans = 0: sk_kr_right with n rows; trans = 1: sk_kr_adjoint with n = m columns of B
 extern "C" size_t sk_kr_workspace_bytes(int64_t n, int64_t P, int64_t dl, int64_t k, int split_f, int trans) {
   if (n < 1 || P < 1 || dl < 1 || k < 1) return 0;
-  return skb::kr_workspace(n, P, dl, k, split_f ? 2 : 1, trans != 0);
+  return skb::kr_workspace(n, P, dl, k, split_f ? 2 : 1, 1, trans != 0);
 }
 
 // Y[n, k] = scale * sum_{P, q} A[i, P * dl + q] * W[P, j] * F[q, j]   (Khatri-Rao, Omega never formed)
@@ -1346,10 +1453,11 @@ extern "C" int sk_kr_right(const float* A, int64_t n, int64_t P, int64_t dl, int
                            const uint16_t* Ft_lo, int64_t ldf, const float* W, int64_t ldw, int64_t k, double scale,
                            float* Y, int64_t ldy, void* ws, size_t ws_bytes, void* stream) {
   using namespace skb;
-  int st = kr_check(A, n, P, dl, lda, P * dl, Ft_hi, Ft_lo, ldf, W, ldw, k, Y, ldy, k, "sk_kr_right");
+  int st = kr_check(A, n, P, dl, lda, P * dl, k, Y, ldy, k, "sk_kr_right");
+  if (st == SK_OK) st = kr_check_f(Ft_hi, Ft_lo, ldf, dl, W, ldw, k, "sk_kr_right");
   if (st != SK_OK || n == 0) return st;
-  return kr_run(false, A, n, P, dl, lda, Ft_hi, Ft_lo, ldf, W, ldw, k, scale, Y, ldy, ws, ws_bytes,
-                as_stream(stream), "sk_kr_right");
+  const KrOperands o{Ft_hi, Ft_lo, ldf, W, ldw, nullptr, nullptr};
+  return kr_run(false, 1, A, n, P, dl, lda, o, k, scale, Y, ldy, ws, ws_bytes, as_stream(stream), "sk_kr_right");
 }
 
 // X[k, m] = scale * Omega^T B for B [P * dl rows][m] (row stride ldb), read in place (no transposed copy)
@@ -1357,8 +1465,40 @@ extern "C" int sk_kr_adjoint(const float* B, int64_t m, int64_t P, int64_t dl, i
                              const uint16_t* Ft_lo, int64_t ldf, const float* W, int64_t ldw, int64_t k,
                              double scale, float* X, int64_t ldx, void* ws, size_t ws_bytes, void* stream) {
   using namespace skb;
-  int st = kr_check(B, m, P, dl, ldb, m, Ft_hi, Ft_lo, ldf, W, ldw, k, X, ldx, m, "sk_kr_adjoint");
+  int st = kr_check(B, m, P, dl, ldb, m, k, X, ldx, m, "sk_kr_adjoint");
+  if (st == SK_OK) st = kr_check_f(Ft_hi, Ft_lo, ldf, dl, W, ldw, k, "sk_kr_adjoint");
   if (st != SK_OK || m == 0) return st;
-  return kr_run(true, B, m, P, dl, ldb, Ft_hi, Ft_lo, ldf, W, ldw, k, scale, X, ldx, ws, ws_bytes, as_stream(stream),
-                "sk_kr_adjoint");
+  const KrOperands o{Ft_hi, Ft_lo, ldf, W, ldw, nullptr, nullptr};
+  return kr_run(true, 1, B, m, P, dl, ldb, o, k, scale, X, ldx, ws, ws_bytes, as_stream(stream), "sk_kr_adjoint");
+}
+
+extern "C" size_t sk_kr2_workspace_bytes(int64_t n, int64_t P, int64_t dl, int64_t k, int trans) {
+  if (n < 1 || P < 1 || dl < 1 || k < 1) return 0;
+  return skb::kr_workspace(n, P, dl, k, 1, 2, trans != 0);
+}
+
+// +-1 factors from sign bits only (SURVEY 8(b) sk_kr2_right): f_neg[j * 2 ceil(dl/64) + w] holds the
+// signs of F^T[j, 32 w ..] (bit q % 32), w_neg[P * ceil(k/32) + j / 32] bit j % 32 the sign of W[P, j]
+extern "C" int sk_kr2_right(const float* A, int64_t n, int64_t P, int64_t dl, int64_t lda, const uint32_t* f_neg,
+                            const uint32_t* w_neg, int64_t k, double scale, float* Y, int64_t ldy, void* ws,
+                            size_t ws_bytes, void* stream) {
+  using namespace skb;
+  int st = kr_check(A, n, P, dl, lda, P * dl, k, Y, ldy, k, "sk_kr2_right");
+  if (st != SK_OK || n == 0) return st;
+  if (!f_neg || !w_neg || (reinterpret_cast<uintptr_t>(f_neg) & 7) || (reinterpret_cast<uintptr_t>(w_neg) & 3))
+    return fail(SK_EINVAL, "sk_kr2_right: sign-bit arrays must be 8-byte aligned");
+  const KrOperands o{nullptr, nullptr, 0, nullptr, 0, f_neg, w_neg};
+  return kr_run(false, 2, A, n, P, dl, lda, o, k, scale, Y, ldy, ws, ws_bytes, as_stream(stream), "sk_kr2_right");
+}
+
+extern "C" int sk_kr2_adjoint(const float* B, int64_t m, int64_t P, int64_t dl, int64_t ldb, const uint32_t* f_neg,
+                              const uint32_t* w_neg, int64_t k, double scale, float* X, int64_t ldx, void* ws,
+                              size_t ws_bytes, void* stream) {
+  using namespace skb;
+  int st = kr_check(B, m, P, dl, ldb, m, k, X, ldx, m, "sk_kr2_adjoint");
+  if (st != SK_OK || m == 0) return st;
+  if (!f_neg || !w_neg || (reinterpret_cast<uintptr_t>(f_neg) & 7) || (reinterpret_cast<uintptr_t>(w_neg) & 3))
+    return fail(SK_EINVAL, "sk_kr2_adjoint: sign-bit arrays must be 8-byte aligned");
+  const KrOperands o{nullptr, nullptr, 0, nullptr, 0, f_neg, w_neg};
+  return kr_run(true, 2, B, m, P, dl, ldb, o, k, scale, X, ldx, ws, ws_bytes, as_stream(stream), "sk_kr2_adjoint");
 }
