@@ -277,23 +277,6 @@ SK_API int sk_kr_adjoint(const float* B, int64_t m, int64_t P, int64_t dl, int64
                          const uint16_t* Ft_lo, int64_t ldf, const float* W, int64_t ldw, int64_t k, double scale,
                          float* X, int64_t ldx, void* ws, size_t ws_bytes, void* stream);
 /*
- * K4s — +-1 factors (Rademacher, config 5) from their sign bits only: SURVEY 8(b)'s sk_kr2_right.
- * Nothing but 1 bit per factor entry is read for Omega: f_neg[j * 2*ceil(dl/64) + w] bit b = sign of
- * F[32 w + b, j] (F = the trailing factors' Khatri-Rao product, 2 words per 64-wide k-block, padding
- * bits ignored), w_neg[P * ceil(k/32) + j/32] bit j%32 = sign of W[P, j].  For config 5 these are
- * factor 1 and factor 0: 2 x 256 x 512 bits = 32 KB.  Each CTA pair synthesises every k-block's
- * +-1 bf16 B tile in shared memory (two warps, SWIZZLE_128B layout) next to the TMA-streamed A,
- * chunks of 1024 of K in TMEM as K-TC.  f_neg 8-byte and w_neg 4-byte aligned; A as sk_kr_right.
- * Workspace: sk_kr2_workspace_bytes(n, P, dl, k, trans).
- */
-SK_API size_t sk_kr2_workspace_bytes(int64_t n, int64_t P, int64_t dl, int64_t k, int trans);
-SK_API int sk_kr2_right(const float* A, int64_t n, int64_t P, int64_t dl, int64_t lda, const uint32_t* f_neg,
-                        const uint32_t* w_neg, int64_t k, double scale, float* Y, int64_t ldy, void* ws,
-                        size_t ws_bytes, void* stream);
-SK_API int sk_kr2_adjoint(const float* B, int64_t m, int64_t P, int64_t dl, int64_t ldb, const uint32_t* f_neg,
-                          const uint32_t* w_neg, int64_t k, double scale, float* X, int64_t ldx, void* ws,
-                          size_t ws_bytes, void* stream);
-/*
  * K4c — the same contractions on the CUDA cores for float64 (the reference's dtype; float64
  * accumulation, parity 1e-12) and float32 shapes the tcgen05 form does not take.  F is dl x k
  * (row stride ldf) and W is P x k (row stride ldw), both of `dtype`.  Adjoint: X[k,m] from B [P*dl][m].

@@ -85,11 +85,6 @@ SIGNATURES = {
                              _c_p, _c_i64, _c_p, _c_size, _c_p]),
     "sk_kr_adjoint": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_p, _c_i64, _c_i64, _c_dbl,
                                _c_p, _c_i64, _c_p, _c_size, _c_p]),
-    "sk_kr2_workspace_bytes": (_c_size, [_c_i64, _c_i64, _c_i64, _c_i64, _c_int]),
-    "sk_kr2_right": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_dbl, _c_p, _c_i64, _c_p,
-                              _c_size, _c_p]),
-    "sk_kr2_adjoint": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_dbl, _c_p, _c_i64, _c_p,
-                                _c_size, _c_p]),
     "sk_kr_right_cc": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_i64,
                                 _c_dbl, _c_p, _c_i64, _c_p]),
     "sk_kr_adjoint_cc": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_i64,

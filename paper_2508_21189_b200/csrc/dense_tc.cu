@@ -55,21 +55,16 @@ struct TcParams {
   float* part;     // ... or partial sums [ksplit][M][N] (ksplit > 1)
   int num_units;
   int mtiles;
-  // Khatri-Rao modes (dense_tc_pair_kernel<.., KR = 1 | 2>): K = (P, q) with q < dl fastest, A read
+  // Khatri-Rao mode (dense_tc_pair_kernel<.., KR = 1>): K = (P, q) with q < dl fastest, A read
   // through a 3-D map (q >= dl of a 64-wide k-block is zero-filled).
   // KR = 1: F^T (k x dl bf16) resident in shared memory, chunk = one P (kr_qb k-blocks), a finished
   //         chunk folded with the column weights W[P][col] (the product of the other factors' rows).
-  // KR = 2: +-1 factors; B tiles synthesised from sign bits: kr_fbits[j * kr_fwords + 2 qq (+1)] =
-  //         the 64 signs of F^T[j, 64 qq ..] (bit q % 32), kr_wbits[P * kr_wwords + j / 32] bit j % 32.
   const float* kr_w;
   int64_t kr_ldw;
-  const uint32_t* kr_fbits;
-  int64_t kr_fwords;
-  const uint32_t* kr_wbits;
-  int64_t kr_wwords;
   int kr_qb;       // k-blocks per P (ceil(dl / 64))
   int kr_ngroups;  // N blocks, one per group of pairs (each pair keeps one N block)
   int out_t;       // result transposed: element (row, col) -> Y[col * ldy + row] (through the reduce)
+  int kr_a2d;      // dl % 64 == 0: A through the 2-D map (k-block kb = columns 64 kb ..), else 3-D
 };
 
 
@@ -427,11 +422,8 @@ __device__ __forceinline__ Unit pair_unit(const TcParams& p, const PairSched& s,
 }
 
 // KR = 0: dense B^T streamed by TMA with A.
-// KR = 1: Khatri-Rao, general factors: F^T resident in shared memory (qb tiles per CTA half), one
-//         P per TMEM chunk, reducers fold each chunk scaled by W[P, :].
-// KR = 2: Khatri-Rao, +-1 factors: warps 2-3 synthesise each k-block's B tile (F^T sign-flipped by
-//         W[P, :]) in the stage from sign bits (F: 2 words per column and k-block; W: one bit per
-//         (P, column)); chunks of CHUNK_KB k-blocks as the dense engine.  Omega is never formed.
+// KR = 1: Khatri-Rao: F^T resident in shared memory (qb tiles per CTA half), one P per TMEM chunk,
+//         reducers fold each chunk scaled by W[P, :].  Omega is never formed.
 template <int NB, bool TA, int KR>
 __global__ void __launch_bounds__(kThreads, 1)
     dense_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
@@ -445,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t stage_bytes = KR == 1 ? kAStageBytes : kAStageBytes + NB * bh_bytes;
   const int S = p.stages;
   const int qb = KR ? p.kr_qb : 1;
-  uint8_t* resident = smem + (size_t)S * stage_bytes;  // KR = 1: [NB][qb] tiles of bh_bytes
+  uint8_t* resident = smem + (size_t)S * stage_bytes;  // KR = 1: [NB][qb] F^T tiles of bh_bytes
   const uint32_t res_bytes = KR == 1 ? (uint32_t)NB * (uint32_t)qb * bh_bytes : 0u;
   uint64_t* tma_full = reinterpret_cast<uint64_t*>(resident + res_bytes);
   uint64_t* full = tma_full + S;       // leader: converted (and, KR = 2, synthesised) in both CTAs
@@ -463,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&tma_full[s], 1);
-      mbar_init(&full[s], KR == 2 ? 12 : 8);  // leader: converter (+ synthesis) warps of both CTAs
+      mbar_init(&full[s], 8);  // leader: the converter warps of both CTAs
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -473,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(res_full, 1);
     fence_mbar_init();
     tma_prefetch_desc(&tm_a);
-    if (KR != 2) tma_prefetch_desc(&tm_b);
+    tma_prefetch_desc(&tm_b);
     if (NB == 2) tma_prefetch_desc(&tm_blo);
   }
   if (warp == 2) {
@@ -494,7 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     setmaxnreg_dec<48>();  // 128 x 48 + 128 x 128 + 256 x 168 = 64K registers
     if (warp == 0 && lane == 0) {
       // -------------------------------------------------------------- producer (this CTA's rows + B half)
-      if constexpr (KR == 1) {  // resident B half of N block sc.nb: qb tiles of 64 (q) x bnh2 (columns)
+      if constexpr (KR == 1) {  // resident F^T half of N block sc.nb: qb tiles of 64 (q) x bnh2 (columns)
         const int brow0 = sc.nb * p.BN + (int)rank * bnh2;
         mbar_arrive_expect_tx(res_full, res_bytes);
         for (int q = 0; q < qb; ++q) {
@@ -502,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (NB == 2) tma_load_2d(resident + (size_t)(qb + q) * bh_bytes, &tm_blo, res_full, q * BK, brow0);
         }
       }
-      const uint32_t tx_bytes = KR == 0 ? stage_bytes : kAStageBytes;
+      const uint32_t tx_bytes = KR == 1 ? kAStageBytes : stage_bytes;
       int s = 0;
       uint32_t ph = 0;
       for (int t = sc.first; t < sc.count; t += sc.step) {
@@ -514,10 +506,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + (size_t)s * stage_bytes;
           mbar_arrive_expect_tx(&tma_full[s], tx_bytes);
-          if constexpr (KR != 0) {  // A as (q, P, row) [TA: (col, q, P)]; box 64 q x 1 P x 128, q >= dl zero-filled
+          if (KR != 0 && !p.kr_a2d) {  // A as (q, P, row) [TA: (col, q, P)]; box 64 q x 1 P x 128, q >= dl zero
             const int P = kb / qb, q0 = (kb - P * qb) * BK;
             if (TA) tma_load_3d(st, &tm_a, &tma_full[s], row0, q0, P);
             else tma_load_3d(st, &tm_a, &tma_full[s], q0, P, row0);
+          } else if (KR != 0) {  // dl % 64 == 0: the plain 2-D map (measured faster than the 3-D box)
+            if (TA) tma_load_2d(st, &tm_a, &tma_full[s], row0, kb * BK);
+            else tma_load_2d(st, &tm_a, &tma_full[s], kb * BK, row0);
           } else {
             if (TA) tma_load_2d(st, &tm_a, &tma_full[s], row0, kb * BK);
             else tma_load_2d(st, &tm_a, &tma_full[s], kb * BK, row0);
@@ -561,57 +556,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (++s == S) { s = 0; ph ^= 1; }
           }
           umma_commit_pair(&acc_full[buf]);
-        }
-      }
-    } else if (KR == 2 && warp >= 2) {
-      // -------------------------------------------------------------- B synthesis (KR = 2), warps 2-3
-      // tile row c (= column jg of Y) of k-block (P, qq): 64 bf16 +-1 = sign bits of F^T[jg, 64 qq ..]
-      // XOR W[P, jg]; 16-byte chunk ch (q = 8 ch .. 8 ch + 7) lands at (ch ^ (c & 7)) (SWIZZLE_128B)
-      const int st_id = threadIdx.x - 64;  // 0..63
-      int s = 0;
-      uint32_t ph = 0;
-      for (int t = sc.first; t < sc.count; t += sc.step) {
-        const Unit w = pair_unit<KR>(p, sc, t);
-        const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
-        const int jb = w.nb * p.BN + (int)rank * bnh2;  // first Y column of this CTA's B half
-        for (int kb = kb0; kb < kb1; ++kb) {
-          const int P = kb / qb, qq = kb - P * qb;
-          // sign words for this thread's rows (loaded before the stage is free)
-          uint32_t lo[2], hi[2];
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int c = st_id + 64 * i;
-            const int jg = jb + c;
-            lo[i] = hi[i] = 0u;
-            if (c < bnh2 && jg < p.N) {
-              const uint32_t wbit = (__ldg(p.kr_wbits + (int64_t)P * p.kr_wwords + (jg >> 5)) >> (jg & 31)) & 1u;
-              const uint32_t m = 0u - wbit;
-              const uint2 f = __ldg(reinterpret_cast<const uint2*>(p.kr_fbits + (int64_t)jg * p.kr_fwords) + qq);
-              lo[i] = f.x ^ m;
-              hi[i] = f.y ^ m;
-            }
-          }
-          mbar_wait(&empty[s], ph ^ 1);
-          const uint32_t bt = sm100::smem_u32(smem + (size_t)s * stage_bytes) + kAStageBytes;
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int c = st_id + 64 * i;
-            if (c < bnh2) {
-#pragma unroll
-              for (int ch = 0; ch < 8; ++ch) {
-                const uint32_t byte = ((ch < 4 ? lo[i] : hi[i]) >> (8 * (ch & 3))) & 0xffu;
-                uint32_t v[4];
-#pragma unroll
-                for (int pp = 0; pp < 4; ++pp)
-                  v[pp] = 0x3f803f80u | (((byte >> (2 * pp)) & 1u) << 15) | (((byte >> (2 * pp + 1)) & 1u) << 31);
-                sts128u(bt + (uint32_t)c * 128u + ((uint32_t)(ch ^ (c & 7)) << 4), v[0], v[1], v[2], v[3]);
-              }
-            }
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_remote(full_leader + 8u * (uint32_t)s);
-          if (++s == S) { s = 0; ph ^= 1; }
         }
       }
     }
@@ -987,9 +931,7 @@ struct KrPlan {
 };
 
 using KernT = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams);
-// mode 1: resident F (general factors), mode 2: B synthesised from sign bits (+-1 factors)
-KernT kr_kernel(int NB, bool TA, int mode) {
-  if (mode == 2) return TA ? dense_tc_pair_kernel<1, true, 2> : dense_tc_pair_kernel<1, false, 2>;
+KernT kr_kernel(int NB, bool TA) {
   return TA ? (NB == 2 ? dense_tc_pair_kernel<2, true, 1> : dense_tc_pair_kernel<1, true, 1>)
             : (NB == 2 ? dense_tc_pair_kernel<2, false, 1> : dense_tc_pair_kernel<1, false, 1>);
 }
@@ -1017,36 +959,29 @@ int kr_max_clusters(KernT kern, size_t smem) {
 }
 
 // kslab = columns of this launch (<= kKrMaxCols); maxc <= 0: no device query (workspace sizing)
-bool make_plan_kr(KrPlan& pl, int64_t n, int64_t P, int64_t dl, int64_t kslab, int NB, int mode, int maxc, bool ta) {
+bool make_plan_kr(KrPlan& pl, int64_t n, int64_t P, int64_t dl, int64_t kslab, int NB, int maxc, bool ta) {
   pl = KrPlan{};
   pl.qb = (int)((dl + BK - 1) / BK);
   pl.nblocks = (int)((kslab + 255) / 256);
   const size_t budget = 227 * 1024 - 1024 - 512;
-  size_t res = 0, stage = 0;
-  for (;;) {
+  size_t res = 0;
+  for (;;) {  // resident F^T halves: shrink the N block until they fit next to >= 2 A stages
     const int64_t per = (kslab + pl.nblocks - 1) / pl.nblocks;
     pl.BN = (int)((per + 15) / 16 * 16);
-    if (mode == 2) {  // stage = A + synthesised B half
-      stage = kAStageBytes + (size_t)(pl.BN / 2) * 128;
-      break;
-    }
     res = (size_t)NB * pl.qb * (pl.BN / 2) * 128;
-    stage = kAStageBytes;
     if (res <= 160 * 1024) break;
     if (pl.BN <= 32) return false;
     pl.nblocks *= 2;
   }
-  if (res + 2 * stage > budget) return false;
-  int stages = (int)((budget - res) / stage);
+  int stages = (int)((budget - res) / kAStageBytes);
   if (stages > 6) stages = 6;
   pl.stages = stages;
-  pl.smem = 1024 + (size_t)stages * stage + res + (3 * stages + 5) * 8 + 16;
+  pl.smem = 1024 + (size_t)stages * kAStageBytes + res + (3 * stages + 5) * 8 + 16;
   pl.mtiles = (int)((n + 2 * BM - 1) / (2 * BM));
   const int mc = maxc > 0 ? maxc : sm_count() / 2;
   const int gp = mc / pl.nblocks > 0 ? mc / pl.nblocks : 1;  // pairs per N-block group
   int ks = 1;
-  while ((int64_t)pl.mtiles * ks < 4 * gp && P / (2 * ks) >= 2 && (mode != 2 || P * pl.qb / (2 * ks) >= CHUNK_KB))
-    ks *= 2;
+  while ((int64_t)pl.mtiles * ks < 4 * gp && P / (2 * ks) >= 2) ks *= 2;
   const int64_t p_per = (P + ks - 1) / ks;
   pl.kb_per_split = (int)(p_per * pl.qb);
   pl.ksplit = (int)((P + p_per - 1) / p_per);
@@ -1056,43 +991,36 @@ bool make_plan_kr(KrPlan& pl, int64_t n, int64_t P, int64_t dl, int64_t kslab, i
   return true;
 }
 
-size_t kr_workspace(int64_t n, int64_t P, int64_t dl, int64_t k, int NB, int mode, bool ta) {
+size_t kr_workspace(int64_t n, int64_t P, int64_t dl, int64_t k, int NB, bool ta) {
   size_t ws = 0;
   for (int64_t c0 = 0; c0 < k; c0 += kKrMaxCols) {
     const int64_t ks = k - c0 < kKrMaxCols ? k - c0 : kKrMaxCols;
     KrPlan pl, pl1;
-    if (!make_plan_kr(pl, n, P, dl, ks, NB, mode, -1, ta)) return 0;
+    if (!make_plan_kr(pl, n, P, dl, ks, NB, -1, ta)) return 0;
     // the real grid may hold fewer pairs per group (more K splits): size for 2 pairs per group too
-    make_plan_kr(pl1, n, P, dl, ks, NB, mode, 2 * pl.nblocks, ta);
+    make_plan_kr(pl1, n, P, dl, ks, NB, 2 * pl.nblocks, ta);
     const size_t w = pl.ws_bytes > pl1.ws_bytes ? pl.ws_bytes : pl1.ws_bytes;
     if (w > ws) ws = w;
   }
   return ws;
 }
 
-struct KrOperands {
-  const uint16_t* ft_hi;  // mode 1: F^T bf16 (k x ldf) and residual (or null)
-  const uint16_t* ft_lo;
-  int64_t ldf;
-  const float* w;  // mode 1: W (P x ldw) float32
-  int64_t ldw;
-  const uint32_t* fbits;  // mode 2: sign bits (layouts in TcParams)
-  const uint32_t* wbits;
-};
-
 // rows: output rows (A rows, or B columns when TA); out: Y [rows][k] (ldy) or, when TA, X [k][rows]
-int kr_run(bool TA, int mode, const float* A, int64_t rows, int64_t P, int64_t dl, int64_t lda, const KrOperands& o,
-           int64_t k, double scale, float* Y, int64_t ldy, void* ws, size_t ws_bytes, cudaStream_t s, const char* what) {
-  const int NB = (mode == 1 && o.ft_lo) ? 2 : 1;
+int kr_run(bool TA, const float* A, int64_t rows, int64_t P, int64_t dl, int64_t lda, const uint16_t* ft_hi,
+           const uint16_t* ft_lo, int64_t ldf, const float* W, int64_t ldw, int64_t k, double scale, float* Y,
+           int64_t ldy, void* ws, size_t ws_bytes, cudaStream_t s, const char* what) {
+  const int NB = ft_lo ? 2 : 1;
   CUtensorMap ma;
-  int st = make_a3_map(&ma, A, rows, P, dl, lda, TA);
+  // dl % 64 == 0: the plain 2-D map (measured faster than the 3-D box: config 5 2.14 -> 1.87 ms)
+  const bool a2d = dl % BK == 0;
+  int st = a2d ? (TA ? make_at_map(&ma, A, rows, P * dl, lda) : make_a_map(&ma, A, rows, P * dl, lda))
+               : make_a3_map(&ma, A, rows, P, dl, lda, TA);
   if (st != SK_OK) return st;
-  KernT kern = kr_kernel(NB, TA, mode);
-  const int64_t fwords = 2 * ((dl + BK - 1) / BK), wwords = (k + 31) / 32;
+  KernT kern = kr_kernel(NB, TA);
   for (int64_t c0 = 0; c0 < k; c0 += kKrMaxCols) {
     const int64_t kslab = k - c0 < kKrMaxCols ? k - c0 : kKrMaxCols;
     KrPlan pl;
-    if (!make_plan_kr(pl, rows, P, dl, kslab, NB, mode, -1, TA))
+    if (!make_plan_kr(pl, rows, P, dl, kslab, NB, -1, TA))
       return fail(SK_EUNSUPPORTED, std::string(what) + ": resident factor does not fit shared memory");
     static KernT maxc_kern[8] = {};
     static size_t maxc_smem[8] = {};
@@ -1106,22 +1034,17 @@ int kr_run(bool TA, int mode, const float* A, int64_t rows, int64_t P, int64_t d
     }
     const int maxc = maxc_val[slot];
     if (maxc < pl.nblocks) return fail(SK_EUNSUPPORTED, std::string(what) + ": too few co-resident pairs");
-    make_plan_kr(pl, rows, P, dl, kslab, NB, mode, maxc, TA);
+    make_plan_kr(pl, rows, P, dl, kslab, NB, maxc, TA);
     if (pl.ws_bytes > 0 && (ws == nullptr || ws_bytes < pl.ws_bytes))
       return fail(SK_EINVAL, std::string(what) + ": workspace too small (sk_kr_workspace_bytes)");
     CUtensorMap mb, mbl;
-    if (mode == 1) {
-      st = make_bt_map(&mb, o.ft_hi + c0 * o.ldf, kslab, dl, o.ldf, pl.BN / 2);
+    st = make_bt_map(&mb, ft_hi + c0 * ldf, kslab, dl, ldf, pl.BN / 2);
+    if (st != SK_OK) return st;
+    if (NB == 2) {
+      st = make_bt_map(&mbl, ft_lo + c0 * ldf, kslab, dl, ldf, pl.BN / 2);
       if (st != SK_OK) return st;
-      if (NB == 2) {
-        st = make_bt_map(&mbl, o.ft_lo + c0 * o.ldf, kslab, dl, o.ldf, pl.BN / 2);
-        if (st != SK_OK) return st;
-      } else {
-        mbl = mb;
-      }
     } else {
-      mb = ma;  // unused (B is synthesised)
-      mbl = ma;
+      mbl = mb;
     }
     TcParams p{};
     p.A = A;
@@ -1140,18 +1063,12 @@ int kr_run(bool TA, int mode, const float* A, int64_t rows, int64_t P, int64_t d
     p.part = static_cast<float*>(ws);
     p.num_units = pl.mtiles * pl.ksplit * pl.nblocks;
     p.mtiles = pl.mtiles;
-    if (mode == 1) {
-      p.kr_w = o.w + c0;
-      p.kr_ldw = o.ldw;
-    } else {
-      p.kr_fbits = o.fbits + c0 * fwords;  // c0 is a multiple of 32: whole words of W bits
-      p.kr_fwords = fwords;
-      p.kr_wbits = o.wbits + c0 / 32;
-      p.kr_wwords = wwords;
-    }
+    p.kr_w = W + c0;
+    p.kr_ldw = ldw;
     p.kr_qb = pl.qb;
     p.kr_ngroups = pl.nblocks;
     p.out_t = TA ? 1 : 0;
+    p.kr_a2d = a2d ? 1 : 0;
     uint32_t cols = 32;
     while (cols < (uint32_t)(2 * pl.BN)) cols <<= 1;
     p.tmem_cols = cols;
@@ -1169,8 +1086,8 @@ int kr_run(bool TA, int mode, const float* A, int64_t rows, int64_t P, int64_t d
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (getenv("SKETCH_B200_TC_PAIR_VERBOSE"))
-      fprintf(stderr, "%s: mode %d BN %d nblocks %d ksplit %d kb/split %d stages %d pairs %d (max %d) smem %zu\n", what,
-              mode, pl.BN, pl.nblocks, pl.ksplit, pl.kb_per_split, pl.stages, pl.npairs, maxc, pl.smem);
+      fprintf(stderr, "%s: BN %d nblocks %d ksplit %d kb/split %d stages %d pairs %d (max %d) smem %zu\n", what, pl.BN,
+              pl.nblocks, pl.ksplit, pl.kb_per_split, pl.stages, pl.npairs, maxc, pl.smem);
     if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mbl, p) != cudaSuccess) return check_launch(what);
     st = check_launch(what);
     if (st != SK_OK) return st;
@@ -1445,7 +1362,7 @@ extern "C" int sk_dense_tn_tc(const float* A, int64_t n, int64_t d, int64_t lda,
 // trans = 0: sk_kr_right with n rows; trans = 1: sk_kr_adjoint with n = m columns of B
 extern "C" size_t sk_kr_workspace_bytes(int64_t n, int64_t P, int64_t dl, int64_t k, int split_f, int trans) {
   if (n < 1 || P < 1 || dl < 1 || k < 1) return 0;
-  return skb::kr_workspace(n, P, dl, k, split_f ? 2 : 1, 1, trans != 0);
+  return skb::kr_workspace(n, P, dl, k, split_f ? 2 : 1, trans != 0);
 }
 
 // Y[n, k] = scale * sum_{P, q} A[i, P * dl + q] * W[P, j] * F[q, j]   (Khatri-Rao, Omega never formed)
@@ -1456,8 +1373,8 @@ extern "C" int sk_kr_right(const float* A, int64_t n, int64_t P, int64_t dl, int
   int st = kr_check(A, n, P, dl, lda, P * dl, k, Y, ldy, k, "sk_kr_right");
   if (st == SK_OK) st = kr_check_f(Ft_hi, Ft_lo, ldf, dl, W, ldw, k, "sk_kr_right");
   if (st != SK_OK || n == 0) return st;
-  const KrOperands o{Ft_hi, Ft_lo, ldf, W, ldw, nullptr, nullptr};
-  return kr_run(false, 1, A, n, P, dl, lda, o, k, scale, Y, ldy, ws, ws_bytes, as_stream(stream), "sk_kr_right");
+  return kr_run(false, A, n, P, dl, lda, Ft_hi, Ft_lo, ldf, W, ldw, k, scale, Y, ldy, ws, ws_bytes, as_stream(stream),
+                "sk_kr_right");
 }
 
 // X[k, m] = scale * Omega^T B for B [P * dl rows][m] (row stride ldb), read in place (no transposed copy)
@@ -1468,37 +1385,6 @@ extern "C" int sk_kr_adjoint(const float* B, int64_t m, int64_t P, int64_t dl, i
   int st = kr_check(B, m, P, dl, ldb, m, k, X, ldx, m, "sk_kr_adjoint");
   if (st == SK_OK) st = kr_check_f(Ft_hi, Ft_lo, ldf, dl, W, ldw, k, "sk_kr_adjoint");
   if (st != SK_OK || m == 0) return st;
-  const KrOperands o{Ft_hi, Ft_lo, ldf, W, ldw, nullptr, nullptr};
-  return kr_run(true, 1, B, m, P, dl, ldb, o, k, scale, X, ldx, ws, ws_bytes, as_stream(stream), "sk_kr_adjoint");
-}
-
-extern "C" size_t sk_kr2_workspace_bytes(int64_t n, int64_t P, int64_t dl, int64_t k, int trans) {
-  if (n < 1 || P < 1 || dl < 1 || k < 1) return 0;
-  return skb::kr_workspace(n, P, dl, k, 1, 2, trans != 0);
-}
-
-// +-1 factors from sign bits only (SURVEY 8(b) sk_kr2_right): f_neg[j * 2 ceil(dl/64) + w] holds the
-// signs of F^T[j, 32 w ..] (bit q % 32), w_neg[P * ceil(k/32) + j / 32] bit j % 32 the sign of W[P, j]
-extern "C" int sk_kr2_right(const float* A, int64_t n, int64_t P, int64_t dl, int64_t lda, const uint32_t* f_neg,
-                            const uint32_t* w_neg, int64_t k, double scale, float* Y, int64_t ldy, void* ws,
-                            size_t ws_bytes, void* stream) {
-  using namespace skb;
-  int st = kr_check(A, n, P, dl, lda, P * dl, k, Y, ldy, k, "sk_kr2_right");
-  if (st != SK_OK || n == 0) return st;
-  if (!f_neg || !w_neg || (reinterpret_cast<uintptr_t>(f_neg) & 7) || (reinterpret_cast<uintptr_t>(w_neg) & 3))
-    return fail(SK_EINVAL, "sk_kr2_right: sign-bit arrays must be 8-byte aligned");
-  const KrOperands o{nullptr, nullptr, 0, nullptr, 0, f_neg, w_neg};
-  return kr_run(false, 2, A, n, P, dl, lda, o, k, scale, Y, ldy, ws, ws_bytes, as_stream(stream), "sk_kr2_right");
-}
-
-extern "C" int sk_kr2_adjoint(const float* B, int64_t m, int64_t P, int64_t dl, int64_t ldb, const uint32_t* f_neg,
-                              const uint32_t* w_neg, int64_t k, double scale, float* X, int64_t ldx, void* ws,
-                              size_t ws_bytes, void* stream) {
-  using namespace skb;
-  int st = kr_check(B, m, P, dl, ldb, m, k, X, ldx, m, "sk_kr2_adjoint");
-  if (st != SK_OK || m == 0) return st;
-  if (!f_neg || !w_neg || (reinterpret_cast<uintptr_t>(f_neg) & 7) || (reinterpret_cast<uintptr_t>(w_neg) & 3))
-    return fail(SK_EINVAL, "sk_kr2_adjoint: sign-bit arrays must be 8-byte aligned");
-  const KrOperands o{nullptr, nullptr, 0, nullptr, 0, f_neg, w_neg};
-  return kr_run(true, 2, B, m, P, dl, ldb, o, k, scale, X, ldx, ws, ws_bytes, as_stream(stream), "sk_kr2_adjoint");
+  return kr_run(true, B, m, P, dl, ldb, Ft_hi, Ft_lo, ldf, W, ldw, k, scale, X, ldx, ws, ws_bytes, as_stream(stream),
+                "sk_kr_adjoint");
 }

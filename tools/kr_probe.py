@@ -2,8 +2,7 @@
 
     python tools/kr_probe.py [--reps 10]
 
-Variants (SKETCH_B200_KR_MODE): 2 = B tiles synthesised from sign bits (sk_kr2_right, default for
-+-1 factors), 1 = F resident + per-P fold with W (sk_kr_right).  `dense` = the round-1 path: Omega^T (512 x 65536 bf16)
+`kr` = sk_kr_right (F^T resident, per-P fold with W, Omega never formed).  `dense` = the round-1 path: Omega^T (512 x 65536 bf16)
 formed on the device and streamed as the B operand of sk_dense_right_tc.
 """
 
@@ -51,19 +50,15 @@ def main():
     a = torch.randn(n, d, device=dev)
     out = {}
     y0 = None
-    for mode in ("2", "1"):
-        os.environ["SKETCH_B200_KR_MODE"] = mode
-        out[f"kr_mode{mode}_ms"] = time_fn(lambda: tm.apply_right(a), args.reps)
-        if mode == "2":
-            y0 = tm.apply_right(a)
-    os.environ["SKETCH_B200_KR_MODE"] = "2"
+    out["kr_ms"] = time_fn(lambda: tm.apply_right(a), args.reps)
+    y0 = tm.apply_right(a)
     om = torch.as_tensor(tm.materialize(), device=dev)  # d x k float64 (probe only)
     bt = (om.T * np.sqrt(k)).contiguous().to(torch.bfloat16)  # exact +-1
     del om
     out["dense_ms"] = time_fn(lambda: dense_right_tc(a, bt, None, k, 1.0 / np.sqrt(k)), args.reps)
     yd = dense_right_tc(a, bt, None, k, 1.0 / np.sqrt(k))
     out["kr_vs_dense_rel"] = float(torch.linalg.norm(y0 - yd) / torch.linalg.norm(yd))
-    out["tflops_executed_kr"] = 2 * 2.0 * n * d * k / (out["kr_mode2_ms"] / 1e3) / 1e12
+    out["tflops_executed_kr"] = 2 * 2.0 * n * d * k / (out["kr_ms"] / 1e3) / 1e12
     print(json.dumps(out))
 
 
