@@ -47,11 +47,19 @@ def sharded_right(tm, a_local):
     return tm.apply_right(a_local)
 
 
+def _row_block_of(tm, r0: int, rows: int):
+    """Rows [r0, r0 + rows) of `tm` (sparse families); other families have no row blocks."""
+    if not hasattr(tm, "row_block"):
+        raise NotImplementedError(f"{type(tm).__name__} has no row blocks: row-sharded adjoints need a sparse "
+                                  "test matrix (SparseUniformTM, SparseStackTM, SparseIIDTM, SparseColTM)")
+    return tm.row_block(r0, r0 + rows)
+
+
 def sharded_adjoint(tm, a_local, r0: int, group=None, dtype=None):
     """S A summed over ranks: rank g applies Omega[r0 : r0 + n_g]^* to its rows, then all-reduce."""
     import torch
 
-    blk = tm.row_block(r0, r0 + a_local.shape[0]) if hasattr(tm, "row_block") else tm
+    blk = _row_block_of(tm, r0, a_local.shape[0])
     part = blk.apply_adjoint(a_local)
     if dtype is not None:
         part = part.to(dtype)
@@ -109,5 +117,5 @@ def sharded_lsqr(a_local, b_local, tm, r0: int, group=None, **kw):
     """Sketch-and-precondition LSQR over row-sharded (A, b): every rank returns the same x."""
     from .rand_nla import sketch_precondition_lsqr
 
-    blk = tm.row_block(r0, r0 + a_local.shape[0]) if hasattr(tm, "row_block") else tm
+    blk = _row_block_of(tm, r0, a_local.shape[0])
     return sketch_precondition_lsqr(a_local, b_local, blk, allreduce=lambda t: allreduce_sum(t, group), **kw)

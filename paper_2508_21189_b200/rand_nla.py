@@ -187,19 +187,18 @@ def _cholqr2_qr(m, max_spread: float = 1e6):
 def _as_device_2d(a):
     import torch
 
-    if isinstance(a, torch.Tensor) and a.dim() == 2 and a.dtype in (torch.float32, torch.float64):
-        return a, ("cuda" if a.is_cuda else "tensor")  # torch input stays where it is
+    if isinstance(a, torch.Tensor) and a.dim() == 2 and a.dtype in (torch.float32, torch.float64) and a.is_cuda:
+        return a, "cuda"  # device input stays where it is
     op = to_operand(a, allow_vector=False)
     return op.tensor, op.kind
 
 
 def _as_vec(b, like):
+    """b as a tensor on A's device (a CPU tensor b with a CUDA A is moved: kernels take device pointers)."""
     import torch
 
-    if isinstance(b, torch.Tensor):
-        t = b
-    else:
-        t = torch.as_tensor(np.asarray(b)).to(like.device)
+    t = b if isinstance(b, torch.Tensor) else torch.as_tensor(np.asarray(b))
+    t = t.to(like.device)
     return t[:, 0] if t.dim() == 2 and t.shape[1] == 1 else t
 
 
@@ -735,6 +734,7 @@ def sketch_precondition_lsqr(a, b, tm_psi, *, atol: float = 1e-6, btol: float = 
     ddnorm = torch.zeros((), dtype=torch.float64, device=A.device)  # read once at the end (no sync)
     istop, itn = 0, 0
     r1norm, arnorm = beta, alpha * beta
+    test1 = test2 = 0.0  # iter_lim = 0 returns the initial estimates
     if arnorm == 0:
         return LsqrResult(_back(rinv(x), kind), 0, 0, r1norm, 0.0, 0.0, t_sketch)
     # float32 A with d = 128 q <= 512: u <- A R^-1 v - alpha u, A^T u and ||u||^2 in one pass over A

@@ -606,13 +606,25 @@ class SparseRowBlockTM(_SignSparseTM):
     """Rows [r0, r1) of a sparse test matrix, as an operator of its own (multi-GPU row shards).
 
     Rank g of a row-sharded job holds A[r0:r1, :] and applies this block: its adjoint partial
-    Omega[r0:r1]^* A_g is summed across ranks by one all-reduce.
+    Omega[r0:r1]^* A_g is summed across ranks by one all-reduce.  When the parent's
+    draws live on the GPU (device-drawn SparseUniform), the block slices those device arrays — no
+    host triplets of the whole operator are formed on any rank; host triplets of the block itself
+    are only built if a host view (`matrix`, `materialize`) is asked for.
     """
 
     def __init__(self, parent: _SignSparseTM, r0: int, r1: int):
         if not (0 <= r0 < r1 <= parent.d):
             raise ValueError(f"bad row block [{r0}, {r1}) of d={parent.d}")
         super().__init__(r1 - r0, parent.k, parent.field, parent.seed)
+        self.parent = parent
+        self.row_offset = int(r0)
+        self._dev = None
+        dd = parent._device_draw() if hasattr(parent, "_device_draw") and parent._coo is None else None
+        if dd is not None:
+            cols, neg = dd
+            self._dev = (cols[r0:r1], neg[r0:r1], 1.0 / np.sqrt(parent.zeta))
+            self.zeta = parent.zeta
+            return
         rows, cols, vals = parent._triplets()
         lo, hi = np.searchsorted(rows, [r0, r1])
         if np.any(np.diff(rows) < 0):  # unsorted rows (SparseCol CSR order is sorted; others row-major)
@@ -620,18 +632,62 @@ class SparseRowBlockTM(_SignSparseTM):
             self._coo = (rows[sel] - r0, cols[sel], vals[sel])
         else:
             self._coo = (rows[lo:hi] - r0, cols[lo:hi], vals[lo:hi])
-        self.parent = parent
-        self.row_offset = int(r0)
+
+    def _device_draw(self):
+        return None if self._dev is None else self._dev[:2]
 
     def _draw(self):
-        return self._coo
+        if self._dev is None:
+            return self._coo
+        cols, neg, mag = self._dev
+        z = cols.shape[1]
+        vals = np.where(neg.cpu().numpy().ravel(), -mag, mag).astype(self.dtype)
+        return np.repeat(np.arange(self.d), z), cols.cpu().numpy().ravel().astype(np.int64), vals
+
+    def _signed_real(self) -> bool:
+        if self._dev is not None and self._coo is None:
+            return self.field == "real"
+        return super()._signed_real()
+
+    def _device_sign_form(self, device):
+        if self._dev is None or self.field != "real":
+            return None
+        cols, neg, mag = self._dev
+        return cols.to(device), neg.to(device), mag
 
     def redraw(self, seed: int):
         raise NotImplementedError("redraw the parent operator instead")
 
 
-def _row_block(self, r0: int, r1: int) -> SparseRowBlockTM:
-    """Rows [r0, r1) as an operator; cached on the parent so repeated sharded calls reuse its encoding."""
+class EmptyRowBlockTM:
+    """A zero-row block (a rank that holds no rows when n < world size): zero partials."""
+
+    def __init__(self, parent, r0: int):
+        self.parent = parent
+        self.row_offset = int(r0)
+        self.d = 0
+        self.k = parent.k
+
+    def apply_adjoint(self, b):
+        import torch
+
+        m = b.shape[1] if b.dim() == 2 else 1
+        out = torch.zeros((self.k, m) if b.dim() == 2 else (self.k,), dtype=b.dtype, device=b.device)
+        return out
+
+    def apply_right(self, a):
+        import torch
+
+        return torch.zeros((a.shape[0], self.k), dtype=a.dtype, device=a.device)
+
+
+def _row_block(self, r0: int, r1: int):
+    """Rows [r0, r1) as an operator; cached on the parent so repeated sharded calls reuse its encoding.
+    An empty range gives an operator with zero partials (ranks without rows when n < world size)."""
+    if r0 == r1:
+        if not 0 <= r0 <= self.d:
+            raise ValueError(f"bad row block [{r0}, {r1}) of d={self.d}")
+        return EmptyRowBlockTM(self, r0)
     cache = self.__dict__.setdefault("_row_blocks", {})
     key = (int(r0), int(r1))
     if key not in cache:

@@ -203,3 +203,30 @@ def test_lsqr_fused_matches_two_pass(cuda, monkeypatch):
     x1, x2 = np.asarray(r1.x.cpu() if hasattr(r1.x, "cpu") else r1.x), np.asarray(r2.x.cpu() if hasattr(r2.x, "cpu") else r2.x)
     assert r1.itn == r2.itn or abs(r1.itn - r2.itn) <= 2
     assert np.linalg.norm(x1 - x2) <= 1e-8 * np.linalg.norm(x2)
+
+
+def test_lsqr_cpu_torch_b_with_cuda_a(cuda):
+    """A CPU torch b with a CUDA A is moved to A's device (kernels take device pointers); a CPU
+    torch A is uploaded and the solution comes back on the host."""
+    import torch
+
+    rng = np.random.default_rng(6)
+    a = rng.standard_normal((5000, 32))
+    b = a @ rng.standard_normal(32) + 1e-3 * rng.standard_normal(5000)
+    tm = skb.SparseUniformTM(5000, 128, 8, seed=1)
+    ref = rand_nla.sketch_precondition_lsqr(a, b, tm, atol=1e-12, btol=1e-12).x
+    x_dev = rand_nla.sketch_precondition_lsqr(torch.from_numpy(a).to(cuda), torch.from_numpy(b), tm, atol=1e-12,
+                                              btol=1e-12).x
+    assert x_dev.is_cuda
+    assert rel_err(x_dev.cpu().numpy(), ref) <= 1e-12
+    x_cpu = rand_nla.sketch_precondition_lsqr(torch.from_numpy(a), torch.from_numpy(b), tm, atol=1e-12, btol=1e-12).x
+    assert isinstance(x_cpu, torch.Tensor) and not x_cpu.is_cuda
+    assert rel_err(x_cpu.numpy(), ref) <= 1e-12
+
+
+def test_lsqr_iter_lim_zero(cuda):
+    rng = np.random.default_rng(7)
+    a = rng.standard_normal((3000, 16))
+    b = rng.standard_normal(3000)
+    res = rand_nla.sketch_precondition_lsqr(a, b, skb.SparseUniformTM(3000, 64, 8, seed=2), iter_lim=0)
+    assert res.itn == 0 and np.all(res.x == 0)
