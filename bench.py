@@ -218,8 +218,15 @@ def _dist(args):
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one process per GPU; SKETCH_B200_DIST_BACKEND=gloo + fewer GPUs than ranks is a functional
+        # dry run only (ranks then share a device: NCCL refuses duplicate GPUs)
+        dev_idx = local % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev_idx)
+        backend = os.environ.get("SKETCH_B200_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
+        else:
+            dist.init_process_group(backend)
     else:
         if torch.cuda.is_available():
             torch.cuda.set_device(0)
@@ -373,6 +380,11 @@ def cpu_reference_step(w, a_host, procs):
     elif name == "cfg5":
         f = orc.kr_factors(tm.d0, tm.ell, tm.k, tm.seed, tm.base)
         fn = lambda x: orc.kr_right(f, x)  # noqa: E731
+    elif name == "cfg4":  # S A restricted to the sample rows: Omega[:rows]^T A[:rows] (scipy, one core)
+        csr = _cfg4_csr(tm)[: a_host.shape[0]]
+        t0 = time.perf_counter()
+        y = orc.csr_adjoint(csr, a_host)
+        return time.perf_counter() - t0, y
     else:
         raise ValueError(name)
     t0 = time.perf_counter()
@@ -380,7 +392,38 @@ def cpu_reference_step(w, a_host, procs):
     return time.perf_counter() - t0, y
 
 
-SAMPLE_ROWS = {"cfg1": 4096, "cfg2": 2048, "cfg3": 512, "cfg5": 16}
+_CSR_CACHE = {}
+
+
+def _cfg4_csr(tm):
+    import oracle as orc
+
+    key = (tm.d, tm.k, tm.zeta, tm.seed)
+    if key not in _CSR_CACHE:
+        _CSR_CACHE[key] = orc.sparse_uniform_csr(*key)
+    return _CSR_CACHE[key]
+
+
+def sample_parity(w, procs):
+    """(cpu_baseline dict, rel-F error of the GPU result vs the oracle) on the config's row sample."""
+    rows = SAMPLE_ROWS[w["name"]]
+    a_host = w["a"][:rows].cpu().numpy()
+    dt, y_ref = cpu_reference_step(w, a_host, procs)
+    if w["op"] == "right":
+        y_gpu = _apply(w, w["a"][:rows]).double().cpu().numpy()
+    else:  # the row block of S that multiplies the sample rows (device-sliced draws)
+        y_gpu = w["tm"].row_block(0, rows).apply_adjoint(w["a"][:rows]).double().cpu().numpy()
+    err = float(np.linalg.norm(y_gpu - y_ref) / np.linalg.norm(y_ref))
+    cores = procs if w["op"] == "right" else 1
+    cpu = {"value": a_host.nbytes / dt / 1e9, "unit": "GB/s", "cores": cores, "kind": "port",
+           "sample": f"{rows} rows of the {w['name']} input ({a_host.nbytes / 1e6:.0f} MB), oracle/ port of the "
+                     f"sketchkit float64 path" + (f", row-parallel over {procs} processes" if cores > 1 else
+                                                  ", scipy sparse on one core (as the reference)"),
+           "parity_rel_fro_err_vs_gpu": err}
+    return cpu, err
+
+
+SAMPLE_ROWS = {"cfg1": 4096, "cfg2": 2048, "cfg3": 512, "cfg4": 1 << 18, "cfg5": 16}
 
 
 def run_reference(args):
@@ -466,6 +509,29 @@ def measure_sharded_sa(torch, world, rank, dev, steps=5, warmup=3):
     return out
 
 
+def measure_strong_cfg2(torch, world, rank, dev, steps=10, warmup=3):
+    """Config 2 with the 65536-row A split across the ranks (strong scaling: 65536 / N rows each,
+    no collective); device time max over ranks."""
+    from paper_2508_21189_b200 import dist as skd
+    from paper_2508_21189_b200.sketch import SparseRttTM
+
+    n, d, k = 65536, 8192, 512
+    r0, r1 = skd.row_range(n, world, rank)
+    tm = SparseRttTM(d, k, 1, "wht", seed=0)
+    g = torch.Generator(device=dev).manual_seed(1000)
+    a = torch.randn(n, d, dtype=torch.float32, device=dev, generator=g)[r0:r1].contiguous()
+    a /= torch.arange(1, d + 1, dtype=torch.float32, device=dev)
+    w = dict(tm=tm, a=a, op="right")
+    total, _ = time_device(torch, w, steps, warmup, world, dev)
+    total = _max_over_ranks(world, total, dev)
+    out = {"workload": f"cfg2 SRTT, A 65536x8192 f32 split into {world} row block(s) of ~{r1 - r0} rows",
+           "scaling": "strong", "value_gbs": n * d * 4 * steps / total / 1e9, "ms_per_step": total / steps * 1e3,
+           "rows_per_gpu": r1 - r0}
+    del a
+    torch.cuda.empty_cache()
+    return out
+
+
 def measure(torch, w, steps, warmup, world, rank, dev, with_e2e, clocks_idx):
     a = w["a"]
     esize = a.element_size()
@@ -510,26 +576,18 @@ def main(argv=None):
     import torch
 
     world, rank, local = _dist(args)
-    dev = torch.device("cuda", local if world > 1 else 0)
+    dev = torch.device("cuda", (local % max(1, torch.cuda.device_count())) if world > 1 else 0)
     peak, peak_src = _peaks()
 
     w = WORKLOADS[args.config](torch, dev, rank)
-    m = measure(torch, w, args.steps, max(3, args.warmup), world, rank, dev, True, local if world > 1 else 0)
+    m = measure(torch, w, args.steps, max(3, args.warmup), world, rank, dev, True, dev.index)
     esize = w["a"].element_size()
     launches = w["launches"]
 
     cpu = None
+    procs = os.cpu_count() or 1
     if world == 1 and rank == 0 and not args.no_cpu:
-        rows = SAMPLE_ROWS[args.config]
-        a_host = w["a"][:rows].cpu().numpy()
-        procs = os.cpu_count() or 1
-        dt, y_ref = cpu_reference_step(w, a_host, procs)
-        y_gpu = _apply(w, w["a"][:rows]).double().cpu().numpy()
-        err = float(np.linalg.norm(y_gpu - y_ref) / np.linalg.norm(y_ref))
-        cpu = {"value": a_host.nbytes / dt / 1e9, "unit": "GB/s", "cores": procs, "kind": "port",
-               "sample": f"{rows} rows of the {args.config} input ({a_host.nbytes / 1e6:.0f} MB), oracle/ port of the "
-                         f"sketchkit float64 path, row-parallel over {procs} processes",
-               "parity_rel_fro_err_vs_gpu": err}
+        cpu, _ = sample_parity(w, procs)
 
     others = {}
     del w["a"]
@@ -539,11 +597,17 @@ def main(argv=None):
             others["cfg4_sharded"] = measure_sharded_sa(torch, world, rank, dev)
         except Exception as exc:  # report, never hide
             others["cfg4_sharded"] = {"error": f"{type(exc).__name__}: {exc}"}
+        if args.config == "cfg2":
+            try:  # the headline workload at fixed total size (strong scaling), next to the weak headline
+                others["cfg2_strong"] = measure_strong_cfg2(torch, world, rank, dev)
+            except Exception as exc:
+                others["cfg2_strong"] = {"error": f"{type(exc).__name__}: {exc}"}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            bf16_sust = float(json.load(f)["bf16_tflops_sustained"])
+            pk = json.load(f)
+        bf16_burst, bf16_sust = float(pk["bf16_tflops"]), float(pk["bf16_tflops_sustained"])
     except (OSError, KeyError, ValueError):
-        bf16_sust = None
+        bf16_burst, bf16_sust = None, None
     if world == 1 and args.others:
         for name in [s for s in args.others.split(",") if s and s != args.config]:
             try:
@@ -555,15 +619,24 @@ def main(argv=None):
                                 "dtype": "f32" if oes == 4 else "f64", "kernel": ow["kernel"],
                                 "pct_hbm_peak": 100.0 * om["achieved_gbs"] / peak,
                                 "roofline_achieved_gbs": om["achieved_gbs"], "alg_bytes": om["alg_bytes"],
-                                "omega_setup_ms": om["omega_setup"]["ms"]}
+                                "traffic": _traffic(name), "omega_setup_ms": om["omega_setup"]["ms"],
+                                "clocks": om["clocks"]}
+                if name in SAMPLE_ROWS and not args.no_cpu:
+                    ocpu, oerr = sample_parity(ow, procs)
+                    others[name]["cpu_baseline"] = ocpu
+                    others[name]["parity_rel_fro_err"] = oerr
                 if downstream:
                     others[name]["downstream"] = downstream
                 if ow.get("flops"):
                     tf = ow["flops"] / (om["kernel_ms"] / 1e3) / 1e12
                     ex = tf * ow["flops_executed_x"]
-                    others[name]["tensor"] = {"useful_tflops": tf, "executed_tflops": ex,
-                                              "executed_frac_of_sustained_bf16": ex / bf16_sust if bf16_sust else None,
-                                              "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"}
+                    others[name]["tensor"] = {
+                        "useful_tflops": tf, "executed_tflops": ex,
+                        "executed_frac_of_burst_bf16": ex / bf16_burst if bf16_burst else None,
+                        "useful_frac_of_burst_bf16": tf / bf16_burst if bf16_burst else None,
+                        "executed_frac_of_sustained_bf16": ex / bf16_sust if bf16_sust else None,
+                        "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst: a kernel timed alone) and "
+                                       "bf16_tflops_sustained"}
                 del ow
                 torch.cuda.empty_cache()
             except Exception as exc:  # report, never hide

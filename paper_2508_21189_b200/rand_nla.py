@@ -184,11 +184,14 @@ def _cholqr2_qr(m, max_spread: float = 1e6):
     return q, r_tot
 
 
-def _as_device_2d(a):
+def _as_device_2d(a, host_scaffold: bool = False):
+    """A as a CUDA tensor (host input is uploaded).  host_scaffold=True keeps a CPU torch A on the host
+    for the driver-logic tests (tests/test_dist_gloo.py), whose operator is a CPU oracle stand-in."""
     import torch
 
-    if isinstance(a, torch.Tensor) and a.dim() == 2 and a.dtype in (torch.float32, torch.float64) and a.is_cuda:
-        return a, "cuda"  # device input stays where it is
+    if isinstance(a, torch.Tensor) and a.dim() == 2 and a.dtype in (torch.float32, torch.float64) and (
+            a.is_cuda or host_scaffold):
+        return a, ("cuda" if a.is_cuda else "tensor")
     op = to_operand(a, allow_vector=False)
     return op.tensor, op.kind
 
@@ -666,7 +669,7 @@ def _rmatvec_blocks(A, u, block_rows):
 
 
 def sketch_precondition_lsqr(a, b, tm_psi, *, atol: float = 1e-6, btol: float = 1e-6, iter_lim: int = 200,
-                             block_rows: int = 1 << 16, allreduce=None) -> LsqrResult:
+                             block_rows: int = 1 << 16, allreduce=None, _host_scaffold: bool = False) -> LsqrResult:
     """min ||A x - b|| by sketch-and-precondition: S A = Q R, then LSQR on A R^-1.
 
     `allreduce(t)` (in place sum across ranks) makes the solver distributed: every rank holds a row
@@ -677,7 +680,7 @@ def sketch_precondition_lsqr(a, b, tm_psi, *, atol: float = 1e-6, btol: float = 
 
     import torch
 
-    A, kind = _as_device_2d(a)
+    A, kind = _as_device_2d(a, _host_scaffold)
     bt = _as_vec(b, A)
     n, d = A.shape
     if tm_psi.d != n:

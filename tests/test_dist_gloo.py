@@ -91,7 +91,7 @@ def _lsqr_job(rank, world):
     a, b, csr = _problem()
     r0, r1 = skd.row_range(a.shape[0], world, rank)
     res = skd.sharded_lsqr(torch.from_numpy(a[r0:r1]), torch.from_numpy(b[r0:r1]), OracleRowOp(csr), r0,
-                           atol=1e-12, btol=1e-12)
+                           atol=1e-12, btol=1e-12, _host_scaffold=True)
     return res.x.numpy() if hasattr(res.x, "numpy") else np.asarray(res.x)
 
 
