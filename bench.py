@@ -233,6 +233,12 @@ def _dist(args):
     return world, rank, local
 
 
+def _backend():
+    import torch.distributed as dist
+
+    return dist.get_backend() if dist.is_available() and dist.is_initialized() else "none"
+
+
 def _barrier(world):
     if world > 1:
         import torch.distributed as dist
@@ -500,7 +506,7 @@ def measure_sharded_sa(torch, world, rank, dev, steps=5, warmup=3):
 
     t_step = timed(step)
     t_ar = timed(lambda: skd.allreduce_sum(part))
-    out = {"workload": f"cfg4 SA, A 4194304x512 f32 split into {world} row block(s), NCCL all-reduce of the "
+    out = {"workload": f"cfg4 SA, A 4194304x512 f32 split into {world} row block(s), all-reduce ({_backend()}) of the "
                        "2048x512 float64 partials", "scaling": "strong",
            "value_gbs": n * d * 4 / t_step / 1e9, "ms_per_step": t_step * 1e3, "allreduce_ms": t_ar * 1e3,
            "rows_per_gpu": r1 - r0, "allreduce_bytes": part.numel() * part.element_size()}
