@@ -80,6 +80,23 @@ SK_API int sk_sparse_right(int dtype, const void* A, int64_t n, int64_t d, int64
                            int64_t k, double scale, void* Y, int64_t ldy, void* stream);
 
 /*
+ * K1r — float64 Y[n,k] = scale * A * Omega (k <= 256) on a warp-specialised ring: producer warps
+ * copy 64 x 64 chunks of A into a 4-stage shared-memory ring with cp.async (8-byte XOR swizzle,
+ * conflict-free column gathers), 16 consumer warps accumulate 16 columns each in registers, and
+ * the chunk stream is split evenly over the SMs (stream-K; tiles cut between two CTAs are combined
+ * in a fixed order).  Replaces `_SparseTM.apply_right` (src/sketch/sparse.py:63-66) for float64
+ * (BASELINE config 1).  Omega in the ring encoding: for unit h (rows 128h ..) and warp w (columns
+ * 16w ..), lists[16*seg[16h + w] ..] = 16 uint8 column counts, then uint8 entries (row % 64) |
+ * ((row / 64) % 2) << 6 | neg << 7 (sketch/encode.py ring_encode); seg has ceil(d/128)*16 + 1 entries.
+ * Workspace: sk_sparse_right_ring_workspace_bytes(n, d).  A 8-byte, lists 16-byte aligned.
+ */
+SK_API int sk_sparse_right_ring_supported(int dtype, int64_t d, int64_t k, int64_t seg_bytes);
+SK_API size_t sk_sparse_right_ring_workspace_bytes(int64_t n, int64_t d);
+SK_API int sk_sparse_right_ring(const double* A, int64_t n, int64_t d, int64_t lda, const uint8_t* lists,
+                                const uint32_t* seg, int64_t seg_bytes, int64_t k, double scale, double* Y,
+                                int64_t ldy, void* ws, size_t ws_bytes, void* stream);
+
+/*
  * K1s — Y[n,k] = scale * A * Omega for a sparse A in CSR (int64 indptr[n+1], int32 indices, values
  * of `dtype`) and a sparse-sign Omega given by rows: int32 indptr[d+1] and int32 entries
  * `c | neg << 31` (magnitude folded into `scale`). A is never densified. Replaces

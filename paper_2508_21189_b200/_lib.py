@@ -85,6 +85,10 @@ SIGNATURES = {
                              _c_p, _c_i64, _c_p, _c_size, _c_p]),
     "sk_kr_adjoint": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_p, _c_i64, _c_i64, _c_dbl,
                                _c_p, _c_i64, _c_p, _c_size, _c_p]),
+    "sk_sparse_right_ring_supported": (_c_int, [_c_int, _c_i64, _c_i64, _c_i64]),
+    "sk_sparse_right_ring_workspace_bytes": (_c_size, [_c_i64, _c_i64]),
+    "sk_sparse_right_ring": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_i64, _c_dbl, _c_p, _c_i64,
+                                      _c_p, _c_size, _c_p]),
     "sk_kr_right_cc": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_i64,
                                 _c_dbl, _c_p, _c_i64, _c_p]),
     "sk_kr_adjoint_cc": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_i64,

@@ -11,7 +11,12 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["bcsc_encode", "bcsc_decode", "bcsc_segments", "srtt_sampler_encode", "sign_bits", "wide_encode_device", "gather_encode"]
+__all__ = ["bcsc_encode", "bcsc_decode", "bcsc_segments", "srtt_sampler_encode", "sign_bits", "wide_encode_device",
+           "gather_encode", "ring_encode", "ring_decode"]
+
+RING_RC = 64     # rows of Omega per stage of the K1r ring kernel (sparse_right_ring.cu RC)
+RING_UC = 128    # rows of Omega per consumer unit (two stages, sparse_right_ring.cu UC)
+RING_WARPS = 16  # consumer warps (NCONS), 16 output columns each (CPW)
 
 ADJ_GROUP = 1024  # output rows per CTA group of the adjoint fast path (sparse_adjoint.cu V2_CG)
 PTR_PAD = 1028    # ints the fast path may read past the pointer array
@@ -168,3 +173,63 @@ def gather_encode(rows, cols, neg, d: int, k: int, piece_rows: int, device):
               + torch.clamp(torch.arange(npieces + 1, device=device, dtype=torch.int64) * piece_rows, max=d)[None, :])
     off = torch.searchsorted(skey, bounds.reshape(-1)).reshape(k, npieces + 1).to(torch.int64)
     return ent.contiguous(), off.contiguous()
+
+
+def ring_encode(rows, cols, neg, d: int, k: int):
+    """(rows, cols, neg) triplets -> (lists uint8 [16-byte units], seg uint32[nunits*16 + 1]) for K1r.
+
+    For unit h (rows h*128 .. h*128+127 of Omega, two 64-row stages) and consumer warp w (columns
+    w*16 .. w*16+15) the segment at byte 16*seg[h*16 + w] holds 16 uint8 column counts, then the
+    entries of those columns in column order, each (row % 64) | stage << 6 | neg << 7 (stage =
+    (row // 64) % 2), padded to 16 bytes.  Duplicated (row, column) entries stay separate (their adds
+    sum, as the reference's CSR duplicates do).
+    """
+    rows = np.asarray(rows, dtype=np.int64).ravel()
+    cols = np.asarray(cols, dtype=np.int64).ravel()
+    neg = np.asarray(neg, dtype=bool).ravel()
+    if k > RING_WARPS * 16:
+        raise ValueError("ring encoding needs k <= 256")
+    nch = (d + RING_UC - 1) // RING_UC
+    nseg = nch * RING_WARPS
+    h = rows // RING_UC
+    w = cols // 16
+    j = cols % 16
+    key = (h * RING_WARPS + w) * 16 + j
+    order = np.lexsort((rows, key))
+    cnt = np.bincount(key, minlength=nseg * 16).reshape(nseg, 16)
+    if cnt.size and cnt.max() > 255:
+        raise ValueError("more than 255 entries of one column in a 128-row unit")
+    per_seg = cnt.sum(axis=1)
+    units = 1 + (per_seg + 15) // 16
+    seg = np.zeros(nseg + 1, dtype=np.int64)
+    np.cumsum(units, out=seg[1:])
+    lists = np.zeros(int(seg[-1]) * 16, dtype=np.uint8)
+    hdr = (seg[:-1] * 16)[:, None] + np.arange(16)[None, :]
+    lists[hdr.ravel()] = cnt.ravel().astype(np.uint8)
+    # entry e of segment s lands at 16*seg[s] + 16 + (its rank inside the segment)
+    skey = key[order] // 16
+    first = np.zeros(nseg + 1, dtype=np.int64)
+    np.cumsum(per_seg, out=first[1:])
+    rank = np.arange(rows.size, dtype=np.int64) - first[skey]
+    pos = seg[skey] * 16 + 16 + rank
+    r = rows[order] % RING_UC
+    lists[pos] = ((r % RING_RC) | ((r // RING_RC) << 6) | (neg[order].astype(np.int64) << 7)).astype(np.uint8)
+    return lists, seg.astype(np.uint32)
+
+
+def ring_decode(lists, seg, d: int, k: int):
+    """Inverse of ring_encode: (rows, cols, neg) sorted by (unit, warp, column, row)."""
+    lists = np.asarray(lists, dtype=np.uint8)
+    seg = np.asarray(seg, dtype=np.int64)
+    nseg = seg.size - 1
+    out_r, out_c, out_n = [], [], []
+    for s in range(nseg):
+        h, w = divmod(s, RING_WARPS)
+        base = int(seg[s]) * 16
+        cnt = lists[base:base + 16].astype(np.int64)
+        ents = lists[base + 16: base + 16 + int(cnt.sum())].astype(np.int64)
+        cols = np.repeat(w * 16 + np.arange(16), cnt)
+        out_r.append(h * RING_UC + ((ents >> 6) & 1) * RING_RC + (ents & 63))
+        out_c.append(cols)
+        out_n.append((ents >> 7).astype(bool))
+    return np.concatenate(out_r), np.concatenate(out_c), np.concatenate(out_n)

@@ -16,7 +16,7 @@ import numpy as np
 
 from .. import _lib
 from ..devrng import DevicePhilox, device_draws_enabled
-from .encode import ENT_PAD, PTR_PAD, bcsc_encode, bcsc_segments, gather_encode, wide_encode_device
+from .encode import ENT_PAD, PTR_PAD, bcsc_encode, bcsc_segments, gather_encode, ring_encode, wide_encode_device
 from .tensorcore import bt_from_triplets, dense_right_tc
 from .testmatrix import TestMatrix, entry_sample
 
@@ -170,6 +170,9 @@ class _SignSparseTM(TestMatrix):
             hi, lo, mag = self._tc_on(a.device)
             return dense_right_tc(a, hi, lo, self.k, mag)
         code = _lib.SK_F32 if a.dtype == torch.float32 else _lib.SK_F64
+        ring = self._ring_on(a.device) if code == _lib.SK_F64 else None
+        if ring is not None:
+            return self._right_ring(a, ring)
         ptr, ent, r, mag, _, _ = self._bcsc_on(a.device, "right", code)
         n = a.shape[0]
         y = torch.empty((n, self.k), dtype=a.dtype, device=a.device)
@@ -181,6 +184,50 @@ class _SignSparseTM(TestMatrix):
                                      ent.numel(), self.k, mag, y.data_ptr(), y.stride(0),
                                      torch.cuda.current_stream().cuda_stream)
         _lib.check(st, "sk_sparse_right")
+        return y
+
+    def _ring_on(self, device):
+        """K1r encoding (float64 right apply on the warp-specialised ring, k <= 256), cached per
+        device; None when the ring kernel does not take this operator (SKETCH_B200_K1=classic
+        forces the round-1 kernel)."""
+        import os
+
+        import torch
+
+        key = ("ring", device)
+        if key not in self._device_cache:
+            res = None
+            if os.environ.get("SKETCH_B200_K1", "ring") != "classic" and self.k <= 256:
+                rows, cols, neg, mag = self._sign_form()
+                try:
+                    lists, seg = ring_encode(rows, cols, neg, self.d, self.k)
+                except ValueError:
+                    lists = None
+                if lists is not None and _lib.load().sk_sparse_right_ring_supported(_lib.SK_F64, self.d, self.k,
+                                                                                     lists.size):
+                    res = (torch.from_numpy(lists).to(device), torch.from_numpy(seg.view(np.int32)).to(device),
+                           int(lists.size), mag)
+            self._device_cache[key] = res
+        return self._device_cache[key]
+
+    def _right_ring(self, a, ring):
+        import torch
+
+        lists, seg, nbytes, mag = ring
+        if a.stride(1) != 1 or a.data_ptr() % 8:
+            a = a.contiguous()
+        n = a.shape[0]
+        y = torch.empty((n, self.k), dtype=a.dtype, device=a.device)
+        if n == 0:
+            return y
+        lib = _lib.load()
+        ws_bytes = lib.sk_sparse_right_ring_workspace_bytes(n, self.d)  # stream-K tail partials + flags
+        ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=a.device)
+        with torch.cuda.device(a.device):
+            st = lib.sk_sparse_right_ring(a.data_ptr(), n, self.d, a.stride(0), lists.data_ptr(), seg.data_ptr(),
+                                          nbytes, self.k, mag, y.data_ptr(), y.stride(0), ws.data_ptr(), ws_bytes,
+                                          torch.cuda.current_stream().cuda_stream)
+        _lib.check(st, "sk_sparse_right_ring")
         return y
 
     def _adjoint_wide_on(self, device):

@@ -290,3 +290,52 @@ def test_right_paths_randomized(cuda):
         ref = a.double().cpu().numpy() @ tm.materialize()
         tol = 1e-5 if dt == torch.float32 else 1e-12
         assert rel_err(y, ref) <= tol, (trial, type(tm).__name__, n, tm.d, tm.k)
+
+
+def test_k1_ring_config1_full_vs_oracle(cuda):
+    """BASELINE config 1 in full on the ring kernel (K1r, stream-K over 148 SMs): every one of the
+    16384 rows against the oracle (csr_right, 1.3 s on the host), float64 bar 1e-12; and equal to
+    the round-1 kernel (SKETCH_B200_K1=classic) to rounding."""
+    import os
+
+    import torch
+
+    tm = skb.SparseUniformTM(4096, 256, 4, seed=0)
+    assert tm._ring_on(cuda) is not None
+    g = torch.Generator(device=cuda).manual_seed(21)
+    a = torch.randn(16384, 4096, dtype=torch.float64, device=cuda, generator=g)
+    y = tm.apply_right(a).cpu().numpy()
+    ref = orc.csr_right(orc.sparse_uniform_csr(4096, 256, 4, 0), a.cpu().numpy())
+    assert rel_err(y, ref) <= 1e-12
+    os.environ["SKETCH_B200_K1"] = "classic"
+    try:
+        tm2 = skb.SparseUniformTM(4096, 256, 4, seed=0)
+        assert tm2._ring_on(cuda) is None
+        y2 = tm2.apply_right(a).cpu().numpy()
+    finally:
+        del os.environ["SKETCH_B200_K1"]
+    assert rel_err(y, y2) <= 1e-14
+
+
+@pytest.mark.parametrize("n,d,k,zeta", [(1, 64, 256, 4), (63, 100, 17, 3), (65, 4097, 200, 4), (1000, 64, 1, 1),
+                                        (3000, 640, 256, 8), (130, 7, 5, 2), (20000, 1000, 64, 4)])
+def test_k1_ring_edge_shapes(n, d, k, zeta, cuda):
+    """Ragged tiles (n % 64), ragged chunks (d % 64), k < 256, a single CTA, tiles cut between CTAs."""
+    import torch
+
+    tm = skb.SparseUniformTM(d, k, zeta, seed=n)
+    assert tm._ring_on(cuda) is not None
+    rng = np.random.default_rng(n + d)
+    a = rng.standard_normal((n, d))
+    y = tm.apply_right(torch.from_numpy(a).to(cuda)).cpu().numpy()
+    assert rel_err(y, orc.csr_right(orc.sparse_uniform_csr(d, k, zeta, n), a)) <= 1e-12
+
+
+def test_k1_ring_stack_family(cuda):
+    import torch
+
+    tm = skb.SparseStackTM(3000, 4, 50, seed=3)
+    rng = np.random.default_rng(9)
+    a = rng.standard_normal((777, 3000))
+    y = tm.apply_right(torch.from_numpy(a).to(cuda)).cpu().numpy()
+    assert rel_err(y, orc.csr_right(orc.sparse_stack_csr(3000, 4, 50, 3), a)) <= 1e-12

@@ -222,3 +222,16 @@ def test_kr_factor_split_reproduces_omega(d0, ell, k, base):
                                    atol=0)  # products regrouped: exact for +-1, 1 ulp otherwise
     if (d0, ell) == (256, 2):
         assert tm._kr_group(True) == 1  # config 5: F = factor 1, W = factor 0 (no Kronecker columns formed)
+
+
+@pytest.mark.parametrize("d,k,zeta", [(4096, 256, 4), (100, 17, 3), (4097, 200, 8), (7, 5, 2)])
+def test_ring_encode_roundtrip(d, k, zeta):
+    """K1r's per-(chunk, warp) segments decode back to exactly Omega's (row, column, sign) triplets."""
+    from paper_2508_21189_b200.sketch.encode import ring_decode, ring_encode
+
+    coo = orc.sparse_uniform_csr(d, k, zeta, 5).tocoo()
+    lists, seg = ring_encode(coo.row, coo.col, coo.data < 0, d, k)
+    assert lists.size == int(seg[-1]) * 16 and seg.size == ((d + 127) // 128) * 16 + 1
+    r, c, n = ring_decode(lists, seg, d, k)
+    assert sorted(zip(coo.row.tolist(), coo.col.tolist(), (coo.data < 0).tolist())) == \
+        sorted(zip(r.tolist(), c.tolist(), n.tolist()))
