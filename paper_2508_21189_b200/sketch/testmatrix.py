@@ -151,10 +151,41 @@ class TestMatrix(ABC):
     def _right_sparse_input(self, a):
         raise NotImplementedError
 
-    def _right_device(self, a):
-        """Dense device GEMM with the materialized Omega (cuBLAS); families override with kernels."""
+    def _dense_cc(self, x, adjoint: bool):
+        """A Omega (or Omega^T B) with the materialized real Omega on the library's CUDA-core
+        contraction kernel (sk_kr_right_cc / sk_kr_adjoint_cc with one block: W = 1, F = Omega),
+        float64 accumulation; float32 or float64 in and out."""
         import torch
 
+        from .. import _lib
+
+        key = ("dense_cc", x.device, x.dtype)
+        if key not in self._device_cache:
+            f = torch.as_tensor(np.ascontiguousarray(self.materialize()), device=x.device).to(x.dtype)
+            self._device_cache[key] = (f, torch.ones((1, self.k), dtype=x.dtype, device=x.device))
+        f, w = self._device_cache[key]
+        if x.stride(1) != 1 or x.stride(0) < x.shape[1]:
+            x = x.contiguous()
+        rows = x.shape[1] if adjoint else x.shape[0]
+        out = torch.empty((self.k, rows) if adjoint else (rows, self.k), dtype=x.dtype, device=x.device)
+        if rows == 0:
+            return out
+        lib = _lib.load()
+        code = _lib.SK_F64 if x.dtype == torch.float64 else _lib.SK_F32
+        fn = lib.sk_kr_adjoint_cc if adjoint else lib.sk_kr_right_cc
+        with torch.cuda.device(x.device):
+            st = fn(code, x.data_ptr(), rows, 1, self.d, x.stride(0), f.data_ptr(), f.stride(0), w.data_ptr(),
+                    w.stride(0), self.k, 1.0, out.data_ptr(), out.stride(0), torch.cuda.current_stream().cuda_stream)
+        _lib.check(st, "sk_kr_adjoint_cc" if adjoint else "sk_kr_right_cc")
+        return out
+
+    def _right_device(self, a):
+        """Dense apply of the materialized Omega: real fields on the library's CUDA-core kernel (K4c
+        with one block), complex fields as a device GEMM through torch; families override with kernels."""
+        import torch
+
+        if self.field == "real" and a.dtype in (torch.float32, torch.float64):
+            return self._dense_cc(a, adjoint=False)
         om = self._dense_on(a.device, a.dtype)
         dt = torch.promote_types(a.dtype, om.dtype)
         return a.to(dt) @ om.to(dt)
@@ -162,6 +193,8 @@ class TestMatrix(ABC):
     def _adjoint_device(self, b):
         import torch
 
+        if self.field == "real" and b.dtype in (torch.float32, torch.float64):
+            return self._dense_cc(b, adjoint=True)
         om = self._dense_on(b.device, b.dtype)
         dt = torch.promote_types(b.dtype, om.dtype)
         return om.to(dt).conj().T @ b.to(dt)

@@ -165,3 +165,23 @@ def test_gaussian_f32(cuda):
     a = rng.standard_normal((333, 1024)).astype(np.float32)
     y = tm.apply_right(torch.from_numpy(a).to(cuda)).double().cpu().numpy()
     assert rel_err(y, orc.dense_right(orc.gaussian_dense(1024, 96, 9), a)) <= 1e-5
+
+
+@pytest.mark.parametrize("dt", ["float64", "float32"])
+def test_gaussian_dense_families_own_kernel(dt, cuda):
+    """float64 Gaussian (the reference's dtype) and every real adjoint of a materialised family run the
+    library's CUDA-core contraction kernel (float64 accumulation), not cuBLAS."""
+    import torch
+
+    tm = skb.GaussianTM(3000, 70, seed=11)
+    rng = np.random.default_rng(4)
+    a = rng.standard_normal((257, 3000))
+    b = rng.standard_normal((3000, 9))
+    tdt = getattr(torch, dt)
+    tol = 1e-12 if dt == "float64" else 1e-5
+    om = orc.gaussian_dense(3000, 70, 11)
+    y = tm.apply_right(torch.from_numpy(a).to(cuda, tdt)).double().cpu().numpy()
+    x = tm.apply_adjoint(torch.from_numpy(b).to(cuda, tdt)).double().cpu().numpy()
+    assert rel_err(y, a.astype(dt).astype(np.float64) @ om) <= tol
+    assert rel_err(x, om.T @ b.astype(dt).astype(np.float64)) <= tol
+    assert any(k[0] == "dense_cc" for k in tm._device_cache)
