@@ -294,6 +294,21 @@ SK_API int sk_kr_adjoint(const float* B, int64_t m, int64_t P, int64_t dl, int64
                          const uint16_t* Ft_lo, int64_t ldf, const float* W, int64_t ldw, int64_t k, double scale,
                          float* X, int64_t ldx, void* ws, size_t ws_bytes, void* stream);
 /*
+ * K6 — fused two-sided sketch: Y[n,k] = sy * A Omega and XT[p,d] = sx * Psi^T A from ONE
+ * read of float32 A, both on tcgen05 (BF16x2 on A).  Replaces the pair `_sketch_right(a, omega)` /
+ * `_sketch_left_adjoint(a, psi)` of the generalized-Nystrom drivers (src/rand_nla.py:191-202,
+ * 230-245).  Omega^T: k x d bf16 (row stride ldb) + residual or NULL; Psi: a sparse-sign matrix with
+ * zeta targets per row of A, given as psi[n][zeta] uint8 = q | neg << 7 (q < p <= 128); k <= 128.
+ * A 16-byte aligned, lda % 4 == 0, ldb % 8 == 0.  Workspace: sk_two_sided_workspace_bytes(n, d, k,
+ * Bt_lo != NULL) (per-CTA partials of XT, reduced in a fixed order).
+ */
+SK_API size_t sk_two_sided_workspace_bytes(int64_t n, int64_t d, int64_t k, int split_omega);
+SK_API int sk_two_sided_sketch(const float* A, int64_t n, int64_t d, int64_t lda, const uint16_t* Bt_hi,
+                               const uint16_t* Bt_lo, int64_t ldb, int64_t k, double sy, const uint8_t* psi,
+                               int32_t zeta, int64_t p, double sx, float* Y, int64_t ldy, float* XT, int64_t ldx,
+                               void* ws, size_t ws_bytes, void* stream);
+
+/*
  * K4c — the same contractions on the CUDA cores for float64 (the reference's dtype; float64
  * accumulation, parity 1e-12) and float32 shapes the tcgen05 form does not take.  F is dl x k
  * (row stride ldf) and W is P x k (row stride ldw), both of `dtype`.  Adjoint: X[k,m] from B [P*dl][m].

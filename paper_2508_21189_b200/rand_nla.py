@@ -382,33 +382,98 @@ def _rank_of(s) -> int:
     return 0 if s.numel() == 0 or float(s[0]) == 0.0 else int((s > DEFAULT_RANK_TOL * s[0]).sum())
 
 
-def two_sided_sketch(a, tm_omega, tm_psi, *, one_pass: bool = False, block_bytes: int = 64 << 20):
+def _omega_bt(tm):
+    """Omega^T in bf16 (hi, lo-or-None, scale) for the fused kernel, cached on the operator: sparse sign
+    operators exactly (+-1, magnitude as the scale), other families through the materialised Omega
+    (small d x k only: the right operand of a generalized-Nystrom sketch)."""
+    import torch
+
+    from .sketch.tensorcore import bt_from_dense, bt_from_triplets
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    key = ("two_sided_bt", dev)
+    if key not in tm._device_cache:
+        sf = tm._sign_form() if hasattr(tm, "_sign_form") else None
+        if sf is not None:
+            rows, cols, neg, mag = sf
+            hi, lo = bt_from_triplets(rows, cols, neg, tm.d, tm.k, dev)
+            tm._device_cache[key] = (hi, lo, mag)
+        else:
+            om = tm.materialize()
+            mag = float(np.abs(om).max()) or 1.0
+            hi, lo = bt_from_dense(om / mag, dev)
+            tm._device_cache[key] = (hi, lo, mag)
+    return tm._device_cache[key]
+
+
+def _psi_rows(tm):
+    """Psi as [n][zeta] uint8 (q | neg << 7) for the fused kernel (exactly zeta targets per row, p <= 128),
+    or None."""
+    import torch
+
+    if tm.k > 128 or tm.field != "real" or not hasattr(tm, "_sign_form"):
+        return None
+    dev = torch.device("cuda", torch.cuda.current_device())
+    key = ("two_sided_psi", dev)
+    if key not in tm._device_cache:
+        res = None
+        dform = tm._device_sign_form(dev)
+        if dform is not None:
+            cols, neg, mag = dform
+            res = ((cols.to(torch.int32) | (neg.to(torch.int32) << 7)).to(torch.uint8).contiguous(), cols.shape[1], mag)
+        else:
+            sf = tm._sign_form()
+            if sf is not None:
+                rows, cols, neg, mag = sf
+                cnt = np.bincount(rows, minlength=tm.d) if rows.size else np.zeros(tm.d, np.int64)
+                if rows.size and cnt.min() == cnt.max() and np.all(np.diff(rows) >= 0):
+                    z = int(cnt[0])
+                    ent = (cols.astype(np.int64) | (neg.astype(np.int64) << 7)).astype(np.uint8).reshape(tm.d, z)
+                    res = (torch.from_numpy(ent).to(dev), z, mag)
+        tm._device_cache[key] = res
+    return tm._device_cache[key]
+
+
+def two_sided_sketch(a, tm_omega, tm_psi, *, fused: bool | None = None):
     """Y = A Omega (n x k) and X = A^* Psi (d x p) for the generalized Nystrom drivers.
 
-    one_pass=True: for a float32 device A and a sparse-sign Psi, A is streamed in
-    row blocks of about `block_bytes` (multiples of 128 rows) that stay resident in the 126 MB L2:
-    the right kernel reads a block from DRAM and the adjoint kernel re-reads it from L2,
-    accumulating Psi[rows]^T A[rows] into X^*. Measured (tools/two_sided_probe.py, A 2M x 512 f32):
-    two passes 7.1 ms; one pass 9.8 ms at 64 MB blocks, 7.5 ms at 1 GB — the adjoint is issue-bound
-    and each block costs two host-side launches, so the default is two passes (same results).
+    float32 device A with a sparse-sign Psi (exactly zeta per row, p <= 128) and k <= 128: ONE pass
+    over A on the fused tcgen05 kernel (`sk_two_sided_sketch`): every tile of A feeds
+    both products from shared memory.  Otherwise (or fused=False) the two applies run separately.
     Returns device tensors in A's precision.
     """
     import torch
 
     A, _ = _as_device_2d(a)
     n, d = A.shape
-    fused = (one_pass and A.is_cuda and A.dtype == torch.float32 and hasattr(tm_psi, "adjoint_rows")
-             and tm_psi.adjoint_path(A) in ("wide", "rowgather"))
-    if not fused:
+    psi = None
+    ok = (A.is_cuda and A.dtype == torch.float32 and tm_omega.k <= 128 and tm_omega.field == "real"
+          and tm_omega.d * tm_omega.k <= (1 << 26) and fused is not False)
+    if ok:
+        psi = _psi_rows(tm_psi)
+    if psi is None:
+        if fused:
+            raise ValueError("the fused two-sided kernel needs float32 CUDA A, k <= 128 and a sparse-sign Psi "
+                             "with exactly zeta nonzeros per row and p <= 128")
         return tm_omega.apply_right(A), tm_psi.apply_adjoint(A).conj().T
-    rows = max(128, (block_bytes // (d * 4)) // 128 * 128)
-    y = torch.empty((n, tm_omega.k), dtype=A.dtype, device=A.device)
-    xt = torch.empty((tm_psi.k, d), dtype=A.dtype, device=A.device)
-    for r0 in range(0, n, rows):
-        r1 = min(n, r0 + rows)
-        blk = A[r0:r1]
-        y[r0:r1] = tm_omega.apply_right(blk)
-        tm_psi.adjoint_rows(blk, r0, r1, xt, accumulate=r0 > 0)
+    from . import _lib
+
+    ent, zeta, mag_psi = psi
+    hi, lo, mag_om = _omega_bt(tm_omega)
+    if A.stride(1) != 1 or A.stride(0) % 4 or A.data_ptr() % 16:
+        A = A.contiguous()
+    k, p = tm_omega.k, tm_psi.k
+    y = torch.empty((n, k), dtype=torch.float32, device=A.device)
+    xt = torch.empty((p, d), dtype=torch.float32, device=A.device)
+    lib = _lib.load()
+    ws_bytes = lib.sk_two_sided_workspace_bytes(max(n, 1), d, k, 1 if lo is not None else 0)
+    ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=A.device)
+    with torch.cuda.device(A.device):
+        st = lib.sk_two_sided_sketch(A.data_ptr(), n, d, A.stride(0), hi.data_ptr(),
+                                     lo.data_ptr() if lo is not None else None, hi.stride(0), k, float(mag_om),
+                                     ent.data_ptr(), zeta, p, float(mag_psi), y.data_ptr(), y.stride(0), xt.data_ptr(),
+                                     xt.stride(0), ws.data_ptr(), ws_bytes, torch.cuda.current_stream().cuda_stream)
+    _lib.check(st, "sk_two_sided_sketch")
     return y, xt.T
 
 

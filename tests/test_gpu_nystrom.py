@@ -52,19 +52,39 @@ def test_validation_errors(cuda):
         rn.nystrom_psd(-apsd, 30, skb.SparseUniformTM(512, 30, 4))
 
 
-def test_two_sided_sketch_one_pass(cuda):
-    """Row blocks through L2 (forced small) give the same Y and X as two full passes."""
+@pytest.mark.parametrize("n,d,k,p,omega", [(20000, 512, 64, 96, "srtt"), (1000, 100, 17, 128, "gauss"),
+                                           (777, 300, 128, 5, "sparse"), (300001, 256, 32, 64, "srtt"),
+                                           (129, 64, 1, 1, "sparse")])
+def test_two_sided_sketch_fused(n, d, k, p, omega, cuda):
+    """The one-pass fused kernel (sk_two_sided_sketch) against the two separate applies and the oracle:
+    ragged M-tiles and column groups (d = 100, 300), one or two column groups, split Omega (Gaussian)."""
+    import torch
+
+    import oracle as orc
+
+    g = torch.Generator(device=cuda).manual_seed(n)
+    a = torch.randn(n, d, device=cuda, generator=g)
+    om = {"srtt": lambda: skb.SparseRttTM(d, k, 1, "wht", seed=1), "gauss": lambda: skb.GaussianTM(d, k, seed=3),
+          "sparse": lambda: skb.SparseUniformTM(d, k, min(4, k), seed=5)}[omega]()
+    ps = skb.SparseUniformTM(n, p, min(8, p), seed=2)
+    assert rn._psi_rows(ps) is not None
+    y, x = rn.two_sided_sketch(a, om, ps, fused=True)
+    assert y.shape == (n, k) and x.shape == (d, p)
+    a64 = a.double().cpu().numpy()
+    y_ref = a64 @ om.materialize()
+    x_ref = orc.csr_adjoint(orc.sparse_uniform_csr(n, p, min(8, p), 2), a64).T
+    assert rel_err(y.double().cpu().numpy(), y_ref) <= 1e-5
+    assert rel_err(x.double().cpu().numpy(), x_ref) <= 1e-5
+    y2, x2 = rn.two_sided_sketch(a, om, ps, fused=False)
+    assert rel_err(y.double().cpu().numpy(), y2.double().cpu().numpy()) <= 1e-5
+
+
+def test_gen_nystrom_float32_device_end_to_end(cuda):
     import torch
 
     n, d, k, p = 20000, 512, 64, 96
     a = torch.randn(n, d, device=cuda)
     om = skb.SparseRttTM(d, k, 1, "wht", seed=1)
     ps = skb.SparseUniformTM(n, p, 8, seed=2)
-    y, x = rn.two_sided_sketch(a, om, ps, one_pass=True, block_bytes=1 << 20)  # 512-row blocks
-    assert y.shape == (n, k) and x.shape == (d, p)
-    y_ref = om.apply_right(a).double()
-    x_ref = ps.apply_adjoint(a).double().T
-    assert float((y.double() - y_ref).norm() / y_ref.norm()) <= 1e-6
-    assert float((x.double() - x_ref).norm() / x_ref.norm()) <= 1e-5
-    fo = rn.gen_nystrom_outer(a[:, :d], k, p, om, ps)  # float32 device path end to end
+    fo = rn.gen_nystrom_outer(a, k, p, om, ps)  # float32 device path end to end (fused sketch)
     assert fo.f.shape[0] == n and fo.g.shape[0] == d

@@ -1,4 +1,4 @@
-"""Time the one-pass two-sided sketch against two separate passes (generalized-Nystrom sketch stage)."""
+"""Time the fused one-pass two-sided sketch against two separate passes (generalized-Nystrom sketch stage)."""
 import os
 import sys
 
@@ -32,6 +32,6 @@ t_right = timed(lambda: om.apply_right(a))
 t_adj = timed(lambda: ps.apply_adjoint(a))
 print(f"A {n}x{d} f32 ({gb:.2f} GB): right {t_right:.3f} ms, adjoint {t_adj:.3f} ms, "
       f"two passes {t_right + t_adj:.3f} ms")
-for mb in (16, 32, 64, 96, 128, 256, 1024):
-    t = timed(lambda: rn.two_sided_sketch(a, om, ps, one_pass=True, block_bytes=mb << 20))
-    print(f"  one pass, {mb:4d} MB row blocks: {t:.3f} ms")
+t = timed(lambda: rn.two_sided_sketch(a, om, ps, fused=True))
+print(f"  fused one-pass kernel (sk_two_sided_sketch): {t:.3f} ms ({gb / t:.1f} TB/s of A, "
+      f"{(t_right + t_adj) / t:.1f}x the two passes)")
