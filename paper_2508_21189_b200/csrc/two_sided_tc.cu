@@ -25,6 +25,7 @@
 #include <cuda.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -59,6 +60,7 @@ struct TsParams {
   int stages;
   int ctas_per_group;
   int nb;                // Omega^T operands: 1 (hi) or 2 (hi + lo)
+  int dbg;               // timing experiments (SKETCH_B200_TS_DBG): 1 no MMA2, 2 no PsiT writes, 4 no Y stores
 };
 
 template <int N>
@@ -183,26 +185,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool fresh = (i % kFold) == 0;  // first M-tile of an XT chunk: overwrite the accumulators
         if (fresh && i > 0) mbar_wait(xt_empty, ((i / kFold) - 1) & 1);
         tc_fence_after();
-        const uint32_t psi = smem_u32(psi_buf + pb * kPsiBytes);
+        const uint64_t dps = sdesc_kmajor_sw128(smem_u32(psi_buf + pb * kPsiBytes));
         const uint32_t dy = tm_y + yb * (uint32_t)p.NY;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + (size_t)s * stage_bytes);
-          const uint32_t a_hi = st, a_lo = st + BM * 128, bt = st + kAStage, btl = bt + b_bytes;
+          // descriptors built once per stage; a K step adds (bytes >> 4) to the 14-bit start address
+          const uint64_t dah = sdesc_kmajor_sw128(st), dal = sdesc_kmajor_sw128(st + BM * 128);
+          const uint64_t dbt = sdesc_kmajor_sw128(st + kAStage), dbl = sdesc_kmajor_sw128(st + kAStage + b_bytes);
+          const uint64_t dmh = sdesc_mnmajor_sw128(st), dml = sdesc_mnmajor_sw128(st + BM * 128);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {  // MMA1: Y += A Omega (K = this k-block's 64 columns)
-            const uint64_t db = sdesc_kmajor_sw128(bt + kk * 32);
-            umma_bf16(dy, sdesc_kmajor_sw128(a_hi + kk * 32), db, id1, (kb > 0 || kk > 0) ? 1u : 0u);
-            umma_bf16(dy, sdesc_kmajor_sw128(a_lo + kk * 32), db, id1, 1u);
-            if (p.nb == 2) umma_bf16(dy, sdesc_kmajor_sw128(a_hi + kk * 32), sdesc_kmajor_sw128(btl + kk * 32), id1, 1u);
+            const uint64_t o = (uint64_t)(kk * 2);
+            umma_bf16(dy, dah + o, dbt + o, id1, (kb > 0 || kk > 0) ? 1u : 0u);
+            umma_bf16(dy, dal + o, dbt + o, id1, 1u);
+            if (p.nb == 2) umma_bf16(dy, dah + o, dbl + o, id1, 1u);
           }
           const uint32_t dx = tm_xt + (uint32_t)kb * BK;
 #pragma unroll
-          for (int kr = 0; kr < BM / 16; ++kr) {  // MMA2: XT[:, kb] += PsiT (K = 128 rows) A_tile
-            const uint64_t da = sdesc_kmajor_sw128(psi + (kr >> 2) * (BM * 128) + (kr & 3) * 32);
-            umma_bf16(dx, da, sdesc_mnmajor_sw128(a_hi + kr * 2048), id2, (!fresh || kr > 0) ? 1u : 0u);
-            umma_bf16(dx, da, sdesc_mnmajor_sw128(a_lo + kr * 2048), id2, 1u);
+          for (int kr = 0; kr < ((p.dbg & 1) ? 0 : BM / 16); ++kr) {  // MMA2: XT[:, kb] += PsiT (K = 128 rows) A_tile
+            const uint64_t da = dps + (uint64_t)((kr >> 2) * ((BM * 128) >> 4) + (kr & 3) * 2);
+            const uint64_t ob = (uint64_t)(kr * (2048 >> 4));
+            umma_bf16(dx, da, dmh + ob, id2, (!fresh || kr > 0) ? 1u : 0u);
+            umma_bf16(dx, da, dml + ob, id2, 1u);
           }
           umma_commit(&empty[s]);
           if (++s == S) { s = 0; ph ^= 1; }
@@ -240,10 +246,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_wait(&psi_empty[pb], pph ^ 1);
         const uint32_t base = smem_u32(psi_buf + pb * kPsiBytes);
-        for (int c = sid; c < (int)(kPsiBytes / 16); c += 64) sts128(base + c * 16, 0u, 0u, 0u, 0u);
+        for (int c = sid; c < (int)((p.dbg & 2) ? 0 : kPsiBytes / 16); c += 64) sts128(base + c * 16, 0u, 0u, 0u, 0u);
         asm volatile("bar.sync 2, 64;" ::: "memory");
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < ((p.dbg & 2) ? 0 : 4); ++u) {
           const int b = (sid + 64 * u) * 16;
           if (b >= nbytes) continue;
           const uint32_t wv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
@@ -320,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld16(ybase + g * 16, r);
         tmem_ld_wait();
         const int col = yc0 + g * 16;
-        if (row < p.n && col < p.k) {
+        if (row < p.n && col < p.k && !(p.dbg & 4)) {
           float* out = p.Y + row * p.ldy + col;
           if (p.ncg == 1) {
 #pragma unroll
@@ -494,6 +500,10 @@ extern "C" int sk_two_sided_sketch(const float* A, int64_t n, int64_t d, int64_t
   prm.stages = pl.stages;
   prm.ctas_per_group = pl.cpg;
   prm.nb = nb;
+  {
+    const char* e = getenv("SKETCH_B200_TS_DBG");
+    prm.dbg = e ? atoi(e) : 0;
+  }
   cudaFuncSetAttribute(two_sided_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
   two_sided_kernel<<<pl.grid, kThreads, pl.smem, s>>>(ma, mb, mbl, prm);
   st = check_launch("sk_two_sided_sketch");

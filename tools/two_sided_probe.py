@@ -35,3 +35,10 @@ print(f"A {n}x{d} f32 ({gb:.2f} GB): right {t_right:.3f} ms, adjoint {t_adj:.3f}
 t = timed(lambda: rn.two_sided_sketch(a, om, ps, fused=True))
 print(f"  fused one-pass kernel (sk_two_sided_sketch): {t:.3f} ms ({gb / t:.1f} TB/s of A, "
       f"{(t_right + t_adj) / t:.1f}x the two passes)")
+
+for dbg in os.environ.get("TS_DBG", "").split(","):
+    if dbg:
+        os.environ["SKETCH_B200_TS_DBG"] = dbg
+        t = timed(lambda: rn.two_sided_sketch(a, om, ps, fused=True))
+        print(f"  SKETCH_B200_TS_DBG={dbg}: {t:.3f} ms")
+        os.environ["SKETCH_B200_TS_DBG"] = "0"
