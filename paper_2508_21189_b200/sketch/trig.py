@@ -341,18 +341,87 @@ class SparseRttTM(TestMatrix):
             return self._right_device(_transposed(b)).T.contiguous()
         return super()._adjoint_device(b)
 
-    def _dct_tc_ok(self, a) -> bool:
-        """float32 DCT with a modest sketch size: the materialised Omega = D C^T S (d x k) on the
-        tensor-core GEMM (BF16x2 on both operands, ~3e-6) beats the FFT route (n d k vs n d log d
-        with cuFFT's passes): 1.3 ms vs 4.4 ms at the config-2 shape."""
+    def _dct_fft_tables(self, device, dtype):
+        """Host tables of the fused DCT-III row kernel (csrc/srtt_dct.cu), cached per device and dtype:
+        w = D / s, (alpha_k, beta_k), the IDFT_M twiddles, the sampled output -> index-in-v map and the
+        scale (sampler magnitude / N)."""
         import torch
 
-        return (a.dtype == torch.float32 and self.k <= 1024 and self.d % 4 == 0
-                and self.d * self.k <= (1 << 26) and _lib.load().sk_dense_tc_supported(self.k) == 1)
+        key = ("srtt_dct_fft", device, dtype)
+        if key not in self._device_cache:
+            n_, m_ = self.d, self.d // 2
+            dvals, sampler = self._parts()
+            rows, neg, mag = sampler.column_draws()
+            s = np.full(n_, np.sqrt(2.0 / n_))
+            s[0] = np.sqrt(1.0 / n_)
+            kk = np.arange(m_)
+            c = np.exp(1j * np.pi * np.arange(m_ + 1) / (2 * n_))
+            om = np.exp(2j * np.pi * kk / n_)
+            alpha = c[:m_] * (1 + 1j * om)
+            beta = np.conj(c[m_ - kk]) * (1 - 1j * om)
+            ab = np.stack([alpha, beta], axis=1)  # (M, 2) complex
+            tw = np.exp(2j * np.pi * np.arange(m_) / m_)
+            j = rows.reshape(-1).astype(np.int64)
+            t = np.where(j % 2 == 0, j // 2, n_ - 1 - (j - 1) // 2)
+            samp = (t | (neg.reshape(-1).astype(np.int64) << 31)).astype(np.uint32).view(np.int32)
+
+            def real(x):
+                return torch.from_numpy(np.ascontiguousarray(np.stack([x.real, x.imag], -1))).to(device, dtype)
+
+            self._device_cache[key] = (torch.from_numpy(np.ascontiguousarray(dvals / s)).to(device, dtype), real(ab),
+                                       real(tw), torch.from_numpy(np.ascontiguousarray(samp)).to(device),
+                                       float(mag) / n_)
+        return self._device_cache[key]
+
+    def _dct_fft_right(self, a):
+        """Y through the fused DCT-III row kernel (sk_srtt_dct_right): no intermediate in HBM."""
+        import torch
+
+        w, ab, tw, samp, scale = self._dct_fft_tables(a.device, a.dtype)
+        if a.stride(1) != 1 or a.data_ptr() % 16 or (a.stride(0) * a.element_size()) % 16:
+            a = a.contiguous()
+        n = a.shape[0]
+        y = torch.empty((n, self.k), dtype=a.dtype, device=a.device)
+        if n == 0:
+            return y
+        lib = _lib.load()
+        code = _lib.SK_F32 if a.dtype == torch.float32 else _lib.SK_F64
+        with torch.cuda.device(a.device):
+            st = lib.sk_srtt_dct_right(code, a.data_ptr(), n, self.d, a.stride(0), w.data_ptr(), ab.data_ptr(),
+                                       tw.data_ptr(), samp.data_ptr(), self.xi, self.k, scale, y.data_ptr(),
+                                       y.stride(0), torch.cuda.current_stream().cuda_stream)
+        _lib.check(st, "sk_srtt_dct_right")
+        return y
+
+    def dct_path(self, dtype) -> str:
+        """'tc' (float32, k <= 1024: the materialised Omega = D C^T S on the tcgen05 GEMM), 'fft' (the fused
+        DCT-III row kernel: float64 and large k, power-of-two d) or 'cufft' (other even d: prep kernel +
+        cuFFT irfft); SKETCH_B200_DCT=tc|fft|cufft overrides."""
+        import os
+
+        import torch
+
+        code = _lib.SK_F32 if dtype == torch.float32 else _lib.SK_F64
+        fft_ok = _lib.load().sk_srtt_dct_supported(code, self.d) == 1
+        forced = os.environ.get("SKETCH_B200_DCT", "auto")
+        if forced == "fft" and fft_ok:
+            return "fft"
+        if forced == "cufft":
+            return "cufft"
+        tc_ok = (dtype == torch.float32 and self.k <= 1024 and self.d % 4 == 0 and self.d * self.k <= (1 << 26)
+                 and _lib.load().sk_dense_tc_supported(self.k) == 1)
+        if tc_ok and forced in ("tc", "auto"):
+            return "tc"  # float32, k <= 1024: config-2 shape 1.21 ms (fused FFT kernel 2.47, cuFFT 4.04)
+        if fft_ok:
+            return "fft"  # float64 (the reference's dtype): 2.31 ms vs 3.97 for cuFFT at 32768 x 8192
+        return "cufft"
 
     def _right_device(self, a):
         if self._dct_ok(a.dtype):
-            if self._dct_tc_ok(a):
+            path = self.dct_path(a.dtype)
+            if path == "fft":
+                return self._dct_fft_right(a)
+            if path == "tc":
                 key = ("srtt_dct_tc", a.device)
                 if key not in self._device_cache:
                     self._device_cache[key] = bt_from_dense(self.materialize(), a.device)

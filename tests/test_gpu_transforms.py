@@ -65,3 +65,45 @@ def test_dct3_rows_matches_scipy(cuda):
         x = np.random.default_rng(n).standard_normal((4, n))
         got = skb.dct3_rows(torch.as_tensor(x, device=cuda)).cpu().numpy()
         assert rel_err(got, scipy.fft.dct(x, type=3, norm="ortho", axis=1)) <= 1e-14
+
+
+@pytest.mark.parametrize("d", [32, 64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384])
+@pytest.mark.parametrize("dt", ["float32", "float64"])
+def test_srtt_dct_fused_kernel_every_pass_pattern(d, dt, cuda, monkeypatch):
+    """K3b (sk_srtt_dct_right) for every power-of-two length it takes: log2(d/2) % 4 = 0..3 selects the
+    radix-32/4/8 extra pass; float64 (the reference's dtype) at 1e-12, float32 at 1e-5; ragged k, xi > 1."""
+    import torch
+
+    if dt == "float64" and d > 8192:
+        pytest.skip("float64 rows of d > 8192 take the cuFFT form")
+    k, xi = 37, 3
+    monkeypatch.setenv("SKETCH_B200_DCT", "fft")
+    tm = skb.SparseRttTM(d, k, xi, "dct", seed=d)
+    tdt = getattr(torch, dt)
+    assert tm.dct_path(tdt) == "fft"
+    rng = np.random.default_rng(d)
+    a = rng.standard_normal((301, d)).astype(dt)
+    y = tm.apply_right(torch.from_numpy(a).to(cuda)).double().cpu().numpy()
+    dv, samp = orc.srtt_parts(d, k, xi, d)
+    ref = orc.srtt_right(dv, samp, a, "dct")
+    assert rel_err(y, ref) <= (1e-12 if dt == "float64" else 1e-5)
+
+
+def test_srtt_dct_paths_agree_config2_shape(cuda, monkeypatch):
+    """Config-2 shape with the DCT transform (the reference default): the fused FFT kernel, the
+    tensor-core form and the cuFFT form agree; a 64-row slab against the oracle."""
+    import torch
+
+    tm = skb.SparseRttTM(8192, 512, 1, "dct", seed=0)
+    g = torch.Generator(device=cuda).manual_seed(5)
+    a = torch.randn(4096, 8192, device=cuda, generator=g)
+    outs = {}
+    for path in ("fft", "tc", "cufft"):
+        monkeypatch.setenv("SKETCH_B200_DCT", path)
+        assert tm.dct_path(torch.float32) == path
+        outs[path] = tm.apply_right(a).double()
+    for path in ("tc", "cufft"):
+        assert float((outs["fft"] - outs[path]).norm() / outs[path].norm()) <= 1e-5
+    dv, samp = orc.srtt_parts(8192, 512, 1, 0)
+    ref = orc.srtt_right(dv, samp, a[:64].cpu().numpy(), "dct")
+    assert rel_err(outs["fft"][:64].cpu().numpy(), ref) <= 1e-5
