@@ -13,7 +13,7 @@ import numpy as np
 
 from .. import _lib
 
-__all__ = ["dense_right_tc", "dense_tn_tc", "bt_from_triplets", "bt_from_dense"]
+__all__ = ["dense_right_tc", "dense_tn_tc", "split_wt", "bt_from_triplets", "bt_from_dense"]
 
 MAX_K = 512
 
@@ -80,24 +80,42 @@ def dense_right_tc(a, bt_hi, bt_lo, k: int, scale: float):
     return y
 
 
-def dense_tn_tc(a, w, scale: float = 1.0):
-    """scale * a^T @ w on the tensor cores (sk_dense_tn_tc) for float32 CUDA `a` (n x d) and a
-    float32/float64 `w` (n x k): BF16x3, fp32 accumulation in bounded chunks. Returns (d x k)."""
+def split_wt(w, device):
+    """W^T as bf16 hi + lo (k x ldw, ldw = n rounded up to 8) for dense_tn_tc, from a float n x k W."""
+    import torch
+
+    n, k = w.shape
+    wt = torch.zeros((k, _pad8(n)), dtype=torch.float64, device=device)
+    wt[:, :n] = torch.as_tensor(w, device=device).T.to(torch.float64)
+    hi = wt.to(torch.bfloat16)
+    lo = (wt - hi.to(torch.float64)).to(torch.bfloat16)
+    return hi, lo
+
+
+def dense_tn_tc(a, w=None, scale: float = 1.0, *, wt=None):
+    """scale * a^T @ w on the tensor cores (sk_dense_tn_tc) for float32 CUDA `a` (n x d), read in place,
+    and a float32/float64 `w` (n x k) or its precomputed split `wt` = (hi, lo) from split_wt: BF16x3,
+    fp32 accumulation in bounded chunks. Returns (d x k)."""
     import torch
 
     if a.dtype != torch.float32 or not a.is_cuda:
         raise TypeError("dense_tn_tc needs a float32 CUDA A")
     n, d = a.shape
-    k = w.shape[1]
+    if n == 0 or d == 0:
+        k = (wt[0].shape[0] if wt is not None else w.shape[1])
+        return torch.zeros((d, k), dtype=torch.float32, device=a.device)
     if a.stride(1) != 1 or a.stride(0) % 4 or a.data_ptr() % 16 or d % 4:
+        if d % 4:  # ragged column count: zero-padded copy (the extra columns give zero rows of the result)
+            pad = torch.zeros((n, d + (-d) % 4), dtype=a.dtype, device=a.device)
+            pad[:, :d] = a
+            return dense_tn_tc(pad, w, scale, wt=wt)[:d]
         a = a.contiguous()
-        if d % 4:
-            raise ValueError("dense_tn_tc needs d % 4 == 0")
-    ldw = _pad8(n)
-    wt = torch.zeros((k, ldw), dtype=torch.float32, device=a.device)
-    wt[:, :n] = w.T.to(device=a.device, dtype=torch.float32)
-    hi = wt.to(torch.bfloat16)
-    lo = (wt - hi.to(torch.float32)).to(torch.bfloat16)
+    if wt is None:
+        wt = split_wt(w.to(device=a.device), a.device)
+        wt = (wt[0], wt[1])
+    hi, lo = wt
+    k = hi.shape[0]
+    ldw = hi.stride(0)
     y = torch.empty((d, k), dtype=torch.float32, device=a.device)
     lib = _lib.load()
     stream = torch.cuda.current_stream(a.device).cuda_stream

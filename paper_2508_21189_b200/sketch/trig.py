@@ -16,10 +16,9 @@ import scipy.fft
 
 from .. import _lib
 from .._device import from_result, to_operand
-from .._device import transposed as _transposed
 from .encode import srtt_sampler_encode
 from .sparse_rows import SparseColTM
-from .tensorcore import bt_from_dense, dense_right_tc
+from .tensorcore import bt_from_dense, dense_right_tc, dense_tn_tc, split_wt
 from .testmatrix import TestMatrix, entry_sample
 
 __all__ = ["wht", "dct2_ortho", "dft_unitary", "dct3_rows", "SparseRttTM", "TRANSFORMS"]
@@ -334,11 +333,19 @@ class SparseRttTM(TestMatrix):
         return y
 
     def _adjoint_device(self, b):
-        """Omega^T B = (B^T Omega)^T for the real transforms: the row kernels on B^T."""
+        """Omega^T B with B read in place (reference rtt.py:142-154): float32 on the tcgen05 TN engine
+        (B^T Omega with Omega = D F S materialised once as exact-or-split bf16, X = its transpose),
+        float64 on the library's CUDA-core contraction kernel (base class)."""
         import torch
 
-        if (self._native_ok(b.dtype) or self._dct_ok(b.dtype)) and b.dim() == 2:
-            return self._right_device(_transposed(b)).T.contiguous()
+        if self.field == "real" and b.dtype == torch.float32 and b.dim() == 2:
+            key = ("srtt_adj_tn", b.device)
+            if key not in self._device_cache:
+                om = self.materialize()
+                mag = float(np.abs(om).max()) or 1.0
+                self._device_cache[key] = (split_wt(om / mag, b.device), mag)
+            wt, mag = self._device_cache[key]
+            return dense_tn_tc(b, scale=mag, wt=wt).T.contiguous()
         return super()._adjoint_device(b)
 
     def _dct_fft_tables(self, device, dtype):
