@@ -69,7 +69,7 @@ def _cfg3(torch, dev, rank):
     tm = make()
     g = torch.Generator(device=dev).manual_seed(3000 + rank)
     a = torch.randn(n, d, dtype=torch.float32, device=dev, generator=g)
-    return dict(name="cfg3", tm=tm, make=make, a=a, n=n, d=d, k=k, launches=1, kernel="dense_tc (sparse sign as bf16 Omega^T)",
+    return dict(name="cfg3", tm=tm, make=make, a=a, n=n, d=d, k=k, launches=1, kernel="dense_tc_pair_kernel<1,0,0> (sparse sign as exact bf16 Omega^T)",
                 workload="cfg3 RSVD sketch Y=A*Omega: A 131072x16384 f32 (iid input for throughput), zeta=8, k=200",
                 op="right")
 
@@ -116,16 +116,50 @@ def _gauss(torch, dev, rank):
                 workload="Gaussian Y=A*Omega at the cfg3 shape: A 131072x16384 f32, k=200", op="right")
 
 
-WORKLOADS = {"cfg1": _cfg1, "cfg2": _cfg2, "cfg3": _cfg3, "cfg4": _cfg4, "cfg5": _cfg5, "gauss": _gauss}
+def _cfg2dct(torch, dev, rank):
+    """Config 2's shape with the reference's DEFAULT real-field transform (DCT, rtt.py:92-93)."""
+    from paper_2508_21189_b200.sketch import SparseRttTM
+
+    w = _cfg2(torch, dev, rank)
+    make = lambda: SparseRttTM(8192, 512, 1, "dct", seed=0)  # noqa: E731
+    w.update(name="cfg2dct", tm=make(), make=make, kernel="dense_tc_pair_kernel<2,0,0> (materialised D C^T S, BF16x3)",
+             workload="cfg2 shape with the DCT SRTT (reference default transform): A 65536x8192 f32, k=512, xi=1")
+    return w
+
+
+def _twosided(torch, dev, rank):
+    """The generalized-Nystrom sketch stage at DESIGN's shape: Y = A Omega and
+    X = A^T Psi from one read of A on the fused kernel."""
+    from paper_2508_21189_b200.sketch import SparseRttTM, SparseUniformTM
+
+    n, d, k, p = 1 << 21, 512, 64, 96
+    g = torch.Generator(device=dev).manual_seed(7000 + rank)
+    a = torch.randn(n, d, dtype=torch.float32, device=dev, generator=g)
+    make = lambda: (SparseRttTM(d, k, 1, "wht", seed=1), SparseUniformTM(n, p, 8, seed=2))  # noqa: E731
+    return dict(name="twosided", tm=make(), make=make, a=a, n=n, d=d, k=k, p=p, launches=2,
+                kernel="two_sided_kernel", op="twosided",
+                workload="two-sided sketch: A 2097152x512 f32, Omega SRTT (k=64), Psi sparse sign (p=96, zeta=8)")
+
+
+WORKLOADS = {"cfg1": _cfg1, "cfg2": _cfg2, "cfg3": _cfg3, "cfg4": _cfg4, "cfg5": _cfg5, "gauss": _gauss,
+             "cfg2dct": _cfg2dct, "twosided": _twosided}
 
 
 def _apply(w, x):
+    if w["op"] == "twosided":
+        from paper_2508_21189_b200 import rand_nla
+
+        om, ps = w["tm"]
+        return rand_nla.two_sided_sketch(x, om, ps)
     return w["tm"].apply_right(x) if w["op"] == "right" else w["tm"].apply_adjoint(x)
 
 
 def _bytes(w, dtype_size):
     a_bytes = w["n"] * w["d"] * dtype_size
-    out_elems = w["n"] * w["k"] if w["op"] == "right" else w["k"] * w["d"]
+    if w["op"] == "twosided":
+        out_elems = w["n"] * w["k"] + w["p"] * w["d"]
+    else:
+        out_elems = w["n"] * w["k"] if w["op"] == "right" else w["k"] * w["d"]
     return a_bytes, a_bytes + out_elems * dtype_size
 
 
@@ -339,11 +373,10 @@ def time_setup(torch, w, steady_s):
     a fresh operator's first apply on the step's input minus one steady apply."""
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    tm = w["make"]()
-    y = (tm.apply_right if w["op"] == "right" else tm.apply_adjoint)(w["a"])
+    y = _apply(dict(w, tm=w["make"]()), w["a"])
     torch.cuda.synchronize()
     first = time.perf_counter() - t0
-    del y, tm
+    del y
     return {"ms": max(0.0, first - steady_s) * 1e3, "first_call_ms": first * 1e3,
             "what": "constructor draws + device encoding and upload of Omega (first apply minus a steady apply)"}
 
@@ -377,8 +410,12 @@ def cpu_reference_step(w, a_host, procs):
 
     name = w["name"]
     tm = w["tm"]
-    if name == "cfg2":
+    if name in ("cfg2", "cfg2dct"):
         dv, samp = orc.srtt_parts(tm.d, tm.k, tm.xi, tm.seed)
+        fn = lambda x: orc.srtt_right(dv, samp, x, tm.transform)  # noqa: E731
+    elif name == "twosided":  # the Y = A Omega half on the sample rows (X needs every row of A)
+        om = tm[0]
+        dv, samp = orc.srtt_parts(om.d, om.k, om.xi, om.seed)
         fn = lambda x: orc.srtt_right(dv, samp, x, "wht")  # noqa: E731
     elif name in ("cfg1", "cfg3"):
         om = orc.sparse_uniform_csr(tm.d, tm.k, tm.zeta, tm.seed)
@@ -417,10 +454,12 @@ def sample_parity(w, procs):
     dt, y_ref = cpu_reference_step(w, a_host, procs)
     if w["op"] == "right":
         y_gpu = _apply(w, w["a"][:rows]).double().cpu().numpy()
+    elif w["op"] == "twosided":
+        y_gpu = _apply(w, w["a"][:rows])[0].double().cpu().numpy()
     else:  # the row block of S that multiplies the sample rows (device-sliced draws)
         y_gpu = w["tm"].row_block(0, rows).apply_adjoint(w["a"][:rows]).double().cpu().numpy()
     err = float(np.linalg.norm(y_gpu - y_ref) / np.linalg.norm(y_ref))
-    cores = procs if w["op"] == "right" else 1
+    cores = procs if w["op"] in ("right", "twosided") else 1
     cpu = {"value": a_host.nbytes / dt / 1e9, "unit": "GB/s", "cores": cores, "kind": "port",
            "sample": f"{rows} rows of the {w['name']} input ({a_host.nbytes / 1e6:.0f} MB), oracle/ port of the "
                      f"sketchkit float64 path" + (f", row-parallel over {procs} processes" if cores > 1 else
@@ -429,7 +468,8 @@ def sample_parity(w, procs):
     return cpu, err
 
 
-SAMPLE_ROWS = {"cfg1": 4096, "cfg2": 2048, "cfg3": 512, "cfg4": 1 << 18, "cfg5": 16}
+SAMPLE_ROWS = {"cfg1": 4096, "cfg2": 2048, "cfg3": 512, "cfg4": 1 << 18, "cfg5": 16, "cfg2dct": 1024,
+               "twosided": 8192}
 
 
 def run_reference(args):
@@ -572,7 +612,8 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
     ap.add_argument("--config", choices=sorted(WORKLOADS), default="cfg2")
-    ap.add_argument("--others", default="cfg1,cfg3,cfg4,cfg5,gauss", help="extra configs measured at N=1 ('' = none)")
+    ap.add_argument("--others", default="cfg1,cfg3,cfg4,cfg5,gauss,cfg2dct,twosided",
+                    help="extra configs measured at N=1 ('' = none)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (quick kernel experiments)")
     ap.add_argument("--no-sharded", action="store_true", help="skip the sharded config-4 SA (NCCL all-reduce) leg")
     args = ap.parse_args(argv)

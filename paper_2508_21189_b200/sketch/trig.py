@@ -106,8 +106,8 @@ def wht(x, axis: int = 0):
         raise ValueError("wht needs at least a 1-d array")
     d = shape[axis]
     _require_pow2(int(d))
-    if isinstance(x, np.ndarray) and np.iscomplexobj(x):
-        return _wht_host(x.real, axis) + 1j * _wht_host(x.imag, axis)
+    if isinstance(x, np.ndarray) and np.iscomplexobj(x):  # real and imaginary parts on the device
+        return wht(np.ascontiguousarray(x.real), axis) + 1j * wht(np.ascontiguousarray(x.imag), axis)
     if isinstance(x, torch.Tensor) and x.is_complex():
         return torch.complex(wht(x.real, axis), wht(x.imag, axis))
     if isinstance(x, torch.Tensor):
