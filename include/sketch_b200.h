@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define SK_ABI_VERSION 1
+#define SK_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define SK_API __attribute__((visibility("default")))

@@ -21,6 +21,7 @@ SK_F64 = 1
 SK_WHT = 0
 SK_DCT3 = 1
 SK_DIAG_PM1 = 0x100
+ABI_VERSION = 2  # include/sketch_b200.h SK_ABI_VERSION
 
 _c_i64 = ctypes.c_int64
 _c_int = ctypes.c_int
@@ -140,7 +141,7 @@ def load(build_if_missing: bool = True):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.sk_abi_version() != 1:
+        if lib.sk_abi_version() != ABI_VERSION:
             raise SketchLibraryError("libsketch_b200.so ABI version mismatch")
         _lib = lib
         return lib

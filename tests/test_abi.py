@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared_symbols():
         assert hasattr(raw, name), name
     assert set(_lib.SIGNATURES) >= declared_symbols()
-    assert lib.sk_abi_version() == 1
+    assert lib.sk_abi_version() == 2
 
 
 def test_error_path_without_device():
