@@ -1,3 +1,5 @@
+# Profile every configuration's dominant kernel once (ncu --set full) and the headline launch list; run on the GPU box:
+#   gpurun -- bash tools/prof_all.sh   (outputs in gpurun_out/, then: python tools/traffic_from_ncu.py gpurun_out/r2_*.ncu-rep)
 set -e
 cd $GRAFT_REPO_ROOT
 for cfg in cfg2 cfg1 cfg3 cfg4 cfg5 cfg2dct; do python tools/prof.py --config $cfg --reps 2; done
