@@ -86,8 +86,8 @@ SK_API int sk_sparse_right(int dtype, const void* A, int64_t n, int64_t d, int64
  * the chunk stream is split evenly over the SMs (stream-K; tiles cut between two CTAs are combined
  * in a fixed order).  Replaces `_SparseTM.apply_right` (src/sketch/sparse.py:63-66) for float64
  * (BASELINE config 1).  Omega in the ring encoding: for unit h (rows 128h ..) and warp w (columns
- * 16w ..), lists[16*seg[16h + w] ..] = 16 uint8 column counts, then uint8 entries (row % 64) |
- * ((row / 64) % 2) << 6 | neg << 7 (sketch/encode.py ring_encode); seg has ceil(d/128)*16 + 1 entries.
+ * 16w ..), lists[16*seg[16h + w] ..] = 16 uint8 column counts, then uint16 entries ((row / 64) % 2) << 15 |
+ * (row % 64) << 3 | neg (sketch/encode.py ring_encode); seg has ceil(d/128)*16 + 1 entries.
  * Workspace: sk_sparse_right_ring_workspace_bytes(n, d).  A 8-byte, lists 16-byte aligned.
  */
 SK_API int sk_sparse_right_ring_supported(int dtype, int64_t d, int64_t k, int64_t seg_bytes);

@@ -5,7 +5,7 @@
 // Round-1 K1 (csrc/sparse_right.cu) staged each chunk of A through registers with a CTA barrier per
 // chunk: the Poisson spread of entries per warp left the fast warps waiting (30 % of HBM).  Here:
 //
-//   * 2 producer warps copy each 64-row x 64-column chunk of A (32 KB) into a 5-stage shared-memory
+//   * 2 producer warps copy each 64-row x 64-column chunk of A (32 KB) into a 4-stage shared-memory
 //     ring with 8-byte cp.async (no registers held), XOR-swizzled at 8-byte granularity:
 //     element (row, r) at row * 512 + ((r ^ (row & 15)) << 3), so the gather "32 lanes = 32 rows,
 //     same column r" hits 16 distinct bank pairs per half-warp (conflict-free);
@@ -13,7 +13,7 @@
 //   * 16 consumer warps own 16 output columns each (k <= 256); lane = rows l and l + 32 of the tile,
 //     so every Omega entry feeds two independent gathers and two float64 adds (register
 //     accumulators).  Entries come from per-(chunk, warp) segments staged once in shared memory:
-//     16 column counts (uint8) then uint8 entries r | stage << 6 | neg << 7; one consumer pass takes
+//     16 column counts (uint8) then uint16 entries stage << 15 | r << 3 | neg; one consumer pass takes
 //     two stages (a 128-row unit of Omega: ~2 entries per column, so the per-column loop overhead is
 //     paid half as often).  Warps release stages through the empty barriers (16 arrivals): no
 //     CTA-wide barrier, a slow warp may lag by up to one unit.
@@ -34,7 +34,7 @@ namespace {
 constexpr int RR = 64;          // rows per tile (2 per lane)
 constexpr int RC = 64;          // columns of A (rows of Omega) per stage
 constexpr int UC = 2 * RC;      // per unit: a consumer pass takes two stages (amortises the column loops)
-constexpr int STAGES = 5;
+constexpr int STAGES = 4;  // even: a unit's two stages are adjacent (one base address per unit)
 constexpr int STAGE_BYTES = RR * RC * 8;  // 32 KB
 constexpr int NPROD = 2;        // producer warps (64 threads: one column of the chunk each)
 constexpr int NCONS = 16;       // consumer warps
@@ -68,9 +68,9 @@ __device__ __forceinline__ double lds_f64(uint32_t a) {
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
   return v;
 }
-__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
   uint32_t v;
-  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
 __device__ __forceinline__ uint4 lds_v4(uint32_t a) {
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_right_ring_kernel(const Rin
     for (int j = 0; j < CPW; ++j) acc0[j] = acc1[j] = 0.0;
     const uint32_t lists_u32 = sm100::smem_u32(lists);
     const uint32_t lane_off = (uint32_t)lane * (RC * 8);
-    const uint32_t lane_x = (uint32_t)(lane & 15);
+    const uint32_t lane_x8 = (uint32_t)(lane & 15) << 3;
     int s = 0;
     uint32_t ph = 0;
 
@@ -209,45 +209,43 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_right_ring_kernel(const Rin
 #pragma unroll
       for (int j = 0; j < CPW; ++j) acc0[j] = acc1[j] = 0.0;
       for (int h = hs; h < he; ++h) {
-        // this warp's segment of unit h (two stages): 16 counts, then the entries r | stage << 6 | neg << 7
+        // this warp's segment of unit h (stages s, s + 1): 16 uint8 counts, then uint16 entries
+        // stage << 15 | (row % 64) << 3 | neg: the byte offset of the row's column in the unit, so a
+        // gather address is one XOR with the lane's swizzle and one add
         const uint32_t sb = lists_u32 + seg_s[h * NCONS + w] * 16u;
         const uint4 cnt = lds_v4(sb);
         uint32_t e = sb + 16;
-        const int s1 = s + 1 == STAGES ? 0 : s + 1;
-        const uint32_t ph1 = s + 1 == STAGES ? ph ^ 1 : ph;
         sm100::mbar_wait(&full[s], ph);
-        sm100::mbar_wait(&full[s1], ph1);
+        sm100::mbar_wait(&full[s + 1], ph);
         const uint32_t a0 = ring_u32 + (uint32_t)s * STAGE_BYTES + lane_off;
-        const uint32_t a1 = ring_u32 + (uint32_t)s1 * STAGE_BYTES + lane_off;
         const uint32_t cw[4] = {cnt.x, cnt.y, cnt.z, cnt.w};
-        auto gaddr = [&](uint32_t en) { return ((en & 64u) ? a1 : a0) + (((en & 63u) ^ lane_x) << 3); };
 #pragma unroll
         for (int j = 0; j < CPW; ++j) {
           const uint32_t nj = (cw[j >> 2] >> (8 * (j & 3))) & 0xffu;
-          const uint32_t eend = e + nj;
-          for (; e + 1 < eend; e += 2) {  // two entries in flight
-            const uint32_t en0 = lds_u8(e), en1 = lds_u8(e + 1);
-            const uint32_t ad0 = gaddr(en0), ad1 = gaddr(en1);
+          const uint32_t eend = e + 2 * nj;
+          for (; e + 2 < eend; e += 4) {  // two entries in flight
+            const uint32_t en0 = lds_u16(e), en1 = lds_u16(e + 2);
+            const uint32_t ad0 = a0 + ((en0 & 0xfff8u) ^ lane_x8), ad1 = a0 + ((en1 & 0xfff8u) ^ lane_x8);
             const double x0 = lds_f64(ad0), y0 = lds_f64(ad0 + 32u * RC * 8u);
             const double x1 = lds_f64(ad1), y1 = lds_f64(ad1 + 32u * RC * 8u);
-            acc0[j] += flip(x0, en0 >> 7) + flip(x1, en1 >> 7);
-            acc1[j] += flip(y0, en0 >> 7) + flip(y1, en1 >> 7);
+            acc0[j] += flip(x0, en0 & 1u) + flip(x1, en1 & 1u);
+            acc1[j] += flip(y0, en0 & 1u) + flip(y1, en1 & 1u);
           }
           if (e < eend) {
-            const uint32_t en = lds_u8(e);
-            const uint32_t addr = gaddr(en);
-            acc0[j] += flip(lds_f64(addr), en >> 7);
-            acc1[j] += flip(lds_f64(addr + 32u * RC * 8u), en >> 7);
-            ++e;
+            const uint32_t en = lds_u16(e);
+            const uint32_t addr = a0 + ((en & 0xfff8u) ^ lane_x8);
+            acc0[j] += flip(lds_f64(addr), en & 1u);
+            acc1[j] += flip(lds_f64(addr + 32u * RC * 8u), en & 1u);
+            e += 2;
           }
         }
         __syncwarp();
         if (lane == 0) {
           sm100::mbar_arrive(&empty[s]);
-          sm100::mbar_arrive(&empty[s1]);
+          sm100::mbar_arrive(&empty[s + 1]);
         }
-        s = s1 + 1 == STAGES ? 0 : s1 + 1;
-        ph = s1 + 1 == STAGES ? ph1 ^ 1 : ph1;
+        s += 2;
+        if (s == STAGES) { s = 0; ph ^= 1; }
       }
       flush(t, hs, he);
       g += he - hs;

@@ -180,9 +180,10 @@ def ring_encode(rows, cols, neg, d: int, k: int):
 
     For unit h (rows h*128 .. h*128+127 of Omega, two 64-row stages) and consumer warp w (columns
     w*16 .. w*16+15) the segment at byte 16*seg[h*16 + w] holds 16 uint8 column counts, then the
-    entries of those columns in column order, each (row % 64) | stage << 6 | neg << 7 (stage =
-    (row // 64) % 2), padded to 16 bytes.  Duplicated (row, column) entries stay separate (their adds
-    sum, as the reference's CSR duplicates do).
+    entries of those columns in column order as little-endian uint16 stage << 15 | (row % 64) << 3 |
+    neg (stage = (row // 64) % 2: the byte offset of the row's column inside the unit's two ring
+    stages of 64 x 64 float64), padded to 16 bytes.  Duplicated (row, column) entries stay separate
+    (their adds sum, as the reference's CSR duplicates do).
     """
     rows = np.asarray(rows, dtype=np.int64).ravel()
     cols = np.asarray(cols, dtype=np.int64).ravel()
@@ -200,20 +201,22 @@ def ring_encode(rows, cols, neg, d: int, k: int):
     if cnt.size and cnt.max() > 255:
         raise ValueError("more than 255 entries of one column in a 128-row unit")
     per_seg = cnt.sum(axis=1)
-    units = 1 + (per_seg + 15) // 16
+    units = 1 + (2 * per_seg + 15) // 16
     seg = np.zeros(nseg + 1, dtype=np.int64)
     np.cumsum(units, out=seg[1:])
     lists = np.zeros(int(seg[-1]) * 16, dtype=np.uint8)
     hdr = (seg[:-1] * 16)[:, None] + np.arange(16)[None, :]
     lists[hdr.ravel()] = cnt.ravel().astype(np.uint8)
-    # entry e of segment s lands at 16*seg[s] + 16 + (its rank inside the segment)
+    # entry e of segment s lands at 16*seg[s] + 16 + 2 * (its rank inside the segment)
     skey = key[order] // 16
     first = np.zeros(nseg + 1, dtype=np.int64)
     np.cumsum(per_seg, out=first[1:])
     rank = np.arange(rows.size, dtype=np.int64) - first[skey]
-    pos = seg[skey] * 16 + 16 + rank
+    pos = seg[skey] * 16 + 16 + 2 * rank
     r = rows[order] % RING_UC
-    lists[pos] = ((r % RING_RC) | ((r // RING_RC) << 6) | (neg[order].astype(np.int64) << 7)).astype(np.uint8)
+    ent = ((r // RING_RC) << 15) | ((r % RING_RC) << 3) | neg[order].astype(np.int64)
+    lists[pos] = (ent & 0xff).astype(np.uint8)
+    lists[pos + 1] = (ent >> 8).astype(np.uint8)
     return lists, seg.astype(np.uint32)
 
 
@@ -227,9 +230,11 @@ def ring_decode(lists, seg, d: int, k: int):
         h, w = divmod(s, RING_WARPS)
         base = int(seg[s]) * 16
         cnt = lists[base:base + 16].astype(np.int64)
-        ents = lists[base + 16: base + 16 + int(cnt.sum())].astype(np.int64)
+        m = int(cnt.sum())
+        b = lists[base + 16: base + 16 + 2 * m].astype(np.int64)
+        ents = b[0::2] | (b[1::2] << 8)
         cols = np.repeat(w * 16 + np.arange(16), cnt)
-        out_r.append(h * RING_UC + ((ents >> 6) & 1) * RING_RC + (ents & 63))
+        out_r.append(h * RING_UC + (ents >> 15) * RING_RC + ((ents >> 3) & 63))
         out_c.append(cols)
-        out_n.append((ents >> 7).astype(bool))
+        out_n.append((ents & 1).astype(bool))
     return np.concatenate(out_r), np.concatenate(out_c), np.concatenate(out_n)
