@@ -52,6 +52,7 @@ def main():
     y0 = None
     out["kr_ms"] = time_fn(lambda: tm.apply_right(a), args.reps)
     y0 = tm.apply_right(a)
+
     om = torch.as_tensor(tm.materialize(), device=dev)  # d x k float64 (probe only)
     bt = (om.T * np.sqrt(k)).contiguous().to(torch.bfloat16)  # exact +-1
     del om
