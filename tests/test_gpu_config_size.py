@@ -1,5 +1,9 @@
 """Parity at BASELINE config size on the production paths (slow GPU tests, one config each).
 
+* config 2 (the headline): all 65536 rows of the SRTT sketch against the CPU oracle.
+* config 3 sketch: all 131072 rows against a float64 device product with the oracle's Omega, plus
+  oracle rows from three tiles.
+
 * config 4 S A: the full 4194304 x 512 float32 sketch (K2g) against the chunked CPU oracle
   (`csr_adjoint_chunked`, the reference's `matrix.conj().T @ b` by row blocks);
   and the same rows split into 3 uneven row blocks (the multi-GPU shards) whose partials sum to it.
@@ -18,6 +22,7 @@ import numpy as np
 import pytest
 
 import oracle as orc
+from _cases import rel_err
 from paper_2508_21189_b200 import rand_nla
 from paper_2508_21189_b200 import sketch as skb
 
@@ -142,3 +147,45 @@ def test_config3_rsvd_full_size(cuda):
     res100_ref = np.sqrt(max(a2 - float((sv[:100] ** 2).sum()), 0.0) / a2)
     assert abs(res_gpu - res_ref) <= 1e-2 * res_ref, (res_gpu, res_ref)
     assert abs(res100_gpu - res100_ref) <= 1e-2 * res100_ref, (res100_gpu, res100_ref)
+
+
+def test_config2_full_vs_oracle(cuda):
+    """The headline: all 65536 rows of the config-2 SRTT sketch (tcgen05 kernel) against the CPU oracle,
+    row-parallel on the host cores (the oracle's float64 WHT path, ~5 s on 16 processes)."""
+    import os
+
+    import torch
+
+    n, d, k = 65536, 8192, 512
+    tm = skb.SparseRttTM(d, k, 1, "wht", seed=0)
+    g = torch.Generator(device=cuda).manual_seed(1000)
+    a = torch.randn(n, d, dtype=torch.float32, device=cuda, generator=g)
+    a /= torch.arange(1, d + 1, dtype=torch.float32, device=cuda)
+    y = tm.apply_right(a).double().cpu().numpy()
+    dv, samp = orc.srtt_parts(d, k, 1, 0)
+    ref = orc.right_multiprocess(lambda x: orc.srtt_right(dv, samp, x, "wht"), a.cpu().numpy(),
+                                 procs=os.cpu_count() or 1, rows=1024)
+    err = np.linalg.norm(y - ref) / np.linalg.norm(ref)
+    assert err <= 1e-5, err
+
+
+def test_config3_sketch_full(cuda):
+    """Config 3's sketch Y = A Omega at full size (131072 x 16384 f32, zeta = 8, k = 200) on the CTA-pair
+    tensor-core engine: against a float64 device product with the oracle's Omega for every row, and
+    the oracle itself on rows from three tiles."""
+    import torch
+
+    n, d, k = 131072, 16384, 200
+    tm = skb.SparseUniformTM(d, k, 8, seed=0)
+    g = torch.Generator(device=cuda).manual_seed(3000)
+    a = torch.randn(n, d, dtype=torch.float32, device=cuda, generator=g)
+    y = tm.apply_right(a).double()
+    csr = orc.sparse_uniform_csr(d, k, 8, 0)
+    om = torch.as_tensor(csr.toarray(), device=cuda)
+    ref = torch.empty_like(y)
+    for r0 in range(0, n, 8192):
+        ref[r0:r0 + 8192] = a[r0:r0 + 8192].double() @ om
+    err = float(torch.linalg.norm(y - ref) / torch.linalg.norm(ref))
+    assert err <= 1e-5, err
+    rows = np.r_[0:8, 65536:65544, n - 8:n]
+    assert rel_err(y[rows].cpu().numpy(), orc.csr_right(csr, a[rows].cpu().numpy())) <= 1e-5

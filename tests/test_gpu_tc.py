@@ -185,3 +185,18 @@ def test_gaussian_dense_families_own_kernel(dt, cuda):
     assert rel_err(y, a.astype(dt).astype(np.float64) @ om) <= tol
     assert rel_err(x, om.T @ b.astype(dt).astype(np.float64)) <= tol
     assert any(k[0] == "dense_cc" for k in tm._device_cache)
+
+
+def test_khatri_rao_wide_k_slabs(cuda):
+    """k > 2048 runs the KR kernel in column slabs (N-block groups per launch): k = 2100 = 2048 + 52."""
+    import torch
+
+    tm = skb.KhatriRaoTM(16, 2, 2100, "real_rademacher", seed=6)
+    rng = np.random.default_rng(2)
+    a = rng.standard_normal((200, 256)).astype(np.float32)
+    b = rng.standard_normal((256, 5)).astype(np.float32)
+    fac = orc.kr_factors(16, 2, 2100, 6)
+    y = tm.apply_right(torch.from_numpy(a).to(cuda)).double().cpu().numpy()
+    x = tm.apply_adjoint(torch.from_numpy(b).to(cuda)).double().cpu().numpy()
+    assert rel_err(y, orc.kr_right(fac, a)) <= 1e-5
+    assert rel_err(x, orc.kr_right(fac, b.T).T) <= 1e-5
