@@ -294,7 +294,7 @@ int gather_run(const T* A, int64_t d, int64_t m, int64_t lda, const int32_t* ent
   p.part = ws;
   p.counter = reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + pl.part_bytes);
   cudaMemsetAsync(p.counter, 0, sizeof(int), s);
-  cudaFuncSetAttribute(sparse_adjoint_gather<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+  allow_smem(sparse_adjoint_gather<T>, pl.smem);
   sparse_adjoint_gather<T><<<(unsigned)sm_count(), G_WARPS * 32, pl.smem, s>>>(tm, p);
   int st = check_launch("sk_sparse_adjoint_gather");
   if (st != SK_OK) return st;

@@ -425,7 +425,7 @@ int wide_rows_t(const T* A, int64_t d, int64_t r0, int64_t r1, int64_t m, int64_
   p.seg_off = seg_off;
   p.part = ws;
   cudaStream_t s = as_stream(stream);
-  cudaFuncSetAttribute(sparse_adjoint_wide<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+  allow_smem(sparse_adjoint_wide<T>, pl.smem);
   sparse_adjoint_wide<T><<<dim3((unsigned)pl.ngroups, (unsigned)pl.nslices, (unsigned)pl.npieces),
                            (W_WARPS + 1) * 32, pl.smem, s>>>(tm, p);
   int st = check_launch("sk_sparse_adjoint_wide");

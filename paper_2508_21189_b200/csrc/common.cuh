@@ -32,6 +32,20 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // SM count of the current device (cached per device).
 int sm_count();
 
+// Bind the current device's primary context to the calling host thread (once per thread and device).
+// The runtime binds it lazily on the first runtime call that needs it; driver-API calls made before
+// that (cuTensorMapEncodeTiled) would fail with "invalid context" on a fresh thread (thread pools).
+void ensure_context();
+
+// Raise a kernel's dynamic shared-memory limit on the current device to at least `smem`.  The limit
+// only ever grows (per device and kernel, under a lock): setting it per launch to that launch's
+// size would let one host thread shrink it under another's launch of the same kernel.
+cudaError_t allow_dynamic_smem(const void* kern, size_t smem);
+template <typename K>
+inline cudaError_t allow_smem(K* kern, size_t smem) {
+  return allow_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
+}
+
 template <typename T>
 struct DT;
 template <>

@@ -26,8 +26,10 @@
 // (dense_tc_pair_kernel, tcgen05 cta_group::2): config 5 1.71 -> 1.59 ms, config 3 1.71 -> 1.55 ms.
 #include <cuda.h>
 
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -734,14 +736,16 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
+  // resolved once (thread-safe static initialisation: trials may run on a host thread pool)
+  static const EncodeTiledFn fn = [] {
     void* ptr = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(ptr);
-  }
+      return reinterpret_cast<EncodeTiledFn>(ptr);
+    return static_cast<EncodeTiledFn>(nullptr);
+  }();
+  ensure_context();
   return fn;
 }
 
@@ -771,7 +775,9 @@ int make_a_map(CUtensorMap* m, const float* a, int64_t M, int64_t K, int64_t lda
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(SK_EINVAL, "cuTensorMapEncodeTiled(A) failed (alignment of A / lda?)");
+  if (r != CUDA_SUCCESS)
+    return fail(SK_EINVAL, "cuTensorMapEncodeTiled(A) failed with CUresult " + std::to_string((int)r) +
+                               " (alignment of A / lda?)");
   return SK_OK;
 }
 
@@ -786,7 +792,9 @@ int make_at_map(CUtensorMap* m, const float* a, int64_t M, int64_t K, int64_t ld
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(SK_EINVAL, "cuTensorMapEncodeTiled(A^T) failed (alignment of A / lda?)");
+  if (r != CUDA_SUCCESS)
+    return fail(SK_EINVAL, "cuTensorMapEncodeTiled(A^T) failed with CUresult " + std::to_string((int)r) +
+                               " (alignment of A / lda?)");
   return SK_OK;
 }
 
@@ -866,7 +874,7 @@ int launch_pair(int NB, bool TA, const CUtensorMap& ma, const CUtensorMap& mb, c
   using KernT = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams);
   KernT kern = TA ? (NB == 2 ? dense_tc_pair_kernel<2, true, 0> : dense_tc_pair_kernel<1, true, 0>)
                   : (NB == 2 ? dense_tc_pair_kernel<2, false, 0> : dense_tc_pair_kernel<1, false, 0>);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_smem(kern, smem);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(2 * (sm_count() / 2)));
   cfg.blockDim = dim3(kThreads);
@@ -881,8 +889,8 @@ int launch_pair(int NB, bool TA, const CUtensorMap& ma, const CUtensorMap& mb, c
   cfg.numAttrs = 1;
   // persistent grid = the clusters that can be co-resident (GPCs with an odd SM count leave an
   // SM without a partner, so this can be below sm_count() / 2)
-  static int max_clusters_v[4] = {0, 0, 0, 0};
-  int& max_clusters = max_clusters_v[(NB - 1) + 2 * (TA ? 1 : 0)];
+  static std::atomic<int> max_clusters_v[4] = {};
+  int max_clusters = max_clusters_v[(NB - 1) + 2 * (TA ? 1 : 0)].load(std::memory_order_relaxed);
   if (max_clusters == 0) {
     int mc = 0;
     if (cudaOccupancyMaxActiveClusters(&mc, kern, &cfg) != cudaSuccess || mc < 1) {
@@ -890,6 +898,7 @@ int launch_pair(int NB, bool TA, const CUtensorMap& ma, const CUtensorMap& mb, c
       mc = sm_count() / 2;
     }
     max_clusters = mc;
+    max_clusters_v[(NB - 1) + 2 * (TA ? 1 : 0)].store(mc, std::memory_order_relaxed);
     if (getenv("SKETCH_B200_TC_PAIR_VERBOSE")) fprintf(stderr, "dense_tc pair: %d co-resident clusters\n", mc);
   }
   const int npairs = p.num_units < max_clusters ? p.num_units : max_clusters;
@@ -938,7 +947,7 @@ KernT kr_kernel(int NB, bool TA) {
 
 // co-resident 2-CTA clusters of a KR kernel at this shared-memory size
 int kr_max_clusters(KernT kern, size_t smem) {
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_smem(kern, smem);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(2 * (sm_count() / 2)));
   cfg.blockDim = dim3(kThreads);
@@ -1022,17 +1031,23 @@ int kr_run(bool TA, const float* A, int64_t rows, int64_t P, int64_t dl, int64_t
     KrPlan pl;
     if (!make_plan_kr(pl, rows, P, dl, kslab, NB, -1, TA))
       return fail(SK_EUNSUPPORTED, std::string(what) + ": resident factor does not fit shared memory");
+    // co-resident pairs per (kernel, smem) — a small cache guarded for concurrent host threads
+    static std::mutex maxc_mu;
     static KernT maxc_kern[8] = {};
     static size_t maxc_smem[8] = {};
     static int maxc_val[8] = {};
-    int slot = 0;
-    while (slot < 7 && maxc_kern[slot] && !(maxc_kern[slot] == kern && maxc_smem[slot] == pl.smem)) ++slot;
-    if (maxc_kern[slot] != kern || maxc_smem[slot] != pl.smem) {
-      maxc_kern[slot] = kern;
-      maxc_smem[slot] = pl.smem;
-      maxc_val[slot] = kr_max_clusters(kern, pl.smem);
+    int maxc = 0;
+    {
+      std::lock_guard<std::mutex> lk(maxc_mu);
+      int slot = 0;
+      while (slot < 7 && maxc_kern[slot] && !(maxc_kern[slot] == kern && maxc_smem[slot] == pl.smem)) ++slot;
+      if (maxc_kern[slot] != kern || maxc_smem[slot] != pl.smem) {
+        maxc_kern[slot] = kern;
+        maxc_smem[slot] = pl.smem;
+        maxc_val[slot] = kr_max_clusters(kern, pl.smem);
+      }
+      maxc = maxc_val[slot];
     }
-    const int maxc = maxc_val[slot];
     if (maxc < pl.nblocks) return fail(SK_EUNSUPPORTED, std::string(what) + ": too few co-resident pairs");
     make_plan_kr(pl, rows, P, dl, kslab, NB, maxc, TA);
     if (pl.ws_bytes > 0 && (ws == nullptr || ws_bytes < pl.ws_bytes))
@@ -1072,7 +1087,7 @@ int kr_run(bool TA, const float* A, int64_t rows, int64_t P, int64_t dl, int64_t
     uint32_t cols = 32;
     while (cols < (uint32_t)(2 * pl.BN)) cols <<= 1;
     p.tmem_cols = cols;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    allow_smem(kern, pl.smem);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(2 * pl.npairs));
     cfg.blockDim = dim3(kThreads);
@@ -1235,10 +1250,10 @@ extern "C" int sk_dense_right_tc(const float* A, int64_t n, int64_t d, int64_t l
   cudaStream_t s = as_stream(stream);
   const int grid = pl.units < sm_count() ? pl.units : sm_count();
   if (NB == 1) {
-    cudaFuncSetAttribute(dense_tc_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    allow_smem(dense_tc_kernel<1, false>, pl.smem);
     dense_tc_kernel<1, false><<<grid, kThreads, pl.smem, s>>>(ma, mh, ml, p);
   } else {
-    cudaFuncSetAttribute(dense_tc_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    allow_smem(dense_tc_kernel<2, false>, pl.smem);
     dense_tc_kernel<2, false><<<grid, kThreads, pl.smem, s>>>(ma, mh, ml, p);
   }
   st = check_launch("sk_dense_right_tc");
@@ -1347,7 +1362,7 @@ extern "C" int sk_dense_tn_tc(const float* A, int64_t n, int64_t d, int64_t lda,
   p.tmem_cols = cols;
   cudaStream_t s = as_stream(stream);
   const int grid = pl.units < sm_count() ? pl.units : sm_count();
-  cudaFuncSetAttribute(dense_tc_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+  allow_smem(dense_tc_kernel<2, true>, pl.smem);
   dense_tc_kernel<2, true><<<grid, kThreads, pl.smem, s>>>(ma, mh, ml, p);
   st = check_launch("sk_dense_tn_tc");
   if (st != SK_OK || pl.ksplit == 1) return st;

@@ -415,7 +415,7 @@ extern "C" int sk_lsqr_step_f32_f64(const float* A, int64_t n, int64_t d, int64_
     switch (d / 128) {
 #define LS_CASE(Q)                                                                                             \
   case Q:                                                                                                      \
-    cudaFuncSetAttribute(lsqr_step_ring<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
+    allow_smem(lsqr_step_ring<Q>, smem);          \
     lsqr_step_ring<Q><<<(unsigned)nsplit, GV_THREADS, smem, s>>>(A, n, lda, v, alpha, u, rps, ws, d + 1);     \
     break;
       LS_CASE(1)
@@ -464,7 +464,7 @@ extern "C" int sk_gemv_f32_f64(const float* A, int64_t n, int64_t d, int64_t lda
     }
     return check_launch("sk_gemv_f32_f64");
   }
-  cudaFuncSetAttribute(gemv_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_smem(gemv_rows, smem);
   int64_t grid = (n + 7) / 8;
   if (grid > 16 * (int64_t)sm_count()) grid = 16 * (int64_t)sm_count();
   gemv_rows<<<(unsigned)grid, GV_THREADS, smem, as_stream(stream)>>>(A, n, d, lda, v, y, vec);

@@ -8,6 +8,10 @@
 #include <stdint.h>
 
 namespace skb {
+void ensure_context();  // abi.cu
+}
+
+namespace skb {
 namespace sm100 {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -138,14 +142,16 @@ typedef CUresult (*EncodeTiledFnT)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 inline EncodeTiledFnT encode_tiled_fn() {
-  static EncodeTiledFnT fn = nullptr;
-  if (!fn) {
+  // resolved once (thread-safe static initialisation: trials may run on a host thread pool)
+  static const EncodeTiledFnT fn = [] {
     void* ptr = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFnT>(ptr);
-  }
+      return reinterpret_cast<EncodeTiledFnT>(ptr);
+    return static_cast<EncodeTiledFnT>(nullptr);
+  }();
+  ensure_context();
   return fn;
 }
 

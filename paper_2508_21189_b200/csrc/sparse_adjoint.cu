@@ -355,7 +355,7 @@ int launch_t(const Plan& pl, const T* A, int64_t d, int64_t m, int64_t lda, cons
   constexpr int R = adj_chunk_rows<T>();
   const size_t smem = (size_t)R * kCols * sizeof(T);
   auto kern = sparse_adjoint_kernel<T, CPW, R, VEC>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_smem(kern, smem);
   dim3 grid(pl.grid_x, pl.grid_y, pl.nsplit);
   kern<<<grid, kWarps * 32, smem, s>>>(A, d, m, lda, ptr, ent, k, pl.nchunks, pl.chunks_per_split, part,
                                        k * m, m);
@@ -367,14 +367,16 @@ typedef CUresult (*EncodeTiledFnA)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 EncodeTiledFnA encode_fn_a() {
-  static EncodeTiledFnA fn = nullptr;
-  if (!fn) {
+  // resolved once (thread-safe static initialisation: trials may run on a host thread pool)
+  static const EncodeTiledFnA fn = [] {
     void* q = nullptr;
     cudaDriverEntryPointQueryResult r;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &q, cudaEnableDefault, &r) == cudaSuccess &&
         r == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFnA>(q);
-  }
+      return reinterpret_cast<EncodeTiledFnA>(q);
+    return static_cast<EncodeTiledFnA>(nullptr);
+  }();
+  ensure_context();
   return fn;
 }
 
@@ -437,7 +439,7 @@ int run_v2(const float* A, int64_t d, int64_t m, int64_t lda, const int32_t* ptr
   p.seg = seg;
   p.ent_cap = ent_cap;
   p.part = static_cast<float*>(ws);
-  cudaFuncSetAttribute(sparse_adjoint_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+  allow_smem(sparse_adjoint_v2, pl.smem);
   const int grid = pl.nslices * pl.ngroups * pl.npieces;
   sparse_adjoint_v2<<<grid, (kWarps + 1) * 32, pl.smem, s>>>(tm, p);
   int st = check_launch("sk_sparse_adjoint(v2)");

@@ -57,7 +57,7 @@ int run(int64_t n, int64_t d, const int64_t* aptr, const int32_t* aidx, const T*
   int64_t grid = (n + CSR_WARPS - 1) / CSR_WARPS;
   if (smem <= 200 * 1024) {
     auto kern = sparse_right_csr<T, true>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_smem(kern, smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CSR_WARPS * 32, smem);
     if (per_sm < 1) per_sm = 1;

@@ -544,7 +544,7 @@ int launch_t(const T* A, int64_t n, int64_t d, int64_t lda, const int32_t* ptr, 
       static_assert(W2 * CPW2 == CB, "column block");
       auto kern = sparse_right_persistent<T, W2, CPW2, R>;
       const int nthreads = W2 * 32;
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      allow_smem(kern, smem);
       const int ncb = (int)((k + CB - 1) / CB);
       const int64_t ntiles = (n + kRowsPerTile - 1) / kRowsPerTile;
       int64_t per_cb = sm_count() / ncb;
@@ -559,12 +559,12 @@ int launch_t(const T* A, int64_t n, int64_t d, int64_t lda, const int32_t* ptr, 
   if (base + oms_bytes <= 200 * 1024) {
     const size_t smem = base + oms_bytes;
     auto kern = sparse_right_kernel<T, kWarps, CPW, R, VEC, true>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_smem(kern, smem);
     kern<<<grid, kWarps * 32, smem, s>>>(A, n, d, lda, ptr, ent, k, nchunks, (int)nnz, (uint32_t)base, (T)scale, Y,
                                          ldy);
   } else {
     auto kern = sparse_right_kernel<T, kWarps, CPW, R, VEC, false>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)base);
+    allow_smem(kern, base);
     kern<<<grid, kWarps * 32, base, s>>>(A, n, d, lda, ptr, ent, k, nchunks, 0, (uint32_t)base, (T)scale, Y, ldy);
   }
   return check_launch("sk_sparse_right");

@@ -330,7 +330,7 @@ extern "C" int sk_sparse_right_ring(const double* A, int64_t n, int64_t d, int64
   p.ws = part;
   p.flags = flags;
   const size_t smem = ring_smem(d, seg_bytes);
-  cudaFuncSetAttribute(sparse_right_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_smem(sparse_right_ring_kernel, smem);
   sparse_right_ring_kernel<<<grid, THREADS, smem, s>>>(p);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

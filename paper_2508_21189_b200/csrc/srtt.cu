@@ -401,7 +401,7 @@ int launch_wide(const float* A, int64_t n, int64_t lda, const float* dv, const i
   constexpr int T = WideCfg<L>::T;
   const size_t smem = sizeof(float) << L;
   auto kern = srtt_wht_wide<L>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_smem(kern, smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem);
   if (per_sm < 1) per_sm = 1;
@@ -522,7 +522,7 @@ int launch_warp(const T* A, int64_t n, int64_t lda, const T* dv, const int32_t* 
                 T* Y, int64_t ldy, bool vec, cudaStream_t s) {
   const size_t smem = sizeof(T) * ((size_t)8 << L);
   auto kern = vec ? srtt_wht_warp<T, L, SIGNS, true> : srtt_wht_warp<T, L, SIGNS, false>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_smem(kern, smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
   if (per_sm < 1) per_sm = 1;
@@ -552,7 +552,7 @@ int launch_fast(const T* A, int64_t n, int64_t lda, const T* dv, const int32_t* 
   constexpr int NT = 1 << (L - 5);
   const size_t smem = sizeof(T) << L;
   auto kern = srtt_wht_fast<T, L, SIGNS>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_smem(kern, smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
   if (per_sm < 1) per_sm = 1;
@@ -620,7 +620,7 @@ int run(const void* A_, int64_t n, int64_t d, int64_t lda, const void* dv_, bool
   }
   const size_t smem = sizeof(T) * (size_t)d;
   if (smem > 200 * 1024) return fail(SK_EUNSUPPORTED, "sk_srtt_right: row does not fit shared memory");
-  cudaFuncSetAttribute(srtt_wht_simple<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_smem(srtt_wht_simple<T>, smem);
   int threads = (int)(d / 2 < 512 ? (d / 2 < 32 ? 32 : d / 2) : 512);
   int64_t grid = n < 4 * (int64_t)sm_count() ? n : 4 * (int64_t)sm_count();
   if (grid < 1) grid = 1;

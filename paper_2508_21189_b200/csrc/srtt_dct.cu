@@ -222,7 +222,7 @@ int dct_run(const T* A, int64_t n, int N, int64_t lda, const T* w, const T* ab, 
          : b == 2 ? srtt_dct_kernel<T, 256, 2>
                   : srtt_dct_kernel<T, 256, 3>;
   }
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_smem(kern, smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   if (per_sm < 1) per_sm = 1;

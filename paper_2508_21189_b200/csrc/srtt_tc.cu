@@ -358,7 +358,7 @@ int launch_tc_t(const float* A, int64_t n, int64_t lda, const float* dv, const i
   using C = TcCfg<L>;
   const int grid = (int)(n < sm_count() ? n : sm_count());
   const size_t smem = 1024 + (size_t)(C::SLOTS + 2) * C::ROW_BYTES + 8 * (3 * C::SLOTS + 2 * TC_ACC + 1);
-  cudaFuncSetAttribute(srtt_wht_tc<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_smem(srtt_wht_tc<L, false>, smem);
   srtt_wht_tc<L, false><<<grid, TC_THREADS, smem, s>>>(A, n, lda, dv, samp, xi, k, (float)scale, Y, ldy, 1);
   return check_launch("sk_srtt_right(tc)");
 }
@@ -396,7 +396,7 @@ extern "C" int sk_wht_segments_f32(const float* A, int64_t n, int64_t d, int64_t
   if (grid < period) grid = period;
   if (grid > rows) grid = rows;
   const size_t smem = 1024 + (size_t)(C::SLOTS + 2) * C::ROW_BYTES + 8 * (3 * C::SLOTS + 2 * TC_ACC + 1);
-  cudaFuncSetAttribute(srtt_wht_tc<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_smem(srtt_wht_tc<L, true>, smem);
   srtt_wht_tc<L, true><<<(unsigned)grid, TC_THREADS, smem, as_stream(stream)>>>(A, rows, lda, dvals, nullptr, 1, 1,
                                                                                 1.f, Z, ldz, (int)period);
   return check_launch("sk_wht_segments_f32");

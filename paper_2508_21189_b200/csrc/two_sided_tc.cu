@@ -504,7 +504,7 @@ extern "C" int sk_two_sided_sketch(const float* A, int64_t n, int64_t d, int64_t
     const char* e = getenv("SKETCH_B200_TS_DBG");
     prm.dbg = e ? atoi(e) : 0;
   }
-  cudaFuncSetAttribute(two_sided_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+  allow_smem(two_sided_kernel, pl.smem);
   two_sided_kernel<<<pl.grid, kThreads, pl.smem, s>>>(ma, mb, mbl, prm);
   st = check_launch("sk_two_sided_sketch");
   if (st != SK_OK) return st;

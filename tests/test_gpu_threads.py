@@ -1,0 +1,50 @@
+"""Concurrent applies from host threads (the reference runs its trials on a thread pool).
+
+The library caches per-kernel launch state (dynamic shared-memory limits, co-resident cluster counts,
+the tensor-map encoder).  Several host threads applying operators whose kernels need different
+shared-memory sizes must give exactly the results of the same calls made one at a time.
+"""
+
+from concurrent.futures import ThreadPoolExecutor
+
+import pytest
+
+from paper_2508_21189_b200 import sketch as skb
+
+pytestmark = pytest.mark.gpu
+
+
+def _cases(cuda):
+    import torch
+
+    g = torch.Generator(device=cuda).manual_seed(77)
+    out = []
+    for d, k, dt in [(512, 64, torch.float64), (2048, 256, torch.float64), (4096, 128, torch.float32)]:
+        out.append((skb.SparseUniformTM(d, k, 8, seed=d), torch.randn(3000, d, device=cuda, dtype=dt, generator=g)))
+    for d, k in [(1024, 64), (8192, 512)]:
+        out.append((skb.SparseRttTM(d, k, 1, "wht", seed=d),
+                    torch.randn(1000, d, device=cuda, dtype=torch.float32, generator=g)))
+    out.append((skb.KhatriRaoTM(64, 2, 1024, "real_gaussian", seed=1),
+                torch.randn(2000, 4096, device=cuda, dtype=torch.float32, generator=g)))
+    out.append((skb.GaussianTM(1024, 200, seed=2), torch.randn(1500, 1024, device=cuda, dtype=torch.float32,
+                                                                generator=g)))
+    return out
+
+
+def test_concurrent_applies_match_sequential(cuda):
+    import torch
+
+    cases = _cases(cuda)
+    ref = [tm.apply_right(a) for tm, a in cases]  # also builds every device cache
+    torch.cuda.synchronize()
+
+    def run(i):
+        tm, a = cases[i % len(cases)]
+        y = tm.apply_right(a)
+        torch.cuda.current_stream().synchronize()
+        return i % len(cases), y
+
+    with ThreadPoolExecutor(max_workers=6) as ex:
+        results = list(ex.map(run, range(6 * len(cases))))
+    for i, y in results:
+        assert torch.equal(y, ref[i]), i
