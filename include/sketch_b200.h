@@ -16,6 +16,9 @@
  *   - Return value: SK_OK (0) or a negative status; sk_last_error() gives a thread-local
  *     message.  Nothing throws across the ABI.
  *   - dtype: SK_F32 or SK_F64, the element type of A and of the output.
+ *   - Device: the calling thread's current CUDA device (cudaSetDevice), which must own the buffers.
+ *     Any host thread may call any entry point concurrently (the reference runs trials on a thread
+ *     pool); launch state cached inside the library is per device and guarded.
  *
  * Omega encodings (built by the host layer from the bit-exact test-matrix arrays):
  *   bcsc ("blocked column lists") for exactly-zeta-per-row sparse Omega (SparseUniform /
