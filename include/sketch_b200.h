@@ -327,9 +327,13 @@ SK_API int sk_two_sided_sketch(const float* A, int64_t n, int64_t d, int64_t lda
                                void* ws, size_t ws_bytes, void* stream);
 
 /*
- * K4c — the same contractions on the CUDA cores for float64 (the reference's dtype; float64
- * accumulation, parity 1e-12) and float32 shapes the tcgen05 form does not take.  F is dl x k
- * (row stride ldf) and W is P x k (row stride ldw), both of `dtype`.  Adjoint: X[k,m] from B [P*dl][m].
+ * K5d / K4c — the same contractions for float64 (the reference's dtype) and for float32 shapes the
+ * tcgen05 form does not take.  F is dl x k (row stride ldf) and W is P x k (row stride ldw), both of
+ * `dtype`; W may be NULL when P == 1 (a dense Omega = F: the Gaussian family and the adjoints of
+ * materialised operators).  Adjoint: X[k,m] from B [P*dl][m], read in place.  float64 runs on the
+ * FP64 tensor cores (K5d: DMMA, the Khatri-Rao tile W[P,:] * F synthesised in shared memory) when
+ * n (m) >= 64, k >= 8, the pointers are 16-byte aligned and the row strides even; otherwise, and for
+ * float32, on the CUDA cores (K4c, float64 accumulation).  Parity 1e-12 (float64).
  */
 SK_API int sk_kr_right_cc(int dtype, const void* A, int64_t n, int64_t P, int64_t dl, int64_t lda, const void* F,
                           int64_t ldf, const void* W, int64_t ldw, int64_t k, double scale, void* Y, int64_t ldy,

@@ -16,6 +16,11 @@
 #include "common.cuh"
 
 namespace skb {
+
+int gemm64_try(bool ta, const double* A, int64_t rows, int64_t P, int64_t dl, int64_t lda, const double* F,
+               int64_t ldf, const double* W, int64_t ldw, int64_t k, double scale, double* Y, int64_t ldy,
+               cudaStream_t s);  // dense64.cu
+
 namespace {
 
 constexpr int TR = 64, TJ = 64, TQ = 16;
@@ -86,7 +91,7 @@ __global__ void __launch_bounds__(256) kr_cc_kernel(const T* __restrict__ A, int
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int64_t j = j0 + tj + 16 * u;
-      const Acc w = j < k ? (Acc)W[pp * ldw + j] : 0.0;
+      const Acc w = j < k ? (W ? (Acc)W[pp * ldw + j] : 1.0) : 0.0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[i][u] = fma(w, (Acc)part[i][u], acc[i][u]);
     }
@@ -123,11 +128,17 @@ int kr_cc_launch(bool ta, const void* A, int64_t rows, int64_t P, int64_t dl, in
 
 int kr_cc(bool ta, int dtype, const void* A, int64_t rows, int64_t P, int64_t dl, int64_t lda, const void* F,
           int64_t ldf, const void* W, int64_t ldw, int64_t k, double scale, void* Y, int64_t ldy, void* stream) {
-  if (rows < 0 || P < 1 || dl < 1 || k < 1 || ldf < k || ldw < k) return fail(SK_EINVAL, "sk_kr_cc: bad shape");
+  if (rows < 0 || P < 1 || dl < 1 || k < 1 || ldf < k || (W && ldw < k)) return fail(SK_EINVAL, "sk_kr_cc: bad shape");
+  if (!W && P != 1) return fail(SK_EINVAL, "sk_kr_cc: W may be NULL only for one block (P = 1)");
   if (ta ? (lda < rows || ldy < rows) : (lda < P * dl || ldy < k)) return fail(SK_EINVAL, "sk_kr_cc: bad leading dimension");
   if (rows == 0) return SK_OK;
-  if (!A || !F || !W || !Y) return fail(SK_EINVAL, "sk_kr_cc: null pointer");
+  if (!A || !F || !Y) return fail(SK_EINVAL, "sk_kr_cc: null pointer");
   cudaStream_t s = as_stream(stream);
+  if (dtype == SK_F64) {
+    const int st = gemm64_try(ta, static_cast<const double*>(A), rows, P, dl, lda, static_cast<const double*>(F), ldf,
+                              static_cast<const double*>(W), ldw, k, scale, static_cast<double*>(Y), ldy, s);
+    if (st != 1) return st;
+  }
   if (dtype == SK_F64) return kr_cc_launch<double>(ta, A, rows, P, dl, lda, F, ldf, W, ldw, k, scale, Y, ldy, s);
   if (dtype == SK_F32) return kr_cc_launch<float>(ta, A, rows, P, dl, lda, F, ldf, W, ldw, k, scale, Y, ldy, s);
   return fail(SK_EINVAL, "sk_kr_cc: dtype");

@@ -152,9 +152,9 @@ class TestMatrix(ABC):
         raise NotImplementedError
 
     def _dense_cc(self, x, adjoint: bool):
-        """A Omega (or Omega^T B) with the materialized real Omega on the library's CUDA-core
-        contraction kernel (sk_kr_right_cc / sk_kr_adjoint_cc with one block: W = 1, F = Omega),
-        float64 accumulation; float32 or float64 in and out."""
+        """A Omega (or Omega^T B) with the materialized real Omega on the library's contraction kernels
+        (sk_kr_right_cc / sk_kr_adjoint_cc with one block: W = NULL, F = Omega): float64 on the FP64
+        tensor cores (K5d), float32 on the CUDA cores with float64 accumulation."""
         import torch
 
         from .. import _lib
@@ -162,8 +162,8 @@ class TestMatrix(ABC):
         key = ("dense_cc", x.device, x.dtype)
         if key not in self._device_cache:
             f = torch.as_tensor(np.ascontiguousarray(self.materialize()), device=x.device).to(x.dtype)
-            self._device_cache[key] = (f, torch.ones((1, self.k), dtype=x.dtype, device=x.device))
-        f, w = self._device_cache[key]
+            self._device_cache[key] = f
+        f = self._device_cache[key]
         if x.stride(1) != 1 or x.stride(0) < x.shape[1]:
             x = x.contiguous()
         rows = x.shape[1] if adjoint else x.shape[0]
@@ -174,8 +174,8 @@ class TestMatrix(ABC):
         code = _lib.SK_F64 if x.dtype == torch.float64 else _lib.SK_F32
         fn = lib.sk_kr_adjoint_cc if adjoint else lib.sk_kr_right_cc
         with torch.cuda.device(x.device):
-            st = fn(code, x.data_ptr(), rows, 1, self.d, x.stride(0), f.data_ptr(), f.stride(0), w.data_ptr(),
-                    w.stride(0), self.k, 1.0, out.data_ptr(), out.stride(0), torch.cuda.current_stream().cuda_stream)
+            st = fn(code, x.data_ptr(), rows, 1, self.d, x.stride(0), f.data_ptr(), f.stride(0), None, 0, self.k, 1.0,
+                    out.data_ptr(), out.stride(0), torch.cuda.current_stream().cuda_stream)
         _lib.check(st, "sk_kr_adjoint_cc" if adjoint else "sk_kr_right_cc")
         return out
 

@@ -1,10 +1,16 @@
-"""The BASELINE configurations with float64 A (the reference's dtype): kernel path and time."""
+"""The BASELINE configurations with float64 A (the reference's dtype): kernel path and time.
+
+    python tools/f64_probe.py
+
+Dense-shaped float64 applies (Khatri-Rao, Gaussian) run K4c on the CUDA cores; their FP64 rate is
+printed next to cuBLAS DGEMM (torch.matmul) on the same shape as the yardstick.
+"""
 import sys
 
 import torch
 
 sys.path.insert(0, "/root/repo")
-from paper_2508_21189_b200.sketch import KhatriRaoTM, SparseRttTM, SparseUniformTM  # noqa: E402
+from paper_2508_21189_b200.sketch import GaussianTM, KhatriRaoTM, SparseRttTM, SparseUniformTM  # noqa: E402
 
 dev = torch.device("cuda", 0)
 
@@ -21,13 +27,25 @@ def timeit(fn, reps=3):
     return e0.elapsed_time(e1) / reps
 
 
-cases = [("cfg2 SRTT f64", SparseRttTM(8192, 512, 1, "wht", seed=0), (65536, 8192)),
-         ("cfg3 sparse f64", SparseUniformTM(16384, 200, 8, seed=0), (65536, 16384)),
-         ("cfg5 KR f64", KhatriRaoTM(256, 2, 512, "real_rademacher", seed=0), (8192, 65536))]
-for name, tm, shape in cases:
+cases = [("cfg2 SRTT f64", SparseRttTM(8192, 512, 1, "wht", seed=0), (65536, 8192), 0),
+         ("cfg3 sparse f64", SparseUniformTM(16384, 200, 8, seed=0), (65536, 16384), 0),
+         ("cfg5 KR f64", KhatriRaoTM(256, 2, 512, "real_rademacher", seed=0), (8192, 65536), 512),
+         ("gauss f64", GaussianTM(16384, 200, seed=0), (32768, 16384), 200),
+         ("gauss f64 k512", GaussianTM(4096, 512, seed=0), (65536, 4096), 512)]
+only = sys.argv[1:]
+for name, tm, shape, kflops in cases:
+    if only and not any(o in name for o in only):
+        continue
     a = torch.randn(*shape, device=dev, dtype=torch.float64)
     ms = timeit(lambda: tm.apply_right(a))
     gb = a.numel() * 8 / 1e9
-    print(f"{name:18s} A {shape} {gb:.1f} GB: {ms:8.2f} ms  {gb / ms * 1e3:7.0f} GB/s", flush=True)
+    line = f"{name:18s} A {shape} {gb:.1f} GB: {ms:8.2f} ms  {gb / ms * 1e3:7.0f} GB/s"
+    if kflops:
+        fl = 2.0 * shape[0] * shape[1] * kflops
+        om = torch.randn(shape[1], kflops, device=dev, dtype=torch.float64)
+        ms_blas = timeit(lambda: a @ om)
+        line += f"  {fl / ms / 1e9:6.1f} TFLOP/s   cuBLAS DGEMM same shape {ms_blas:8.2f} ms {fl / ms_blas / 1e9:6.1f} TFLOP/s"
+        del om
+    print(line, flush=True)
     del a
     torch.cuda.empty_cache()
