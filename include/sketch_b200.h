@@ -92,12 +92,18 @@ SK_API int sk_sparse_right(int dtype, const void* A, int64_t n, int64_t d, int64
  * 16w ..), lists[16*seg[16h + w] ..] = 16 uint8 column counts, then uint16 entries ((row / 64) % 2) << 15 |
  * (row % 64) << 3 | neg (sketch/encode.py ring_encode); seg has ceil(d/128)*16 + 1 entries.
  * Workspace: sk_sparse_right_ring_workspace_bytes(n, d).  A 8-byte, lists 16-byte aligned.
+ * sk_sparse_right_ring_slab: the same on a row slab of Omega (A pointing at the slab's first column,
+ * d = the slab's width, lists encoded with slab-local rows) with Y += when `accumulate` is set, so an
+ * Omega whose lists exceed shared memory runs as a fixed sequence of slabs (deterministic sums).
  */
 SK_API int sk_sparse_right_ring_supported(int dtype, int64_t d, int64_t k, int64_t seg_bytes);
 SK_API size_t sk_sparse_right_ring_workspace_bytes(int64_t n, int64_t d);
 SK_API int sk_sparse_right_ring(const double* A, int64_t n, int64_t d, int64_t lda, const uint8_t* lists,
                                 const uint32_t* seg, int64_t seg_bytes, int64_t k, double scale, double* Y,
                                 int64_t ldy, void* ws, size_t ws_bytes, void* stream);
+SK_API int sk_sparse_right_ring_slab(const double* A, int64_t n, int64_t d, int64_t lda, const uint8_t* lists,
+                                     const uint32_t* seg, int64_t seg_bytes, int64_t k, double scale, double* Y,
+                                     int64_t ldy, int accumulate, void* ws, size_t ws_bytes, void* stream);
 
 /*
  * K1s — Y[n,k] = scale * A * Omega for a sparse A in CSR (int64 indptr[n+1], int32 indices, values

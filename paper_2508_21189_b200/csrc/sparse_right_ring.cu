@@ -55,6 +55,7 @@ struct RingParams {
   int64_t ldy;
   double* ws;               // [grid][RR][256] tail partials
   int* flags;               // [grid] (zeroed before the launch)
+  int accumulate;           // Y += (a column slab of a wider Omega) instead of Y =
 };
 
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, bool valid) {
@@ -192,11 +193,21 @@ __global__ void __launch_bounds__(THREADS, 1) sparse_right_ring_kernel(const Rin
       double* y1 = y0 + 32 * p.ldy;
       const int kc = p.k - c0;
       const bool ok0 = r0 < p.n, ok1 = r1 < p.n;
+      if (p.accumulate) {
 #pragma unroll
-      for (int j = 0; j < CPW; ++j) {
-        if (j < kc) {
-          if (ok0) y0[j] = acc0[j] * p.scale;
-          if (ok1) y1[j] = acc1[j] * p.scale;
+        for (int j = 0; j < CPW; ++j) {
+          if (j < kc) {
+            if (ok0) y0[j] += acc0[j] * p.scale;
+            if (ok1) y1[j] += acc1[j] * p.scale;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < CPW; ++j) {
+          if (j < kc) {
+            if (ok0) y0[j] = acc0[j] * p.scale;
+            if (ok1) y1[j] = acc1[j] * p.scale;
+          }
         }
       }
     };
@@ -292,10 +303,11 @@ extern "C" size_t sk_sparse_right_ring_workspace_bytes(int64_t n, int64_t d) {
   return (size_t)grid * (skb::RR * 256 * sizeof(double) + sizeof(int));
 }
 
-extern "C" int sk_sparse_right_ring(const double* A, int64_t n, int64_t d, int64_t lda, const uint8_t* lists,
-                                    const uint32_t* seg, int64_t seg_bytes, int64_t k, double scale, double* Y,
-                                    int64_t ldy, void* ws, size_t ws_bytes, void* stream) {
-  using namespace skb;
+namespace skb {
+namespace {
+int ring_run(const double* A, int64_t n, int64_t d, int64_t lda, const uint8_t* lists, const uint32_t* seg,
+             int64_t seg_bytes, int64_t k, double scale, double* Y, int64_t ldy, int accumulate, void* ws,
+             size_t ws_bytes, void* stream) {
   if (n < 0 || d < 1 || k < 1 || lda < d || ldy < k) return fail(SK_EINVAL, "sk_sparse_right_ring: bad shape");
   if (!sk_sparse_right_ring_supported(SK_F64, d, k, seg_bytes))
     return fail(SK_EUNSUPPORTED, "sk_sparse_right_ring: k > 256 or segments too large for shared memory");
@@ -329,6 +341,7 @@ extern "C" int sk_sparse_right_ring(const double* A, int64_t n, int64_t d, int64
   p.ldy = ldy;
   p.ws = part;
   p.flags = flags;
+  p.accumulate = accumulate;
   const size_t smem = ring_smem(d, seg_bytes);
   allow_smem(sparse_right_ring_kernel, smem);
   sparse_right_ring_kernel<<<grid, THREADS, smem, s>>>(p);
@@ -341,4 +354,19 @@ extern "C" int sk_sparse_right_ring(const double* A, int64_t n, int64_t d, int64
                               ", smem " + std::to_string(smem) + ")");
   }
   return SK_OK;
+}
+}  // namespace
+}  // namespace skb
+
+extern "C" int sk_sparse_right_ring(const double* A, int64_t n, int64_t d, int64_t lda, const uint8_t* lists,
+                                    const uint32_t* seg, int64_t seg_bytes, int64_t k, double scale, double* Y,
+                                    int64_t ldy, void* ws, size_t ws_bytes, void* stream) {
+  return skb::ring_run(A, n, d, lda, lists, seg, seg_bytes, k, scale, Y, ldy, 0, ws, ws_bytes, stream);
+}
+
+extern "C" int sk_sparse_right_ring_slab(const double* A, int64_t n, int64_t d, int64_t lda, const uint8_t* lists,
+                                         const uint32_t* seg, int64_t seg_bytes, int64_t k, double scale, double* Y,
+                                         int64_t ldy, int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  return skb::ring_run(A, n, d, lda, lists, seg, seg_bytes, k, scale, Y, ldy, accumulate ? 1 : 0, ws, ws_bytes,
+                       stream);
 }

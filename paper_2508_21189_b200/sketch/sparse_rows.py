@@ -16,7 +16,8 @@ import numpy as np
 
 from .. import _lib
 from ..devrng import DevicePhilox, device_draws_enabled
-from .encode import ENT_PAD, PTR_PAD, bcsc_encode, bcsc_segments, gather_encode, ring_encode, wide_encode_device
+from .encode import (ENT_PAD, PTR_PAD, RING_UC, RING_WARPS, bcsc_encode, bcsc_segments, gather_encode, ring_encode,
+                     wide_encode_device)
 from .tensorcore import bt_from_triplets, dense_right_tc
 from .testmatrix import TestMatrix, entry_sample
 
@@ -188,8 +189,9 @@ class _SignSparseTM(TestMatrix):
 
     def _ring_on(self, device):
         """K1r encoding (float64 right apply on the warp-specialised ring, k <= 256), cached per
-        device; None when the ring kernel does not take this operator (SKETCH_B200_K1=classic
-        forces the round-1 kernel)."""
+        device: a list of row slabs of Omega (s0, width, lists, seg, bytes) whose lists each fit
+        shared memory (one slab when the whole operator does), and the magnitude; None when the ring
+        kernel does not take this operator (SKETCH_B200_K1=classic forces the round-1 kernel)."""
         import os
 
         import torch
@@ -203,17 +205,47 @@ class _SignSparseTM(TestMatrix):
                     lists, seg = ring_encode(rows, cols, neg, self.d, self.k)
                 except ValueError:
                     lists = None
-                if lists is not None and _lib.load().sk_sparse_right_ring_supported(_lib.SK_F64, self.d, self.k,
-                                                                                     lists.size):
-                    res = (torch.from_numpy(lists).to(device), torch.from_numpy(seg.view(np.int32)).to(device),
-                           int(lists.size), mag)
+                if lists is not None:
+                    slabs = self._ring_slabs(lists, seg, device)
+                    if slabs is not None:
+                        res = (slabs, mag)
             self._device_cache[key] = res
         return self._device_cache[key]
+
+    def _ring_slabs(self, lists, seg, device):
+        """Cut the unit sequence (128 rows of Omega each; entries are unit-local, so a slab's lists are a
+        contiguous byte range of the full encoding) into the fewest slabs that fit shared memory."""
+        import torch
+
+        lib = _lib.load()
+        nunits = (self.d + RING_UC - 1) // RING_UC
+        w = RING_WARPS  # segments per unit (consumer warps)
+        off = seg.astype(np.int64) * 16
+        out = []
+        h0 = 0
+        while h0 < nunits:
+            h1 = h0 + 1
+            if not self._slab_fits(lib, off, w, h0, h1):
+                return None
+            while h1 < nunits and self._slab_fits(lib, off, w, h0, h1 + 1):
+                h1 += 1
+            s0, s1 = h0 * RING_UC, min(self.d, h1 * RING_UC)
+            b0, b1 = int(off[h0 * w]), int(off[h1 * w])
+            sl = np.ascontiguousarray(lists[b0:b1])
+            sg = (seg[h0 * w:h1 * w + 1].astype(np.int64) - seg[h0 * w]).astype(np.uint32)
+            out.append((s0, s1 - s0, torch.from_numpy(sl).to(device), torch.from_numpy(sg.view(np.int32)).to(device),
+                        int(b1 - b0)))
+            h0 = h1
+        return out
+
+    def _slab_fits(self, lib, off, w, h0, h1):
+        width = min(self.d, h1 * RING_UC) - h0 * RING_UC
+        return bool(lib.sk_sparse_right_ring_supported(_lib.SK_F64, width, self.k, int(off[h1 * w] - off[h0 * w])))
 
     def _right_ring(self, a, ring):
         import torch
 
-        lists, seg, nbytes, mag = ring
+        slabs, mag = ring
         if a.stride(1) != 1 or a.data_ptr() % 8:
             a = a.contiguous()
         n = a.shape[0]
@@ -221,13 +253,15 @@ class _SignSparseTM(TestMatrix):
         if n == 0:
             return y
         lib = _lib.load()
-        ws_bytes = lib.sk_sparse_right_ring_workspace_bytes(n, self.d)  # stream-K tail partials + flags
+        ws_bytes = max(lib.sk_sparse_right_ring_workspace_bytes(n, s[1]) for s in slabs)  # stream-K partials
         ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=a.device)
         with torch.cuda.device(a.device):
-            st = lib.sk_sparse_right_ring(a.data_ptr(), n, self.d, a.stride(0), lists.data_ptr(), seg.data_ptr(),
-                                          nbytes, self.k, mag, y.data_ptr(), y.stride(0), ws.data_ptr(), ws_bytes,
-                                          torch.cuda.current_stream().cuda_stream)
-        _lib.check(st, "sk_sparse_right_ring")
+            stream = torch.cuda.current_stream().cuda_stream
+            for i, (s0, width, lists, seg, nbytes) in enumerate(slabs):
+                st = lib.sk_sparse_right_ring_slab(a.data_ptr() + 8 * s0, n, width, a.stride(0), lists.data_ptr(),
+                                                   seg.data_ptr(), nbytes, self.k, mag, y.data_ptr(), y.stride(0),
+                                                   1 if i else 0, ws.data_ptr(), ws_bytes, stream)
+                _lib.check(st, "sk_sparse_right_ring_slab")
         return y
 
     def _adjoint_wide_on(self, device):

@@ -331,6 +331,28 @@ def test_k1_ring_edge_shapes(n, d, k, zeta, cuda):
     assert rel_err(y, orc.csr_right(orc.sparse_uniform_csr(d, k, zeta, n), a)) <= 1e-12
 
 
+@pytest.mark.parametrize("n,d,k,zeta", [(700, 16384, 200, 8), (129, 30000, 256, 4), (3000, 9000, 33, 16)])
+def test_k1_ring_slabs(n, d, k, zeta, cuda):
+    """Omega whose ring lists exceed shared memory runs as a fixed sequence of row slabs (Y =, then Y +=
+    per slab): against the oracle at 1e-12, slab count > 1, and a strided A (padded rows)."""
+    import torch
+
+    tm = skb.SparseUniformTM(d, k, zeta, seed=d)
+    ring = tm._ring_on(cuda)
+    assert ring is not None and len(ring[0]) > 1
+    widths = [w for _, w, _, _, _ in ring[0]]
+    assert sum(widths) == d
+    rng = np.random.default_rng(n)
+    a = rng.standard_normal((n, d))
+    ref = orc.csr_right(orc.sparse_uniform_csr(d, k, zeta, d), a)
+    y = tm.apply_right(torch.from_numpy(a).to(cuda)).cpu().numpy()
+    assert rel_err(y, ref) <= 1e-12
+    buf = torch.zeros((n, d + 6), dtype=torch.float64, device=cuda)
+    buf[:, 3:3 + d] = torch.from_numpy(a).to(cuda)
+    y2 = tm.apply_right(buf[:, 3:3 + d]).cpu().numpy()
+    assert rel_err(y2, ref) <= 1e-12
+
+
 def test_k1_ring_stack_family(cuda):
     import torch
 
