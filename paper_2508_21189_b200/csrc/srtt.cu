@@ -111,6 +111,11 @@ struct Phase3 {
   }
 };
 
+// One-instruction bulk prefetch of [p, p + bytes) into L2 (TMA unit; bytes % 16 == 0).
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 template <typename T, int L, bool SIGNS>
 __global__ void __launch_bounds__((1 << (L - 5)), (sizeof(T) == 4 ? (L <= 12 ? 3 : (L == 13 ? 2 : 1)) : (L <= 12 ? 2 : (L == 13 ? 2 : 1))))
     srtt_wht_fast(const T* __restrict__ A, int64_t n, int64_t lda, const T* __restrict__ dvals,
@@ -137,6 +142,9 @@ __global__ void __launch_bounds__((1 << (L - 5)), (sizeof(T) == 4 ? (L <= 12 ? 3
 
   for (int64_t row = blockIdx.x; row < n; row += gridDim.x) {
     const T* a = A + row * lda;
+    // the CTA's next row heads for L2 while this one is transformed (its loads then hit L2)
+    if (t == 0 && row + gridDim.x < n && ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && ((lda * sizeof(T)) & 15) == 0)
+      prefetch_l2_bulk(a + gridDim.x * lda, (uint32_t)(D * sizeof(T)));
     T x[32];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -253,10 +261,7 @@ __device__ __forceinline__ void upk(u64 p, float& lo, float& hi) {
 }
 __device__ __forceinline__ int swz4(int j) { return j ^ (((j >> 7) & 7) << 2); }
 
-// One-instruction bulk prefetch of [p, p + bytes) into L2 (TMA unit; bytes % 16 == 0).
-__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
+
 
 template <int L>
 struct WideCfg {
