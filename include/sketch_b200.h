@@ -306,16 +306,15 @@ SK_API int sk_kr_adjoint(const float* B, int64_t m, int64_t P, int64_t dl, int64
  * K3b — SRTT with the DCT transform (the reference's real-field default, src/sketch/rtt.py:92-93,
  * 129-140) in ONE kernel for power-of-two d: per row, Makhoul's real-IFFT form of the DCT-III folded
  * into a length-d/2 complex IDFT (Stockham radix-16 passes in shared memory), then the sampled
- * outputs.  w = D / s (s the orthonormal DCT weights, d values of `dtype`); ab = (alpha_k, beta_k),
- * k < d/2, complex interleaved; tw = e^{2 pi i t / (d/2)}; samp[c*xi + x] = t | neg << 31, t the index
- * of the sampled output in the transformed row's IDFT order; scale = sampler magnitude / d (tables:
- * sketch/trig.py _dct_fft_tables).  Rows 16-byte aligned; float32 d <= 16384, float64 d <= 8192
- * (sk_srtt_dct_supported).
+ * outputs.  w = D / s (s the orthonormal DCT weights, d values of `dtype`); samp[c*xi + x] = t | neg << 31,
+ * t the index of the sampled output in the transformed row's IDFT order; scale = sampler magnitude / d
+ * (sketch/trig.py _dct_fft_tables); the trig tables are formed on the device.  Rows 16-byte aligned;
+ * float32 d <= 16384, float64 d <= 8192 (sk_srtt_dct_supported).
  */
 SK_API int sk_srtt_dct_supported(int dtype, int64_t d);
 SK_API int sk_srtt_dct_right(int dtype, const void* A, int64_t n, int64_t d, int64_t lda, const void* w,
-                             const void* ab, const void* tw, const int32_t* samp, int32_t xi, int64_t k,
-                             double scale, void* Y, int64_t ldy, void* stream);
+                             const int32_t* samp, int32_t xi, int64_t k, double scale, void* Y, int64_t ldy,
+                             void* stream);
 
 /*
  * K6 — fused two-sided sketch: Y[n,k] = sy * A Omega and XT[p,d] = sx * Psi^T A from ONE

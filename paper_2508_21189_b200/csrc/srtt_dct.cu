@@ -1,16 +1,20 @@
 // K3b — SRTT with the DCT transform (the reference's real-field default, src/sketch/rtt.py:92-93,
 // 129-140):  Y[r, c] = scale * sum_x sign_{c,x} * DCT-III(A[r, :] D)[j_{c,x}]   for power-of-two d.
 //
-// One CTA per row (persistent over rows), everything in shared memory, no intermediate in HBM:
-//   1. the raw row lands by one cp.async.bulk (prefetched while the previous row is transformed);
+// One CTA per row (persistent over rows, several CTAs per SM), everything in shared memory, no
+// intermediate in HBM; a CTA keeps one row-sized buffer (plus ~3 KB of twiddles):
+//   1. the raw row lands in it by one cp.async.bulk (issued as soon as the previous row's gather is done;
+//      the other CTAs on the SM overlap the load);
 //   2. Makhoul's real-IFFT form of the DCT-III, folded with the split of a length-N real inverse FFT
 //      into a length-M = N/2 complex one:  with Z = A D / s (s the ortho weights),
 //         U_k = alpha_k (Z_k - i Z_{N-k}) + beta_k (Z_{M-k} + i Z_{M+k}),   k = 0..M-1  (Z_N := 0),
 //      alpha_k = c_k (1 + i w^k), beta_k = conj(c_{M-k}) (1 - i w^k), c_k = e^{i pi k / 2N},
-//      w = e^{2 pi i / N} (host tables, weights w = D / s folded into the load);
+//      w = e^{2 pi i / N} = c^4 (c_k from two short shared tables formed by sincospi at CTA start; the
+//      weights w = D / s folded into the load, a +-1 diagonal as a shared sign mask); every thread forms
+//      its U_k in registers before any is stored, because u overwrites the raw row in place;
 //   3. u = IDFT_M(U) by Stockham passes in shared memory (radix 16, plus one radix-4/8/32 pass when M is
 //      not a power of 16), one butterfly group per thread, in place (loads, barrier, stores); each group
-//      is an in-register DIF DFT; twiddles e^{2 pi i t / M} from a shared table;
+//      is an in-register DIF DFT; twiddles e^{2 pi i t / M} as products of two short shared tables;
 //   4. the transformed row is v = (re u_0, im u_0, re u_1, ...) / N (u XOR-swizzled in shared memory)
 //      and the DCT-III output is
 //      x_{2n} = v_n, x_{2n+1} = v_{N-1-n}: the host maps every sampled output j to its index t in v,
@@ -89,19 +93,25 @@ __device__ __forceinline__ void dft_inv_dif(C2<T> (&x)[R]) {
 // bank-conflict free
 __device__ __forceinline__ int sw(int i) { return i ^ ((i >> 4) & 15); }
 
-// one Stockham pass of radix R on u (M complex, in shared memory), twiddles tw[t] = e^{2 pi i t / M}:
-// element q of group g is multiplied by W^q with W = tw[k * M / (L R)] (k = g mod L; powers by a
-// complex-multiply chain, one table read per group); one butterfly group per thread (blockDim >= M / R),
-// in place (loads, barrier, stores, barrier)
+// twiddle e^{2 pi i t / M} from two short shared tables: t0[l] = e^{2 pi i l / M} (l < 64) and
+// t1[h] = e^{2 pi i 64 h / M}, so the CTA keeps ~3 KB of twiddles instead of M complex values
+template <typename T>
+__device__ __forceinline__ C2<T> twid(const C2<T>* t0, const C2<T>* t1, int t) {
+  return t < 64 ? t0[t] : cmul(t1[t >> 6], t0[t & 63]);
+}
+
+// one Stockham pass of radix R on u (M complex, in shared memory): element q of group g is multiplied
+// by W^q with W = e^{2 pi i k / (L R)} (k = g mod L; powers by a complex-multiply chain, one twiddle per
+// group); one butterfly group per thread (blockDim >= M / R), in place (loads, barrier, stores, barrier)
 template <typename T, int R>
-__device__ __forceinline__ void stockham_pass(C2<T>* u, const C2<T>* tw, int M, int L) {
+__device__ __forceinline__ void stockham_pass(C2<T>* u, const C2<T>* t0, const C2<T>* t1, int M, int L) {
   const int G = M / R;
   const int g = threadIdx.x;
   const int stride_tw = M / (L * R);
   C2<T> v[R];
   const int k = g % L;
   if (g < G) {
-    const C2<T> w1 = tw[k * stride_tw];
+    const C2<T> w1 = twid(t0, t1, k * stride_tw);
     C2<T> wq = w1;
     v[0] = u[sw(g)];
 #pragma unroll
@@ -121,20 +131,58 @@ __device__ __forceinline__ void stockham_pass(C2<T>* u, const C2<T>* tw, int M, 
   __syncthreads();
 }
 
+template <typename T>
+__device__ __forceinline__ C2<T> cis_pi(double x) {  // e^{i pi x}
+  double s, c;
+  sincospi(x, &s, &c);
+  return {(T)c, (T)s};
+}
+
 template <typename T, int THREADS, int B>  // B = log2(M) % 4: the extra pass (0 none, 1 radix 32, 2 radix 4, 3 radix 8)
-__global__ void __launch_bounds__(THREADS) srtt_dct_kernel(const T* __restrict__ A, int64_t n, int N, int64_t lda,
-                                                               const T* __restrict__ w, const C2<T>* __restrict__ ab,
-                                                               const C2<T>* __restrict__ twg,
-                                                               const int32_t* __restrict__ samp, int xi, int k,
-                                                               T scale, T* __restrict__ Y, int64_t ldy) {
+__global__ void __launch_bounds__(THREADS, THREADS == 512 ? 1 : 2)
+    srtt_dct_kernel(const T* __restrict__ A, int64_t n, int N, int64_t lda, const T* __restrict__ w,
+                    const int32_t* __restrict__ samp, int xi, int k, T scale, T* __restrict__ Y, int64_t ldy) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int M = N / 2;
-  T* raw = reinterpret_cast<T*>(smem);                         // N reals (the bulk-copied row)
-  C2<T>* u = reinterpret_cast<C2<T>*>(raw + N);                 // M complex
-  C2<T>* tw = u + M;                                            // M twiddles
-  uint64_t* bar = reinterpret_cast<uint64_t*>(tw + M);
+  const int nt1 = M >= 64 ? M / 64 : 1;
+  C2<T>* u = reinterpret_cast<C2<T>*>(smem);  // M complex; the raw row (N reals) lands here
+  const T* raw = reinterpret_cast<const T*>(smem);
+  C2<T>* t0 = u + M;                          // e^{2 pi i l / M}, l < 64
+  C2<T>* t1 = t0 + 64;                        // e^{2 pi i 64 h / M}, h < M / 64
+  C2<T>* r0 = t1 + nt1;                       // c_l = e^{i pi l / 2N}, l < 64
+  C2<T>* r1 = r0 + 64;                        // e^{i pi 64 h / 2N}, h < M / 64
+  C2<T>* q0 = r1 + nt1;                       // c_l^5 = e^{i 5 pi l / 2N}, l < 64
+  C2<T>* q1 = q0 + 64;                        // e^{i 5 pi 64 h / 2N}, h < M / 64
+  uint32_t* sbits = reinterpret_cast<uint32_t*>(q1 + nt1);  // sign of w[i], N bits
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sbits + ((N / 32 + 1) & ~1));  // 8-byte aligned
   const int tid = threadIdx.x;
-  for (int i = tid; i < M; i += blockDim.x) tw[i] = twg[i];
+  // every trig table is formed here (sincospi, float64), ~3 KB per CTA: no table is re-read from L2
+  for (int i = tid; i < 64; i += THREADS) {
+    t0[i] = cis_pi<T>(2.0 * (i < M ? i : 0) / M);
+    r0[i] = cis_pi<T>((double)i / (2.0 * N));
+    q0[i] = cis_pi<T>(5.0 * i / (2.0 * N));
+  }
+  for (int i = tid; i < nt1; i += THREADS) {
+    t1[i] = cis_pi<T>(M >= 64 ? 128.0 * i / M : 0.0);
+    r1[i] = cis_pi<T>(64.0 * i / (2.0 * N));
+    q1[i] = cis_pi<T>(5.0 * 64.0 * i / (2.0 * N));
+  }
+  // w = D / s: with a +-1 diagonal |w| is one value past index 0, so the signs go to a bit mask and
+  // the loads below never touch the table (any other w is read as given)
+  const T wm0 = fabs(w[0]), wm1 = fabs(w[1]);
+  bool uni = true;
+  for (int i = tid; i < N; i += THREADS) {
+    const T v = w[i];
+    const unsigned bits = __ballot_sync(0xffffffffu, v < T(0));
+    if ((i & 31) == 0) sbits[i >> 5] = bits;
+    if (i > 0 && fabs(v) != wm1) uni = false;
+  }
+  uni = __syncthreads_and(uni);
+  auto wv = [=](int i) -> T {
+    if (!uni) return w[i];
+    const T m = i ? wm1 : wm0;
+    return ((sbits[i >> 5] >> (i & 31)) & 1u) ? -m : m;
+  };
   if (tid == 0) {
     sm100::mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -153,36 +201,63 @@ __global__ void __launch_bounds__(THREADS) srtt_dct_kernel(const T* __restrict__
   for (; r < n; r += gridDim.x) {
     sm100::mbar_wait(bar, ph);
     ph ^= 1;
-    // 2. U_k from the raw row (weights w = D / s), Z_N := 0
-    for (int kk = tid; kk < M; kk += blockDim.x) {
-      const T z0 = raw[kk] * w[kk];
-      const T zn = kk ? raw[N - kk] * w[N - kk] : T(0);
-      const T zm = raw[M - kk] * w[M - kk];
-      const T zp = raw[M + kk] * w[M + kk];
-      const C2<T> al = ab[2 * kk], be = ab[2 * kk + 1];
-      const C2<T> p = cmul(al, C2<T>{z0, -zn});
-      const C2<T> q = cmul(be, C2<T>{zm, zp});
-      u[sw(kk)] = cadd(p, q);
+    // 2. U_k from the raw row (weights w = D / s), Z_N := 0.  The row and u share the buffer, so every
+    //    thread forms its U_k in registers first, then a barrier, then the stores.  U_k and U_{M-k} read
+    //    the same four inputs; with c = c_k, c5 = c_k^5 (om = c^4): alpha_k = c + i c5,
+    //    beta_k = e^{-i pi/4} (c - i c5), alpha_{M-k} = e^{i pi/4} conj(alpha_k),
+    //    beta_{M-k} = e^{-i pi/4} conj(beta_k).  Pairs k = 1 .. M/2 - 1; k = 0 and M/2 by threads 0, 1.
+    constexpr int PPT = 8;  // (M/2 - 1) / THREADS <= 8 for every supported (d, THREADS)
+    // the thread index re-read per row: the pair indices below are row-invariant, and hoisting their
+    // address / weight arithmetic out of the row loop only spills it to local memory
+    int tr;
+    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tr));
+    const C2<T> ep = {(T)0.70710678118654752440, (T)0.70710678118654752440};  // e^{i pi / 4}
+    const C2<T> em = {ep.x, -ep.y};
+    C2<T> ua[PPT], ub[PPT];
+#pragma unroll
+    for (int i = 0; i < PPT; ++i) {
+      const int kk = 1 + tr + i * THREADS;
+      if (kk < M / 2) {
+        const T za = raw[kk] * wv(kk), zb = raw[N - kk] * wv(N - kk);
+        const T zc = raw[M - kk] * wv(M - kk), ze = raw[M + kk] * wv(M + kk);
+        const C2<T> c = twid(r0, r1, kk), c5 = twid(q0, q1, kk);
+        const C2<T> al = {c.x - c5.y, c.y + c5.x};
+        const C2<T> be = cmul(em, C2<T>{c.x + c5.y, c.y - c5.x});
+        ua[i] = cadd(cmul(al, C2<T>{za, -zb}), cmul(be, C2<T>{zc, ze}));
+        const C2<T> al2 = cmul(ep, C2<T>{al.x, -al.y}), be2 = cmul(em, C2<T>{be.x, -be.y});
+        ub[i] = cadd(cmul(al2, C2<T>{zc, -ze}), cmul(be2, C2<T>{za, zb}));
+      }
+    }
+    C2<T> ux = {T(0), T(0)};
+    const int kx = tid == 0 ? 0 : M / 2;  // threads 0 and 1
+    if (tid < 2) {
+      const T z0 = raw[kx] * wv(kx), zn = kx ? raw[N - kx] * wv(N - kx) : T(0);
+      const T zm = raw[M - kx] * wv(M - kx), zp = raw[M + kx] * wv(M + kx);
+      const C2<T> c = twid(r0, r1, kx), c5 = twid(q0, q1, kx);
+      const C2<T> al = {c.x - c5.y, c.y + c5.x};
+      const C2<T> be = cmul(em, C2<T>{c.x + c5.y, c.y - c5.x});
+      ux = cadd(cmul(al, C2<T>{z0, -zn}), cmul(be, C2<T>{zm, zp}));
     }
     __syncthreads();
-    // the raw buffer is free: prefetch the next row while this one is transformed
-    const int64_t rn = r + gridDim.x;
-    if (tid == 0 && rn < n) {
-      sm100::mbar_arrive_expect_tx(bar, row_bytes);
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       sm100::smem_u32(raw)),
-                   "l"(A + rn * lda), "r"(row_bytes), "r"(sm100::smem_u32(bar))
-                   : "memory");
+#pragma unroll
+    for (int i = 0; i < PPT; ++i) {
+      const int kk = 1 + tid + i * THREADS;
+      if (kk < M / 2) {
+        u[sw(kk)] = ua[i];
+        u[sw(M - kk)] = ub[i];
+      }
     }
+    if (tid < 2) u[sw(kx)] = ux;
+    __syncthreads();
     // 3. u = IDFT_M(U): M = 2^m, m = 4a + b: one pass of radix 4 (b = 2), 8 (b = 3) or 32 (b = 1, replacing
     //    a radix-16 pass), then radix-16 passes
     {
       int L = 1;
-      if constexpr (B == 1) { stockham_pass<T, 32>(u, tw, M, L); L = 32; }
-      if constexpr (B == 2) { stockham_pass<T, 4>(u, tw, M, L); L = 4; }
-      if constexpr (B == 3) { stockham_pass<T, 8>(u, tw, M, L); L = 8; }
+      if constexpr (B == 1) { stockham_pass<T, 32>(u, t0, t1, M, L); L = 32; }
+      if constexpr (B == 2) { stockham_pass<T, 4>(u, t0, t1, M, L); L = 4; }
+      if constexpr (B == 3) { stockham_pass<T, 8>(u, t0, t1, M, L); L = 8; }
       while (L < M) {
-        stockham_pass<T, 16>(u, tw, M, L);
+        stockham_pass<T, 16>(u, t0, t1, M, L);
         L *= 16;
       }
     }
@@ -200,16 +275,30 @@ __global__ void __launch_bounds__(THREADS) srtt_dct_kernel(const T* __restrict__
       y[c] = s * scale;
     }
     __syncthreads();
+    // u is free: the CTA's next row lands in it (other CTAs on the SM overlap this load)
+    const int64_t rn = r + gridDim.x;
+    if (tid == 0 && rn < n) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      sm100::mbar_arrive_expect_tx(bar, row_bytes);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       sm100::smem_u32(u)),
+                   "l"(A + rn * lda), "r"(row_bytes), "r"(sm100::smem_u32(bar))
+                   : "memory");
+    }
   }
 }
 
+size_t dct_smem(int64_t N, size_t esz) {
+  const int64_t M = N / 2;
+  return (size_t)N * esz + (size_t)(64 + (M >= 64 ? M / 64 : 1)) * 3 * 2 * esz + (size_t)((N / 32 + 1) & ~1) * 4 + 16;
+}
+
 template <typename T>
-int dct_run(const T* A, int64_t n, int N, int64_t lda, const T* w, const T* ab, const T* tw, const int32_t* samp,
-            int xi, int k, double scale, T* Y, int64_t ldy, cudaStream_t s) {
-  const size_t smem = (size_t)N * sizeof(T) + (size_t)N * sizeof(T) + (size_t)N * sizeof(T) + 16;
+int dct_run(const T* A, int64_t n, int N, int64_t lda, const T* w, const int32_t* samp, int xi, int k, double scale,
+            T* Y, int64_t ldy, cudaStream_t s) {
+  const size_t smem = dct_smem(N, sizeof(T));
   if (smem > 227 * 1024) return fail(SK_EUNSUPPORTED, "sk_srtt_dct_right: row too long for shared memory");
-  using KernT = void (*)(const T*, int64_t, int, int64_t, const T*, const C2<T>*, const C2<T>*, const int32_t*, int,
-                         int, T, T*, int64_t);
+  using KernT = void (*)(const T*, int64_t, int, int64_t, const T*, const int32_t*, int, int, T, T*, int64_t);
   const int b = (31 - __builtin_clz((unsigned)(N / 2))) & 3;
   const int threads = N / 2 > 4096 ? 512 : 256;  // one butterfly group per thread (M / 16 groups at most)
   KernT kern;
@@ -228,41 +317,38 @@ int dct_run(const T* A, int64_t n, int N, int64_t lda, const T* w, const T* ab, 
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)per_sm * sm_count();
   if (grid > n) grid = n;
-  kern<<<(unsigned)grid, threads, smem, s>>>(A, n, N, lda, w, reinterpret_cast<const C2<T>*>(ab),
-                                             reinterpret_cast<const C2<T>*>(tw), samp, xi, k, (T)scale, Y, ldy);
+  kern<<<(unsigned)grid, threads, smem, s>>>(A, n, N, lda, w, samp, xi, k, (T)scale, Y, ldy);
   return check_launch("sk_srtt_dct_right");
 }
 
 }  // namespace
 }  // namespace skb
 
-// ab: [M][2] complex (alpha_k, beta_k) interleaved re/im; tw: [M] complex e^{2 pi i t / M}; w: [N] = D / s;
-// samp[c * xi + x] = t | neg << 31 with t the index in v of the sampled DCT output; scale includes 1 / N.
+// w: [N] = D / s; samp[c * xi + x] = t | neg << 31 with t the index in v of the sampled DCT output;
+// scale includes 1 / N.  The trig tables are formed on the device.
 extern "C" int sk_srtt_dct_right(int dtype, const void* A, int64_t n, int64_t d, int64_t lda, const void* w,
-                                 const void* ab, const void* tw, const int32_t* samp, int32_t xi, int64_t k,
-                                 double scale, void* Y, int64_t ldy, void* stream) {
+                                 const int32_t* samp, int32_t xi, int64_t k, double scale, void* Y, int64_t ldy,
+                                 void* stream) {
   using namespace skb;
   if (n < 0 || d < 32 || (d & (d - 1)) || lda < d || k < 1 || xi < 1 || ldy < k)
     return fail(SK_EINVAL, "sk_srtt_dct_right: bad shape (d a power of two >= 32)");
   if (n == 0) return SK_OK;
-  if (!A || !w || !ab || !tw || !samp || !Y) return fail(SK_EINVAL, "sk_srtt_dct_right: null pointer");
+  if (!A || !w || !samp || !Y) return fail(SK_EINVAL, "sk_srtt_dct_right: null pointer");
   const size_t esz = dtype == SK_F64 ? 8 : 4;
   if ((reinterpret_cast<uintptr_t>(A) & 15) || ((lda * esz) & 15))
     return fail(SK_EINVAL, "sk_srtt_dct_right: rows must be 16-byte aligned");
   cudaStream_t s = as_stream(stream);
   if (dtype == SK_F32)
-    return dct_run<float>(static_cast<const float*>(A), n, (int)d, lda, static_cast<const float*>(w),
-                          static_cast<const float*>(ab), static_cast<const float*>(tw), samp, xi, (int)k, scale,
-                          static_cast<float*>(Y), ldy, s);
+    return dct_run<float>(static_cast<const float*>(A), n, (int)d, lda, static_cast<const float*>(w), samp, xi,
+                          (int)k, scale, static_cast<float*>(Y), ldy, s);
   if (dtype == SK_F64)
-    return dct_run<double>(static_cast<const double*>(A), n, (int)d, lda, static_cast<const double*>(w),
-                           static_cast<const double*>(ab), static_cast<const double*>(tw), samp, xi, (int)k, scale,
-                           static_cast<double*>(Y), ldy, s);
+    return dct_run<double>(static_cast<const double*>(A), n, (int)d, lda, static_cast<const double*>(w), samp, xi,
+                           (int)k, scale, static_cast<double*>(Y), ldy, s);
   return fail(SK_EINVAL, "sk_srtt_dct_right: dtype");
 }
 
 extern "C" int sk_srtt_dct_supported(int dtype, int64_t d) {
   if (d < 32 || (d & (d - 1))) return 0;
-  const size_t esz = dtype == SK_F64 ? 8 : 4;
-  return 3 * (size_t)d * esz + 16 <= 227 * 1024 ? 1 : 0;
+  if (dtype == SK_F64 ? d > 8192 : d > 16384) return 0;  // one butterfly group per thread (<= 512 threads)
+  return skb::dct_smem(d, dtype == SK_F64 ? 8 : 4) <= 227 * 1024 ? 1 : 0;
 }

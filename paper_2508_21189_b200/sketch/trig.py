@@ -350,8 +350,8 @@ class SparseRttTM(TestMatrix):
 
     def _dct_fft_tables(self, device, dtype):
         """Host tables of the fused DCT-III row kernel (csrc/srtt_dct.cu), cached per device and dtype:
-        w = D / s, (alpha_k, beta_k), the IDFT_M twiddles, the sampled output -> index-in-v map and the
-        scale (sampler magnitude / N)."""
+        w = D / s, the sampled output -> index-in-v map and the scale (sampler magnitude / N); the
+        kernel forms its trig tables itself."""
         import torch
 
         key = ("srtt_dct_fft", device, dtype)
@@ -361,30 +361,18 @@ class SparseRttTM(TestMatrix):
             rows, neg, mag = sampler.column_draws()
             s = np.full(n_, np.sqrt(2.0 / n_))
             s[0] = np.sqrt(1.0 / n_)
-            kk = np.arange(m_)
-            c = np.exp(1j * np.pi * np.arange(m_ + 1) / (2 * n_))
-            om = np.exp(2j * np.pi * kk / n_)
-            alpha = c[:m_] * (1 + 1j * om)
-            beta = np.conj(c[m_ - kk]) * (1 - 1j * om)
-            ab = np.stack([alpha, beta], axis=1)  # (M, 2) complex
-            tw = np.exp(2j * np.pi * np.arange(m_) / m_)
             j = rows.reshape(-1).astype(np.int64)
             t = np.where(j % 2 == 0, j // 2, n_ - 1 - (j - 1) // 2)
             samp = (t | (neg.reshape(-1).astype(np.int64) << 31)).astype(np.uint32).view(np.int32)
-
-            def real(x):
-                return torch.from_numpy(np.ascontiguousarray(np.stack([x.real, x.imag], -1))).to(device, dtype)
-
-            self._device_cache[key] = (torch.from_numpy(np.ascontiguousarray(dvals / s)).to(device, dtype), real(ab),
-                                       real(tw), torch.from_numpy(np.ascontiguousarray(samp)).to(device),
-                                       float(mag) / n_)
+            self._device_cache[key] = (torch.from_numpy(np.ascontiguousarray(dvals / s)).to(device, dtype),
+                                       torch.from_numpy(np.ascontiguousarray(samp)).to(device), float(mag) / n_)
         return self._device_cache[key]
 
     def _dct_fft_right(self, a):
         """Y through the fused DCT-III row kernel (sk_srtt_dct_right): no intermediate in HBM."""
         import torch
 
-        w, ab, tw, samp, scale = self._dct_fft_tables(a.device, a.dtype)
+        w, samp, scale = self._dct_fft_tables(a.device, a.dtype)
         if a.stride(1) != 1 or a.data_ptr() % 16 or (a.stride(0) * a.element_size()) % 16:
             a = a.contiguous()
         n = a.shape[0]
@@ -394,9 +382,9 @@ class SparseRttTM(TestMatrix):
         lib = _lib.load()
         code = _lib.SK_F32 if a.dtype == torch.float32 else _lib.SK_F64
         with torch.cuda.device(a.device):
-            st = lib.sk_srtt_dct_right(code, a.data_ptr(), n, self.d, a.stride(0), w.data_ptr(), ab.data_ptr(),
-                                       tw.data_ptr(), samp.data_ptr(), self.xi, self.k, scale, y.data_ptr(),
-                                       y.stride(0), torch.cuda.current_stream().cuda_stream)
+            st = lib.sk_srtt_dct_right(code, a.data_ptr(), n, self.d, a.stride(0), w.data_ptr(), samp.data_ptr(),
+                                       self.xi, self.k, scale, y.data_ptr(), y.stride(0),
+                                       torch.cuda.current_stream().cuda_stream)
         _lib.check(st, "sk_srtt_dct_right")
         return y
 

@@ -89,6 +89,34 @@ def test_srtt_dct_fused_kernel_every_pass_pattern(d, dt, cuda, monkeypatch):
     assert rel_err(y, ref) <= (1e-12 if dt == "float64" else 1e-5)
 
 
+@pytest.mark.parametrize("dt", ["float32", "float64"])
+def test_srtt_dct_kernel_general_weights(dt, cuda):
+    """K3b with weights that are not +-1 / s (the kernel's table path) against the same kernel on the
+    +-1 path with the extra factors folded into A: sk_srtt_dct_right(A, w * v) == sk_srtt_dct_right(A * v, w)."""
+    import torch
+
+    from paper_2508_21189_b200 import _lib
+
+    d, k, xi = 2048, 40, 2
+    tm = skb.SparseRttTM(d, k, xi, "dct", seed=3)
+    tdt = getattr(torch, dt)
+    w, samp, scale = tm._dct_fft_tables(cuda, tdt)
+    g = torch.Generator(device=cuda).manual_seed(2)
+    a = torch.randn(300, d, device=cuda, dtype=tdt, generator=g)
+    v = 0.5 + torch.rand(d, device=cuda, dtype=tdt, generator=g)
+    lib = _lib.load()
+    code = _lib.SK_F64 if dt == "float64" else _lib.SK_F32
+    outs = []
+    for x, ww in ((a, (w * v).contiguous()), ((a * v).contiguous(), w)):
+        y = torch.empty(300, k, device=cuda, dtype=tdt)
+        _lib.check(lib.sk_srtt_dct_right(code, x.data_ptr(), 300, d, x.stride(0), ww.data_ptr(), samp.data_ptr(), xi,
+                                         k, scale, y.data_ptr(), y.stride(0), torch.cuda.current_stream().cuda_stream),
+                   "sk_srtt_dct_right")
+        outs.append(y.double())
+    err = float(torch.linalg.norm(outs[0] - outs[1]) / torch.linalg.norm(outs[1]))
+    assert err <= (1e-13 if dt == "float64" else 1e-6), err
+
+
 def test_srtt_dct_paths_agree_config2_shape(cuda, monkeypatch):
     """Config-2 shape with the DCT transform (the reference default): the fused FFT kernel, the
     tensor-core form and the cuFFT form agree; a 64-row slab against the oracle."""
