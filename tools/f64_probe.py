@@ -33,6 +33,15 @@ cases = [("cfg2 SRTT f64", SparseRttTM(8192, 512, 1, "wht", seed=0), (65536, 819
          ("gauss f64", GaussianTM(16384, 200, seed=0), (32768, 16384), 200),
          ("gauss f64 k512", GaussianTM(4096, 512, seed=0), (65536, 4096), 512)]
 only = sys.argv[1:]
+if not only or any("adj" in o for o in only):
+    tm = SparseUniformTM(1 << 20, 2048, 8, seed=0)
+    a = torch.randn(1 << 20, 512, device=dev, dtype=torch.float64)
+    ms = timeit(lambda: tm.apply_adjoint(a))
+    gb = (a.numel() + 2048 * 512) * 8 / 1e9
+    print(f"{'cfg4 adj f64':18s} A (1048576, 512) {a.numel() * 8 / 1e9:.1f} GB: {ms:8.2f} ms  {gb / ms * 1e3:7.0f} GB/s",
+          flush=True)
+    del a
+    torch.cuda.empty_cache()
 for name, tm, shape, kflops in cases:
     if only and not any(o in name for o in only):
         continue
