@@ -6,7 +6,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KEYS = ["UTCHMMA", "UTCQMMA", "UTCBAR", "UTMALDG", "UBLKCP", "UTMASTG", "LDTM", "STTM", "SYNCS", "LDGSTS", "DADD",
+KEYS = ["UTCHMMA", "UTCQMMA", "DMMA", "UTCBAR", "UTMALDG", "UBLKCP", "UTMASTG", "LDTM", "STTM", "SYNCS", "LDGSTS", "DADD",
         "DFMA", "FFMA", "LDS", "STS", "REDG", "BRX"]
 
 
