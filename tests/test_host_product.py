@@ -235,3 +235,32 @@ def test_ring_encode_roundtrip(d, k, zeta):
     r, c, n = ring_decode(lists, seg, d, k)
     assert sorted(zip(coo.row.tolist(), coo.col.tolist(), (coo.data < 0).tolist())) == \
         sorted(zip(r.tolist(), c.tolist(), n.tolist()))
+
+
+@pytest.mark.parametrize("d,k,zeta", [(16384, 200, 8), (30000, 256, 4), (4096, 256, 4)])
+def test_ring_slabs_partition_omega(d, k, zeta):
+    """K1r row slabs (wide Omega): widths tile [0, d) on 128-row unit boundaries, every slab's lists
+    fit shared memory (the library's own check, no device needed), and the slabs' lists, decoded with
+    slab-local rows, are exactly Omega's triplets."""
+    from paper_2508_21189_b200 import _lib
+    from paper_2508_21189_b200.sketch.encode import ring_decode
+
+    tm = skb.SparseUniformTM(d, k, zeta, seed=d)
+    rows, cols, neg, _ = tm._sign_form()
+    from paper_2508_21189_b200.sketch.encode import ring_encode
+
+    lists, seg = ring_encode(rows, cols, neg, d, k)
+    slabs = tm._ring_slabs(lists, seg, "cpu")
+    assert slabs is not None
+    lib = _lib.load()
+    got = []
+    s_expect = 0
+    for s0, width, sl, sg, nbytes in slabs:
+        assert s0 == s_expect and s0 % 128 == 0 and width > 0
+        s_expect = s0 + width
+        assert lib.sk_sparse_right_ring_supported(_lib.SK_F64, width, k, nbytes)
+        r, c, n = ring_decode(sl.numpy(), sg.numpy().view(np.uint32), width, k)
+        got += list(zip((r + s0).tolist(), c.tolist(), n.tolist()))
+    assert s_expect == d
+    assert (len(slabs) > 1) == (d > 4096)
+    assert sorted(got) == sorted(zip(rows.tolist(), cols.tolist(), neg.astype(bool).tolist()))
