@@ -347,6 +347,23 @@ SK_API int sk_kr_adjoint_cc(int dtype, const void* B, int64_t m, int64_t P, int6
                             int64_t ldf, const void* W, int64_t ldw, int64_t k, double scale, void* X, int64_t ldx,
                             void* stream);
 
+/*
+ * Complex fields (the reference's default Khatri-Rao base is complex_spherical; Gaussian and SRTT
+ * have complex variants) on the same float64 DMMA engine, one real product per call over planar
+ * data: Y (+)= scale * A * Re(Omega) (part 0) or Im(Omega) (part 1), A a real plane (n x P*dl);
+ * Omega = W (x) F given as the real / imaginary planes of F (dl x k) and W (P x k), or W = NULL with
+ * Fi = NULL for a dense plane Omega_part = Fr (P = 1).  accumulate != 0 adds into Y.  A complex
+ * product is the caller's sum of such calls, e.g. Re(A Omega) = Ar Re(Omega) - Ai Im(Omega).  The
+ * adjoint form reads B (P*dl x m) in place and writes X (k x m).  16-byte aligned planes, even row
+ * strides.
+ */
+SK_API int sk_kr_right_z(const double* A, int64_t n, int64_t P, int64_t dl, int64_t lda, const double* Fr,
+                         const double* Fi, int64_t ldf, const double* Wr, const double* Wi, int64_t ldw, int64_t k,
+                         int part, double scale, int accumulate, double* Y, int64_t ldy, void* stream);
+SK_API int sk_kr_adjoint_z(const double* B, int64_t m, int64_t P, int64_t dl, int64_t ldb, const double* Fr,
+                           const double* Fi, int64_t ldf, const double* Wr, const double* Wi, int64_t ldw, int64_t k,
+                           int part, double scale, int accumulate, double* X, int64_t ldx, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

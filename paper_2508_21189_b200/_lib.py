@@ -99,6 +99,10 @@ SIGNATURES = {
     "sk_srtt_dct_supported": (_c_int, [_c_int, _c_i64]),
     "sk_srtt_dct_right": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, ctypes.c_int32, _c_i64, _c_dbl,
                                    _c_p, _c_i64, _c_p]),
+    "sk_kr_right_z": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_p, _c_p, _c_i64, _c_i64,
+                               _c_int, _c_dbl, _c_int, _c_p, _c_i64, _c_p]),
+    "sk_kr_adjoint_z": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_p, _c_p, _c_i64, _c_i64,
+                                 _c_int, _c_dbl, _c_int, _c_p, _c_i64, _c_p]),
     "sk_kr_right_cc": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_i64,
                                 _c_dbl, _c_p, _c_i64, _c_p]),
     "sk_kr_adjoint_cc": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_i64,

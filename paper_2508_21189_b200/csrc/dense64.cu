@@ -50,13 +50,17 @@ struct G64 {
   int64_t ldb;
   const double* W;  // Khatri-Rao leading weights (P x N, ldw) or nullptr
   int64_t ldw, dl;
+  const double* Bi;  // complex Khatri-Rao: imaginary planes of F and W (same strides)
+  const double* Wi;
+  int part;          // complex Khatri-Rao: 0 = Re(W F), 1 = Im(W F)
+  int accumulate;    // C += instead of C =
   int64_t N;
   double scale;
   double* C;
   int64_t ldc;
 };
 
-template <bool TA, bool TC, bool KR, int WM, int WN, int GM, int GN>
+template <bool TA, bool TC, bool KR, int WM, int WN, int GM, int GN, bool CPLX = false>
 __global__ void __launch_bounds__(GM * GN * 32, 1) gemm64_kernel(const G64 p) {
   constexpr int THREADS = GM * GN * 32;
   constexpr int BM = GM * WM, BN = GN * WN;
@@ -134,6 +138,22 @@ __global__ void __launch_bounds__(GM * GN * 32, 1) gemm64_kernel(const G64 p) {
           fr[e].x = __ldg(f);
           wr[e].x = __ldg(w);
         }
+        if (CPLX) {  // (wr + i wi)(fr + i fi): keep the requested part as fr * 1
+          double2 fi = make_double2(0.0, 0.0), wi = make_double2(0.0, 0.0);
+          const double* f2 = p.Bi + q * p.ldb + n;
+          const double* w2 = p.Wi + P * p.ldw + n;
+          if (n + 1 < p.N) {
+            fi = __ldg(reinterpret_cast<const double2*>(f2));
+            wi = __ldg(reinterpret_cast<const double2*>(w2));
+          } else {
+            fi.x = __ldg(f2);
+            wi.x = __ldg(w2);
+          }
+          const double2 a = fr[e], b = wr[e];
+          fr[e] = p.part ? make_double2(b.x * fi.x + wi.x * a.x, b.y * fi.y + wi.y * a.y)
+                         : make_double2(b.x * a.x - wi.x * fi.x, b.y * a.y - wi.y * fi.y);
+          wr[e] = make_double2(1.0, 1.0);
+        }
       }
     }
   };
@@ -210,29 +230,36 @@ __global__ void __launch_bounds__(GM * GN * 32, 1) gemm64_kernel(const G64 p) {
       const int64_t n = n0 + wn * WN + j * 8 + 2 * t;
       const double v0 = acc[i][j][0] * p.scale, v1 = acc[i][j][1] * p.scale;
       if (TC) {
-        if (n < p.N) p.C[n * p.ldc + m] = v0;
-        if (n + 1 < p.N) p.C[(n + 1) * p.ldc + m] = v1;
+        double* c0 = p.C + n * p.ldc + m;
+        if (n < p.N) *c0 = p.accumulate ? *c0 + v0 : v0;
+        if (n + 1 < p.N) c0[p.ldc] = p.accumulate ? c0[p.ldc] + v1 : v1;
       } else {
         double* c = p.C + m * p.ldc + n;
         if (n + 1 < p.N && ((reinterpret_cast<uintptr_t>(c) & 15) == 0)) {
-          *reinterpret_cast<double2*>(c) = make_double2(v0, v1);
+          double2 v = make_double2(v0, v1);
+          if (p.accumulate) {
+            const double2 o = *reinterpret_cast<const double2*>(c);
+            v.x += o.x;
+            v.y += o.y;
+          }
+          *reinterpret_cast<double2*>(c) = v;
         } else {
-          if (n < p.N) c[0] = v0;
-          if (n + 1 < p.N) c[1] = v1;
+          if (n < p.N) c[0] = p.accumulate ? c[0] + v0 : v0;
+          if (n + 1 < p.N) c[1] = p.accumulate ? c[1] + v1 : v1;
         }
       }
     }
   }
 }
 
-template <bool TA, bool TC, bool KR, int WM, int WN, int GM, int GN>
+template <bool TA, bool TC, bool KR, int WM, int WN, int GM, int GN, bool CPLX = false>
 int launch64(const G64& p, cudaStream_t s) {
   constexpr int BM = GM * WM, BN = GN * WN;
   constexpr int SA = TA ? BM + 4 : BK + 4;
   constexpr int A_ELEMS = TA ? BK * SA : BM * SA;
   constexpr int B_ELEMS = BK * (BN + 4);
   const size_t smem = (size_t)STAGES * (A_ELEMS + B_ELEMS) * sizeof(double);
-  auto kern = gemm64_kernel<TA, TC, KR, WM, WN, GM, GN>;
+  auto kern = gemm64_kernel<TA, TC, KR, WM, WN, GM, GN, CPLX>;
   allow_smem(kern, smem);
   const int64_t gx = (p.M + BM - 1) / BM, gy = (p.N + BN - 1) / BN;
   if (gy > 65535 || gx > 0x7fffffff) return fail(SK_EUNSUPPORTED, "sk_gemm64: grid too large");
@@ -242,6 +269,7 @@ int launch64(const G64& p, cudaStream_t s) {
 
 template <bool TA, bool TC, bool KR>
 int pick_tile(const G64& p, cudaStream_t s) {
+  if (KR && p.Bi) return launch64<TA, TC, KR, 32, 32, 4, 2, true>(p, s);  // complex synthesis: 8 warps
   // 128 x 128 CTA tiles of 16 warps (warp 32 x 32) unless N is small or the grid would not fill the
   // SMs twice over, then 128 x 64 tiles of 8 warps
   const int64_t tiles128 = ((p.M + 127) / 128) * ((p.N + 127) / 128);
@@ -255,10 +283,14 @@ int pick_tile(const G64& p, cudaStream_t s) {
 // shape/alignment is not taken (the caller then runs the CUDA-core kernel), else an SK status.
 int gemm64_try(bool ta, const double* A, int64_t rows, int64_t P, int64_t dl, int64_t lda, const double* F,
                int64_t ldf, const double* W, int64_t ldw, int64_t k, double scale, double* Y, int64_t ldy,
-               cudaStream_t s) {
+               cudaStream_t s, const double* Fi, const double* Wi, int part, int accumulate, bool force) {
+  // force: the complex-plane entry points (no CUDA-core alternative); otherwise 1 = not taken
   const auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-  if (rows < 64 || k < 8) return 1;  // tiny products: the CUDA-core tiles waste less
-  if (!al16(A) || (lda & 1) || !al16(F) || (ldf & 1) || (W && (!al16(W) || (ldw & 1)))) return 1;
+  const bool cplx = Fi != nullptr;
+  if (!force && (rows < 64 || k < 8)) return 1;  // tiny products: the CUDA-core tiles waste less
+  if (!al16(A) || (lda & 1) || !al16(F) || (ldf & 1) || (W && (!al16(W) || (ldw & 1))) ||
+      (cplx && (!al16(Fi) || !W || !Wi || !al16(Wi))))
+    return force ? fail(SK_EINVAL, "sk_kr_*_z: 16-byte aligned planes, even row strides") : 1;
   G64 p{};
   p.A = A;
   p.M = rows;
@@ -273,9 +305,42 @@ int gemm64_try(bool ta, const double* A, int64_t rows, int64_t P, int64_t dl, in
   p.scale = scale;
   p.C = Y;
   p.ldc = ldy;
+  p.Bi = Fi;
+  p.Wi = Wi;
+  p.part = part;
+  p.accumulate = accumulate;
   const bool kr = W != nullptr;
   if (ta) return kr ? pick_tile<true, true, true>(p, s) : pick_tile<true, true, false>(p, s);
   return kr ? pick_tile<false, false, true>(p, s) : pick_tile<false, false, false>(p, s);
 }
 
 }  // namespace skb
+
+// float64 GEMM engine on the planes of a complex Omega (the complex fields of the reference: its
+// default Khatri-Rao base is complex_spherical, Gaussian and SRTT have complex variants).
+extern "C" int sk_kr_right_z(const double* A, int64_t n, int64_t P, int64_t dl, int64_t lda, const double* Fr,
+                             const double* Fi, int64_t ldf, const double* Wr, const double* Wi, int64_t ldw, int64_t k,
+                             int part, double scale, int accumulate, double* Y, int64_t ldy, void* stream) {
+  using namespace skb;
+  if (n < 0 || P < 1 || dl < 1 || k < 1 || ldf < k || lda < P * dl || ldy < k || (Wr && ldw < k) || part < 0 ||
+      part > 1 || (!Wr && P != 1) || (!Wr && Fi))
+    return fail(SK_EINVAL, "sk_kr_right_z: bad shape");
+  if (n == 0) return SK_OK;
+  if (!A || !Fr || !Y || (Wr && (!Fi || !Wi))) return fail(SK_EINVAL, "sk_kr_right_z: null pointer");
+  return gemm64_try(false, A, n, P, dl, lda, Fr, ldf, Wr, ldw, k, scale, Y, ldy, as_stream(stream), Fi, Wi, part,
+                    accumulate ? 1 : 0, true);
+}
+
+extern "C" int sk_kr_adjoint_z(const double* B, int64_t m, int64_t P, int64_t dl, int64_t ldb, const double* Fr,
+                               const double* Fi, int64_t ldf, const double* Wr, const double* Wi, int64_t ldw,
+                               int64_t k, int part, double scale, int accumulate, double* X, int64_t ldx,
+                               void* stream) {
+  using namespace skb;
+  if (m < 0 || P < 1 || dl < 1 || k < 1 || ldf < k || ldb < m || ldx < m || (Wr && ldw < k) || part < 0 ||
+      part > 1 || (!Wr && P != 1) || (!Wr && Fi))
+    return fail(SK_EINVAL, "sk_kr_adjoint_z: bad shape");
+  if (m == 0) return SK_OK;
+  if (!B || !Fr || !X || (Wr && (!Fi || !Wi))) return fail(SK_EINVAL, "sk_kr_adjoint_z: null pointer");
+  return gemm64_try(true, B, m, P, dl, ldb, Fr, ldf, Wr, ldw, k, scale, X, ldx, as_stream(stream), Fi, Wi, part,
+                    accumulate ? 1 : 0, true);
+}

@@ -19,7 +19,8 @@ namespace skb {
 
 int gemm64_try(bool ta, const double* A, int64_t rows, int64_t P, int64_t dl, int64_t lda, const double* F,
                int64_t ldf, const double* W, int64_t ldw, int64_t k, double scale, double* Y, int64_t ldy,
-               cudaStream_t s);  // dense64.cu
+               cudaStream_t s, const double* Fi = nullptr, const double* Wi = nullptr, int part = 0,
+               int accumulate = 0, bool force = false);  // dense64.cu
 
 namespace {
 

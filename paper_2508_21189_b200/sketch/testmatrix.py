@@ -151,6 +151,20 @@ class TestMatrix(ABC):
     def _right_sparse_input(self, a):
         raise NotImplementedError
 
+    # dense complex families (Gaussian, explicit) whose complex128 applies run on the FP64 DMMA engine
+    # over the planes of the materialised Omega; the sparse families keep their own paths
+    _planar_complex = False
+
+    def _dense_z(self, x, adjoint: bool):
+        """Complex-field A Omega / Omega^H B (float64 or complex128 operand) on the FP64 DMMA engine over
+        the real and imaginary planes of the materialised Omega (sk_kr_right_z / sk_kr_adjoint_z)."""
+        from .zplanes import z_apply, z_operands
+
+        key = ("dense_z", x.device)
+        if key not in self._device_cache:
+            self._device_cache[key] = z_operands(None, np.asarray(self.materialize()), x.device)
+        return z_apply(self._device_cache[key], x, adjoint, 1.0)
+
     def _dense_cc(self, x, adjoint: bool):
         """A Omega (or Omega^T B) with the materialized real Omega on the library's contraction kernels
         (sk_kr_right_cc / sk_kr_adjoint_cc with one block: W = NULL, F = Omega): float64 on the FP64
@@ -186,6 +200,8 @@ class TestMatrix(ABC):
 
         if self.field == "real" and a.dtype in (torch.float32, torch.float64):
             return self._dense_cc(a, adjoint=False)
+        if self._planar_complex and a.dtype in (torch.float64, torch.complex128):
+            return self._dense_z(a, adjoint=False)
         om = self._dense_on(a.device, a.dtype)
         dt = torch.promote_types(a.dtype, om.dtype)
         return a.to(dt) @ om.to(dt)
@@ -195,6 +211,8 @@ class TestMatrix(ABC):
 
         if self.field == "real" and b.dtype in (torch.float32, torch.float64):
             return self._dense_cc(b, adjoint=True)
+        if self._planar_complex and b.dtype in (torch.float64, torch.complex128):
+            return self._dense_z(b, adjoint=True)
         om = self._dense_on(b.device, b.dtype)
         dt = torch.promote_types(b.dtype, om.dtype)
         return om.to(dt).conj().T @ b.to(dt)
@@ -231,6 +249,8 @@ class TestMatrix(ABC):
 
 class ExplicitTM(TestMatrix):
     """A user-supplied explicit matrix wrapped as a sketching operator (reference base.py:116-130)."""
+
+    _planar_complex = True
 
     def __init__(self, matrix, field: str | None = None):
         matrix = np.asarray(matrix)

@@ -82,8 +82,10 @@ def product(name):
 
 
 def rel_err(x, ref) -> float:
-    x = np.asarray(x, dtype=np.float64)
-    ref = np.asarray(ref, dtype=np.float64)
+    """Relative Frobenius error; complex arrays compare in complex128 (both parts)."""
+    cplx = np.iscomplexobj(x) or np.iscomplexobj(ref)
+    x = np.asarray(x, dtype=np.complex128 if cplx else np.float64)
+    ref = np.asarray(ref, dtype=np.complex128 if cplx else np.float64)
     return float(np.linalg.norm(x - ref) / max(np.linalg.norm(ref), 1e-300))
 
 

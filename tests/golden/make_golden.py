@@ -69,6 +69,11 @@ SMALL = {
     "kr_8_3_20_gauss_s3": lambda: KhatriRaoTM(8, 3, 20, "real_gaussian", seed=3),
     "gauss_40_12_s21": lambda: GaussianTM(40, 12, "real", 21),
     "gauss_128_32_s9": lambda: GaussianTM(128, 32, "real", 9),
+    # complex fields (the reference's default Khatri-Rao base is complex_spherical)
+    "kr_16_2_48_csph_s4": lambda: KhatriRaoTM(16, 2, 48, seed=4),
+    "kr_8_3_20_cgauss_s3": lambda: KhatriRaoTM(8, 3, 20, "complex_gaussian", seed=3),
+    "kr_6_2_70_stein_s8": lambda: KhatriRaoTM(6, 2, 70, "steinhaus", seed=8),
+    "gauss_c_128_32_s9": lambda: GaussianTM(128, 32, "complex", 9),
 }
 
 
@@ -87,6 +92,13 @@ def small_fixtures() -> dict:
         out[f"{name}__adjoint_vec"] = tm.apply_adjoint(b[:, 0])
         if tm.d * tm.k <= 100_000:
             out[f"{name}__dense"] = tm.materialize()
+        if tm.field == "complex":  # complex inputs too (drawn after the real ones: those stay unchanged)
+            ac = a + 1j * rng.standard_normal((n_rows, tm.d))
+            bc = b + 1j * rng.standard_normal((tm.d, 3))
+            out[f"{name}__Ac"] = ac
+            out[f"{name}__Bc"] = bc
+            out[f"{name}__right_c"] = tm.apply_right(ac)
+            out[f"{name}__adjoint_c"] = tm.apply_adjoint(bc)
         if isinstance(tm, (SparseUniformTM, SparseStackTM, SparseColTM)):
             m = tm.matrix
             out[f"{name}__indptr"] = m.indptr.astype(np.int64)

@@ -264,3 +264,26 @@ def test_ring_slabs_partition_omega(d, k, zeta):
     assert s_expect == d
     assert (len(slabs) > 1) == (d > 4096)
     assert sorted(got) == sorted(zip(rows.tolist(), cols.tolist(), neg.astype(bool).tolist()))
+
+
+@pytest.mark.parametrize("name,make", [
+    ("kr_16_2_48_csph_s4", lambda: skb.KhatriRaoTM(16, 2, 48, seed=4)),
+    ("kr_8_3_20_cgauss_s3", lambda: skb.KhatriRaoTM(8, 3, 20, "complex_gaussian", seed=3)),
+    ("kr_6_2_70_stein_s8", lambda: skb.KhatriRaoTM(6, 2, 70, "steinhaus", seed=8)),
+    ("gauss_c_128_32_s9", lambda: skb.GaussianTM(128, 32, "complex", 9))])
+def test_complex_fields_match_reference(name, make, golden):
+    """Complex-field constructors (the reference's default Khatri-Rao base is complex_spherical):
+    factors bit-exact and Omega equal to the reference's; the planes the DMMA engine reads rebuild it."""
+    from paper_2508_21189_b200.sketch.zplanes import z_operands
+
+    tm = make()
+    if f"{name}__factors" in golden:
+        assert np.array_equal(tm.factors, golden[f"{name}__factors"])
+    assert rel_err(tm.materialize(), golden[f"{name}__dense"]) <= 1e-13
+    if isinstance(tm, skb.KhatriRaoTM):
+        w, f = tm._kr_split_arrays(tm._kr_group(False))
+        ops = z_operands(None if w.shape[0] == 1 else w, f, "cpu")
+        fz = ops.fr[:, :tm.k].numpy() + 1j * ops.fi[:, :tm.k].numpy()
+        wz = np.ones((1, tm.k)) if ops.wr is None else ops.wr[:, :tm.k].numpy() + 1j * ops.wi[:, :tm.k].numpy()
+        om = (wz[:, None, :] * fz[None, :, :]).reshape(-1, tm.k) / np.sqrt(tm.k)
+        assert rel_err(om, golden[f"{name}__dense"]) <= 1e-13
