@@ -42,6 +42,22 @@ if not only or any("adj" in o for o in only):
           flush=True)
     del a
     torch.cuda.empty_cache()
+if not only or any("complex" in o for o in only):
+    from paper_2508_21189_b200.sketch.kron import _device_contract_rows
+
+    tm = KhatriRaoTM(256, 2, 512, seed=0)  # the reference's default base: complex_spherical
+    for cplx in (False, True):
+        a = torch.randn(4096, 65536, device=dev, dtype=torch.float64)
+        if cplx:
+            a = torch.complex(a, torch.randn_like(a))
+        ms = timeit(lambda: tm.apply_right(a))
+        f = tm._factors_on(dev, torch.complex128)
+        ac = a.to(torch.complex128)
+        ms_t = timeit(lambda: _device_contract_rows(f, ac, conjugate=False))
+        print(f"{'KR complex':18s} A (4096, 65536) {'complex128' if cplx else 'float64'}: {ms:8.2f} ms (K5d planes)"
+              f"  torch mode contraction {ms_t:8.2f} ms", flush=True)
+        del a, ac
+        torch.cuda.empty_cache()
 for name, tm, shape, kflops in cases:
     if only and not any(o in name for o in only):
         continue
