@@ -60,6 +60,7 @@ struct TsParams {
   int stages;
   int ctas_per_group;
   int nb;                // Omega^T operands: 1 (hi) or 2 (hi + lo)
+  int omega_res;         // 1: the column group's Omega^T tiles stay resident in shared memory (loaded once)
   int dbg;               // timing experiments (SKETCH_B200_TS_DBG): 1 no MMA2, 2 no PsiT writes, 4 no Y stores
 };
 
@@ -84,10 +85,10 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
 // MN-major SWIZZLE_128B descriptor (B operand read with N contiguous): 8 K-rows x 64 N-elements per
 // 1024-byte atom; K steps between atoms of 1024 B.  N = 64 fits one atom, so both byte offsets are set
 // to the atom stride.
-__device__ __forceinline__ uint64_t sdesc_mnmajor_sw128(uint32_t saddr) {
+__device__ __forceinline__ uint64_t sdesc_mnmajor_sw128(uint32_t saddr, uint32_t n_stride = 1024) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)(1024 >> 4) << 16;
+  d |= (uint64_t)((n_stride >> 4) & 0x3FFF) << 16;  // LBO: the next 64 N-elements (another stage for N = 128)
   d |= (uint64_t)(1024 >> 4) << 32;
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)2 << 61;
@@ -104,9 +105,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
   const uint32_t b_bytes = (uint32_t)p.NY * 128;        // Omega^T tile: NY rows x 64 (K) bf16
-  const uint32_t stage_bytes = kAStage + (uint32_t)p.nb * b_bytes;
+  const uint32_t om_kb = (uint32_t)p.nb * b_bytes;      // one k-block of Omega^T (hi [+ lo])
+  const uint32_t stage_bytes = kAStage + (p.omega_res ? 0u : om_kb);
   const int S = p.stages;
-  uint8_t* psi_buf = smem + (size_t)S * stage_bytes;    // [2][kPsiBytes]
+  uint8_t* om_buf = smem + (size_t)S * stage_bytes;     // resident Omega^T: [4 k-blocks][hi, lo]
+  uint8_t* psi_buf = om_buf + (p.omega_res ? 4 * (size_t)om_kb : 0);  // [2][kPsiBytes]
   uint64_t* bars = reinterpret_cast<uint64_t*>(psi_buf + 2 * kPsiBytes);
   uint64_t* tma_full = bars;           // [S]
   uint64_t* full = tma_full + S;       // [S] converted (4 converter warps)
@@ -117,7 +120,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* y_empty = y_full + 2;      // [2] Y tile drained (8 epilogue warps)
   uint64_t* xt_full = y_empty + 2;     // XT chunk complete (commit)
   uint64_t* xt_empty = xt_full + 1;    // XT folded (8 epilogue warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xt_empty + 1);
+  uint64_t* om_full = xt_empty + 1;    // resident Omega^T landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(om_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cg = blockIdx.x % p.ncg;                 // column group
@@ -142,6 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(xt_full, 1);
     mbar_init(xt_empty, 8);
+    mbar_init(om_full, 1);
     fence_mbar_init();
     tma_prefetch_desc(&tm_a);
     tma_prefetch_desc(&tm_b);
@@ -159,6 +164,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     setmaxnreg_dec<48>();
     if (warp == 0 && lane == 0) {
       // ---------------------------------------------------------------- TMA producer
+      if (p.omega_res && ntiles > 0) {  // the group's Omega^T k-blocks, once
+        mbar_arrive_expect_tx(om_full, (uint32_t)nkb * om_kb);
+        for (int kb = 0; kb < nkb; ++kb) {
+          tma_load_2d(om_buf + (size_t)kb * om_kb, &tm_b, om_full, c0 + kb * BK, 0);
+          if (p.nb == 2) tma_load_2d(om_buf + (size_t)kb * om_kb + b_bytes, &tm_blo, om_full, c0 + kb * BK, 0);
+        }
+      }
       int s = 0;
       uint32_t ph = 0;
       for (int t = t0; t < t1; ++t)
@@ -167,14 +179,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* st = smem + (size_t)s * stage_bytes;
           mbar_arrive_expect_tx(&tma_full[s], stage_bytes);
           tma_load_2d(st, &tm_a, &tma_full[s], c0 + kb * BK, t * BM);
-          tma_load_2d(st + kAStage, &tm_b, &tma_full[s], c0 + kb * BK, 0);
-          if (p.nb == 2) tma_load_2d(st + kAStage + b_bytes, &tm_blo, &tma_full[s], c0 + kb * BK, 0);
+          if (!p.omega_res) {
+            tma_load_2d(st + kAStage, &tm_b, &tma_full[s], c0 + kb * BK, 0);
+            if (p.nb == 2) tma_load_2d(st + kAStage + b_bytes, &tm_blo, &tma_full[s], c0 + kb * BK, 0);
+          }
           if (++s == S) { s = 0; ph ^= 1; }
         }
     } else if (warp == 1 && lane == 0) {
       // ---------------------------------------------------------------- MMA issuer
       const uint32_t id1 = idesc_bf16_f32(BM, p.NY);
       const uint32_t id2 = idesc_bf16_f32_bmn(BM, BK);
+      const uint32_t id2w = idesc_bf16_f32_bmn(BM, 2 * BK);
+      const bool pairing = !(p.dbg & 8);
+      if (p.omega_res && ntiles > 0) mbar_wait(om_full, 0);
       int s = 0;
       uint32_t ph = 0;
       for (int i = 0; i < ntiles; ++i) {
@@ -187,13 +204,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint64_t dps = sdesc_kmajor_sw128(smem_u32(psi_buf + pb * kPsiBytes));
         const uint32_t dy = tm_y + yb * (uint32_t)p.NY;
+        int s_first = -1;  // first stage of a k-block pair held for one N = 128 MMA2
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t st = smem_u32(smem + (size_t)s * stage_bytes);
           // descriptors built once per stage; a K step adds (bytes >> 4) to the 14-bit start address
           const uint64_t dah = sdesc_kmajor_sw128(st), dal = sdesc_kmajor_sw128(st + BM * 128);
-          const uint64_t dbt = sdesc_kmajor_sw128(st + kAStage), dbl = sdesc_kmajor_sw128(st + kAStage + b_bytes);
+          const uint32_t ob = p.omega_res ? smem_u32(om_buf) + (uint32_t)kb * om_kb : st + kAStage;
+          const uint64_t dbt = sdesc_kmajor_sw128(ob), dbl = sdesc_kmajor_sw128(ob + b_bytes);
           const uint64_t dmh = sdesc_mnmajor_sw128(st), dml = sdesc_mnmajor_sw128(st + BM * 128);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {  // MMA1: Y += A Omega (K = this k-block's 64 columns)
@@ -202,15 +221,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma_bf16(dy, dal + o, dbt + o, id1, 1u);
             if (p.nb == 2) umma_bf16(dy, dah + o, dbl + o, id1, 1u);
           }
-          const uint32_t dx = tm_xt + (uint32_t)kb * BK;
+          // MMA2: XT[:, k-blocks] += PsiT (K = 128 rows) A_tiles.  Two k-blocks in consecutive stages go
+          // in one N = 128 MMA (the PsiT operand is read once for both); otherwise N = 64.
+          const bool hold = pairing && s_first < 0 && (kb & 1) == 0 && kb + 1 < nkb && s + 1 < S;
+          if (hold) {
+            s_first = s;
+          } else {
+            const bool pair = s_first >= 0;
+            const uint32_t sb = pair ? smem_u32(smem + (size_t)s_first * stage_bytes) : st;
+            const uint64_t bh = pair ? sdesc_mnmajor_sw128(sb, stage_bytes) : dmh;
+            const uint64_t bl = pair ? sdesc_mnmajor_sw128(sb + BM * 128, stage_bytes) : dml;
+            const uint32_t dx = tm_xt + (uint32_t)(pair ? kb - 1 : kb) * BK;
 #pragma unroll
-          for (int kr = 0; kr < ((p.dbg & 1) ? 0 : BM / 16); ++kr) {  // MMA2: XT[:, kb] += PsiT (K = 128 rows) A_tile
-            const uint64_t da = dps + (uint64_t)((kr >> 2) * ((BM * 128) >> 4) + (kr & 3) * 2);
-            const uint64_t ob = (uint64_t)(kr * (2048 >> 4));
-            umma_bf16(dx, da, dmh + ob, id2, (!fresh || kr > 0) ? 1u : 0u);
-            umma_bf16(dx, da, dml + ob, id2, 1u);
+            for (int kr = 0; kr < ((p.dbg & 1) ? 0 : BM / 16); ++kr) {
+              const uint64_t da = dps + (uint64_t)((kr >> 2) * ((BM * 128) >> 4) + (kr & 3) * 2);
+              const uint64_t ob = (uint64_t)(kr * (2048 >> 4));
+              umma_bf16(dx, da, bh + ob, pair ? id2w : id2, (!fresh || kr > 0) ? 1u : 0u);
+              umma_bf16(dx, da, bl + ob, pair ? id2w : id2, 1u);
+            }
+            if (pair) umma_commit(&empty[s_first]);
+            umma_commit(&empty[s]);
+            s_first = -1;
           }
-          umma_commit(&empty[s]);
           if (++s == S) { s = 0; ph ^= 1; }
         }
         umma_commit(&psi_empty[pb]);
@@ -413,7 +445,7 @@ int map2d(CUtensorMap* m, CUtensorMapDataType dt, int esz, const void* base, int
 }
 
 struct TsPlan {
-  int ncg, cpg, grid, stages, NY;
+  int ncg, cpg, grid, stages, NY, omega_res;
   size_t smem, ws;
 };
 
@@ -427,12 +459,18 @@ TsPlan ts_plan(int64_t n, int64_t d, int64_t k, int nb) {
   if (cpg > mtiles) cpg = mtiles;
   pl.cpg = cpg;
   pl.grid = cpg * pl.ncg;
-  const size_t stage = kAStage + (size_t)nb * pl.NY * 128;
+  const size_t om_kb = (size_t)nb * pl.NY * 128;
   const size_t fixed = 1024 + 2 * (size_t)kPsiBytes + 64 * 8 + 16;
-  int stages = (int)((227 * 1024 - fixed) / stage);
-  if (stages > 6) stages = 6;
-  pl.stages = stages;
-  pl.smem = fixed + (size_t)stages * stage;
+  // Omega^T resident (loaded once per CTA) when that still leaves as deep an A ring as streaming it
+  // with every stage would; otherwise it rides in each stage
+  int st_stream = (int)((227 * 1024 - fixed) / (kAStage + om_kb));
+  int st_res = (int)((227 * 1024 - fixed - 4 * om_kb) / kAStage);
+  if (st_stream > 6) st_stream = 6;
+  if (st_res > 6) st_res = 6;
+  const bool res = getenv("SKETCH_B200_TS_OMEGA") ? getenv("SKETCH_B200_TS_OMEGA")[0] == 'r' : st_res >= st_stream;
+  pl.omega_res = res ? 1 : 0;
+  pl.stages = res ? st_res : st_stream;
+  pl.smem = res ? fixed + 4 * om_kb + (size_t)st_res * kAStage : fixed + (size_t)st_stream * (kAStage + om_kb);
   pl.ws = (size_t)pl.grid * BM * kColsPerGroup * sizeof(float);
   return pl;
 }
@@ -500,6 +538,7 @@ extern "C" int sk_two_sided_sketch(const float* A, int64_t n, int64_t d, int64_t
   prm.stages = pl.stages;
   prm.ctas_per_group = pl.cpg;
   prm.nb = nb;
+  prm.omega_res = pl.omega_res;
   {
     const char* e = getenv("SKETCH_B200_TS_DBG");
     prm.dbg = e ? atoi(e) : 0;

@@ -54,10 +54,12 @@ def test_validation_errors(cuda):
 
 @pytest.mark.parametrize("n,d,k,p,omega", [(20000, 512, 64, 96, "srtt"), (1000, 100, 17, 128, "gauss"),
                                            (777, 300, 128, 5, "sparse"), (300001, 256, 32, 64, "srtt"),
-                                           (129, 64, 1, 1, "sparse")])
+                                           (129, 64, 1, 1, "sparse"), (5000, 448, 40, 96, "gauss"),
+                                           (3000, 1024, 100, 33, "sparse")])
 def test_two_sided_sketch_fused(n, d, k, p, omega, cuda):
     """The one-pass fused kernel (sk_two_sided_sketch) against the two separate applies and the oracle:
-    ragged M-tiles and column groups (d = 100, 300), one or two column groups, split Omega (Gaussian)."""
+    ragged M-tiles and column groups (d = 100, 300, 448: an odd k-block count next to paired ones), one,
+    two or four column groups, split Omega (Gaussian), 3-stage rings (k = 100, 128)."""
     import torch
 
     import oracle as orc
