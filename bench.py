@@ -423,6 +423,9 @@ def cpu_reference_step(w, a_host, procs):
     elif name == "cfg5":
         f = orc.kr_factors(tm.d0, tm.ell, tm.k, tm.seed, tm.base)
         fn = lambda x: orc.kr_right(f, x)  # noqa: E731
+    elif name == "gauss":  # the reference: a dense float64 GEMM with its Omega (gaussian.py:19-30)
+        om = orc.gaussian_dense(tm.d, tm.k, tm.seed)
+        fn = lambda x: orc.dense_right(om, x)  # noqa: E731
     elif name == "cfg4":  # S A restricted to the sample rows: Omega[:rows]^T A[:rows] (scipy, one core)
         csr = _cfg4_csr(tm)[: a_host.shape[0]]
         t0 = time.perf_counter()
@@ -469,7 +472,7 @@ def sample_parity(w, procs):
 
 
 SAMPLE_ROWS = {"cfg1": 4096, "cfg2": 2048, "cfg3": 512, "cfg4": 1 << 18, "cfg5": 16, "cfg2dct": 1024,
-               "twosided": 8192}
+               "twosided": 8192, "gauss": 2048}
 
 
 def run_reference(args):

@@ -14,4 +14,5 @@ ncu $F -k regex:sparse_adjoint_gather -s 1 -o gpurun_out/r2_cfg4 python tools/pr
 ncu $F -k regex:dense_tc_pair -s 1 -o gpurun_out/r2_cfg5 python tools/prof.py --config cfg5 --reps 3 > /dev/null 2>&1
 ncu $F -k regex:dense_tc_pair -s 1 -o gpurun_out/r2_cfg2dct python tools/prof.py --config cfg2dct --reps 3 > /dev/null 2>&1
 ncu $F -k regex:two_sided_kernel -s 1 -o gpurun_out/r2_twosided python tools/two_sided_prof.py > /dev/null 2>&1
+ncu $F -k regex:dense_tc_pair -s 1 -o gpurun_out/r2_gauss python tools/prof.py --config gauss --reps 3 > /dev/null 2>&1
 echo all-done

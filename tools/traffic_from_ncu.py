@@ -37,6 +37,9 @@ def duration_us(m):
 def main(reps):
     path = os.path.join(ROOT, "profiles", "traffic.json")
     table = {}
+    if os.path.exists(path):  # captures not given keep their entries
+        with open(path) as f:
+            table = json.load(f)
     for rep in reps:
         name = os.path.basename(rep).replace(".ncu-rep", "")
         cfg = name[len("r2_"):] if name.startswith("r2_") else name
