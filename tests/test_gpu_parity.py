@@ -292,6 +292,46 @@ def test_right_paths_randomized(cuda):
         assert rel_err(y, ref) <= tol, (trial, type(tm).__name__, n, tm.d, tm.k)
 
 
+def test_adjoint_and_dense_paths_randomized(cuda):
+    """Random shapes / families / dtypes through the adjoint paths (K2g / K2w / K2 / narrow, SRTT TN,
+    Khatri-Rao in place, K5d) and the float64 dense families on the DMMA engine (K5d, both tile sizes,
+    Khatri-Rao tile synthesis), against the materialized Omega."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    for trial in range(24):
+        dt = torch.float32 if trial % 2 else torch.float64
+        fam = trial % 6
+        if fam == 0:
+            d, k = int(rng.integers(1, 20000)), int(rng.integers(1, 600))
+            tm = skb.SparseUniformTM(d, k, int(rng.integers(1, min(k, 8) + 1)), seed=trial)
+        elif fam == 1:
+            d = 2 ** int(rng.integers(3, 14))
+            tm = skb.SparseRttTM(d, int(rng.integers(1, min(d, 400) + 1)), int(rng.integers(1, 3)),
+                                 "wht" if trial % 4 < 2 else "dct", seed=trial)
+        elif fam == 2:
+            d0 = int(rng.integers(2, 60))
+            tm = skb.KhatriRaoTM(d0, 2, int(rng.integers(1, 300)), "real_rademacher", seed=trial)
+        elif fam == 3:
+            tm = skb.GaussianTM(int(rng.integers(1, 3000)), int(rng.integers(1, 300)), seed=trial)
+        elif fam == 4:
+            tm = skb.KhatriRaoTM(int(rng.integers(2, 12)), 3, int(rng.integers(1, 200)), "real_gaussian", seed=trial)
+        else:
+            tm = skb.SparseStackTM(int(rng.integers(1, 9000)), int(rng.integers(1, 5)), int(rng.integers(1, 90)),
+                                   seed=trial)
+        m = int(rng.integers(1, 400))
+        b = torch.randn(tm.d, m, device=cuda, dtype=dt)
+        x = tm.apply_adjoint(b).double().cpu().numpy()
+        om = tm.materialize()
+        tol = 1e-5 if dt == torch.float32 else 1e-12
+        assert rel_err(x, om.T @ b.double().cpu().numpy()) <= tol, (trial, type(tm).__name__, tm.d, tm.k, m)
+        if fam in (2, 3, 4):  # dense-shaped families: the right apply too (float64: K5d)
+            n = int(rng.integers(1, 2000))
+            a = torch.randn(n, tm.d, device=cuda, dtype=dt)
+            y = tm.apply_right(a).double().cpu().numpy()
+            assert rel_err(y, a.double().cpu().numpy() @ om) <= tol, (trial, type(tm).__name__, n, tm.d, tm.k)
+
+
 def test_k1_ring_config1_full_vs_oracle(cuda):
     """BASELINE config 1 in full on the ring kernel (K1r, stream-K over 148 SMs): every one of the
     16384 rows against the oracle (csr_right, 1.3 s on the host), float64 bar 1e-12; and equal to
