@@ -10,21 +10,23 @@
 //                                               synthesised in shared memory (KR: Omega never formed)
 //     C   = row-major M x N                  or stored transposed (TC: the adjoint writes X = C^T)
 //
-// CTA = GM x GN warps, warp tile 32 x 32 of m8n8k4 DMMAs (16 independent accumulators per k step),
-// CTA tile 128 x 128 (16 warps) or 128 x 64 (8 warps), K in stages of 32 through a 3-deep cp.async
-// ring (one CTA barrier per stage).  Shared tiles are padded to a row stride = 4 (mod 16) doubles so
+// CTA = GM x GN warps, warp tile 32 x 32 of m8n8k4 DMMAs (16 independent accumulators per k step):
+// 128 x 64 CTA tiles of 8 warps, K in stages of 16 through a 3-deep cp.async ring (one CTA barrier
+// per stage), two CTAs per SM.  Shared tiles are padded to a row stride = 4 (mod 16) doubles so
 // the fragment loads (8 rows x 4 k, or 4 k x 8 columns, per half-warp) hit 16 distinct bank pairs.  The Khatri-Rao tile goes through registers (F and W loads
 // issued before the stage's MMAs, the product stored after them).  Accumulation is float64 (DMMA is
 // an IEEE fma chain per element), so parity with the reference holds to rounding (~1e-15).
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "common.cuh"
 
 namespace skb {
 namespace {
 
-constexpr int BK = 32;
-constexpr int STAGES = 3;
+constexpr int BK_DEF = 32;
+constexpr int STAGES_DEF = 3;
 
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src, int bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
@@ -60,8 +62,9 @@ struct G64 {
   int64_t ldc;
 };
 
-template <bool TA, bool TC, bool KR, int WM, int WN, int GM, int GN, bool CPLX = false>
-__global__ void __launch_bounds__(GM * GN * 32, 1) gemm64_kernel(const G64 p) {
+template <bool TA, bool TC, bool KR, int WM, int WN, int GM, int GN, bool CPLX = false, int BK = BK_DEF,
+          int STAGES = STAGES_DEF, int MINB = 1>
+__global__ void __launch_bounds__(GM * GN * 32, MINB) gemm64_kernel(const G64 p) {
   constexpr int THREADS = GM * GN * 32;
   constexpr int BM = GM * WM, BN = GN * WN;
   constexpr int SA = TA ? BM + 4 : BK + 4;  // A tile row stride (doubles): [BK][BM+4] or [BM][BK+4]
@@ -252,14 +255,15 @@ __global__ void __launch_bounds__(GM * GN * 32, 1) gemm64_kernel(const G64 p) {
   }
 }
 
-template <bool TA, bool TC, bool KR, int WM, int WN, int GM, int GN, bool CPLX = false>
+template <bool TA, bool TC, bool KR, int WM, int WN, int GM, int GN, bool CPLX = false, int BK = BK_DEF,
+          int STAGES = STAGES_DEF, int MINB = 1>
 int launch64(const G64& p, cudaStream_t s) {
   constexpr int BM = GM * WM, BN = GN * WN;
   constexpr int SA = TA ? BM + 4 : BK + 4;
   constexpr int A_ELEMS = TA ? BK * SA : BM * SA;
   constexpr int B_ELEMS = BK * (BN + 4);
   const size_t smem = (size_t)STAGES * (A_ELEMS + B_ELEMS) * sizeof(double);
-  auto kern = gemm64_kernel<TA, TC, KR, WM, WN, GM, GN, CPLX>;
+  auto kern = gemm64_kernel<TA, TC, KR, WM, WN, GM, GN, CPLX, BK, STAGES, MINB>;
   allow_smem(kern, smem);
   const int64_t gx = (p.M + BM - 1) / BM, gy = (p.N + BN - 1) / BN;
   if (gy > 65535 || gx > 0x7fffffff) return fail(SK_EUNSUPPORTED, "sk_gemm64: grid too large");
@@ -269,12 +273,11 @@ int launch64(const G64& p, cudaStream_t s) {
 
 template <bool TA, bool TC, bool KR>
 int pick_tile(const G64& p, cudaStream_t s) {
-  if (KR && p.Bi) return launch64<TA, TC, KR, 32, 32, 4, 2, true>(p, s);  // complex synthesis: 8 warps
-  // 128 x 128 CTA tiles of 16 warps (warp 32 x 32) unless N is small or the grid would not fill the
-  // SMs twice over, then 128 x 64 tiles of 8 warps
-  const int64_t tiles128 = ((p.M + 127) / 128) * ((p.N + 127) / 128);
-  if (p.N > 64 && tiles128 >= 2 * sm_count()) return launch64<TA, TC, KR, 32, 32, 4, 4>(p, s);
-  return launch64<TA, TC, KR, 32, 32, 4, 2>(p, s);
+  if (KR && p.Bi) return launch64<TA, TC, KR, 32, 32, 4, 2, true, 16, 3, 2>(p, s);  // complex synthesis
+  // 128 x 64 tiles of 8 warps, 16-deep stages, two CTAs per SM (one CTA's barrier wait is the other's
+  // issue slot, and twice the tiles per wave): 32.6 TFLOP/s at k = 512 and 25.0 on the Khatri-Rao
+  // config-5 shape, against 31.3 / 21.5 for 128 x 128 tiles of 16 warps with 32-deep stages
+  return launch64<TA, TC, KR, 32, 32, 4, 2, false, 16, 3, 2>(p, s);
 }
 
 }  // namespace
