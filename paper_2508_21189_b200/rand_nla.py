@@ -710,6 +710,67 @@ def _lsqr_step(A, v, alpha, u):
     return zb
 
 
+def _lsqr_fused_loop(A, u, v, R, alpha, beta, bnorm, red, atol, btol, iter_lim, kind, t_sketch):
+    """LSQR iterations on the fused step (sk_lsqr_step_f32_f64) with the d-length recurrences on the host.
+
+    Per iteration the device runs one pass over A and the host exchanges two d-vectors with it (R^-1 v
+    up, [A^T u, ||u||^2] down: one synchronisation); v, w, x and the scalar recurrences (Paige &
+    Saunders, as in the device loop above) are float64 NumPy.  The device u is kept unnormalised
+    (u_dev = c u), so the step takes alpha / c and no pass rescales it.  R^-1 is formed once.
+    """
+    import torch
+
+    d = A.shape[1]
+    rinv_h = torch.linalg.solve_triangular(R, torch.eye(d, dtype=R.dtype, device=R.device), upper=True).cpu().numpy()
+    vh = v.double().cpu().numpy()
+    wh = vh.copy()
+    xh = np.zeros(d)
+    dev_v = torch.empty(d, dtype=torch.float64, device=A.device)
+    c = 1.0  # u on the device is normalised on entry
+    phibar, rhobar = beta, alpha
+    anorm2 = ddnorm = 0.0
+    istop, itn = 0, 0
+    r1norm, arnorm, test2 = beta, alpha * beta, 0.0
+    while itn < iter_lim:
+        itn += 1
+        dev_v.copy_(torch.from_numpy(rinv_h @ vh))
+        zb = _lsqr_step(A, dev_v, alpha / c, u)
+        red(zb)
+        zh = zb.cpu().numpy()
+        beta = float(np.sqrt(zh[d]))
+        if beta > 0:
+            c = beta
+            anorm2 += alpha * alpha + beta * beta
+            vh = (rinv_h.T @ zh[:d]) / beta - beta * vh
+            alpha = float(np.linalg.norm(vh))
+            if alpha > 0:
+                vh /= alpha
+        rho = float(np.hypot(rhobar, beta))
+        cs, sn = rhobar / rho, beta / rho
+        theta = sn * alpha
+        rhobar = -cs * alpha
+        phi = cs * phibar
+        phibar = sn * phibar
+        tau = sn * phi
+        xh += (phi / rho) * wh
+        ddnorm += float(wh @ wh) / (rho * rho)
+        wh = vh - (theta / rho) * wh
+        anorm = np.sqrt(anorm2)
+        r1norm = phibar
+        arnorm = alpha * abs(tau)
+        test1 = r1norm / bnorm if bnorm > 0 else 0.0
+        test2 = arnorm / (anorm * r1norm) if anorm * r1norm > 0 else 0.0
+        if test2 <= atol:
+            istop = 2
+            break
+        if btol > 0 and test1 <= btol + atol * anorm * float(np.linalg.norm(xh)) / bnorm:
+            istop = 1
+            break
+    acond = float(np.sqrt(anorm2) * np.sqrt(ddnorm))
+    x = torch.from_numpy(rinv_h @ xh).to(A.device)
+    return LsqrResult(_back(x, kind), istop, itn, float(r1norm), float(arnorm), acond, t_sketch, float(test2))
+
+
 def _rmatvec_blocks(A, u, block_rows):
     """A^T @ u in float64 (sk_gemv_t_f32_f64 for float32 A: one pass, ordered float64 reduction)."""
     import torch
@@ -760,7 +821,10 @@ def sketch_precondition_lsqr(a, b, tm_psi, *, atol: float = 1e-6, btol: float = 
     red(sa)
     sync()
     t_sketch = time.perf_counter() - t0
-    _, R = torch.linalg.qr(sa, mode="reduced")
+    # R of S A = Q R: CholeskyQR2 (two d x d Gram matrices, ~1 ms at config 4) unless S A is too
+    # ill-conditioned for it, then Householder QR (cuSOLVER geqrf: 3.9 ms at 2048 x 512)
+    qr2 = _cholqr2_qr(sa) if sa.is_cuda else None
+    R = qr2[1] if qr2 is not None else torch.linalg.qr(sa, mode="reduced")[1]
     # guard rank deficiency: columns with a vanishing pivot are regularised
     diag = R.diagonal().abs()
     if float(diag.min()) <= DEFAULT_RANK_TOL * float(diag.max()):
@@ -809,7 +873,8 @@ def sketch_precondition_lsqr(a, b, tm_psi, *, atol: float = 1e-6, btol: float = 
     # (sk_lsqr_step_f32_f64), one all-reduce of [A^T u, ||u||^2] per iteration when distributed
     fused = _lsqr_fused_ok(A) and os.environ.get("SKETCH_B200_LSQR_FUSED", "1") != "0"
     if fused:
-        u = u.contiguous()
+        return _lsqr_fused_loop(A, u.contiguous(), v, R, alpha, beta, bnorm, red, atol, btol, iter_lim, kind,
+                                t_sketch)
     while itn < iter_lim:
         itn += 1
         if fused:
