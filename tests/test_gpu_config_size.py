@@ -16,6 +16,8 @@
   host with the same Omega; ||A - QB|| / ||A|| and the rank-100 truncation error within 1e-2
   relative.  The float64 products use a dense copy of Omega with BLAS (the sparse
   `csc_matvecs` path is single-threaded: ~70 s at this size, App. B); same arithmetic up to rounding.
+* float64 (the reference's dtype) at the config-2 (WHT and DCT), config-3 and config-5 shapes: row
+  samples from several tiles against the oracle at 1e-12.
 """
 
 import numpy as np
@@ -189,3 +191,37 @@ def test_config3_sketch_full(cuda):
     assert err <= 1e-5, err
     rows = np.r_[0:8, 65536:65544, n - 8:n]
     assert rel_err(y[rows].cpu().numpy(), orc.csr_right(csr, a[rows].cpu().numpy())) <= 1e-5
+
+
+def test_float64_config_shapes_vs_oracle(cuda):
+    """The reference's own dtype at the BASELINE shapes (what a NumPy float64 caller runs): config-2
+    SRTT with the WHT (K3) and with the DCT default (K3b), config-3 sparse sign (K1r row slabs) and
+    config-5 Khatri-Rao (K5d, the tile synthesised from the factors) — row samples from several tiles
+    against the oracle at 1e-12."""
+    import torch
+
+    rows = np.r_[0:16, 20000:20008, -16:0]
+
+    def check(tm, n, d, ref_fn, seed):
+        g = torch.Generator(device=cuda).manual_seed(seed)
+        a = torch.randn(n, d, dtype=torch.float64, device=cuda, generator=g)
+        y = tm.apply_right(a)
+        idx = rows % n
+        got = y[torch.as_tensor(idx, device=cuda)].cpu().numpy()
+        ref = ref_fn(a[torch.as_tensor(idx, device=cuda)].cpu().numpy())
+        assert rel_err(got, ref) <= 1e-12, type(tm).__name__
+        del a, y
+        torch.cuda.empty_cache()
+
+    tm = skb.SparseRttTM(8192, 512, 1, "wht", seed=0)
+    dv, samp = orc.srtt_parts(8192, 512, 1, 0)
+    check(tm, 65536, 8192, lambda x: orc.srtt_right(dv, samp, x, "wht"), 1)
+    tm = skb.SparseRttTM(8192, 512, 1, "dct", seed=0)
+    check(tm, 32768, 8192, lambda x: orc.srtt_right(dv, samp, x, "dct"), 2)
+    tm = skb.SparseUniformTM(16384, 200, 8, seed=0)
+    csr = orc.sparse_uniform_csr(16384, 200, 8, 0)
+    assert len(tm._ring_on(cuda)[0]) > 1  # row slabs
+    check(tm, 65536, 16384, lambda x: orc.csr_right(csr, x), 3)
+    tm = skb.KhatriRaoTM(256, 2, 512, "real_rademacher", seed=0)
+    fac = orc.kr_factors(256, 2, 512, 0)
+    check(tm, 8192, 65536, lambda x: orc.kr_right(fac, x), 4)
