@@ -45,21 +45,47 @@ __device__ __forceinline__ C2<T> csub(C2<T> a, C2<T> b) {
   return {a.x - b.x, a.y - b.y};
 }
 
-// e^{2 pi i j / 32}, j < 32 (twiddles of the in-register DFTs, R | 32)
-__constant__ double kW32c[32] = {
-    1.0, 0.9807852804032304, 0.9238795325112867, 0.8314696123025452, 0.7071067811865476, 0.5555702330196023,
-    0.38268343236508984, 0.19509032201612833, 0.0, -0.1950903220161282, -0.3826834323650897, -0.555570233019602,
-    -0.7071067811865475, -0.8314696123025453, -0.9238795325112867, -0.9807852804032304, -1.0, -0.9807852804032304,
-    -0.9238795325112868, -0.8314696123025455, -0.7071067811865477, -0.5555702330196022, -0.38268343236509034,
-    -0.19509032201612866, 0.0, 0.1950903220161283, 0.38268343236509, 0.5555702330196018, 0.7071067811865474,
-    0.8314696123025452, 0.9238795325112865, 0.9807852804032303};
-__constant__ double kW32s[32] = {
-    0.0, 0.19509032201612825, 0.3826834323650898, 0.5555702330196022, 0.7071067811865475, 0.8314696123025452,
-    0.9238795325112867, 0.9807852804032304, 1.0, 0.9807852804032304, 0.9238795325112867, 0.8314696123025455,
-    0.7071067811865476, 0.5555702330196022, 0.3826834323650899, 0.1950903220161286, 0.0, -0.19509032201612836,
-    -0.38268343236508967, -0.555570233019602, -0.7071067811865475, -0.8314696123025452, -0.9238795325112865,
-    -0.9807852804032303, -1.0, -0.9807852804032304, -0.9238795325112866, -0.8314696123025455, -0.7071067811865477,
-    -0.5555702330196022, -0.3826834323650904, -0.19509032201612872};
+// a * e^{2 pi i e / 32} with e a compile-time constant after unrolling: quarter turns are swaps and
+// negations, odd multiples of pi/4 two multiplies, the rest a complex multiply by literals
+template <typename T>
+__device__ __forceinline__ C2<T> mul_w32(C2<T> a, int e) {
+  constexpr double r2 = 0.70710678118654752440;
+  switch (e & 31) {
+    case 0: return a;
+    case 8: return {-a.y, a.x};
+    case 16: return {-a.x, -a.y};
+    case 24: return {a.y, -a.x};
+    case 4: return {(T)r2 * (a.x - a.y), (T)r2 * (a.x + a.y)};
+    case 12: return {(T)(-r2) * (a.x + a.y), (T)r2 * (a.x - a.y)};
+    case 20: return {(T)r2 * (a.y - a.x), (T)(-r2) * (a.x + a.y)};
+    case 28: return {(T)r2 * (a.x + a.y), (T)r2 * (a.y - a.x)};
+    case 1: return cmul(a, C2<T>{(T)(0.9807852804032304), (T)(0.19509032201612825)});
+    case 2: return cmul(a, C2<T>{(T)(0.9238795325112867), (T)(0.3826834323650898)});
+    case 3: return cmul(a, C2<T>{(T)(0.8314696123025452), (T)(0.5555702330196022)});
+    case 5: return cmul(a, C2<T>{(T)(0.5555702330196023), (T)(0.8314696123025452)});
+    case 6: return cmul(a, C2<T>{(T)(0.38268343236508984), (T)(0.9238795325112867)});
+    case 7: return cmul(a, C2<T>{(T)(0.19509032201612833), (T)(0.9807852804032304)});
+    case 9: return cmul(a, C2<T>{(T)(-0.1950903220161282), (T)(0.9807852804032304)});
+    case 10: return cmul(a, C2<T>{(T)(-0.3826834323650897), (T)(0.9238795325112867)});
+    case 11: return cmul(a, C2<T>{(T)(-0.555570233019602), (T)(0.8314696123025455)});
+    case 13: return cmul(a, C2<T>{(T)(-0.8314696123025453), (T)(0.5555702330196022)});
+    case 14: return cmul(a, C2<T>{(T)(-0.9238795325112867), (T)(0.3826834323650899)});
+    case 15: return cmul(a, C2<T>{(T)(-0.9807852804032304), (T)(0.1950903220161286)});
+    case 17: return cmul(a, C2<T>{(T)(-0.9807852804032304), (T)(-0.19509032201612836)});
+    case 18: return cmul(a, C2<T>{(T)(-0.9238795325112868), (T)(-0.38268343236508967)});
+    case 19: return cmul(a, C2<T>{(T)(-0.8314696123025455), (T)(-0.555570233019602)});
+    case 21: return cmul(a, C2<T>{(T)(-0.5555702330196022), (T)(-0.8314696123025452)});
+    case 22: return cmul(a, C2<T>{(T)(-0.38268343236509034), (T)(-0.9238795325112865)});
+    case 23: return cmul(a, C2<T>{(T)(-0.19509032201612866), (T)(-0.9807852804032303)});
+    case 25: return cmul(a, C2<T>{(T)(0.1950903220161283), (T)(-0.9807852804032304)});
+    case 26: return cmul(a, C2<T>{(T)(0.38268343236509), (T)(-0.9238795325112866)});
+    case 27: return cmul(a, C2<T>{(T)(0.5555702330196018), (T)(-0.8314696123025455)});
+    case 29: return cmul(a, C2<T>{(T)(0.8314696123025452), (T)(-0.5555702330196022)});
+    case 30: return cmul(a, C2<T>{(T)(0.9238795325112865), (T)(-0.3826834323650904)});
+    case 31: return cmul(a, C2<T>{(T)(0.9807852804032303), (T)(-0.19509032201612872)});
+    default: return a;
+  }
+}
 
 __host__ __device__ constexpr int bitrev(int v, int bits) {
   int r = 0;
@@ -82,7 +108,7 @@ __device__ __forceinline__ void dft_inv_dif(C2<T> (&x)[R]) {
         x[b + j] = cadd(a, c);
         const C2<T> dlt = csub(a, c);
         const int e = j * (32 / (2 * span));  // W_{2 span}^j = W_32^(j * 32 / (2 span))
-        x[b + j + span] = e ? cmul(dlt, C2<T>{(T)kW32c[e], (T)kW32s[e]}) : dlt;
+        x[b + j + span] = mul_w32(dlt, e);
       }
     }
   }
