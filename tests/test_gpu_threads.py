@@ -28,6 +28,13 @@ def _cases(cuda):
                 torch.randn(2000, 4096, device=cuda, dtype=torch.float32, generator=g)))
     out.append((skb.GaussianTM(1024, 200, seed=2), torch.randn(1500, 1024, device=cuda, dtype=torch.float32,
                                                                 generator=g)))
+    # float64: the DMMA engine (K5d) and the fused DCT kernel (K3b); a complex Khatri-Rao (planes)
+    out.append((skb.GaussianTM(2048, 96, seed=3), torch.randn(700, 2048, device=cuda, dtype=torch.float64,
+                                                               generator=g)))
+    out.append((skb.SparseRttTM(4096, 64, 2, "dct", seed=4), torch.randn(900, 4096, device=cuda,
+                                                                         dtype=torch.float64, generator=g)))
+    out.append((skb.KhatriRaoTM(32, 2, 80, seed=5), torch.randn(300, 1024, device=cuda, dtype=torch.float64,
+                                                                 generator=g)))
     return out
 
 
