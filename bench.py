@@ -57,7 +57,7 @@ def _cfg1(torch, dev, rank):
     tm = make()
     g = torch.Generator(device=dev).manual_seed(2000 + rank)
     a = torch.randn(n, d, dtype=torch.float64, device=dev, generator=g)
-    return dict(name="cfg1", tm=tm, make=make, a=a, n=n, d=d, k=k, launches=1, kernel="sparse_right_ring_kernel",
+    return dict(name="cfg1", tm=tm, make=make, a=a, n=n, d=d, k=k, launches=1, kernel="sparse_right_cols_kernel",
                 workload="cfg1 sparse sign Y=A*Omega: A 16384x4096 f64, zeta=4, k=256", op="right")
 
 

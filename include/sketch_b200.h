@@ -106,6 +106,31 @@ SK_API int sk_sparse_right_ring_slab(const double* A, int64_t n, int64_t d, int6
                                      int64_t ldy, int accumulate, void* ws, size_t ws_bytes, void* stream);
 
 /*
+ * K1c — Y[n,k] (=, or += with `accumulate`) scale * A * Omega for a sparse-sign Omega with lanes =
+ * output columns: each lane holds its column's whole list of Omega entries in registers (half byte
+ * offsets into a row of A, sign in bit 31) and one thread streams pairs of whole rows of A into a
+ * shared-memory ring (cp.async.bulk).  Replaces `_SparseTM.apply_right` (src/sketch/sparse.py:63-66)
+ * for float32 / float64 A (BASELINE config 1).  Columns go 256 per CTA group (groups =
+ * sk_sparse_right_cols_groups(k)); colmap [groups*256] (lane -> column, -1 none), tw [groups*8]
+ * (positions per warp, multiples of 8) and ent [groups*8][maxp][32] come from
+ * sk_sparse_right_cols_encode over the (row, column, neg) triplets of Omega (host arrays): call it
+ * with ent = NULL to get `need` (the longest warp's positions), pick maxp in {32, 64, 96, 128} >=
+ * need, then call again with ent.  The encoder orders each lane's list so that the lanes of one
+ * 128-byte wavefront read distinct bank slots where possible (Omega is fixed, so this is paid once).
+ * A 16-byte aligned with 16-byte aligned rows, d * sizeof(T) a multiple of 16; an Omega whose
+ * lists exceed maxp = 128 runs as row slabs of Omega (A offset to the slab, accumulate = 1 after
+ * the first).
+ */
+SK_API int sk_sparse_right_cols_groups(int64_t k);
+SK_API int sk_sparse_right_cols_supported(int dtype, int64_t d, int64_t k, int32_t maxp);
+SK_API int sk_sparse_right_cols_encode(int dtype, int64_t d, int64_t k, int64_t nnz, const int64_t* rows,
+                                       const int64_t* cols, const uint8_t* neg, int32_t maxp, uint32_t* ent,
+                                       int32_t* colmap, int32_t* tw, int32_t* need);
+SK_API int sk_sparse_right_cols(int dtype, const void* A, int64_t n, int64_t d, int64_t lda, const uint32_t* ent,
+                                const int32_t* colmap, const int32_t* tw, int64_t k, int32_t maxp, double scale,
+                                void* Y, int64_t ldy, int accumulate, void* stream);
+
+/*
  * K1s — Y[n,k] = scale * A * Omega for a sparse A in CSR (int64 indptr[n+1], int32 indices, values
  * of `dtype`) and a sparse-sign Omega given by rows: int32 indptr[d+1] and int32 entries
  * `c | neg << 31` (magnitude folded into `scale`). A is never densified. Replaces

@@ -92,6 +92,12 @@ SIGNATURES = {
                                       _c_p, _c_size, _c_p]),
     "sk_sparse_right_ring_slab": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_i64, _c_dbl, _c_p,
                                            _c_i64, _c_int, _c_p, _c_size, _c_p]),
+    "sk_sparse_right_cols_groups": (_c_int, [_c_i64]),
+    "sk_sparse_right_cols_supported": (_c_int, [_c_int, _c_i64, _c_i64, ctypes.c_int32]),
+    "sk_sparse_right_cols_encode": (_c_int, [_c_int, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, ctypes.c_int32, _c_p,
+                                             _c_p, _c_p, _c_p]),
+    "sk_sparse_right_cols": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_i64, ctypes.c_int32,
+                                      _c_dbl, _c_p, _c_i64, _c_int, _c_p]),
     "sk_two_sided_workspace_bytes": (_c_size, [_c_i64, _c_i64, _c_i64, _c_int]),
     "sk_two_sided_sketch": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_i64, _c_dbl, _c_p,
                                      ctypes.c_int32, _c_i64, _c_dbl, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_size,

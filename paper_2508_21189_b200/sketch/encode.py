@@ -12,11 +12,13 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = ["bcsc_encode", "bcsc_decode", "bcsc_segments", "srtt_sampler_encode", "sign_bits", "wide_encode_device",
-           "gather_encode", "ring_encode", "ring_decode"]
+           "gather_encode", "ring_encode", "ring_decode", "cols_encode", "COLS_MAXP"]
 
 RING_RC = 64     # rows of Omega per stage of the K1r ring kernel (sparse_right_ring.cu RC)
 RING_UC = 128    # rows of Omega per consumer unit (two stages, sparse_right_ring.cu UC)
 RING_WARPS = 16  # consumer warps (NCONS), 16 output columns each (CPW)
+
+COLS_MAXP = (32, 64, 96, 128)  # list positions per lane the K1c kernel is built for (sparse_right_cols.cu)
 
 ADJ_GROUP = 1024  # output rows per CTA group of the adjoint fast path (sparse_adjoint.cu V2_CG)
 PTR_PAD = 1028    # ints the fast path may read past the pointer array
@@ -238,3 +240,38 @@ def ring_decode(lists, seg, d: int, k: int):
         out_c.append(cols)
         out_n.append((ents & 1).astype(bool))
     return np.concatenate(out_r), np.concatenate(out_c), np.concatenate(out_n)
+
+
+def cols_encode(lib, code: int, rows, cols, neg, d: int, k: int):
+    """(rows, cols, neg) triplets -> K1c encoding (ent uint32[groups*8, maxp, 32], colmap int32[groups*256],
+    tw int32[groups*8], maxp) through sk_sparse_right_cols_encode, or None when the longest warp needs
+    more than 128 positions (the caller cuts Omega into row slabs).
+
+    Lane l of warp w computes column colmap[32 w + l]; ent[w, t, l] is half the byte offset into a row
+    of A of that lane's t-th entry with its sign in bit 31 (the kernel forms base + 2 * ent, which
+    drops the sign bit) (t < tw[w]; positions past a lane's list read
+    the zeroed pad after the row).  Columns are dealt to lanes by decreasing list length and each
+    lane's order is chosen so that lanes of one 128-byte wavefront read distinct bank slots.
+    """
+    import ctypes
+
+    from .. import _lib
+
+    rows = np.ascontiguousarray(rows, dtype=np.int64).ravel()
+    cols = np.ascontiguousarray(cols, dtype=np.int64).ravel()
+    neg = np.ascontiguousarray(neg, dtype=np.uint8).ravel()
+    groups = int(lib.sk_sparse_right_cols_groups(k))
+    colmap = np.empty(groups * 256, np.int32)
+    tw = np.empty(groups * 8, np.int32)
+    need = ctypes.c_int32(0)
+    args = (code, d, k, rows.size, rows.ctypes.data, cols.ctypes.data, neg.ctypes.data)
+    st = lib.sk_sparse_right_cols_encode(*args, 0, None, colmap.ctypes.data, tw.ctypes.data, ctypes.byref(need))
+    _lib.check(st, "sk_sparse_right_cols_encode")
+    maxp = next((m for m in COLS_MAXP if m >= need.value), None)
+    if maxp is None:
+        return None
+    ent = np.empty(groups * 8 * maxp * 32, np.uint32)
+    st = lib.sk_sparse_right_cols_encode(*args, maxp, ent.ctypes.data, colmap.ctypes.data, tw.ctypes.data,
+                                         ctypes.byref(need))
+    _lib.check(st, "sk_sparse_right_cols_encode")
+    return ent.reshape(groups * 8, maxp, 32), colmap, tw, maxp

@@ -16,7 +16,8 @@ import numpy as np
 
 from .. import _lib
 from ..devrng import DevicePhilox, device_draws_enabled
-from .encode import (ENT_PAD, PTR_PAD, RING_UC, RING_WARPS, bcsc_encode, bcsc_segments, gather_encode, ring_encode,
+from .encode import (ENT_PAD, PTR_PAD, RING_UC, RING_WARPS, bcsc_encode, bcsc_segments, cols_encode, gather_encode,
+                     ring_encode,
                      wide_encode_device)
 from .tensorcore import bt_from_triplets, dense_right_tc
 from .testmatrix import TestMatrix, entry_sample
@@ -171,6 +172,11 @@ class _SignSparseTM(TestMatrix):
             hi, lo, mag = self._tc_on(a.device)
             return dense_right_tc(a, hi, lo, self.k, mag)
         code = _lib.SK_F32 if a.dtype == torch.float32 else _lib.SK_F64
+        cols = self._cols_on(a.device, code)
+        if cols is not None:
+            y = self._right_cols(a, cols, code)
+            if y is not None:
+                return y
         ring = self._ring_on(a.device) if code == _lib.SK_F64 else None
         if ring is not None:
             return self._right_ring(a, ring)
@@ -185,6 +191,68 @@ class _SignSparseTM(TestMatrix):
                                      ent.numel(), self.k, mag, y.data_ptr(), y.stride(0),
                                      torch.cuda.current_stream().cuda_stream)
         _lib.check(st, "sk_sparse_right")
+        return y
+
+    def _cols_on(self, device, code):
+        """K1c encoding (lanes = output columns, sparse_right_cols.cu), cached per device and dtype: a
+        list of up to 4 row slabs of Omega (s0, width, ent, colmap, tw, maxp) — one slab unless a
+        column's list exceeds 128 entries or a row of A exceeds the shared-memory ring — and the
+        magnitude; None when the kernel does not take this operator (SKETCH_B200_K1=ring / classic
+        select the older kernels)."""
+        import os
+
+        import torch
+
+        key = ("cols", device, code)
+        if key not in self._device_cache:
+            res = None
+            if os.environ.get("SKETCH_B200_K1", "cols") == "cols":
+                lib = _lib.load()
+                rows, cols, neg, mag = self._sign_form()
+                es = 8 if code == _lib.SK_F64 else 4
+                nslab = 1
+                # beyond 4 slabs (lists of > ~400 entries per column) the Y re-reads and the spilling
+                # 128-position variant lose to K1r's per-unit walk (tools/k1c_probe.py)
+                while res is None and nslab <= 4 and (self.d * es) % 16 == 0:
+                    # slab boundaries on multiples of 8 columns of A (16-byte aligned slab starts)
+                    cuts = sorted({min(self.d, (self.d * i // nslab) // 8 * 8) for i in range(nslab)} | {self.d})
+                    slabs = []
+                    for s0, s1 in zip(cuts[:-1], cuts[1:]):
+                        m = (rows >= s0) & (rows < s1)
+                        enc = cols_encode(lib, code, rows[m] - s0, cols[m], neg[m], s1 - s0, self.k)
+                        if enc is None or not lib.sk_sparse_right_cols_supported(code, s1 - s0, self.k, enc[3]):
+                            slabs = None
+                            break
+                        ent, colmap, tw, maxp = enc
+                        slabs.append((s0, s1 - s0, torch.from_numpy(ent.view(np.int32)).to(device),
+                                      torch.from_numpy(colmap).to(device), torch.from_numpy(tw).to(device), maxp))
+                    if slabs:
+                        res = (slabs, mag)
+                    nslab *= 2
+            self._device_cache[key] = res
+        return self._device_cache[key]
+
+    def _right_cols(self, a, plan, code):
+        """Y = A Omega through K1c (slabs in order, Y = then Y +=); None when A's rows are not 16-byte
+        aligned (the caller takes K1r / K1)."""
+        import torch
+
+        slabs, mag = plan
+        es = a.element_size()
+        if a.stride(1) != 1 or a.data_ptr() % 16 or (a.stride(0) * es) % 16:
+            return None
+        n = a.shape[0]
+        y = torch.empty((n, self.k), dtype=a.dtype, device=a.device)
+        if n == 0:
+            return y
+        lib = _lib.load()
+        with torch.cuda.device(a.device):
+            stream = torch.cuda.current_stream().cuda_stream
+            for i, (s0, width, ent, colmap, tw, maxp) in enumerate(slabs):
+                st = lib.sk_sparse_right_cols(code, a.data_ptr() + es * s0, n, width, a.stride(0), ent.data_ptr(),
+                                              colmap.data_ptr(), tw.data_ptr(), self.k, maxp, mag, y.data_ptr(),
+                                              y.stride(0), 1 if i else 0, stream)
+                _lib.check(st, "sk_sparse_right_cols")
         return y
 
     def _ring_on(self, device):
