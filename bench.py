@@ -96,7 +96,7 @@ def _cfg5(torch, dev, rank):
     tm = make()
     g = torch.Generator(device=dev).manual_seed(5000 + rank)
     a = torch.randn(n, d, dtype=torch.float32, device=dev, generator=g)
-    return dict(name="cfg5", tm=tm, make=make, a=a, n=n, d=d, k=k, launches=None, kernel="dense_tc_pair_kernel<1,0,1> (sk_kr_right: F resident, Omega never formed)",
+    return dict(name="cfg5", tm=tm, make=make, a=a, n=n, d=d, k=k, launches=None, kernel="dense_tc_pair_kernel<1,0,1> (sk_kr_right_signs: F resident, +-1 weights as sign bits, Omega never formed)",
                 flops=2.0 * n * d * k, flops_executed_x=2,
                 workload="cfg5 Khatri-Rao sketch: A 16384x65536 f32, ell=2, d0=256, k=512", op="right")
 

@@ -319,6 +319,14 @@ SK_API size_t sk_kr_workspace_bytes(int64_t n, int64_t P, int64_t dl, int64_t k,
 SK_API int sk_kr_right(const float* A, int64_t n, int64_t P, int64_t dl, int64_t lda, const uint16_t* Ft_hi,
                        const uint16_t* Ft_lo, int64_t ldf, const float* W, int64_t ldw, int64_t k, double scale,
                        float* Y, int64_t ldy, void* ws, size_t ws_bytes, void* stream);
+/* sk_kr_right with +-1 column weights (W[P,j] = wabs * (1 - 2 bit), bit j % 32 of
+ * Wbits[P * ldwb + j / 32]; e.g. BASELINE config 5's Rademacher factors): the reducer warps prefetch a
+ * chunk's 128 sign bits one chunk ahead instead of loading 128 float weights per chunk.  W (the same
+ * weights as float32) is still required; N blocks not starting on 32-column boundaries use it. */
+SK_API int sk_kr_right_signs(const float* A, int64_t n, int64_t P, int64_t dl, int64_t lda, const uint16_t* Ft_hi,
+                             const uint16_t* Ft_lo, int64_t ldf, const float* W, int64_t ldw, const uint32_t* Wbits,
+                             int64_t ldwb, double wabs, int64_t k, double scale, float* Y, int64_t ldy, void* ws,
+                             size_t ws_bytes, void* stream);
 /*
  * K4 adjoint — X[k,m] = scale * Omega^T B for B [P*dl rows][m] float32 (row stride ldb), read in
  * place (no transposed copy).  Replaces `KhatriRaoTM.apply_adjoint` (src/sketch/khatri_rao.py:147-156).

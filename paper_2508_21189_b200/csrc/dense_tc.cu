@@ -63,6 +63,12 @@ struct TcParams {
   //         chunk folded with the column weights W[P][col] (the product of the other factors' rows).
   const float* kr_w;
   int64_t kr_ldw;
+  // +-1 column weights (every W[P][col] = +-wabs, wabs folded into scale): bit col % 32 of
+  // kr_wbits[P * kr_ldwb + col / 32] set when negative; NULL = the float32 weights above.  The
+  // reducers load a chunk's 128 bits per warp (four words, issued before the accumulator wait)
+  // instead of waiting on a float load per group of 16 columns.
+  const uint32_t* kr_wbits;
+  int64_t kr_ldwb;
   int kr_qb;       // k-blocks per P (ceil(dl / 64))
   int kr_ngroups;  // N blocks, one per group of pairs (each pair keeps one N block)
   int out_t;       // result transposed: element (row, col) -> Y[col * ldy + row] (through the reduce)
@@ -88,6 +94,21 @@ __device__ __forceinline__ void sts128u(uint32_t addr, uint32_t a, uint32_t b, u
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
+__device__ __forceinline__ uint32_t ldg_nc_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+// the sign words of columns col .. col + 127 of one weight row (words past the slab's n columns: 0)
+__device__ __forceinline__ uint4 ldg_wbits(const uint32_t* row, int col, int n) {
+  uint4 v = make_uint4(0u, 0u, 0u, 0u);
+  const uint32_t* q = row + (col >> 5);
+  if (col < n) v.x = ldg_nc_u32(q);
+  if (col + 32 < n) v.y = ldg_nc_u32(q + 1);
+  if (col + 64 < n) v.z = ldg_nc_u32(q + 2);
+  if (col + 96 < n) v.w = ldg_nc_u32(q + 3);
+  return v;
+}
 __device__ __forceinline__ float4 ldg_nc_v4(const float4* p) {
   float4 v;
   asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
@@ -643,11 +664,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       float sum[kMaxBNH];
 #pragma unroll
       for (int j = 0; j < kMaxBNH; ++j) sum[j] = 0.f;
+      // KR = 1 with +-1 weights: the chunk's sign words for columns col0 .. col0 + 127 (col0 is a
+      // multiple of 32 whenever kr_wbits is set), loaded before the wait for the chunk's accumulator
+      const bool wsign = KR == 1 && p.kr_wbits != nullptr;
       for (int c0 = kb0; c0 < kb1; c0 += cqb, ++chunk_seq) {
         const uint32_t buf = chunk_seq & 1, use = chunk_seq >> 1;
+        uint4 wb = make_uint4(0u, 0u, 0u, 0u);
+        if (wsign) wb = ldg_wbits(p.kr_wbits + (int64_t)(c0 / qb) * p.kr_ldwb, col0, p.N);
         mbar_wait(&acc_full[buf], use & 1);
         tc_fence_after();
         const uint32_t base = tmem + ((uint32_t)(32 * lg) << 16) + buf * (uint32_t)p.BN + hoff;
+        if (wsign) {
+#pragma unroll
+          for (int g = 0; g < kMaxBNH / 16; ++g) {
+            if (g * 16 < bnh) {
+              uint32_t r[16];
+              tmem_ld16(base + g * 16, r);
+              const uint32_t word = (g >> 1) == 0 ? wb.x : (g >> 1) == 1 ? wb.y : (g >> 1) == 2 ? wb.z : wb.w;
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const int bit = (g & 1) * 16 + j;
+                sum[g * 16 + j] += __uint_as_float(r[j] ^ ((word << (31 - bit)) & 0x80000000u));
+              }
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote(acc_empty_leader + 8u * buf);
+          continue;
+        }
         // KR = 1: the chunk's column weights W[P][col0 ...] (the same address in every lane: broadcast)
         const float4* wrow = nullptr;
         if constexpr (KR == 1) wrow = reinterpret_cast<const float4*>(p.kr_w + (int64_t)(c0 / qb) * p.kr_ldw + col0);
@@ -1017,7 +1063,8 @@ size_t kr_workspace(int64_t n, int64_t P, int64_t dl, int64_t k, int NB, bool ta
 // rows: output rows (A rows, or B columns when TA); out: Y [rows][k] (ldy) or, when TA, X [k][rows]
 int kr_run(bool TA, const float* A, int64_t rows, int64_t P, int64_t dl, int64_t lda, const uint16_t* ft_hi,
            const uint16_t* ft_lo, int64_t ldf, const float* W, int64_t ldw, int64_t k, double scale, float* Y,
-           int64_t ldy, void* ws, size_t ws_bytes, cudaStream_t s, const char* what) {
+           int64_t ldy, void* ws, size_t ws_bytes, cudaStream_t s, const char* what,
+           const uint32_t* wbits = nullptr, int64_t ldwb = 0, double wabs = 1.0) {
   const int NB = ft_lo ? 2 : 1;
   CUtensorMap ma;
   // dl % 64 == 0: the plain 2-D map (measured faster than the 3-D box: config 5 2.14 -> 1.87 ms)
@@ -1080,6 +1127,13 @@ int kr_run(bool TA, const float* A, int64_t rows, int64_t P, int64_t dl, int64_t
     p.mtiles = pl.mtiles;
     p.kr_w = W + c0;
     p.kr_ldw = ldw;
+    // sign-bit weights when every reducer half starts on a 32-column boundary (16-byte word loads)
+    const bool use_bits = wbits != nullptr && pl.BN % 64 == 0 && c0 % 32 == 0;
+    if (use_bits) {
+      p.kr_wbits = wbits + c0 / 32;
+      p.kr_ldwb = ldwb;
+      p.scale = (float)(scale * wabs);
+    }
     p.kr_qb = pl.qb;
     p.kr_ngroups = pl.nblocks;
     p.out_t = TA ? 1 : 0;
@@ -1390,6 +1444,22 @@ extern "C" int sk_kr_right(const float* A, int64_t n, int64_t P, int64_t dl, int
   if (st != SK_OK || n == 0) return st;
   return kr_run(false, A, n, P, dl, lda, Ft_hi, Ft_lo, ldf, W, ldw, k, scale, Y, ldy, ws, ws_bytes, as_stream(stream),
                 "sk_kr_right");
+}
+
+// sk_kr_right with +-1 column weights given as sign bits (W[P, j] = wabs * (1 - 2 * bit)), e.g. the
+// Rademacher factors of BASELINE config 5; W (float32, the same values) serves N blocks that do not
+// start on 32-column boundaries.
+extern "C" int sk_kr_right_signs(const float* A, int64_t n, int64_t P, int64_t dl, int64_t lda, const uint16_t* Ft_hi,
+                                 const uint16_t* Ft_lo, int64_t ldf, const float* W, int64_t ldw, const uint32_t* Wbits,
+                                 int64_t ldwb, double wabs, int64_t k, double scale, float* Y, int64_t ldy, void* ws,
+                                 size_t ws_bytes, void* stream) {
+  using namespace skb;
+  int st = kr_check(A, n, P, dl, lda, P * dl, k, Y, ldy, k, "sk_kr_right_signs");
+  if (st == SK_OK && (!Wbits || ldwb < (k + 31) / 32)) st = fail(SK_EINVAL, "sk_kr_right_signs: bad sign words");
+  if (st == SK_OK) st = kr_check_f(Ft_hi, Ft_lo, ldf, dl, W, ldw, k, "sk_kr_right_signs");
+  if (st != SK_OK || n == 0) return st;
+  return kr_run(false, A, n, P, dl, lda, Ft_hi, Ft_lo, ldf, W, ldw, k, scale, Y, ldy, ws, ws_bytes, as_stream(stream),
+                "sk_kr_right_signs", Wbits, ldwb, wabs);
 }
 
 // X[k, m] = scale * Omega^T B for B [P * dl rows][m] (row stride ldb), read in place (no transposed copy)

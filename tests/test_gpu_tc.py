@@ -108,6 +108,26 @@ def test_khatri_rao_config5_full(cuda):
     assert rel_err(y[rows].cpu().numpy(), ref_o) <= 1e-5
 
 
+@pytest.mark.parametrize("d0,ell,k", [(256, 2, 512), (16, 2, 48), (4, 4, 600), (5, 2, 70), (64, 2, 100)])
+def test_khatri_rao_sign_bits_match_float_weights(d0, ell, k, cuda, monkeypatch):
+    """sk_kr_right_signs (+-1 weights as sign bits) against sk_kr_right (float32 weights): the fold
+    adds +-z either way, so the results agree bit for bit; both against the oracle."""
+    import torch
+
+    tm = skb.KhatriRaoTM(d0, ell, k, "real_rademacher", seed=3)
+    if tm.right_path(torch.float32) != "tc":
+        pytest.skip("not a tensor-core shape")
+    assert tm._tc_operands(cuda)[5] is not None
+    rng = np.random.default_rng(k)
+    a = torch.from_numpy(rng.standard_normal((300, d0 ** ell)).astype(np.float32)).to(cuda)
+    y = tm.apply_right(a)
+    monkeypatch.setenv("SKETCH_B200_KR_SIGNS", "0")
+    y0 = tm.apply_right(a)
+    assert torch.equal(y, y0)
+    ref = orc.kr_right(orc.kr_factors(d0, ell, k, 3), a.cpu().numpy())
+    assert rel_err(y.double().cpu().numpy(), ref) <= 1e-5
+
+
 def test_khatri_rao_config5_adjoint_in_place(cuda):
     """Omega^T B for a tall B (65536 x 40) read in place by the transposing KR kernel."""
     import torch
