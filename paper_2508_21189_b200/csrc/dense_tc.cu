@@ -44,7 +44,8 @@ constexpr int BK = 64;               // bf16 elements per 128-byte swizzle row
 constexpr int CHUNK_KB = 16;         // k-blocks accumulated in TMEM before a register fold
 constexpr int kThreads = 512;
 constexpr uint32_t kAStageBytes = BM * BK * 4;  // fp32 A staging tile (TMA, no swizzle): 32 KB
-constexpr int kMaxBNH = 128;         // columns per reducer thread (BN <= 256)
+constexpr int kMaxBNH = 128;
+constexpr int kKrLag = 8;             // KR lockstep: k-blocks a producer may run ahead of its partner         // columns per reducer thread (BN <= 256)
 
 struct TcParams {
   const float* A;
@@ -69,6 +70,10 @@ struct TcParams {
   // instead of waiting on a float load per group of 16 columns.
   const uint32_t* kr_wbits;
   int64_t kr_ldwb;
+  // KR with N-block groups: per-CTA count of A k-blocks its producer has issued (zeroed per launch);
+  // a producer stays within kKrLag k-blocks of the same-rank CTA of the next group's pair, which
+  // reads the same A tiles, so the second read of each tile is an L2 hit.  NULL: no lockstep.
+  int* kr_progress;
   int kr_qb;       // k-blocks per P (ceil(dl / 64))
   int kr_ngroups;  // N blocks, one per group of pairs (each pair keeps one N block)
   int out_t;       // result transposed: element (row, col) -> Y[col * ldy + row] (through the reduce)
@@ -451,17 +456,19 @@ template <int NB, bool TA, int KR>
 __global__ void __launch_bounds__(kThreads, 1)
     dense_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                          const __grid_constant__ CUtensorMap tm_blo, const TcParams p) {
+  // KR = 1: Khatri-Rao with float32 weights; KR = 3: the same with +-1 weights as sign bits
+  constexpr bool KR1 = KR == 1 || KR == 3;
   extern __shared__ uint8_t smem_dyn[];
   uint8_t* smem = smem_dyn + ((1024u - (sm100::smem_u32(smem_dyn) & 1023u)) & 1023u);
   const uint32_t a_bytes = BM * 128;
   const int bnh2 = p.BN >> 1;                      // B^T rows staged by each CTA
   const uint32_t bh_bytes = (uint32_t)bnh2 * 128;
   // stage = {A, B half (, B_lo half)}; KR = 1: stage = {A}, the B halves of all q blocks resident
-  const uint32_t stage_bytes = KR == 1 ? kAStageBytes : kAStageBytes + NB * bh_bytes;
+  const uint32_t stage_bytes = KR1 ? kAStageBytes : kAStageBytes + NB * bh_bytes;
   const int S = p.stages;
   const int qb = KR ? p.kr_qb : 1;
   uint8_t* resident = smem + (size_t)S * stage_bytes;  // KR = 1: [NB][qb] F^T tiles of bh_bytes
-  const uint32_t res_bytes = KR == 1 ? (uint32_t)NB * (uint32_t)qb * bh_bytes : 0u;
+  const uint32_t res_bytes = KR1 ? (uint32_t)NB * (uint32_t)qb * bh_bytes : 0u;
   uint64_t* tma_full = reinterpret_cast<uint64_t*>(resident + res_bytes);
   uint64_t* full = tma_full + S;       // leader: converted (and, KR = 2, synthesised) in both CTAs
   uint64_t* empty = full + S;          // consumed by the pair MMA (multicast commit)
@@ -474,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t rank = cluster_rank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const PairSched sc = pair_sched<KR>(p, pair, npairs);
-  const int cqb = KR == 1 ? qb : CHUNK_KB;  // k-blocks per TMEM chunk
+  const int cqb = KR1 ? qb : CHUNK_KB;  // k-blocks per TMEM chunk
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&tma_full[s], 1);
@@ -509,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     setmaxnreg_dec<48>();  // 128 x 48 + 128 x 128 + 256 x 168 = 64K registers
     if (warp == 0 && lane == 0) {
       // -------------------------------------------------------------- producer (this CTA's rows + B half)
-      if constexpr (KR == 1) {  // resident F^T half of N block sc.nb: qb tiles of 64 (q) x bnh2 (columns)
+      if constexpr (KR1) {  // resident F^T half of N block sc.nb: qb tiles of 64 (q) x bnh2 (columns)
         const int brow0 = sc.nb * p.BN + (int)rank * bnh2;
         mbar_arrive_expect_tx(res_full, res_bytes);
         for (int q = 0; q < qb; ++q) {
@@ -517,15 +524,43 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (NB == 2) tma_load_2d(resident + (size_t)(qb + q) * bh_bytes, &tm_blo, res_full, q * BK, brow0);
         }
       }
-      const uint32_t tx_bytes = KR == 1 ? kAStageBytes : stage_bytes;
+      const uint32_t tx_bytes = KR1 ? kAStageBytes : stage_bytes;
       int s = 0;
       uint32_t ph = 0;
+      // KR lockstep with the partner pair (same A rows, next N block)
+      int* my_prog = nullptr;
+      const volatile int* partner_prog = nullptr;
+      if (KR != 0 && p.kr_progress != nullptr && p.kr_ngroups > 1) {
+        const int partner = sc.first * p.kr_ngroups + (sc.nb + 1) % p.kr_ngroups;
+        if (partner < npairs && partner != pair) {
+          my_prog = p.kr_progress + blockIdx.x;
+          partner_prog = p.kr_progress + 2 * partner + (int)rank;
+        }
+      }
+      int issued = 0, partner_seen = 0;
       for (int t = sc.first; t < sc.count; t += sc.step) {
         const Unit w = pair_unit<KR>(p, sc, t);
         const int kb0 = w.ks * p.kb_per_split, kb1 = min(nk, kb0 + p.kb_per_split);
         const int row0 = (2 * w.mt + (int)rank) * BM;
         const int brow0 = w.nb * p.BN + (int)rank * bnh2;
         for (int kb = kb0; kb < kb1; ++kb) {
+          if (my_prog != nullptr) {
+            if ((issued & 3) == 0) *reinterpret_cast<volatile int*>(my_prog) = issued;
+            if (issued > partner_seen + kKrLag) {
+              // bounded wait: a partner that is not resident (another kernel holds its SM) must not
+              // hold this CTA, so after ~50 us without progress the lockstep is dropped
+              const long long t0 = clock64();
+              while (issued > (partner_seen = *partner_prog) + kKrLag) {
+                if (clock64() - t0 > 100000) {
+                  *reinterpret_cast<volatile int*>(my_prog) = 1 << 30;
+                  my_prog = nullptr;
+                  break;
+                }
+                __nanosleep(128);
+              }
+            }
+            ++issued;
+          }
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + (size_t)s * stage_bytes;
           mbar_arrive_expect_tx(&tma_full[s], tx_bytes);
@@ -545,6 +580,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++s == S) { s = 0; ph ^= 1; }
         }
       }
+      if (KR != 0 && p.kr_progress != nullptr)  // done (or lockstep dropped): never hold the partner
+        *reinterpret_cast<volatile int*>(p.kr_progress + blockIdx.x) = 1 << 30;
     } else if (warp == 1 && lane == 0 && rank == 0) {
       // -------------------------------------------------------------- MMA issuer (leader only)
       const uint32_t idesc = idesc_bf16_f32(2 * BM, p.BN);
@@ -565,8 +602,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const uint32_t st = sm100::smem_u32(smem + (size_t)s * stage_bytes);
             const uint32_t a_hi = st, a_lo = st + a_bytes;
-            const uint32_t b = KR == 1 ? sm100::smem_u32(resident) + (uint32_t)(kb - c0) * bh_bytes : st + kAStageBytes;
-            const uint32_t blo = KR == 1 ? b + (uint32_t)qb * bh_bytes : b + bh_bytes;
+            const uint32_t b = KR1 ? sm100::smem_u32(resident) + (uint32_t)(kb - c0) * bh_bytes : st + kAStageBytes;
+            const uint32_t blo = KR1 ? b + (uint32_t)qb * bh_bytes : b + bh_bytes;
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
               const uint64_t db = sdesc_kmajor_sw128(b + kk * 32);
@@ -590,7 +627,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int rsub = ct >> 4;
     // KR = 1: the leader's first MMA reads both CTAs' resident B halves; it waits for every converter
     // warp of both CTAs, so each CTA's converters first wait for their own CTA's resident half
-    if constexpr (KR == 1) mbar_wait(res_full, 0);
+    if constexpr (KR1) mbar_wait(res_full, 0);
     int s = 0;
     uint32_t ph = 0;
     for (int t = sc.first; t < sc.count; t += sc.step) {
@@ -666,7 +703,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < kMaxBNH; ++j) sum[j] = 0.f;
       // KR = 1 with +-1 weights: the chunk's sign words for columns col0 .. col0 + 127 (col0 is a
       // multiple of 32 whenever kr_wbits is set), loaded before the wait for the chunk's accumulator
-      const bool wsign = KR == 1 && p.kr_wbits != nullptr;
+      constexpr bool wsign = KR == 3;
       for (int c0 = kb0; c0 < kb1; c0 += cqb, ++chunk_seq) {
         const uint32_t buf = chunk_seq & 1, use = chunk_seq >> 1;
         uint4 wb = make_uint4(0u, 0u, 0u, 0u);
@@ -674,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&acc_full[buf], use & 1);
         tc_fence_after();
         const uint32_t base = tmem + ((uint32_t)(32 * lg) << 16) + buf * (uint32_t)p.BN + hoff;
-        if (wsign) {
+        if constexpr (wsign) {
 #pragma unroll
           for (int g = 0; g < kMaxBNH / 16; ++g) {
             if (g * 16 < bnh) {
@@ -986,7 +1023,10 @@ struct KrPlan {
 };
 
 using KernT = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams);
-KernT kr_kernel(int NB, bool TA) {
+KernT kr_kernel(int NB, bool TA, bool wsign = false) {
+  if (wsign)
+    return TA ? (NB == 2 ? dense_tc_pair_kernel<2, true, 3> : dense_tc_pair_kernel<1, true, 3>)
+              : (NB == 2 ? dense_tc_pair_kernel<2, false, 3> : dense_tc_pair_kernel<1, false, 3>);
   return TA ? (NB == 2 ? dense_tc_pair_kernel<2, true, 1> : dense_tc_pair_kernel<1, true, 1>)
             : (NB == 2 ? dense_tc_pair_kernel<2, false, 1> : dense_tc_pair_kernel<1, false, 1>);
 }
@@ -1046,6 +1086,7 @@ bool make_plan_kr(KrPlan& pl, int64_t n, int64_t P, int64_t dl, int64_t kslab, i
   return true;
 }
 
+constexpr size_t kKrProgressBytes = 2048;  // one int per CTA (<= 512 CTAs)
 size_t kr_workspace(int64_t n, int64_t P, int64_t dl, int64_t k, int NB, bool ta) {
   size_t ws = 0;
   for (int64_t c0 = 0; c0 < k; c0 += kKrMaxCols) {
@@ -1057,7 +1098,7 @@ size_t kr_workspace(int64_t n, int64_t P, int64_t dl, int64_t k, int NB, bool ta
     const size_t w = pl.ws_bytes > pl1.ws_bytes ? pl.ws_bytes : pl1.ws_bytes;
     if (w > ws) ws = w;
   }
-  return ws;
+  return ((ws + 255) & ~(size_t)255) + kKrProgressBytes;  // + the lockstep counters
 }
 
 // rows: output rows (A rows, or B columns when TA); out: Y [rows][k] (ldy) or, when TA, X [k][rows]
@@ -1072,12 +1113,15 @@ int kr_run(bool TA, const float* A, int64_t rows, int64_t P, int64_t dl, int64_t
   int st = a2d ? (TA ? make_at_map(&ma, A, rows, P * dl, lda) : make_a_map(&ma, A, rows, P * dl, lda))
                : make_a3_map(&ma, A, rows, P, dl, lda, TA);
   if (st != SK_OK) return st;
-  KernT kern = kr_kernel(NB, TA);
   for (int64_t c0 = 0; c0 < k; c0 += kKrMaxCols) {
     const int64_t kslab = k - c0 < kKrMaxCols ? k - c0 : kKrMaxCols;
     KrPlan pl;
     if (!make_plan_kr(pl, rows, P, dl, kslab, NB, -1, TA))
       return fail(SK_EUNSUPPORTED, std::string(what) + ": resident factor does not fit shared memory");
+    // sign-bit weights when every reducer half starts on a 32-column boundary (the BN of the first plan
+    // is the one launched: the second plan only changes the pair count and K split)
+    const bool use_bits = wbits != nullptr && pl.BN % 64 == 0 && c0 % 32 == 0;
+    KernT kern = kr_kernel(NB, TA, use_bits);
     // co-resident pairs per (kernel, smem) — a small cache guarded for concurrent host threads
     static std::mutex maxc_mu;
     static KernT maxc_kern[8] = {};
@@ -1099,6 +1143,14 @@ int kr_run(bool TA, const float* A, int64_t rows, int64_t P, int64_t dl, int64_t
     make_plan_kr(pl, rows, P, dl, kslab, NB, maxc, TA);
     if (pl.ws_bytes > 0 && (ws == nullptr || ws_bytes < pl.ws_bytes))
       return fail(SK_EINVAL, std::string(what) + ": workspace too small (sk_kr_workspace_bytes)");
+    // lockstep counters after the partials when the caller's workspace has room (sk_kr_workspace_bytes)
+    int* progress = nullptr;
+    const size_t prog_off = (pl.ws_bytes + 255) & ~(size_t)255;
+    if (ws != nullptr && pl.nblocks > 1 && 2 * pl.npairs * sizeof(int) <= kKrProgressBytes &&
+        ws_bytes >= prog_off + kKrProgressBytes && std::getenv("SKETCH_B200_KR_LOCKSTEP") == nullptr) {
+      progress = reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + prog_off);
+      if (cudaMemsetAsync(progress, 0, 2 * pl.npairs * sizeof(int), s) != cudaSuccess) return check_launch(what);
+    }
     CUtensorMap mb, mbl;
     st = make_bt_map(&mb, ft_hi + c0 * ldf, kslab, dl, ldf, pl.BN / 2);
     if (st != SK_OK) return st;
@@ -1127,8 +1179,7 @@ int kr_run(bool TA, const float* A, int64_t rows, int64_t P, int64_t dl, int64_t
     p.mtiles = pl.mtiles;
     p.kr_w = W + c0;
     p.kr_ldw = ldw;
-    // sign-bit weights when every reducer half starts on a 32-column boundary (16-byte word loads)
-    const bool use_bits = wbits != nullptr && pl.BN % 64 == 0 && c0 % 32 == 0;
+    p.kr_progress = progress;
     if (use_bits) {
       p.kr_wbits = wbits + c0 / 32;
       p.kr_ldwb = ldwb;
