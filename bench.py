@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import sys
@@ -662,10 +663,16 @@ def main(argv=None):
         for name in [s for s in args.others.split(",") if s and s != args.config]:
             try:
                 ow = WORKLOADS[name](torch, dev, rank)
-                om = measure(torch, ow, 3, 3, 1, 0, dev, False, 0)
+                # sized by time, not count: >= 30 ms of warm-up launches (clocks ramp back up after the
+                # previous leg's setup) and >= 10 ms timed, so a 0.1 ms kernel is not timed on 3 launches
+                est, _ = time_device(torch, ow, 1, 1, 1, dev)
+                o_warm = int(min(300, max(3, math.ceil(0.03 / max(est, 1e-6)))))
+                o_steps = int(min(200, max(3, math.ceil(0.01 / max(est, 1e-6)))))
+                om = measure(torch, ow, o_steps, o_warm, 1, 0, dev, False, 0)
                 oes = ow["a"].element_size()
                 downstream = _downstream(torch, ow, dev)
                 others[name] = {"workload": ow["workload"], "value_gbs": om["value"], "ms_per_step": om["ms_per_step"],
+                                "steps": o_steps, "warmup": o_warm,
                                 "dtype": "f32" if oes == 4 else "f64", "kernel": ow["kernel"],
                                 "pct_hbm_peak": 100.0 * om["achieved_gbs"] / peak,
                                 "roofline_achieved_gbs": om["achieved_gbs"], "alg_bytes": om["alg_bytes"],
