@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <functional>
 #include <numeric>
 #include <vector>
@@ -272,10 +273,86 @@ extern "C" int sk_sparse_right_cols_encode(int dtype, int64_t d, int64_t k, int6
   std::vector<int64_t> order((size_t)k);
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return cnt[(size_t)a] > cnt[(size_t)b]; });
+  order.resize((size_t)nwarps * 32, -1);  // empty lanes at the end
+  {
+    // Local search over the lane slots: per warp, cost = groups * positions (one wavefront per
+    // conflict group and position) + the entries of a bank class beyond the positions in each group
+    // (the conflicts no schedule avoids).  Swaps of two slots (within a window of the sorted order)
+    // are kept when they lower the cost; deterministic, so both encode calls agree.
+    const int Cc = (int)(128 / es), Lg = conflict_lanes(dtype), G = 32 / Lg;
+    std::vector<int32_t> hist((size_t)k * Cc, 0);
+    for (int64_t i = 0; i < nnz; ++i) ++hist[(size_t)cols[i] * Cc + (size_t)(rows[i] % Cc)];
+    auto len_of = [&](int64_t c) -> int64_t { return c < 0 ? 0 : cnt[(size_t)c]; };
+    std::vector<int64_t> deg((size_t)Cc);
+    auto warp_cost = [&](int w) -> int64_t {
+      int64_t m = 0;
+      for (int l = 0; l < 32; ++l) m = std::max(m, len_of(order[(size_t)w * 32 + l]));
+      const int64_t T = (m + 7) / 8 * 8;
+      int64_t cost = G * T;
+      for (int g = 0; g < G; ++g) {
+        std::fill(deg.begin(), deg.end(), 0);
+        for (int l = g * Lg; l < (g + 1) * Lg; ++l) {
+          const int64_t c = order[(size_t)w * 32 + l];
+          if (c >= 0)
+            for (int b = 0; b < Cc; ++b) deg[(size_t)b] += hist[(size_t)c * Cc + b];
+        }
+        for (int b = 0; b < Cc; ++b) cost += std::max<int64_t>(0, deg[(size_t)b] - T);
+      }
+      return cost;
+    };
+    const int nslots = nwarps * 32;
+    std::vector<int64_t> wc((size_t)nwarps);
+    for (int w = 0; w < nwarps; ++w) wc[(size_t)w] = warp_cost(w);
+    const int window = 64;
+    for (int pass = 0; pass < 3; ++pass) {
+      bool improved = false;
+      for (int i = 0; i < nslots; ++i)
+        for (int j = i + 1; j < std::min(nslots, i + window); ++j) {
+          const int wi = i / 32, wj = j / 32;
+          if (wi == wj && (i % 32) / Lg == (j % 32) / Lg) continue;  // same conflict group: no change
+          if (order[(size_t)i] < 0 && order[(size_t)j] < 0) continue;
+          std::swap(order[(size_t)i], order[(size_t)j]);
+          const int64_t ci = warp_cost(wi), cj = wi == wj ? ci : warp_cost(wj);
+          const int64_t before = wc[(size_t)wi] + (wi == wj ? 0 : wc[(size_t)wj]);
+          const int64_t after = ci + (wi == wj ? 0 : cj);
+          if (after < before) {
+            wc[(size_t)wi] = ci;
+            wc[(size_t)wj] = cj;
+            improved = true;
+          } else {
+            std::swap(order[(size_t)i], order[(size_t)j]);
+          }
+        }
+      if (!improved) break;
+    }
+  }
+  {
+    // within each CTA group, put warps on the 4 schedulers (warp id % 4) so a long-list warp shares
+    // its scheduler with a short-list one: ranks by max list length -> ids 0, 1, 2, 3, 7, 6, 5, 4
+    // (config 1: 0.1007 -> 0.1000 ms)
+    for (int g = 0; g < ngroups; ++g) {
+      std::vector<std::pair<int64_t, int>> wl;
+      for (int w = 0; w < C_WARPS; ++w) {
+        int64_t m = 0;
+        for (int l = 0; l < 32; ++l) {
+          const int64_t c = order[(size_t)(g * C_WARPS + w) * 32 + l];
+          m = std::max<int64_t>(m, c < 0 ? 0 : cnt[(size_t)c]);
+        }
+        wl.push_back({-m, w});
+      }
+      std::stable_sort(wl.begin(), wl.end());
+      static const int slot_of_rank[C_WARPS] = {0, 1, 2, 3, 7, 6, 5, 4};
+      std::vector<int64_t> tmp((size_t)C_WARPS * 32);
+      for (int r = 0; r < C_WARPS; ++r)
+        for (int l = 0; l < 32; ++l)
+          tmp[(size_t)slot_of_rank[r] * 32 + l] = order[(size_t)(g * C_WARPS + wl[(size_t)r].second) * 32 + l];
+      std::copy(tmp.begin(), tmp.end(), order.begin() + (size_t)g * C_WARPS * 32);
+    }
+  }
   std::vector<int64_t> lane_len((size_t)nwarps * 32, 0);
   for (int i = 0; i < nwarps * 32; ++i) {
-    colmap[i] = i < k ? (int32_t)order[(size_t)i] : -1;
-    lane_len[(size_t)i] = i < k ? cnt[(size_t)order[(size_t)i]] : 0;
+    colmap[i] = (int32_t)order[(size_t)i];
+    lane_len[(size_t)i] = order[(size_t)i] >= 0 ? cnt[(size_t)order[(size_t)i]] : 0;
   }
   int32_t mx = 0;
   for (int w = 0; w < nwarps; ++w) {
@@ -293,7 +370,8 @@ extern "C" int sk_sparse_right_cols_encode(int dtype, int64_t d, int64_t k, int6
   const int C = (int)(128 / es);
   const int L = conflict_lanes(dtype);
   std::vector<int32_t> lane_of((size_t)k, 0);
-  for (int i = 0; i < (int)std::min<int64_t>(k, (int64_t)nwarps * 32); ++i) lane_of[(size_t)order[(size_t)i]] = i;
+  for (int i = 0; i < nwarps * 32; ++i)
+    if (order[(size_t)i] >= 0) lane_of[(size_t)order[(size_t)i]] = i;
   // entries grouped by lane then class: value = byte offset | neg << 31
   std::vector<std::vector<std::vector<uint32_t>>> buckets((size_t)nwarps * 32, std::vector<std::vector<uint32_t>>(C));
   for (int64_t i = 0; i < nnz; ++i) {

@@ -57,26 +57,28 @@ def test_cols_encode_roundtrip(code, es, d, k, zeta):
     groups = (k + 255) // 256
     assert ent.shape == (groups * 8, maxp, 32) and maxp in (32, 64, 96, 128)
     assert np.all(tw % 8 == 0) and tw.max() <= maxp
-    # lanes cover the columns once, longest lists first
+    # lanes cover the columns once; every warp's positions cover its longest list
     used = colmap[colmap >= 0]
     assert sorted(used.tolist()) == list(range(k))
     got, _ = _decode(ent, colmap, tw, d, es)
     assert got == sorted(zip(rows.tolist(), cols.tolist(), neg.astype(int).tolist()))
     counts = np.bincount(cols, minlength=k)
-    lens = counts[used]
-    assert np.all(np.diff(lens) <= 0)
+    for w in range(tw.size):
+        lane_cols = colmap[32 * w:32 * w + 32]
+        assert tw[w] >= max([counts[c] for c in lane_cols if c >= 0] + [0])
 
 
 def test_cols_encode_config1_schedule():
-    """Config 1 operator shape: positions within 10 % of the entries, extra wavefronts below 20 %."""
+    """Config 1 operator shape: the shared-memory wavefronts of one row's gathers (one per half-warp
+    and position, plus bank conflicts) within 20 % of the entries' floor (16 lane-loads each)."""
     lib = _lib.load()
     d, k = 4096, 256
     rows, cols, neg = _triplets(d, k, 4, 0)
     ent, colmap, tw, maxp = cols_encode(lib, _lib.SK_F64, rows, cols, neg, d, k)
     assert maxp == 96
-    assert int(tw.sum()) * 32 <= 1.12 * rows.size
     extra, total = _extra_wavefronts(ent, tw, d, 8)
-    assert extra <= 0.2 * total
+    assert total + extra <= 1.2 * rows.size / 16
+    assert extra <= 0.05 * total
 
 
 def test_cols_encode_duplicates_and_long_lists():
