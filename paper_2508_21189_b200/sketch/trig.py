@@ -11,6 +11,8 @@ the sampled gather in a single pass over A.  Other transforms / fields use the d
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 import scipy.fft
 
@@ -253,6 +255,34 @@ class SparseRttTM(TestMatrix):
         fs = TRANSFORMS[self.transform][0](sampler.materialize(), axis=0)
         return (dvals[:, None] * fs).astype(self.dtype)
 
+    def _dct_bt_device(self, device):
+        """Omega^T = (D C^T S)^T for the real DCT, formed on the device (bf16 hi + lo, k x ldb) from the
+        closed form of `materialize` (dct2_ortho of the sampler's columns, rtt.py:129-140):
+        Omega[j, c] = d_j s_j sum_x v_{c,x} cos(pi j (2 r_{c,x} + 1) / 2N), s the ortho weights, with the
+        angle reduced exactly in integers (j (2r + 1) mod 4N) before the float64 cosine."""
+        import torch
+
+        dvals, sampler = self._parts()
+        coo = sampler.matrix.tocoo()
+        n = self.d
+        ldb = (n + 7) // 8 * 8
+        omt = torch.zeros((self.k, ldb), dtype=torch.float64, device=device)
+        j = torch.arange(n, dtype=torch.int64, device=device)
+        rows = torch.as_tensor(coo.row.astype(np.int64), device=device)
+        cols = torch.as_tensor(coo.col.astype(np.int64), device=device)
+        vals = torch.as_tensor(np.real(coo.data).astype(np.float64), device=device)
+        step = max(1, (1 << 22) // max(n, 1))  # entries per chunk: <= 4M cosines at a time
+        for e0 in range(0, rows.numel(), step):
+            r, c, v = rows[e0:e0 + step], cols[e0:e0 + step], vals[e0:e0 + step]
+            ang = (j[None, :] * (2 * r[:, None] + 1)) % (4 * n)
+            omt[:, :n].index_add_(0, c, torch.cos(ang.to(torch.float64) * (math.pi / (2 * n))) * v[:, None])
+        w = torch.full((n,), math.sqrt(2.0 / n), dtype=torch.float64, device=device)
+        w[0] = math.sqrt(1.0 / n)
+        omt[:, :n] *= (torch.as_tensor(np.asarray(dvals, dtype=np.float64), device=device) * w)[None, :]
+        hi = omt.to(torch.bfloat16)
+        lo = (omt - hi.to(torch.float64)).to(torch.bfloat16)
+        return hi, lo
+
     def _native_ok(self, dtype) -> bool:
         import torch
 
@@ -419,7 +449,7 @@ class SparseRttTM(TestMatrix):
             if path == "tc":
                 key = ("srtt_dct_tc", a.device)
                 if key not in self._device_cache:
-                    self._device_cache[key] = bt_from_dense(self.materialize(), a.device)
+                    self._device_cache[key] = self._dct_bt_device(a.device)
                 hi, lo = self._device_cache[key]
                 return dense_right_tc(a, hi, lo, self.k, 1.0)
             return self._dct_right(a)
