@@ -283,36 +283,46 @@ extern "C" int sk_sparse_right_cols_encode(int dtype, int64_t d, int64_t k, int6
     std::vector<int32_t> hist((size_t)k * Cc, 0);
     for (int64_t i = 0; i < nnz; ++i) ++hist[(size_t)cols[i] * Cc + (size_t)(rows[i] % Cc)];
     auto len_of = [&](int64_t c) -> int64_t { return c < 0 ? 0 : cnt[(size_t)c]; };
-    std::vector<int64_t> deg((size_t)Cc);
-    auto warp_cost = [&](int w) -> int64_t {
+    // incremental state: per conflict group its bank-class degrees, per warp its lane lengths
+    const int nslots = nwarps * 32;
+    const int ngrp = nwarps * G;
+    std::vector<int64_t> deg((size_t)ngrp * Cc, 0);
+    for (int i = 0; i < nslots; ++i) {
+      const int64_t c = order[(size_t)i];
+      if (c >= 0)
+        for (int b = 0; b < Cc; ++b) deg[(size_t)(i / Lg) * Cc + b] += hist[(size_t)c * Cc + b];
+    }
+    auto warp_T = [&](int w) -> int64_t {
       int64_t m = 0;
       for (int l = 0; l < 32; ++l) m = std::max(m, len_of(order[(size_t)w * 32 + l]));
-      const int64_t T = (m + 7) / 8 * 8;
+      return (m + 7) / 8 * 8;
+    };
+    auto warp_cost = [&](int w, int64_t T) -> int64_t {
       int64_t cost = G * T;
-      for (int g = 0; g < G; ++g) {
-        std::fill(deg.begin(), deg.end(), 0);
-        for (int l = g * Lg; l < (g + 1) * Lg; ++l) {
-          const int64_t c = order[(size_t)w * 32 + l];
-          if (c >= 0)
-            for (int b = 0; b < Cc; ++b) deg[(size_t)b] += hist[(size_t)c * Cc + b];
-        }
-        for (int b = 0; b < Cc; ++b) cost += std::max<int64_t>(0, deg[(size_t)b] - T);
-      }
+      for (int g = w * G; g < (w + 1) * G; ++g)
+        for (int b = 0; b < Cc; ++b) cost += std::max<int64_t>(0, deg[(size_t)g * Cc + b] - T);
       return cost;
     };
-    const int nslots = nwarps * 32;
+    auto move = [&](int slot, int64_t c, int sign) {  // add / remove column c's classes at slot's group
+      if (c < 0) return;
+      int64_t* dg = &deg[(size_t)(slot / Lg) * Cc];
+      const int32_t* hc = &hist[(size_t)c * Cc];
+      for (int b = 0; b < Cc; ++b) dg[b] += sign * hc[b];
+    };
     std::vector<int64_t> wc((size_t)nwarps);
-    for (int w = 0; w < nwarps; ++w) wc[(size_t)w] = warp_cost(w);
+    for (int w = 0; w < nwarps; ++w) wc[(size_t)w] = warp_cost(w, warp_T(w));
     const int window = 64;
     for (int pass = 0; pass < 3; ++pass) {
       bool improved = false;
       for (int i = 0; i < nslots; ++i)
         for (int j = i + 1; j < std::min(nslots, i + window); ++j) {
           const int wi = i / 32, wj = j / 32;
-          if (wi == wj && (i % 32) / Lg == (j % 32) / Lg) continue;  // same conflict group: no change
-          if (order[(size_t)i] < 0 && order[(size_t)j] < 0) continue;
+          if (i / Lg == j / Lg) continue;  // same conflict group: no change
+          const int64_t ci0 = order[(size_t)i], cj0 = order[(size_t)j];
+          if (ci0 < 0 && cj0 < 0) continue;
+          move(i, ci0, -1), move(j, cj0, -1), move(i, cj0, 1), move(j, ci0, 1);
           std::swap(order[(size_t)i], order[(size_t)j]);
-          const int64_t ci = warp_cost(wi), cj = wi == wj ? ci : warp_cost(wj);
+          const int64_t ci = warp_cost(wi, warp_T(wi)), cj = wi == wj ? ci : warp_cost(wj, warp_T(wj));
           const int64_t before = wc[(size_t)wi] + (wi == wj ? 0 : wc[(size_t)wj]);
           const int64_t after = ci + (wi == wj ? 0 : cj);
           if (after < before) {
@@ -321,6 +331,7 @@ extern "C" int sk_sparse_right_cols_encode(int dtype, int64_t d, int64_t k, int6
             improved = true;
           } else {
             std::swap(order[(size_t)i], order[(size_t)j]);
+            move(i, cj0, -1), move(j, ci0, -1), move(i, ci0, 1), move(j, cj0, 1);
           }
         }
       if (!improved) break;
