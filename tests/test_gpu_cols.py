@@ -113,3 +113,33 @@ def test_cols_empty_and_single_row(cuda):
     a1 = torch.randn(1, 256, dtype=torch.float64, device=cuda)
     ref = orc.csr_right(orc.sparse_uniform_csr(256, 40, 2, 1), a1.cpu().numpy())
     assert rel_err(tm.apply_right(a1).cpu().numpy(), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("d,k,zeta,dt", [(2, 1, 1, np.float64), (6, 3, 2, np.float64), (8, 40, 3, np.float32),
+                                         (1001, 33, 4, np.float64), (1002, 257, 9, np.float32),
+                                         (4100, 512, 4, np.float64)])
+def test_cols_odd_shapes(d, k, zeta, dt, cuda):
+    """Tiny / odd d (odd d or d * 4 % 16 != 0 cannot bulk-copy rows and falls back), k of one lane,
+    ragged groups of 256 columns; every case against the oracle."""
+    import torch
+
+    rng = np.random.default_rng(d + 3 * k)
+    a = rng.standard_normal((77, d)).astype(dt)
+    tm = skb.SparseUniformTM(d, k, min(zeta, k), seed=9)
+    at = torch.as_tensor(a).to(cuda)
+    y = tm.apply_right(at).cpu().numpy()
+    ref = orc.csr_right(orc.sparse_uniform_csr(d, k, min(zeta, k), 9), a)
+    assert rel_err(y, ref) <= TOL[dt]
+
+
+def test_cols_stack_and_iid_families(cuda):
+    """SparseStack (zeta blocks) and SparseIID (variable nonzeros per row) take K1c as well."""
+    import torch
+
+    a = torch.randn(500, 2048, dtype=torch.float64, device=cuda)
+    for tm in (skb.SparseStackTM(2048, 4, 24, seed=1), skb.SparseIIDTM(2048, 96, 4.0, seed=2)):
+        plan = _plan(tm, a)
+        assert plan is not None
+        y = tm.apply_right(a).cpu().numpy()
+        ref = a.cpu().numpy() @ tm.materialize()
+        assert rel_err(y, ref) <= 1e-12
