@@ -210,7 +210,9 @@ class _SignSparseTM(TestMatrix):
                 lib = _lib.load()
                 rows, cols, neg, mag = self._sign_form()
                 es = 8 if code == _lib.SK_F64 else 4
-                nslab = 1
+                # a column longer than 4 slabs x 128 positions cannot fit: skip the encodes outright
+                longest = int(np.bincount(cols, minlength=self.k).max()) if cols.size else 0
+                nslab = 1 if longest <= 4 * 128 + 64 else 8
                 # beyond 4 slabs (lists of > ~400 entries per column) the Y re-reads and the spilling
                 # 128-position variant lose to K1r's per-unit walk (tools/k1c_probe.py)
                 while res is None and nslab <= 4 and (self.d * es) % 16 == 0:
