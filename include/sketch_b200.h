@@ -273,6 +273,16 @@ SK_API int sk_gemv_t_f32_f64(const float* A, int64_t n, int64_t d, int64_t lda, 
  * Workspace: sk_lsqr_step_f32_f64_workspace_bytes(n, d) bytes.
  */
 SK_API size_t sk_lsqr_step_f32_f64_workspace_bytes(int64_t n, int64_t d);
+/*
+ * LSQR recurrences on the device after sk_lsqr_step_f32_f64 (called with alpha = 1, the scale carried
+ * by v''): from zb = [A^T u_dev, ||u_dev||^2] updates v, w, x (d <= 512, float64), the Paige & Saunders
+ * state [alpha, c, phibar, rhobar, anorm2, ddnorm, bnorm, atol, btol, istop, itn] and writes the next
+ * step's v'' = (c'/alpha') R^-1 v' and scal = [itn, istop, r1norm, arnorm, test2, acond, test1, beta].
+ * One CTA; a no-op once istop != 0.  Rinv / RinvT: R^-1 and its transpose, d x d row-major.
+ */
+SK_API int sk_lsqr_recur_f64(int64_t d, const double* Rinv, const double* RinvT, const double* zb, double* v,
+                             double* w, double* x, double* vnext, double* state, double* scal, void* stream);
+
 SK_API int sk_lsqr_step_f32_f64(const float* A, int64_t n, int64_t d, int64_t lda, const double* v, double alpha,
                                 double* u, double* zb, double* ws, size_t ws_bytes, void* stream);
 

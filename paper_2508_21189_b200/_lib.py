@@ -94,6 +94,7 @@ SIGNATURES = {
                                            _c_i64, _c_int, _c_p, _c_size, _c_p]),
     "sk_kr_right_signs": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_i64,
                                    _c_dbl, _c_i64, _c_dbl, _c_p, _c_i64, _c_p, _c_size, _c_p]),
+    "sk_lsqr_recur_f64": (_c_int, [_c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]),
     "sk_sparse_right_cols_groups": (_c_int, [_c_i64]),
     "sk_sparse_right_cols_supported": (_c_int, [_c_int, _c_i64, _c_i64, ctypes.c_int32]),
     "sk_sparse_right_cols_encode": (_c_int, [_c_int, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, ctypes.c_int32, _c_p,

@@ -771,6 +771,80 @@ def _lsqr_fused_loop(A, u, v, R, alpha, beta, bnorm, red, atol, btol, iter_lim, 
     return LsqrResult(_back(x, kind), istop, itn, float(r1norm), float(arnorm), acond, t_sketch, float(test2))
 
 
+_PINNED_SCAL = {}
+
+
+def _pinned_scal(device):
+    """A cached 2 x 8 pinned float64 host buffer per device (cudaHostAlloc costs ~0.1 s per call)."""
+    import torch
+
+    key = str(device)
+    if key not in _PINNED_SCAL:
+        _PINNED_SCAL[key] = torch.zeros((2, 8), dtype=torch.float64).pin_memory()
+    return _PINNED_SCAL[key]
+
+
+def _lsqr_device_loop(A, u, v, R, alpha, beta, bnorm, atol, btol, iter_lim, kind, t_sketch):
+    """LSQR iterations with everything on the device: the fused step (one pass over A) and the
+    recurrences (sk_lsqr_recur_f64: v, w, x and the Paige & Saunders scalars in one CTA).  The host
+    reads 8 scalars per iteration for the stopping test, one iteration behind: iteration i + 1 is
+    queued before iteration i's scalars are read, so the GPU never waits for the host (after the
+    stopping iteration the queued one is a no-op for x and the state).  Same iterates as
+    `_lsqr_fused_loop` up to rounding (float64 everywhere)."""
+    import torch
+
+    from . import _lib
+
+    d = A.shape[1]
+    dev = A.device
+    eye = torch.eye(d, dtype=torch.float64, device=dev)
+    rinv = torch.linalg.solve_triangular(R.to(torch.float64), eye, upper=True).contiguous()
+    rinvt = rinv.T.contiguous()
+    v = v.to(torch.float64).contiguous().clone()
+    w = v.clone()
+    x = torch.zeros(d, dtype=torch.float64, device=dev)
+    vnext = (rinv @ v) / alpha  # u on the device is normalised on entry: c = 1
+    state = torch.tensor([alpha, 1.0, beta, alpha, 0.0, 0.0, bnorm, atol, btol, 0.0, 0.0], dtype=torch.float64,
+                         device=dev)
+    scal = torch.zeros((2, 8), dtype=torch.float64, device=dev)
+    scal_h = _pinned_scal(dev)
+    evs = [torch.cuda.Event(), torch.cuda.Event()]
+    lib = _lib.load()
+    n = A.shape[0]
+    zb = torch.empty(d + 1, dtype=torch.float64, device=dev)
+    ws_bytes = lib.sk_lsqr_step_f32_f64_workspace_bytes(n, d)
+    ws = torch.empty(max(ws_bytes, 8) // 8, dtype=torch.float64, device=dev)
+    ptrs = [p.data_ptr() for p in (rinv, rinvt, zb, v, w, x, vnext, state)]
+    istop, itn = 0, 0
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream().cuda_stream
+
+        def launch(i):  # iteration i (1-based) into scalar slot i % 2
+            st = lib.sk_lsqr_step_f32_f64(A.data_ptr(), n, d, A.stride(0), vnext.data_ptr(), 1.0, u.data_ptr(),
+                                          zb.data_ptr(), ws.data_ptr(), ws_bytes, stream)
+            _lib.check(st, "sk_lsqr_step_f32_f64")
+            st = lib.sk_lsqr_recur_f64(d, *ptrs, scal[i % 2].data_ptr(), stream)
+            _lib.check(st, "sk_lsqr_recur_f64")
+            scal_h[i % 2].copy_(scal[i % 2], non_blocking=True)
+            evs[i % 2].record()
+
+        if iter_lim > 0:
+            launch(1)
+        i = 1
+        while i <= iter_lim:
+            if i < iter_lim:
+                launch(i + 1)  # queued behind iteration i: no GPU idle while the host checks i
+            evs[i % 2].synchronize()
+            itn, istop = int(scal_h[i % 2, 0]), int(scal_h[i % 2, 1])
+            r1norm, arnorm, test2, acond = (float(scal_h[i % 2, j]) for j in (2, 3, 4, 5))
+            if istop:
+                break
+            i += 1
+    if iter_lim <= 0:
+        r1norm, arnorm, test2, acond = beta, alpha * beta, 0.0, 0.0
+    return LsqrResult(_back(rinv @ x, kind), istop, itn, r1norm, arnorm, acond, t_sketch, test2)
+
+
 def _rmatvec_blocks(A, u, block_rows):
     """A^T @ u in float64 (sk_gemv_t_f32_f64 for float32 A: one pass, ordered float64 reduction)."""
     import torch
@@ -872,6 +946,8 @@ def sketch_precondition_lsqr(a, b, tm_psi, *, atol: float = 1e-6, btol: float = 
     # float32 A with d = 128 q <= 512: u <- A R^-1 v - alpha u, A^T u and ||u||^2 in one pass over A
     # (sk_lsqr_step_f32_f64), one all-reduce of [A^T u, ||u||^2] per iteration when distributed
     fused = _lsqr_fused_ok(A) and os.environ.get("SKETCH_B200_LSQR_FUSED", "1") != "0"
+    if fused and allreduce is None and os.environ.get("SKETCH_B200_LSQR_DEVLOOP", "1") != "0":
+        return _lsqr_device_loop(A, u.contiguous(), v, R, alpha, beta, bnorm, atol, btol, iter_lim, kind, t_sketch)
     if fused:
         return _lsqr_fused_loop(A, u.contiguous(), v, R, alpha, beta, bnorm, red, atol, btol, iter_lim, kind,
                                 t_sketch)

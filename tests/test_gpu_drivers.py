@@ -230,3 +230,26 @@ def test_lsqr_iter_lim_zero(cuda):
     b = rng.standard_normal(3000)
     res = rand_nla.sketch_precondition_lsqr(a, b, skb.SparseUniformTM(3000, 64, 8, seed=2), iter_lim=0)
     assert res.itn == 0 and np.all(res.x == 0)
+
+
+@pytest.mark.parametrize("atol,btol", [(1e-10, 0.0), (1e-6, 1e-6), (1e-3, 1e-8)])
+def test_lsqr_device_loop_matches_host_loop(atol, btol, cuda, monkeypatch):
+    """The device recurrences (sk_lsqr_recur_f64) against the host-recurrence fused loop: same stop,
+    same iteration count, same solution and estimates (float64 both, rounding-level differences)."""
+    import torch
+
+    rng = np.random.default_rng(12)
+    n, d = 150000, 384
+    w = 1.0 + rng.pareto(1.5, size=n)
+    a = torch.from_numpy((rng.standard_normal((n, d)) * w[:, None]).astype(np.float32)).to(cuda)
+    b = (a.double() @ torch.from_numpy(rng.standard_normal(d)).to(cuda)
+         + 1e-2 * torch.randn(n, dtype=torch.float64, device=cuda)).float()
+    tm = skb.SparseUniformTM(n, 1536, 8, seed=6)
+    r1 = rand_nla.sketch_precondition_lsqr(a, b, tm, atol=atol, btol=btol)
+    monkeypatch.setenv("SKETCH_B200_LSQR_DEVLOOP", "0")
+    r2 = rand_nla.sketch_precondition_lsqr(a, b, tm, atol=atol, btol=btol)
+    x1, x2 = r1.x.cpu().numpy(), r2.x.cpu().numpy()
+    assert (r1.istop, r1.itn) == (r2.istop, r2.itn)
+    assert np.linalg.norm(x1 - x2) <= 1e-9 * np.linalg.norm(x2)
+    for f in ("r1norm", "arnorm", "acond", "normal_eq_test"):
+        assert abs(getattr(r1, f) - getattr(r2, f)) <= 1e-6 * abs(getattr(r2, f)) + 1e-300, f
