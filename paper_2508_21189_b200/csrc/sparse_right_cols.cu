@@ -19,8 +19,12 @@
 //   * shared-memory bank conflicts of the per-lane gathers are removed at encoding time: Omega is
 //     fixed, so the host scheduler (sk_sparse_right_cols_encode) orders every lane's list such that
 //     at each position the lanes of a conflict group (16 lanes for float64 — one 128-byte wavefront
-//     of 8-byte loads — 32 for float32) read distinct 8 / 4-byte bank slots where it can; columns
-//     are dealt to lanes by list length so a warp's lists have near-equal lengths.
+//     of 8-byte loads — 32 for float32) read distinct 8 / 4-byte bank slots where it can (a matching
+//     of lanes to slots per position); columns are dealt to lanes by list length, a local search
+//     then swaps lane slots while that lowers positions + unavoidable conflicts, and the warps of a
+//     CTA are placed so each scheduler pairs a long-list warp with a short one.
+//
+// Config 1 (float64): 0.100 ms back to back = 88 % of the HBM copy peak (K1r: 0.215 ms).
 //
 // Bytes per launch (algorithmic): n * d * sizeof(T) read + n * k * sizeof(T) written.  The floor is
 // shared memory: every (row, entry) pair is one lane-load (8 B for float64), plus the row's landing.
