@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(C_THREADS, 1) sparse_right_cols_kernel(const C
   }
   const int npos = __ldg(p.tw + wg);
   const int col = __ldg(p.colmap + wg * 32 + lane);
-  T* ybase = static_cast<T*>(p.Y) + col;
+  T* ybase = static_cast<T*>(p.Y) + (col >= 0 ? col : 0);  // stores only when col >= 0
   const T scale = (T)p.scale;
   // row copies: issued by lane 0 of warp 0 (the warp with the longest lists, so the slot it refills
   // — released by every warp after the previous pair of rows — is normally free when it asks)

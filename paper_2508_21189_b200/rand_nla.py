@@ -20,6 +20,8 @@ from dataclasses import dataclass
 
 import os
 
+import threading
+
 import numpy as np
 
 from ._device import require_cuda, to_operand
@@ -771,17 +773,22 @@ def _lsqr_fused_loop(A, u, v, R, alpha, beta, bnorm, red, atol, btol, iter_lim, 
     return LsqrResult(_back(x, kind), istop, itn, float(r1norm), float(arnorm), acond, t_sketch, float(test2))
 
 
-_PINNED_SCAL = {}
+_PINNED_SCAL = threading.local()
 
 
 def _pinned_scal(device):
-    """A cached 2 x 8 pinned float64 host buffer per device (cudaHostAlloc costs ~0.1 s per call)."""
+    """A cached 2 x 8 pinned float64 host buffer per host thread and device (pinning costs far more
+    than an iteration; per thread, so concurrent solves — the reference runs trials on a thread pool —
+    never share one)."""
     import torch
 
+    cache = getattr(_PINNED_SCAL, "bufs", None)
+    if cache is None:
+        cache = _PINNED_SCAL.bufs = {}
     key = str(device)
-    if key not in _PINNED_SCAL:
-        _PINNED_SCAL[key] = torch.zeros((2, 8), dtype=torch.float64).pin_memory()
-    return _PINNED_SCAL[key]
+    if key not in cache:
+        cache[key] = torch.zeros((2, 8), dtype=torch.float64).pin_memory()
+    return cache[key]
 
 
 def _lsqr_device_loop(A, u, v, R, alpha, beta, bnorm, atol, btol, iter_lim, kind, t_sketch):

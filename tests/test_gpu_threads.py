@@ -55,3 +55,36 @@ def test_concurrent_applies_match_sequential(cuda):
         results = list(ex.map(run, range(6 * len(cases))))
     for i, y in results:
         assert torch.equal(y, ref[i]), i
+
+
+def test_concurrent_lsqr_solves(cuda):
+    """Sketch-and-precondition LSQR from several host threads at once: the device loop's pinned scalar
+    buffer is per thread, so every solve stops where it stops alone and returns the same x."""
+    import numpy as np
+    import torch
+
+    from paper_2508_21189_b200 import rand_nla
+
+    rng = np.random.default_rng(3)
+    probs = []
+    for i, (n, d) in enumerate([(60000, 128), (80000, 256), (50000, 384)]):
+        a = torch.from_numpy((rng.standard_normal((n, d)) * (1.0 + rng.pareto(1.5, size=n))[:, None])
+                             .astype(np.float32)).to(cuda)
+        b = (a.double() @ torch.from_numpy(rng.standard_normal(d)).to(cuda)).float()
+        probs.append((a, b, skb.SparseUniformTM(n, 4 * d, 8, seed=i)))
+    ref = [rand_nla.sketch_precondition_lsqr(a, b, tm, atol=1e-8, btol=0.0) for a, b, tm in probs]
+    torch.cuda.synchronize()
+
+    def run(i):
+        with torch.cuda.stream(torch.cuda.Stream()):
+            a, b, tm = probs[i % len(probs)]
+            r = rand_nla.sketch_precondition_lsqr(a, b, tm, atol=1e-8, btol=0.0)
+            torch.cuda.current_stream().synchronize()
+            return i % len(probs), r
+
+    with ThreadPoolExecutor(max_workers=3) as ex:
+        results = list(ex.map(run, range(6)))
+    for i, r in results:
+        assert (r.itn, r.istop) == (ref[i].itn, ref[i].istop)
+        x, xr = r.x.cpu().numpy(), ref[i].x.cpu().numpy()
+        assert np.linalg.norm(x - xr) <= 1e-10 * np.linalg.norm(xr)
