@@ -229,6 +229,111 @@ __global__ void __launch_bounds__((1 << (L - 5)), (sizeof(T) == 4 ? (L <= 12 ? 3
 
 
 // ---------------------------------------------------------------------------------------------
+// Float64 wide path (d = 8192, +-1 diagonal): 128 threads per row and 64 values per thread (128
+// registers), so 12 of the 13 butterfly stages run in two register phases with ONE shared-memory
+// transpose between them, and the last stage (index bit 7) is folded into the sampled gather:
+//   phase 1: registers hold index bits {0, 8..12}    (32 coalesced 16-byte loads per thread)
+//   phase 2: registers hold bits {1..6}              (one transpose; each thread writes back the
+//            same positions it read, so no barrier between the read and the write-back)
+//   gather : out = sum_x sign (X[j & ~128] +- X[j | 128])  (bit 7: top = sum, bottom = difference)
+// The 3-phase fast path moves every row through shared memory five times (≈4200 wavefronts per
+// row at config-2 shape, shared memory 64 % busy, 1.52 ms); this one three times: 1.07 ms (4.0 TB/s),
+// latency-bound at 8 warps per SM (long-scoreboard on the row loads, float64 add chains).
+// SKETCH_B200_SRTT64=3 selects the 3-phase kernel.
+// Shared address of index j: j ^ (((j >> 7) & 7) << 1): the phase-1 16-byte stores and the phase-2
+// 8-byte accesses are conflict free.
+__device__ __forceinline__ int swz64(int j) { return j ^ (((j >> 7) & 7) << 1); }
+
+__device__ __forceinline__ void wht64_regs(double (&x)[64]) {
+#pragma unroll
+  for (int h = 1; h < 64; h <<= 1) {
+#pragma unroll
+    for (int v = 0; v < 64; ++v) {
+      if ((v & h) == 0) butterfly(x[v], x[v | h]);
+    }
+  }
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB)
+    srtt_wht64_wide(const double* __restrict__ A, int64_t n, int64_t lda, const double* __restrict__ dvals,
+                    const int32_t* __restrict__ samp, int xi, int k, double scale, double* __restrict__ Y,
+                    int64_t ldy) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* buf = reinterpret_cast<double*>(smem_raw);
+  const int t = threadIdx.x, w = t >> 5, l = t & 31;
+  const int base1 = 2 * l + 64 * w;              // phase-1 index of register pair q: base1 + 256 q
+  const int base2 = (t & 1) | ((t >> 1) << 7);   // phase-2 index of register r: base2 | (r << 1)
+  uint64_t dmask = 0;                            // D < 0 at the phase-1 positions (register e + 2 q)
+#pragma unroll 1
+  for (int q = 0; q < 32; ++q)
+    for (int e = 0; e < 2; ++e)
+      if (dvals[base1 + 256 * q + e] < 0.0) dmask |= 1ull << (e + 2 * q);
+  for (int64_t row = blockIdx.x; row < n; row += gridDim.x) {
+    const double* a = A + row * lda;
+    if (t == 0 && row + gridDim.x < n)
+      prefetch_l2_bulk(a + gridDim.x * lda, 8192u * 8u);  // the CTA's next row heads for L2
+    double x[64];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      double2 v;
+      asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y)
+                   : "l"(a + base1 + 256 * q));
+      x[2 * q] = v.x;
+      x[2 * q + 1] = v.y;
+    }
+#pragma unroll
+    for (int r = 0; r < 64; ++r) x[r] = flip_if(x[r], (uint32_t)((dmask >> r) & 1u));
+    wht64_regs(x);
+    __syncthreads();  // the previous row's gather is done with buf
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      double* dst = buf + swz64(base1 + 256 * q);
+      asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "d"(x[2 * q]),
+                   "d"(x[2 * q + 1])
+                   : "memory");
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 64; ++r) x[r] = buf[swz64(base2 | (r << 1))];
+    wht64_regs(x);
+#pragma unroll
+    for (int r = 0; r < 64; ++r) buf[swz64(base2 | (r << 1))] = x[r];
+    __syncthreads();
+    double* y = Y + row * ldy;
+    for (int c = t; c < k; c += 128) {
+      double sacc = 0.0;
+      for (int u = 0; u < xi; ++u) {
+        const uint32_t e = (uint32_t)__ldg(samp + (int64_t)c * xi + u);
+        const int j = (int)(e & 0x7fffffffu);
+        const double x0 = buf[swz64(j & ~128)], x1 = buf[swz64(j | 128)];
+        sacc += flip_if((j & 128) ? x0 - x1 : x0 + x1, e >> 31);
+      }
+      y[c] = sacc * scale;
+    }
+  }
+}
+
+template <int MINB>
+int launch_wide64_t(const double* A, int64_t n, int64_t lda, const double* dv, const int32_t* samp, int xi, int k,
+                    double scale, double* Y, int64_t ldy, cudaStream_t s) {
+  const size_t smem = 8192 * sizeof(double);
+  allow_smem(srtt_wht64_wide<MINB>, smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, srtt_wht64_wide<MINB>, 128, smem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)sm_count() * per_sm;
+  if (grid > n) grid = n;
+  srtt_wht64_wide<MINB><<<(unsigned)grid, 128, smem, s>>>(A, n, lda, dv, samp, xi, k, scale, Y, ldy);
+  return check_launch("sk_srtt_right(f64 wide)");
+}
+// two CTAs per SM (254 registers): three (168 registers) spill the values and ran 1.15 vs 1.07 ms
+int launch_wide64(const double* A, int64_t n, int64_t lda, const double* dv, const int32_t* samp, int xi, int k,
+                  double scale, double* Y, int64_t ldy, cudaStream_t s) {
+  return launch_wide64_t<2>(A, n, lda, dv, samp, xi, k, scale, Y, ldy, s);
+}
+
+// ---------------------------------------------------------------------------------------------
 // Wide fast path (float32, +-1 diagonal, d = 2^L, 12 <= L <= 14): T = d/128 threads per row and
 // 128 values per thread held as 64 packed float pairs, so 12 of the 13 (L=13) butterfly stages run
 // as Blackwell FADD2/FSUB2 (add.rn.f32x2) on register pairs.
@@ -610,6 +715,12 @@ int run(const void* A_, int64_t n, int64_t d, int64_t lda, const void* dv_, bool
       if (L == 13) return launch_wide<13>(Af, n, lda, dvf, samp, xi, (int)k, scale, Yf, ldy, s);
       return launch_wide<14>(Af, n, lda, dvf, samp, xi, (int)k, scale, Yf, ldy, s);
     }
+  }
+  if constexpr (sizeof(T) == 8) {
+    const char* e = getenv("SKETCH_B200_SRTT64");
+    if (pm1 && aligned && L == 13 && (int64_t(1) << L) == d && !(e && e[0] == '3'))
+      return launch_wide64(reinterpret_cast<const double*>(A), n, lda, reinterpret_cast<const double*>(dv), samp,
+                           xi, (int)k, scale, reinterpret_cast<double*>(Y), ldy, s);
   }
   const int max_fast = sizeof(T) == 4 ? 14 : 13;
   if (L >= 10 && L <= max_fast && aligned) {
