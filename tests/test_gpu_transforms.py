@@ -135,3 +135,26 @@ def test_srtt_dct_paths_agree_config2_shape(cuda, monkeypatch):
     dv, samp = orc.srtt_parts(8192, 512, 1, 0)
     ref = orc.srtt_right(dv, samp, a[:64].cpu().numpy(), "dct")
     assert rel_err(outs["fft"][:64].cpu().numpy(), ref) <= 1e-5
+
+
+@pytest.mark.parametrize("k,xi,n", [(512, 1, 301), (200, 3, 17), (1000, 2, 1)])
+def test_srtt_float64_wide_d8192(k, xi, n, cuda, monkeypatch):
+    """float64 SRTT-WHT at d = 8192 on the wide kernel (two register phases, bit 7 folded into the
+    gather) against the oracle and against the 3-phase kernel (SKETCH_B200_SRTT64=3)."""
+    import numpy as np
+    import torch
+
+    import oracle as orc
+    from paper_2508_21189_b200 import sketch as skb
+
+    rng = np.random.default_rng(k + xi)
+    a = rng.standard_normal((n, 8192)) / np.arange(1, 8193)
+    tm = skb.SparseRttTM(8192, k, xi, "wht", seed=7)
+    at = torch.from_numpy(a).to(cuda)
+    y = tm.apply_right(at).cpu().numpy()
+    dv, samp = orc.srtt_parts(8192, k, xi, 7)
+    ref = orc.srtt_right(dv, samp, a, "wht")
+    assert np.linalg.norm(y - ref) <= 1e-12 * np.linalg.norm(ref)
+    monkeypatch.setenv("SKETCH_B200_SRTT64", "3")
+    y3 = tm.apply_right(at).cpu().numpy()
+    assert np.linalg.norm(y - y3) <= 1e-14 * np.linalg.norm(y3)
