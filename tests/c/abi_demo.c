@@ -7,7 +7,10 @@
  *      float32 A, +-1 diagonal, xi = 2 signed samples per output column.
  *   2. A dense float64 apply, Y = A * Omega (the Gaussian / materialised families, base.py:75-79),
  *      through sk_kr_right_cc with one block (W = NULL), and its adjoint X = Omega^T * B in place.
- *   3. The error contract: a bad shape returns SK_EINVAL with a message from sk_last_error().
+ *   3. The sparse-sign right apply of config 1 (reference _SparseTM.apply_right, sparse.py:63-66): Omega
+ *      with zeta distinct +-1 columns per row, encoded once by sk_sparse_right_cols_encode (two calls:
+ *      the positions needed, then the schedule), applied to float64 A by sk_sparse_right_cols.
+ *   4. The error contract: a bad shape returns SK_EINVAL with a message from sk_last_error().
  *
  * Build (tests/test_c_abi.py does this):
  *   gcc -O2 -std=c11 tests/c/abi_demo.c -Iinclude -I<cuda>/include -L<lib dir> -lsketch_b200
@@ -183,6 +186,79 @@ static int check_dense64(void) {
   return (ey <= 1e-12 && ex <= 1e-12) ? 0 : 1;
 }
 
+static int check_sparse_cols(void) {
+  const int n = 700, d = 2048, k = 300, zeta = 4;
+  const double mag = 1.0 / sqrt((double)zeta);
+  int64_t* rows = malloc(sizeof(int64_t) * d * zeta);
+  int64_t* cols = malloc(sizeof(int64_t) * d * zeta);
+  uint8_t* neg = malloc((size_t)d * zeta);
+  for (int r = 0; r < d; ++r)
+    for (int z = 0; z < zeta; ++z) {
+      int c, dup;
+      do { /* zeta distinct columns per row */
+        c = (int)(next_u64() % k);
+        dup = 0;
+        for (int q = 0; q < z; ++q) dup |= cols[r * zeta + q] == c;
+      } while (dup);
+      rows[r * zeta + z] = r;
+      cols[r * zeta + z] = c;
+      neg[r * zeta + z] = (uint8_t)(next_u64() & 1);
+    }
+  const int groups = sk_sparse_right_cols_groups(k);
+  int32_t* colmap = malloc(sizeof(int32_t) * groups * 256);
+  int32_t* tw = malloc(sizeof(int32_t) * groups * 8);
+  int32_t need = 0;
+  SK(sk_sparse_right_cols_encode(SK_F64, d, k, (int64_t)d * zeta, rows, cols, neg, 0, NULL, colmap, tw, &need));
+  const int32_t maxp = need <= 32 ? 32 : need <= 64 ? 64 : need <= 96 ? 96 : 128;
+  if (need > 128 || !sk_sparse_right_cols_supported(SK_F64, d, k, maxp)) {
+    fprintf(stderr, "sparse cols: unexpected plan (need %d)\n", need);
+    return 1;
+  }
+  uint32_t* ent = malloc(sizeof(uint32_t) * groups * 8 * maxp * 32);
+  SK(sk_sparse_right_cols_encode(SK_F64, d, k, (int64_t)d * zeta, rows, cols, neg, maxp, ent, colmap, tw, &need));
+  double* a = malloc(sizeof(double) * n * d);
+  for (int i = 0; i < n * d; ++i) a[i] = normal();
+  double *da, *dy;
+  uint32_t* dent;
+  int32_t *dcolmap, *dtw;
+  CK(cudaMalloc((void**)&da, sizeof(double) * n * d));
+  CK(cudaMalloc((void**)&dy, sizeof(double) * n * k));
+  CK(cudaMalloc((void**)&dent, sizeof(uint32_t) * groups * 8 * maxp * 32));
+  CK(cudaMalloc((void**)&dcolmap, sizeof(int32_t) * groups * 256));
+  CK(cudaMalloc((void**)&dtw, sizeof(int32_t) * groups * 8));
+  CK(cudaMemcpy(da, a, sizeof(double) * n * d, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dent, ent, sizeof(uint32_t) * groups * 8 * maxp * 32, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dcolmap, colmap, sizeof(int32_t) * groups * 256, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dtw, tw, sizeof(int32_t) * groups * 8, cudaMemcpyHostToDevice));
+  SK(sk_sparse_right_cols(SK_F64, da, n, d, d, dent, dcolmap, dtw, k, maxp, mag, dy, k, 0, NULL));
+  CK(cudaDeviceSynchronize());
+  double* y = malloc(sizeof(double) * n * k);
+  CK(cudaMemcpy(y, dy, sizeof(double) * n * k, cudaMemcpyDeviceToHost));
+  double* ref = calloc((size_t)n * k, sizeof(double));
+  for (int i = 0; i < n; ++i)
+    for (int e = 0; e < d * zeta; ++e) {
+      const double v = a[(size_t)i * d + rows[e]] * mag;
+      ref[(size_t)i * k + cols[e]] += neg[e] ? -v : v;
+    }
+  const double err = rel_err(y, ref, (size_t)n * k);
+  printf("sparse sign f64 (K1c, maxp %d): rel err %.3e\n", maxp, err);
+  cudaFree(da);
+  cudaFree(dy);
+  cudaFree(dent);
+  cudaFree(dcolmap);
+  cudaFree(dtw);
+  free(rows);
+  free(cols);
+  free(neg);
+  free(colmap);
+  free(tw);
+  free(ent);
+  free(a);
+  free(y);
+  free(ref);
+  return err <= 1e-12 ? 0 : 1;
+}
+
 static int check_errors(void) {
   const int st = sk_srtt_right(SK_F32, NULL, 10, 1000 /* not a power of two */, 1000, NULL, SK_WHT, NULL, 1, 4, 1.0,
                                NULL, 4, NULL);
@@ -196,7 +272,7 @@ int main(void) {
     return 4;
   }
   printf("libsketch_b200 ABI %d, %d SMs on device 0\n", sk_abi_version(), sk_device_sm_count(0));
-  const int fails = check_srtt() + check_dense64() + check_errors();
+  const int fails = check_srtt() + check_dense64() + check_sparse_cols() + check_errors();
   printf(fails ? "FAILED\n" : "ok\n");
   return fails ? 1 : 0;
 }
