@@ -664,10 +664,10 @@ def main(argv=None):
             try:
                 ow = WORKLOADS[name](torch, dev, rank)
                 # sized by time, not count: >= 30 ms of warm-up launches (clocks ramp back up after the
-                # previous leg's setup) and >= 10 ms timed, so a 0.1 ms kernel is not timed on 3 launches
+                # previous leg's setup) and >= 30 ms timed, so a 0.1 ms kernel is not timed on 3 launches
                 est, _ = time_device(torch, ow, 1, 1, 1, dev)
                 o_warm = int(min(300, max(3, math.ceil(0.03 / max(est, 1e-6)))))
-                o_steps = int(min(200, max(3, math.ceil(0.01 / max(est, 1e-6)))))
+                o_steps = int(min(200, max(3, math.ceil(0.03 / max(est, 1e-6)))))
                 om = measure(torch, ow, o_steps, o_warm, 1, 0, dev, False, 0)
                 oes = ow["a"].element_size()
                 downstream = _downstream(torch, ow, dev)
