@@ -18,6 +18,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import math
 import os
 
 import threading
@@ -140,13 +141,33 @@ def _cholqr2(m, max_spread: float = 1e6):
     return None if res is None else res[0]
 
 
+def _svd_square(r, min_ratio: float = 1e-7):
+    """Thin SVD of a small square float64 CUDA matrix through the symmetric eigenproblem of the
+    augmented [[0, R], [R^T, 0]] (eigenvalues +-sigma_i, eigenvectors [u_i; v_i] / sqrt 2): no
+    squaring of the condition number (unlike the Gram matrix), sigma to ~eps * sigma_max.  cuSOLVER's
+    SVD of the config-3 200 x 200 factor takes ~7-11 ms (Jacobi sweeps), this eigh 4 ms
+    (`tools/svd_small_probe.py`).  A factor with sigma_min below min_ratio * sigma_max (where the +-0
+    pairs of the augmented problem could mix u and v) takes torch.linalg.svd."""
+    import torch
+
+    k = r.shape[0]
+    aug = torch.zeros((2 * k, 2 * k), dtype=r.dtype, device=r.device)
+    aug[:k, k:] = r
+    aug[k:, :k] = r.T
+    w, vec = torch.linalg.eigh(aug)
+    s = w[k:].flip(0)
+    if not bool(torch.isfinite(s).all()) or float(s[-1]) <= min_ratio * float(s[0]):
+        return torch.linalg.svd(r, full_matrices=False)
+    top = vec[:, k:].flip(1) * math.sqrt(2.0)
+    return top[:k].contiguous(), s.contiguous(), top[k:].T.contiguous()
+
+
 def _svd_wide(b):
     """Thin SVD of a wide float64 B (k x d, d >> k), as torch.linalg.svd(b, full_matrices=False).
 
-    The rsvd core step (reference rand_nla.py:105, svd_econ of B = Q^* A). cuSOLVER's SVD of the
-    config-3 B (200 x 16384) takes ~4.4 ms; CholeskyQR2 of B^T (two k x k Gram matrices) and the SVD
-    of the k x k triangular factor take ~1.2 ms at the same accuracy (B^T = Q_B R, R = U_R S V_R^T:
-    B = V_R S (Q_B U_R)^T). Ill-conditioned or rank-deficient B (where CholeskyQR2 loses
+    The rsvd core step (reference rand_nla.py:105, svd_econ of B = Q^* A): CholeskyQR2 of B^T (two
+    k x k Gram matrices) and the SVD of the k x k triangular factor (`_svd_square`) at the accuracy of
+    the direct SVD (B^T = Q_B R, R = U_R S V_R^T: B = V_R S (Q_B U_R)^T). Ill-conditioned or rank-deficient B (where CholeskyQR2 loses
     orthogonality, or the reference's rank cut applies) takes the direct SVD.
     """
     import torch
@@ -156,7 +177,7 @@ def _svd_wide(b):
         res = _cholqr2_qr(b.T)
         if res is not None:
             qb, r = res
-            ur, s, vrh = torch.linalg.svd(r, full_matrices=False)
+            ur, s, vrh = _svd_square(r) if r.shape[0] <= 512 else torch.linalg.svd(r, full_matrices=False)
             return vrh.T, s, (qb @ ur).T
     return torch.linalg.svd(b, full_matrices=False)
 

@@ -253,3 +253,31 @@ def test_lsqr_device_loop_matches_host_loop(atol, btol, cuda, monkeypatch):
     assert np.linalg.norm(x1 - x2) <= 1e-9 * np.linalg.norm(x2)
     for f in ("r1norm", "arnorm", "acond", "normal_eq_test"):
         assert abs(getattr(r1, f) - getattr(r2, f)) <= 1e-6 * abs(getattr(r2, f)) + 1e-300, f
+
+
+@pytest.mark.parametrize("k,kind", [(1, "rand"), (7, "rand"), (200, "decay"), (200, "repeated"), (300, "illcond"),
+                                    (512, "rand")])
+def test_svd_square_augmented_eigh(k, kind, cuda):
+    """`_svd_square` (eigh of [[0, R], [R^T, 0]]) against torch.linalg.svd: singular values, the
+    reconstruction and orthonormal factors; an ill-conditioned R takes the direct SVD."""
+    import torch
+
+    g = torch.Generator(device=cuda).manual_seed(k)
+    u, _ = torch.linalg.qr(torch.randn(k, k, dtype=torch.float64, device=cuda, generator=g))
+    v, _ = torch.linalg.qr(torch.randn(k, k, dtype=torch.float64, device=cuda, generator=g))
+    if kind == "decay":
+        s = torch.arange(1, k + 1, dtype=torch.float64, device=cuda) ** -2.0
+    elif kind == "repeated":
+        s = torch.ones(k, dtype=torch.float64, device=cuda)
+        s[k // 2:] = 0.5
+    elif kind == "illcond":
+        s = torch.logspace(0, -12, k, dtype=torch.float64, device=cuda)
+    else:
+        s = torch.rand(k, dtype=torch.float64, device=cuda, generator=g) + 0.1
+    r = (u * s) @ v.T
+    uu, ss, vh = rand_nla._svd_square(r)
+    s_ref = torch.linalg.svdvals(r)
+    assert float((ss - s_ref).abs().max()) <= 1e-12 * float(s_ref[0])
+    assert float(((uu * ss) @ vh - r).norm()) <= 1e-12 * float(r.norm())
+    eye = torch.eye(k, dtype=torch.float64, device=cuda)
+    assert float((uu.T @ uu - eye).norm()) <= 1e-10 and float((vh @ vh.T - eye).norm()) <= 1e-10
