@@ -346,12 +346,15 @@ def _qr_solve_if_well_conditioned(m, b, rel_tol, iters: int = 12, margin: float 
 
     With every singular value above rel_tol * sigma_max the truncated pseudo-inverse is the exact
     least-squares solution, so R^-1 Q^* b equals it up to rounding. cuSOLVER's SVD of the config-4
-    sketch (2048 x 512 float64) takes ~32 ms, latency-bound; QR + a condition estimate ~5 ms. The
+    sketch (2048 x 512 float64) takes ~32 ms, latency-bound; QR + a condition estimate a few ms. The
     estimate (power iteration on R^T R, inverse iteration through two triangular solves) is only
     trusted with a margin of `margin` below the cut (kappa < 1 / (margin * rel_tol))."""
     import torch
 
-    q, r = torch.linalg.qr(m, mode="reduced")
+    # CholeskyQR2 (two k x k Gram matrices: ~1 ms at 2048 x 512) unless R's diagonal spread says the
+    # Gram matrix is too ill-conditioned for it; then Householder QR (cuSOLVER geqrf, ~4 ms)
+    qr2 = _cholqr2_qr(m) if m.shape[0] >= 2 * m.shape[1] else None
+    q, r = qr2 if qr2 is not None else torch.linalg.qr(m, mode="reduced")
     d = r.diagonal().abs()
     if float(d.min()) == 0.0:
         return None
