@@ -819,8 +819,10 @@ def _lsqr_device_loop(A, u, v, R, alpha, beta, bnorm, atol, btol, iter_lim, kind
     """LSQR iterations with everything on the device: the fused step (one pass over A) and the
     recurrences (sk_lsqr_recur_f64: v, w, x and the Paige & Saunders scalars in one CTA).  The host
     reads 8 scalars per iteration for the stopping test, one iteration behind: iteration i + 1 is
-    queued before iteration i's scalars are read, so the GPU never waits for the host (after the
-    stopping iteration the queued one is a no-op for x and the state).  Same iterates as
+    queued before iteration i's scalars are read, so the GPU never waits for the host — except once
+    the normal-equation (or residual) test is within 30x of its tolerance, where the next pass is
+    only queued after the check (a pass queued after the stopping iteration would be wasted; it is
+    a no-op for x and the state).  Same iterates as
     `_lsqr_fused_loop` up to rounding (float64 everywhere)."""
     import torch
 
@@ -861,15 +863,22 @@ def _lsqr_device_loop(A, u, v, R, alpha, beta, bnorm, atol, btol, iter_lim, kind
 
         if iter_lim > 0:
             launch(1)
-        i = 1
+        i, launched = 1, 1
+        near = False  # close to the stopping test: no speculative iteration (it would be a wasted pass)
         while i <= iter_lim:
-            if i < iter_lim:
+            if launched == i and i < iter_lim and not near:
                 launch(i + 1)  # queued behind iteration i: no GPU idle while the host checks i
+                launched = i + 1
             evs[i % 2].synchronize()
             itn, istop = int(scal_h[i % 2, 0]), int(scal_h[i % 2, 1])
             r1norm, arnorm, test2, acond = (float(scal_h[i % 2, j]) for j in (2, 3, 4, 5))
+            test1 = float(scal_h[i % 2, 6])
             if istop:
                 break
+            near = test2 <= 30.0 * atol or (btol > 0 and test1 <= 30.0 * btol)
+            if launched == i and i < iter_lim:
+                launch(i + 1)
+                launched = i + 1
             i += 1
     if iter_lim <= 0:
         r1norm, arnorm, test2, acond = beta, alpha * beta, 0.0, 0.0
