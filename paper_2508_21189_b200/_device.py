@@ -91,10 +91,9 @@ def from_result(y: "torch.Tensor", op: Operand):
         return y
     if op.kind == "torch-cpu":
         return y.cpu()
-    host = y.cpu().numpy()
-    if np.iscomplexobj(host):
-        return host.astype(np.complex128, copy=False)
-    return host.astype(np.float64, copy=False)
+    # widen before the copy back (on the device: a NumPy astype of a large result runs single-threaded)
+    y = y.to(torch.complex128 if y.is_complex() else torch.float64)
+    return y.cpu().numpy()
 
 
 PIPELINE_MIN_BYTES = 256 << 20  # host operands at least this large stream through the device in chunks

@@ -127,7 +127,11 @@ class TestMatrix(ABC):
                 host.numel() * host.element_size() >= _device.PIPELINE_MIN_BYTES:
             y = _device.pipelined_right(self._right_device, host, self.k)
             if kind == "numpy":
-                return y.numpy().astype(np.complex128 if y.is_complex() else np.float64, copy=False)
+                # widened by torch's multi-threaded CPU copy (NumPy's astype is single-threaded: ~47 ms for
+                # a config-2 result)
+                import torch
+
+                return y.to(torch.complex128 if y.is_complex() else torch.float64).numpy()
             return y
         op = to_operand(a, allow_vector=False)
         return from_result(self._right_device(op.tensor), op)
