@@ -74,13 +74,49 @@ def to_operand(x, *, allow_vector: bool, complex_ok: bool = True) -> Operand:
     if t.dim() != 2:
         raise ValueError(f"expected a 2-d operand, got shape {tuple(t.shape)}")
     dt = _compute_dtype(t.dtype, complex_ok)
-    if not t.is_cuda:
+    if not t.is_cuda and not pinned and t.numel() * t.element_size() >= STAGED_UPLOAD_MIN_BYTES:
+        t = _upload_staged(t, torch.device("cuda", torch.cuda.current_device()), dt)
+    elif not t.is_cuda:
         t = t.to(device=torch.device("cuda", torch.cuda.current_device()), dtype=dt, non_blocking=pinned)
     elif t.dtype != dt:
         t = t.to(dt)
     if t.shape[1] > 1 and t.stride(1) != 1 or (t.shape[0] > 1 and t.stride(0) < t.shape[1]):
         t = t.contiguous()
     return Operand(t, kind, squeeze, pinned)
+
+
+STAGED_UPLOAD_MIN_BYTES = 64 << 20
+
+
+def _upload_staged(t, dev, dt):
+    """Pageable host tensor -> device through a pinned double buffer of 128 MB chunks: torch's
+    multi-threaded host copy (with the dtype conversion) into one buffer while the other's H2D runs
+    on a side stream (a pageable cudaMemcpy runs through the driver's own staging at a fraction of
+    the PCIe rate)."""
+    if t.dim() == 1 or not t.is_contiguous():
+        t = t.reshape(t.shape[0], -1).contiguous() if t.dim() != 1 else t.contiguous()
+    out = torch.empty(t.shape, dtype=dt, device=dev)
+    row_bytes = max(1, (t.numel() // max(1, t.shape[0])) * out.element_size())
+    rows = max(1, PIPELINE_CHUNK_BYTES // row_bytes)
+    n = t.shape[0]
+    stage = [torch.empty((min(rows, n),) + tuple(t.shape[1:]), dtype=dt, pin_memory=True) for _ in range(2)]
+    evs = [torch.cuda.Event(), torch.cuda.Event()]
+    side = _pipeline_streams(dev)[0]
+    cur = torch.cuda.current_stream(dev)
+    side.wait_stream(cur)
+    for i, r0 in enumerate(range(0, n, rows)):
+        b = i % 2
+        m = min(rows, n - r0)
+        if i >= 2:
+            evs[b].synchronize()  # the H2D out of this buffer has finished
+        stage[b][:m].copy_(t[r0:r0 + m])
+        with torch.cuda.stream(side):
+            out[r0:r0 + m].copy_(stage[b][:m], non_blocking=True)
+            evs[b].record(side)
+    cur.wait_stream(side)
+    for e in evs:
+        e.synchronize()  # the staging buffers return to the pinned cache only when their copies are done
+    return out
 
 
 def from_result(y: "torch.Tensor", op: Operand):
