@@ -142,24 +142,79 @@ def _cholqr2(m, max_spread: float = 1e6):
 
 
 def _svd_square(r, min_ratio: float = 1e-7):
-    """Thin SVD of a small square float64 CUDA matrix through the symmetric eigenproblem of the
-    augmented [[0, R], [R^T, 0]] (eigenvalues +-sigma_i, eigenvectors [u_i; v_i] / sqrt 2): no
-    squaring of the condition number (unlike the Gram matrix), sigma to ~eps * sigma_max.  cuSOLVER's
-    SVD of the config-3 200 x 200 factor takes ~7-11 ms (Jacobi sweeps), this eigh 4 ms
-    (`tools/svd_small_probe.py`).  A factor with sigma_min below min_ratio * sigma_max (where the +-0
-    pairs of the augmented problem could mix u and v) takes torch.linalg.svd."""
+    """Thin SVD (U, S, Vh) of a small float64 CUDA matrix (m x n) through the symmetric eigenproblem
+    of the augmented [[0, R], [R^T, 0]] (eigenvalues +-sigma_i and |m - n| zeros, eigenvectors
+    [u_i; v_i] / sqrt 2): no squaring of the condition number (unlike the Gram matrix), sigma to
+    ~eps * sigma_max.  cuSOLVER's SVD of the config-3 200 x 200 factor takes ~7-11 ms (Jacobi
+    sweeps), this eigh 4 ms (`tools/svd_small_probe.py`).  A matrix with sigma_min below
+    min_ratio * sigma_max (where the zero eigenvalues could mix u and v) takes torch.linalg.svd."""
     import torch
 
-    k = r.shape[0]
-    aug = torch.zeros((2 * k, 2 * k), dtype=r.dtype, device=r.device)
-    aug[:k, k:] = r
-    aug[k:, :k] = r.T
+    m, n = r.shape
+    q = min(m, n)
+    if q == 0:
+        return torch.linalg.svd(r, full_matrices=False)
+    aug = torch.zeros((m + n, m + n), dtype=r.dtype, device=r.device)
+    aug[:m, m:] = r
+    aug[m:, :m] = r.T
     w, vec = torch.linalg.eigh(aug)
-    s = w[k:].flip(0)
+    s = w[m + n - q:].flip(0)
     if not bool(torch.isfinite(s).all()) or float(s[-1]) <= min_ratio * float(s[0]):
         return torch.linalg.svd(r, full_matrices=False)
-    top = vec[:, k:].flip(1) * math.sqrt(2.0)
-    return top[:k].contiguous(), s.contiguous(), top[k:].T.contiguous()
+    top = vec[:, m + n - q:].flip(1) * math.sqrt(2.0)
+    return top[:m].contiguous(), s.contiguous(), top[m:].T.contiguous()
+
+
+def _qr_tall(m):
+    """Reduced QR of a tall float64 matrix: CholeskyQR2 on the device for tall, well-conditioned m
+    (the generalized-Nystrom Y at the DESIGN section-6 shape, 2M x 64: cuSOLVER's Householder QR
+    ~40 ms, CholeskyQR2 a few), else torch.linalg.qr.  Q differs from Householder's by column signs
+    only (R with a positive diagonal); every caller consumes it sign-invariantly."""
+    import torch
+
+    n, k = m.shape
+    if m.is_cuda and not m.is_complex() and k > 0 and n >= 16 * k and n * k >= (1 << 20):
+        res = _cholqr2_qr(m)
+        if res is None:
+            res = _qr_tall_split(m)
+        if res is not None:
+            return res
+    return torch.linalg.qr(m, mode="reduced")
+
+
+def _qr_tall_split(m, gap: float = 1e10, kept_cond: float = 1e8):
+    """Orthonormal Q (n x k) and R = Q^T m for a tall m whose Gram spectrum splits cleanly into a
+    well-conditioned part and exact zeros — e.g. an SRTT sketch whose sampler drew the same row for
+    two columns (sampling with replacement), where CholeskyQR2 cannot run: Q = [m V_r L_r^-1/2
+    re-orthonormalised by CholeskyQR2, a seeded orthonormal completion].  Householder QR's Q also
+    completes the rank-deficient part arbitrarily; callers use Q's span and m = Q R only.  None when
+    the spectrum has no clean split (Householder QR then runs)."""
+    import torch
+
+    n, k = m.shape
+    lam, vec = torch.linalg.eigh(m.T @ m)  # ascending
+    lmax = float(lam[-1])
+    if not lmax > 0.0:
+        return None
+    lam_h = lam.cpu().numpy()
+    nz = int((lam_h > lmax / kept_cond).sum())  # eigenvalues of the kept, well-conditioned part
+    if nz == 0 or nz == k or not lam_h[k - nz] > gap * max(float(lam_h[k - nz - 1]), 0.0):
+        return None
+    keep = slice(k - nz, k)
+    qr_ = m @ (vec[:, keep] / lam[keep].sqrt())
+    res = _cholqr2_qr(qr_)
+    if res is None:
+        return None
+    q1 = res[0]
+    g = torch.Generator(device=m.device).manual_seed(20250821)
+    c = torch.randn(n, k - nz, dtype=m.dtype, device=m.device, generator=g)
+    for _ in range(2):
+        c = c - q1 @ (q1.T @ c)
+    res_c = _cholqr2_qr(c)
+    if res_c is None:
+        return None
+    q = torch.cat([q1, res_c[0]], dim=1)
+    return q, q.T @ m
 
 
 def _svd_wide(b):
@@ -400,7 +455,11 @@ def default_left_dim(k: int) -> int:
 def _svd_econ(m):
     import torch
 
-    u, s, vh = torch.linalg.svd(_t64(m), full_matrices=False)
+    m = _t64(m)
+    if m.is_cuda and not m.is_complex() and 0 < m.shape[0] + m.shape[1] <= 512:
+        u, s, vh = _svd_square(m)  # small real factors: the augmented eigh (see _svd_square)
+    else:
+        u, s, vh = torch.linalg.svd(m, full_matrices=False)
     return u, s, vh.conj().T
 
 
@@ -557,8 +616,8 @@ def _gn_svd_core(A, tm_omega, tm_psi) -> SvdFactorization:
     import torch
 
     y, x = two_sided_sketch(A, tm_omega, tm_psi)
-    q, _ = torch.linalg.qr(_t64(y), mode="reduced")
-    pmat, t = torch.linalg.qr(_t64(x), mode="reduced")
+    q, _ = _qr_tall(_t64(y))
+    pmat, t = _qr_tall(_t64(x))
     w = _t64(tm_psi.apply_adjoint(q))  # p x k
     u1, s1, v1 = _svd_econ(w)
     r = _rank_of(s1)

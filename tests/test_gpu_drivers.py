@@ -281,3 +281,42 @@ def test_svd_square_augmented_eigh(k, kind, cuda):
     assert float(((uu * ss) @ vh - r).norm()) <= 1e-12 * float(r.norm())
     eye = torch.eye(k, dtype=torch.float64, device=cuda)
     assert float((uu.T @ uu - eye).norm()) <= 1e-10 and float((vh @ vh.T - eye).norm()) <= 1e-10
+
+
+@pytest.mark.parametrize("dup", [0, 1, 3])
+def test_qr_tall_paths(dup, cuda):
+    """`_qr_tall` on a tall float64 matrix with `dup` duplicated columns (an SRTT sketch sampled with
+    replacement): Q orthonormal with k columns, m = Q R, and Q's span contains m's columns."""
+    import torch
+
+    g = torch.Generator(device=cuda).manual_seed(dup)
+    n, k = 1 << 18, 48
+    m = torch.randn(n, k, dtype=torch.float64, device=cuda, generator=g)
+    for i in range(dup):
+        m[:, 2 * i + 1] = -m[:, 2 * i]
+    q, r = rand_nla._qr_tall(m)
+    eye = torch.eye(k, dtype=torch.float64, device=cuda)
+    assert q.shape == (n, k)
+    assert float((q.T @ q - eye).norm()) <= 1e-12
+    assert float((q @ r - m).norm()) <= 1e-12 * float(m.norm())
+    assert float((m - q @ (q.T @ m)).norm()) <= 1e-12 * float(m.norm())
+
+
+def test_gen_nystrom_svd_srtt_with_repeats(cuda):
+    """Generalized Nystrom with an SRTT Omega whose sampler repeats rows (rank-deficient Y): the
+    factorization reproduces a low-rank A to rounding."""
+    import torch
+
+    g = torch.Generator(device=cuda).manual_seed(4)
+    n, d, r = 200000, 512, 20
+    a = (torch.randn(n, r, dtype=torch.float64, device=cuda, generator=g)
+         @ torch.randn(r, d, dtype=torch.float64, device=cuda, generator=g)).float()
+    om = skb.SparseRttTM(d, 64, 1, "wht", seed=1)
+    ps = skb.SparseUniformTM(n, 96, 8, seed=2)
+    fs = rn_gn(a, om, ps)
+    approx = (fs.u * fs.sigma) @ fs.v.T
+    assert float((approx - a.double()).norm() / a.double().norm()) <= 1e-5
+
+
+def rn_gn(a, om, ps):
+    return rand_nla.gen_nystrom_svd(a, 64, 96, om, ps)
