@@ -320,7 +320,8 @@ def time_device(torch, w, steps, warmup, world, dev):
 
 def _downstream(torch, w, dev):
     """The config's downstream pipeline on the same input (warm, wall clock around a synchronized
-    call): config 3 rsvd (sketch, orth, Q^T A, SVD), config 4 sketch-and-precondition LSQR."""
+    call): config 3 rsvd (sketch, orth, Q^T A, SVD), config 4 sketch-and-precondition LSQR and
+    sketch-and-solve, the two-sided leg's generalized Nystrom SVD (the paper's headline application)."""
     from paper_2508_21189_b200 import rand_nla
 
     def timed(fn):
@@ -366,6 +367,11 @@ def _downstream(torch, w, dev):
         return {"lsqr_ms": ms, "iterations": res.itn, "istop": res.istop, "sketch_and_solve_ms": ms_ss,
                 "what": "sketch-and-precondition LSQR to the 1e-6 normal-equation test (SA, QR(SA), LSQR on A R^-1); "
                         "sketch-and-solve (SA, Sb, truncated pseudo-inverse)"}
+    if w["name"] == "twosided":
+        om, ps = w["tm"]
+        fac, ms = timed(lambda: rand_nla.gen_nystrom_svd(w["a"], w["k"], w["p"], om, ps))
+        return {"gen_nystrom_svd_ms": ms, "rank": int(fac.sigma.numel()),
+                "what": "generalized Nystrom in SVD form (two-sided sketch, QR of Y and of X, the core SVDs) on the leg's A"}
     return None
 
 
