@@ -61,7 +61,8 @@ struct TsParams {
   int ctas_per_group;
   int nb;                // Omega^T operands: 1 (hi) or 2 (hi + lo)
   int omega_res;         // 1: the column group's Omega^T tiles stay resident in shared memory (loaded once)
-  int dbg;               // timing experiments (SKETCH_B200_TS_DBG): 1 no MMA2, 2 no PsiT writes, 4 no Y stores
+  int dbg;               // timing experiments (SKETCH_B200_TS_DBG): 1 no MMA2, 2 no PsiT writes, 4 no Y stores,
+                         // 16 per-lane row adds instead of the lane-pair sector adds
 };
 
 template <int N>
@@ -358,7 +359,42 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld16(ybase + g * 16, r);
         tmem_ld_wait();
         const int col = yc0 + g * 16;
-        if (row < p.n && col < p.k && !(p.dbg & 4)) {
+        if (col + 16 <= p.k && (p.ldy & 7) == 0 && !(p.dbg & 4) && !(p.dbg & 16)) {
+          // lane pairs complete 32-byte sectors: the even lane of a pair writes / adds columns [b, b+4)
+          // and the odd lane [b+4, b+8) of the SAME row, one row per instruction (an exchange of 4
+          // values per 8 columns through shfl.xor 1), instead of every lane writing 16 bytes of its
+          // own row (section-6 shape: 1.47 -> 1.30 ms)
+          const bool odd = lane & 1;
+          const int64_t row_e = row - (odd ? 1 : 0), row_o = row_e + 1;
+#pragma unroll
+          for (int b = 0; b < 16; b += 8) {
+            float mine[4], got[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float send = __uint_as_float(r[b + (odd ? q : 4 + q)]);
+              got[q] = __shfl_xor_sync(0xffffffffu, send, 1);
+              mine[q] = __uint_as_float(r[b + (odd ? 4 + q : q)]);
+            }
+            // even lane: (row_e, b..b+3) = mine, (row_o, b..b+3) = got
+            // odd lane:  (row_e, b+4..b+7) = got, (row_o, b+4..b+7) = mine
+            const int c0 = col + b + (odd ? 4 : 0);
+            const float* v1 = odd ? got : mine;   // row_e part
+            const float* v2 = odd ? mine : got;   // row_o part
+            if (p.ncg > 1) {  // two column groups add onto a zeroed Y
+              if (row_e < p.n)
+                red_add_v4(p.Y + row_e * p.ldy + c0, v1[0] * p.sy, v1[1] * p.sy, v1[2] * p.sy, v1[3] * p.sy);
+              if (row_o < p.n)
+                red_add_v4(p.Y + row_o * p.ldy + c0, v2[0] * p.sy, v2[1] * p.sy, v2[2] * p.sy, v2[3] * p.sy);
+            } else {
+              if (row_e < p.n)
+                *reinterpret_cast<float4*>(p.Y + row_e * p.ldy + c0) =
+                    make_float4(v1[0] * p.sy, v1[1] * p.sy, v1[2] * p.sy, v1[3] * p.sy);
+              if (row_o < p.n)
+                *reinterpret_cast<float4*>(p.Y + row_o * p.ldy + c0) =
+                    make_float4(v2[0] * p.sy, v2[1] * p.sy, v2[2] * p.sy, v2[3] * p.sy);
+            }
+          }
+        } else if (row < p.n && col < p.k && !(p.dbg & 4)) {
           float* out = p.Y + row * p.ldy + col;
           if (p.ncg == 1) {
 #pragma unroll
