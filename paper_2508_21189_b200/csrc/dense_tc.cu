@@ -764,6 +764,44 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive_remote(acc_empty_leader + 8u * buf);
       }
       const int64_t row = (int64_t)(2 * w.mt + (int)rank) * BM + 32 * lg + lane;
+      if constexpr (KR == 0) {
+        const bool direct = p.ksplit == 1 && !p.out_t;
+        // partial sums (or a transposed result): tc_splitk_reduce forms Y
+        float* const obase = direct ? p.Y : p.part + (int64_t)w.ks * p.M * p.N;
+        const int64_t ld = direct ? p.ldy : (int64_t)p.N;
+        const float sc2 = direct ? p.scale : 1.0f;
+        // (dense engine only: the Khatri-Rao reducers' register budget, 128 sums + the fold, would spill)
+        if ((bnh & 7) == 0 && (col0 & 7) == 0 && (ld & 7) == 0 && col0 + bnh <= p.N &&
+            (reinterpret_cast<uintptr_t>(obase) & 31) == 0) {
+          // lane pairs complete 32-byte sectors (each lane holds one row: a lane's own 16-byte store
+          // would cover half a sector): the even lane writes columns [b, b+4) and the odd lane
+          // [b+4, b+8) of the same row, one row per instruction, after a shfl.xor exchange of 4 values
+          const bool odd = lane & 1;
+          const int64_t row_e = row - (odd ? 1 : 0), row_o = row_e + 1;
+#pragma unroll
+          for (int b = 0; b < kMaxBNH; b += 8) {
+            if (b < bnh) {
+              float mine[4], got[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {  // static register indices (a runtime index would spill sum[])
+                const float lo = sum[b + q], hi = sum[b + 4 + q];
+                got[q] = __shfl_xor_sync(0xffffffffu, odd ? lo : hi, 1);
+                mine[q] = odd ? hi : lo;
+              }
+              const float* v1 = odd ? got : mine;  // row_e's part
+              const float* v2 = odd ? mine : got;  // row_o's part
+              const int c = col0 + b + (odd ? 4 : 0);
+              if (row_e < p.M)
+                *reinterpret_cast<float4*>(obase + row_e * ld + c) =
+                    make_float4(v1[0] * sc2, v1[1] * sc2, v1[2] * sc2, v1[3] * sc2);
+              if (row_o < p.M)
+                *reinterpret_cast<float4*>(obase + row_o * ld + c) =
+                    make_float4(v2[0] * sc2, v2[1] * sc2, v2[2] * sc2, v2[3] * sc2);
+            }
+          }
+          continue;
+        }
+      }
       if (row < p.M) {
         float* out;
         float sc2;

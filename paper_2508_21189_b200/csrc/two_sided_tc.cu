@@ -370,10 +370,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int b = 0; b < 16; b += 8) {
             float mine[4], got[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float send = __uint_as_float(r[b + (odd ? q : 4 + q)]);
-              got[q] = __shfl_xor_sync(0xffffffffu, send, 1);
-              mine[q] = __uint_as_float(r[b + (odd ? 4 + q : q)]);
+            for (int q = 0; q < 4; ++q) {  // static register indices
+              const float lo = __uint_as_float(r[b + q]), hi = __uint_as_float(r[b + 4 + q]);
+              got[q] = __shfl_xor_sync(0xffffffffu, odd ? lo : hi, 1);
+              mine[q] = odd ? hi : lo;
             }
             // even lane: (row_e, b..b+3) = mine, (row_o, b..b+3) = got
             // odd lane:  (row_e, b+4..b+7) = got, (row_o, b+4..b+7) = mine
