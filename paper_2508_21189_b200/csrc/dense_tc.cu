@@ -801,6 +801,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           continue;
         }
+      } else {
+        // Khatri-Rao reducers: 16-byte stores of the row's columns (no exchange: 168 registers hold
+        // the 128 sums), a quarter of the scalar stores' instructions
+        const bool direct = p.ksplit == 1 && !p.out_t;
+        float* const obase = direct ? p.Y : p.part + (int64_t)w.ks * p.M * p.N;
+        const int64_t ld = direct ? p.ldy : (int64_t)p.N;
+        const float sc2 = direct ? p.scale : 1.0f;
+        if ((bnh & 3) == 0 && (col0 & 3) == 0 && (ld & 3) == 0 && col0 + bnh <= p.N &&
+            (reinterpret_cast<uintptr_t>(obase) & 15) == 0) {
+          if (row < p.M) {
+            float* out = obase + row * ld + col0;
+#pragma unroll
+            for (int c = 0; c < kMaxBNH; c += 4)
+              if (c < bnh)
+                *reinterpret_cast<float4*>(out + c) =
+                    make_float4(sum[c] * sc2, sum[c + 1] * sc2, sum[c + 2] * sc2, sum[c + 3] * sc2);
+          }
+          continue;
+        }
       }
       if (row < p.M) {
         float* out;
