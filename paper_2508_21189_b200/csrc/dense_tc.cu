@@ -853,6 +853,36 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Y = scale * sum_s part[s] (fixed order); out_t: element (r, c) -> Y[c * ldy + r]
 __global__ void tc_splitk_reduce(const float* __restrict__ part, int ksplit, int64_t M, int N, float scale,
                                  float* __restrict__ Y, int64_t ldy, int out_t = 0) {
+  if (!out_t && (N & 3) == 0 && (ldy & 3) == 0 && ((reinterpret_cast<uintptr_t>(part) | reinterpret_cast<uintptr_t>(Y)) & 15) == 0) {
+    // float4 elements; the (row, column) position advances by the grid stride without a division per
+    // element (the 64-bit divide / modulo of the generic loop dominated this memory-bound kernel)
+    const int64_t n4 = N >> 2, total4 = M * n4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i0 >= total4) return;
+    int64_t r = i0 / n4, c = i0 - r * n4;
+    const int64_t dr = stride / n4, dc = stride - dr * n4;
+    const float4* p4 = reinterpret_cast<const float4*>(part);
+    for (int64_t i = i0; i < total4; i += stride) {
+      float4 acc = p4[r * n4 + c];
+      for (int q = 1; q < ksplit; ++q) {
+        const float4 v = p4[(q * M + r) * n4 + c];
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+      *reinterpret_cast<float4*>(Y + r * ldy + 4 * c) =
+          make_float4(acc.x * scale, acc.y * scale, acc.z * scale, acc.w * scale);
+      r += dr;
+      c += dc;
+      if (c >= n4) {
+        c -= n4;
+        ++r;
+      }
+    }
+    return;
+  }
   const int64_t total = M * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t r, c;
