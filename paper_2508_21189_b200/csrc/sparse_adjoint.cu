@@ -164,14 +164,24 @@ template <typename T>
 __global__ void adjoint_reduce(const T* __restrict__ part, int nsplit, int64_t split_stride, int64_t ldp,
                                int64_t k, int64_t m, T scale, T* __restrict__ SA, int64_t ldsa, int accumulate) {
   const int64_t total = k * m;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = idx / m, col = idx % m;
+  // the (row, column) position advances by the grid stride: no 64-bit divide / modulo per element
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i0 >= total) return;
+  int64_t c = i0 / m, col = i0 - c * m;
+  const int64_t dc = stride / m, dcol = stride - dc * m;
+  for (int64_t idx = i0; idx < total; idx += stride) {
     double s = 0.0;
     for (int q = 0; q < nsplit; ++q) s += (double)part[q * split_stride + c * ldp + col];
     T v = (T)(s * (double)scale);
     if (accumulate) v += SA[c * ldsa + col];
     SA[c * ldsa + col] = v;
+    c += dc;
+    col += dcol;
+    if (col >= m) {
+      col -= m;
+      ++c;
+    }
   }
 }
 
